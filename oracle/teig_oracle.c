@@ -1,0 +1,1047 @@
+/*
+ * oracle/teig_oracle.c -- TEST INFRASTRUCTURE ONLY (see teig_oracle.h).
+ *
+ * A plain-C restatement of the reference's reorder path.  Every function
+ * cites the reference file:line it restates; the arithmetic is performed in
+ * the same order as the reference so that, compiled with the same flags
+ * (oracle/Makefile), results agree BIT-FOR-BIT with oracle/_ref
+ * (tests/test_oracle.py).  Never used by the product path.
+ */
+#include "teig_oracle.h"
+
+#include <float.h>
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define EPS 2.220446049250313e-16 /* 2^-52, kernels.cpp:16 */
+#define SAFMIN DBL_MIN            /* kernels.cpp:17 */
+#define A_(m, i, j, ld) ((m)[(size_t)(i) + (size_t)(j) * (size_t)(ld)])
+
+static double sgn(double x) { return x >= 0.0 ? 1.0 : -1.0; } /* kernels.cpp:19 */
+
+/* ======================================================================= */
+/* Philox4x32-10, philox.hpp:18-84                                          */
+
+void teo_philox_round10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+    uint32_t k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+        const uint32_t n1 = (uint32_t)p1;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+        const uint32_t n3 = (uint32_t)p0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+void teo_philox_init(teo_philox* p, uint64_t seed) {
+    p->key[0] = (uint32_t)seed;
+    p->key[1] = (uint32_t)(seed >> 32);
+    p->counter = 0;
+    p->have = 0;
+}
+
+uint64_t teo_philox_next_u64(teo_philox* p) {
+    if (p->have == 0) {
+        const uint32_t ctr[4] = {(uint32_t)p->counter, (uint32_t)(p->counter >> 32), 0u, 0u};
+        teo_philox_round10(ctr, p->key, p->buf);
+        p->counter++;
+        p->have = 2;
+    }
+    const int i = 2 - p->have;
+    p->have--;
+    return ((uint64_t)p->buf[2 * i + 1] << 32) | p->buf[2 * i];
+}
+
+double teo_philox_uniform_sym(teo_philox* p) {
+    const uint64_t u = teo_philox_next_u64(p) >> 11;
+    return (double)u * (2.0 / 9007199254740992.0) - 1.0;
+}
+
+double teo_philox_uniform01(teo_philox* p) {
+    const uint64_t u = teo_philox_next_u64(p) >> 11;
+    return (double)u * (1.0 / 9007199254740992.0);
+}
+
+uint64_t teo_philox_bounded(teo_philox* p, uint64_t n) { return teo_philox_next_u64(p) % n; }
+
+/* ======================================================================= */
+/* generators, generate.cpp                                                 */
+
+void teo_default_spectrum(size_t n, double* re, double* im) {
+    /* generate.cpp:68-91: n - 2*floor(n/4) reals on [-10,10], then floor(n/4)
+     * conjugate pairs, re on [-9.7,9.7], im cycling 1,3,5 */
+    const size_t npairs = n / 4, nreal = n - 2 * npairs;
+    size_t k = 0;
+    for (size_t i = 0; i < nreal; ++i, ++k) {
+        re[k] = (nreal == 1) ? 1.0 : -10.0 + 20.0 * (double)i / (double)(nreal - 1);
+        im[k] = 0.0;
+    }
+    for (size_t i = 0; i < npairs; ++i) {
+        const double r = (npairs == 1) ? 0.5 : -9.7 + 19.4 * (double)i / (double)(npairs - 1);
+        const double m = 1.0 + 2.0 * (double)(i % 3);
+        re[k] = r; im[k] = m; ++k;
+        re[k] = r; im[k] = -m; ++k;
+    }
+}
+
+uint64_t teo_known_spectrum_seed(uint64_t seed) {
+    /* generate.cpp:184 with ProblemKind::known_spectrum == 1 */
+    return seed * 0x9E3779B97F4A7C15ull + 1ull;
+}
+
+void teo_schur_input(size_t n, uint64_t fill_seed, double* s, size_t ld) {
+    /* generate.cpp:115-150.  The default spectrum lists reals first and then
+     * pairs, so the layout is nreal 1x1 blocks followed by 2x2 blocks
+     * [[a, b], [-b, a]] (b = |im|); the strictly upper part outside the
+     * blocks is filled row by row from the Philox stream. */
+    double* re = (double*)malloc(n * sizeof(double));
+    double* im = (double*)malloc(n * sizeof(double));
+    teo_default_spectrum(n, re, im);
+    for (size_t j = 0; j < n; ++j) memset(&A_(s, 0, j, ld), 0, n * sizeof(double));
+    size_t pos = 0;
+    for (size_t i = 0; i < n;) {
+        if (im[i] == 0.0) {
+            A_(s, pos, pos, ld) = re[i];
+            pos += 1;
+            i += 1;
+        } else { /* default spectrum stores the conjugate right after */
+            const double a = re[i], b = fabs(im[i]);
+            A_(s, pos, pos, ld) = a;
+            A_(s, pos, pos + 1, ld) = b;
+            A_(s, pos + 1, pos, ld) = -b;
+            A_(s, pos + 1, pos + 1, ld) = a;
+            pos += 2;
+            i += 2;
+        }
+    }
+    teo_philox rng;
+    teo_philox_init(&rng, fill_seed);
+    for (size_t i = 0; i < n; ++i)
+        for (size_t j = i + 1; j < n; ++j) {
+            const int in_block = (j == i + 1) && (A_(s, i + 1, i, ld) != 0.0);
+            if (!in_block && A_(s, i, j, ld) == 0.0) A_(s, i, j, ld) = teo_philox_uniform_sym(&rng);
+        }
+    free(re);
+    free(im);
+}
+
+void teo_hessenberg_random(size_t n, uint64_t seed, double* h, size_t ld) {
+    /* generate.cpp:184 (kind hessenberg_random == 4) and :192-198, row-major
+     * draw order */
+    teo_philox rng;
+    teo_philox_init(&rng, seed * 0x9E3779B97F4A7C15ull + 4ull);
+    for (size_t j = 0; j < n; ++j) memset(&A_(h, 0, j, ld), 0, n * sizeof(double));
+    for (size_t i = 0; i < n; ++i)
+        for (size_t j = (i == 0 ? 0 : i - 1); j < n; ++j) A_(h, i, j, ld) = teo_philox_uniform_sym(&rng);
+}
+
+/* ======================================================================= */
+/* selection, reorder.cpp:21-43, 80-97                                      */
+
+size_t teo_scan_blocks(size_t n, const double* s, size_t ld, uint8_t* sizes) {
+    size_t nb = 0;
+    for (size_t i = 0; i < n;) {
+        if (i + 1 < n && A_(s, i + 1, i, ld) != 0.0) {
+            sizes[nb++] = 2;
+            i += 2;
+        } else {
+            sizes[nb++] = 1;
+            i += 1;
+        }
+    }
+    return nb;
+}
+
+void teo_select_fraction(size_t nb, double fraction, uint64_t seed, uint8_t* flags) {
+    const size_t want = (size_t)(fraction * (double)nb);
+    size_t* idx = (size_t*)malloc((nb ? nb : 1) * sizeof(size_t));
+    for (size_t i = 0; i < nb; ++i) idx[i] = i;
+    teo_philox rng;
+    teo_philox_init(&rng, seed ^ 0x5e1ec7u);
+    for (size_t i = 0; i < want && i + 1 < nb; ++i) {
+        const size_t j = i + (size_t)teo_philox_bounded(&rng, nb - i);
+        const size_t t = idx[i];
+        idx[i] = idx[j];
+        idx[j] = t;
+    }
+    memset(flags, 0, nb);
+    for (size_t i = 0; i < want; ++i) flags[idx[i]] = 1;
+    free(idx);
+}
+
+/* ======================================================================= */
+/* dense helpers, dense.hpp:64-82, :145-156                                 */
+
+void teo_gemm(int ta, int tb, size_t m, size_t n, size_t k, double alpha, const double* a,
+              size_t lda, const double* b, size_t ldb, double* c, size_t ldc) {
+    if (m == 0 || n == 0) return;
+    for (size_t j = 0; j < n; ++j) {
+        double* cj = c + j * ldc;
+        for (size_t p = 0; p < k; ++p) {
+            const double sc = alpha * (tb ? b[p * ldb + j] : b[j * ldb + p]);
+            if (sc == 0.0) continue;
+            if (!ta) {
+                const double* ap = a + p * lda;
+                for (size_t i = 0; i < m; ++i) cj[i] += sc * ap[i];
+            } else {
+                for (size_t i = 0; i < m; ++i) cj[i] += sc * a[i * lda + p];
+            }
+        }
+    }
+}
+
+static double nrm2(size_t n, const double* x) {
+    double mx = 0.0;
+    for (size_t i = 0; i < n; ++i) mx = fmax(mx, fabs(x[i]));
+    if (mx == 0.0) return 0.0;
+    double acc = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+        const double t = x[i] / mx;
+        acc += t * t;
+    }
+    return mx * sqrt(acc);
+}
+
+/* ======================================================================= */
+/* reflectors and rotations, kernels.cpp:24-120                             */
+
+typedef struct {
+    size_t len;
+    double v[8];
+    double tau;
+} refl8; /* reflectors inside the swap kernel have length <= 4 */
+
+/* make_reflector, kernels.cpp:24-58; len <= 8; returns beta */
+static double make_refl(const double* x, size_t len, refl8* h) {
+    h->len = len;
+    h->tau = 0.0;
+    for (size_t i = 0; i < len; ++i) h->v[i] = 0.0;
+    if (len == 0) return 0.0;
+    h->v[0] = 1.0;
+    if (len == 1) return x[0];
+    const double alpha = x[0];
+    const double tail = nrm2(len - 1, x + 1);
+    if (tail == 0.0) return alpha == 0.0 ? 0.0 : alpha;
+    double beta = -sgn(alpha) * hypot(alpha, tail);
+    double tl[8];
+    for (size_t i = 1; i < len; ++i) tl[i - 1] = x[i];
+    double a = alpha, t;
+    int rescale = 0;
+    while (fabs(beta) < SAFMIN / EPS && rescale < 20) {
+        const double big = 1.0 / (SAFMIN / EPS);
+        for (size_t i = 0; i + 1 < len; ++i) tl[i] *= big;
+        a *= big;
+        t = nrm2(len - 1, tl);
+        beta = -sgn(a) * hypot(a, t);
+        ++rescale;
+    }
+    h->tau = (beta - a) / beta;
+    const double inv = 1.0 / (a - beta);
+    for (size_t i = 1; i < len; ++i) h->v[i] = tl[i - 1] * inv;
+    for (int r = 0; r < rescale; ++r) beta *= SAFMIN / EPS;
+    return beta;
+}
+
+/* apply_reflector_left, kernels.cpp:60-70 */
+static void refl_left(double* a, size_t ld, const refl8* h, size_t r0, size_t c0, size_t c1) {
+    if (h->tau == 0.0) return;
+    for (size_t j = c0; j < c1; ++j) {
+        double w = 0.0;
+        for (size_t i = 0; i < h->len; ++i) w += h->v[i] * A_(a, r0 + i, j, ld);
+        w *= h->tau;
+        for (size_t i = 0; i < h->len; ++i) A_(a, r0 + i, j, ld) -= w * h->v[i];
+    }
+}
+
+/* apply_reflector_right, kernels.cpp:72-82 (kept for the Schur restatement) */
+static void refl_right(double* a, size_t ld, const refl8* h, size_t c0, size_t r0, size_t r1)
+    __attribute__((unused));
+static void refl_right(double* a, size_t ld, const refl8* h, size_t c0, size_t r0, size_t r1) {
+    if (h->tau == 0.0) return;
+    for (size_t i = r0; i < r1; ++i) {
+        double w = 0.0;
+        for (size_t j = 0; j < h->len; ++j) w += A_(a, i, c0 + j, ld) * h->v[j];
+        w *= h->tau;
+        for (size_t j = 0; j < h->len; ++j) A_(a, i, c0 + j, ld) -= w * h->v[j];
+    }
+}
+
+void teo_make_givens(double a, double b, double* c, double* s) {
+    if (b == 0.0) {
+        *c = 1.0;
+        *s = 0.0;
+    } else if (a == 0.0) {
+        *c = 0.0;
+        *s = 1.0;
+    } else {
+        const double r = hypot(a, b);
+        *c = a / r;
+        *s = b / r;
+    }
+}
+
+/* apply_givens_left on rows (i, j), columns [c0, c1): kernels.cpp:104-111 */
+static void rot_rows(double* a, size_t ld, double c, double s, size_t i, size_t j, size_t c0,
+                     size_t c1) {
+    for (size_t k = c0; k < c1; ++k) {
+        const double x = A_(a, i, k, ld), y = A_(a, j, k, ld);
+        A_(a, i, k, ld) = c * x + s * y;
+        A_(a, j, k, ld) = -s * x + c * y;
+    }
+}
+
+/* apply_givens_right on columns (i, j), rows [r0, r1): kernels.cpp:113-120 */
+static void rot_cols(double* a, size_t ld, double c, double s, size_t i, size_t j, size_t r0,
+                     size_t r1) {
+    for (size_t k = r0; k < r1; ++k) {
+        const double x = A_(a, k, i, ld), y = A_(a, k, j, ld);
+        A_(a, k, i, ld) = c * x + s * y;
+        A_(a, k, j, ld) = -s * x + c * y;
+    }
+}
+
+/* ======================================================================= */
+/* 2x2 standardization, kernels.cpp:126-219                                 */
+
+void teo_standardize_2x2(double a, double b, double c, double d, double out[10]) {
+    double cs = 1.0, sn = 0.0;
+    const double mx = fmax(fmax(fabs(a), fabs(b)), fmax(fabs(c), fabs(d)));
+    int ex = 0;
+    if (mx > 0.0 && (mx > 1e150 || mx < 1e-150)) { /* power-of-two prescale */
+        ex = ilogb(mx);
+        const double sc = ldexp(1.0, -ex);
+        a *= sc; b *= sc; c *= sc; d *= sc;
+    }
+    if (c == 0.0) {
+        /* triangular already */
+    } else if (b == 0.0) {
+        cs = 0.0;
+        sn = 1.0;
+        const double ta = a;
+        a = d;
+        d = ta;
+        b = -c;
+        c = 0.0;
+    } else if ((a - d) == 0.0 && sgn(b) != sgn(c)) {
+        /* standard complex pair already */
+    } else {
+        const double p = 0.5 * (a - d);
+        const double qq = b + c;
+        const double r2 = hypot(2.0 * p, qq);
+        const double sig = sgn(qq);
+        const double cos2 = sig * qq / r2;
+        const double sin2 = -sig * 2.0 * p / r2;
+        cs = sqrt(0.5 * (1.0 + cos2));
+        sn = sin2 / (2.0 * cs);
+        {
+            const double aa = cs * a + sn * c, bb = cs * b + sn * d;
+            const double cc = -sn * a + cs * c, dd = -sn * b + cs * d;
+            a = aa * cs + bb * sn;
+            b = -aa * sn + bb * cs;
+            c = cc * cs + dd * sn;
+            d = -cc * sn + dd * cs;
+        }
+        const double m = 0.5 * (a + d);
+        a = m;
+        d = m;
+        if (c == 0.0) {
+        } else if (b == 0.0) {
+            const double tc = cs;
+            cs = -sn;
+            sn = tc;
+            b = -c;
+            c = 0.0;
+        } else if (sgn(b) != sgn(c)) {
+        } else { /* real pair: rotate onto the eigenvector basis */
+            const double sab = sqrt(fabs(b));
+            const double sac = sqrt(fabs(c));
+            const double pp = sab * sac;
+            const double tau = 1.0 / sqrt(fabs(b + c));
+            const double cs1 = sab * tau;
+            const double sn1 = sgn(c) * sac * tau;
+            a = m + pp;
+            d = m - pp;
+            b = b - c;
+            c = 0.0;
+            const double tc = cs * cs1 - sn * sn1;
+            sn = cs * sn1 + sn * cs1;
+            cs = tc;
+        }
+    }
+    const double back = ldexp(1.0, ex);
+    out[0] = cs;
+    out[1] = sn;
+    out[2] = a * back;
+    out[3] = b * back;
+    out[4] = c * back;
+    out[5] = d * back;
+    if (c == 0.0) {
+        out[6] = out[2]; out[7] = 0.0;
+        out[8] = out[5]; out[9] = 0.0;
+    } else {
+        const double beta = sqrt(fabs(b)) * sqrt(fabs(c)) * back;
+        out[6] = out[2]; out[7] = beta;
+        out[8] = out[2]; out[9] = -beta;
+    }
+}
+
+/* ======================================================================= */
+/* adjacent block swap, kernels.cpp:419-631                                 */
+
+/* complete-pivoting elimination on a d x d (d <= 4) system, kernels.cpp:419-464.
+ * m is taken by value (copied), rhs overwritten by the solution. */
+static int gecp_solve(const double* m_in, size_t d, double* rhs, double* rcond) {
+    double m[16];
+    size_t colperm[4];
+    memcpy(m, m_in, d * d * sizeof(double));
+    for (size_t i = 0; i < d; ++i) colperm[i] = i;
+    double amax = 0.0, smin = 0.0;
+    for (size_t k = 0; k < d; ++k) {
+        size_t pi = k, pj = k;
+        double pv = 0.0;
+        for (size_t i = k; i < d; ++i)
+            for (size_t j = k; j < d; ++j)
+                if (fabs(A_(m, i, j, d)) > pv) {
+                    pv = fabs(A_(m, i, j, d));
+                    pi = i;
+                    pj = j;
+                }
+        if (k == 0) amax = pv;
+        smin = pv;
+        if (pv == 0.0) {
+            *rcond = 0.0;
+            return 0;
+        }
+        if (pi != k) {
+            for (size_t j = 0; j < d; ++j) {
+                const double t = A_(m, k, j, d);
+                A_(m, k, j, d) = A_(m, pi, j, d);
+                A_(m, pi, j, d) = t;
+            }
+            const double t = rhs[k];
+            rhs[k] = rhs[pi];
+            rhs[pi] = t;
+        }
+        if (pj != k) {
+            for (size_t i = 0; i < d; ++i) {
+                const double t = A_(m, i, k, d);
+                A_(m, i, k, d) = A_(m, i, pj, d);
+                A_(m, i, pj, d) = t;
+            }
+            const size_t t = colperm[k];
+            colperm[k] = colperm[pj];
+            colperm[pj] = t;
+        }
+        for (size_t i = k + 1; i < d; ++i) {
+            const double f = A_(m, i, k, d) / A_(m, k, k, d);
+            A_(m, i, k, d) = 0.0;
+            for (size_t j = k + 1; j < d; ++j) A_(m, i, j, d) -= f * A_(m, k, j, d);
+            rhs[i] -= f * rhs[k];
+        }
+    }
+    double x[4];
+    for (size_t kk = d; kk-- > 0;) {
+        double acc = rhs[kk];
+        for (size_t j = kk + 1; j < d; ++j) acc -= A_(m, kk, j, d) * x[j];
+        x[kk] = acc / A_(m, kk, kk, d);
+    }
+    for (size_t i = 0; i < d; ++i) rhs[colperm[i]] = x[i];
+    *rcond = (amax > 0.0) ? smin / amax : 0.0;
+    return 1;
+}
+
+/* A X - X C = B, Kronecker form + one refinement, kernels.cpp:468-506.
+ * a p x p, c q x q, b p x q, x p x q, all col-major with ld = rows. */
+static int small_sylvester(size_t p, size_t q, const double* a, const double* c,
+                           const double* b, double* x, double* rcond) {
+    const size_t d = p * q;
+    double k[16], rhs[4];
+    for (size_t j = 0; j < q; ++j)
+        for (size_t i = 0; i < p; ++i) {
+            const size_t row = j * p + i;
+            for (size_t l = 0; l < q; ++l)
+                for (size_t kk = 0; kk < p; ++kk) {
+                    double val = 0.0;
+                    if (l == j) val += A_(a, i, kk, p);
+                    if (kk == i) val -= A_(c, l, j, q);
+                    A_(k, row, l * p + kk, d) = val;
+                }
+        }
+    for (size_t j = 0; j < q; ++j)
+        for (size_t i = 0; i < p; ++i) rhs[j * p + i] = A_(b, i, j, p);
+    if (!gecp_solve(k, d, rhs, rcond)) return 0;
+    for (size_t j = 0; j < q; ++j)
+        for (size_t i = 0; i < p; ++i) A_(x, i, j, p) = rhs[j * p + i];
+    double r[4], dr[4], rc2;
+    memcpy(r, b, p * q * sizeof(double));
+    teo_gemm(0, 0, p, q, p, -1.0, a, p, x, p, r, p);
+    teo_gemm(0, 0, p, q, q, 1.0, x, p, c, q, r, p);
+    for (size_t j = 0; j < q; ++j)
+        for (size_t i = 0; i < p; ++i) dr[j * p + i] = A_(r, i, j, p);
+    if (gecp_solve(k, d, dr, &rc2))
+        for (size_t j = 0; j < q; ++j)
+            for (size_t i = 0; i < p; ++i) A_(x, i, j, p) += dr[j * p + i];
+    return 1;
+}
+
+/* standardize the 2x2 block at bp of an m x m s and fold the rotation into
+ * acc, kernels.cpp:616-627 */
+static void restandardize(size_t m, double* s, size_t ar, double* acc, size_t bp) {
+    double st[10];
+    teo_standardize_2x2(A_(s, bp, bp, m), A_(s, bp, bp + 1, m), A_(s, bp + 1, bp, m),
+                        A_(s, bp + 1, bp + 1, m), st);
+    rot_rows(s, m, st[0], st[1], bp, bp + 1, bp + 2, m);
+    rot_cols(s, m, st[0], st[1], bp, bp + 1, 0, bp);
+    A_(s, bp, bp, m) = st[2];
+    A_(s, bp, bp + 1, m) = st[3];
+    A_(s, bp + 1, bp, m) = st[4];
+    A_(s, bp + 1, bp + 1, m) = st[5];
+    rot_cols(acc, ar, st[0], st[1], bp, bp + 1, 0, ar);
+}
+
+int teo_swap_adjacent_blocks(size_t m, double* s, size_t ar, double* acc, size_t pos,
+                             size_t p, size_t q) {
+    const size_t d = p + q;
+    if (p == 1 && q == 1) { /* kernels.cpp:515-527 */
+        const double t11 = A_(s, pos, pos, m), t12 = A_(s, pos, pos + 1, m);
+        const double t22 = A_(s, pos + 1, pos + 1, m);
+        double c, sn;
+        teo_make_givens(t12, t22 - t11, &c, &sn);
+        if (t12 == 0.0 && t22 - t11 == 0.0) return 0;
+        rot_rows(s, m, c, sn, pos, pos + 1, pos + 2, m);
+        rot_cols(s, m, c, sn, pos, pos + 1, 0, pos);
+        A_(s, pos, pos, m) = t22;
+        A_(s, pos + 1, pos + 1, m) = t11;
+        A_(s, pos + 1, pos, m) = 0.0;
+        rot_cols(acc, ar, c, sn, pos, pos + 1, 0, ar);
+        return 0;
+    }
+    double a[4], c[4], b[4], x[4];
+    for (size_t j = 0; j < p; ++j)
+        for (size_t i = 0; i < p; ++i) A_(a, i, j, p) = A_(s, pos + i, pos + j, m);
+    for (size_t j = 0; j < q; ++j)
+        for (size_t i = 0; i < q; ++i) A_(c, i, j, q) = A_(s, pos + p + i, pos + p + j, m);
+    for (size_t j = 0; j < q; ++j)
+        for (size_t i = 0; i < p; ++i) A_(b, i, j, p) = A_(s, pos + i, pos + p + j, m);
+    double rcond = 0.0;
+    if (!small_sylvester(p, q, a, c, b, x, &rcond)) return 1;
+    if (rcond < pow(EPS, 0.75)) return 1; /* kernels.cpp:540 */
+
+    /* Householder QR of [-X; I] (d x q), kernels.cpp:542-559 */
+    double z[16];
+    memset(z, 0, sizeof z);
+    for (size_t j = 0; j < q; ++j) {
+        for (size_t i = 0; i < p; ++i) A_(z, i, j, d) = -A_(x, i, j, p);
+        A_(z, p + j, j, d) = 1.0;
+    }
+    refl8 rf[2];
+    for (size_t j = 0; j < q; ++j) {
+        double col[4];
+        for (size_t i = j; i < d; ++i) col[i - j] = A_(z, i, j, d);
+        const double beta = make_refl(col, d - j, &rf[j]);
+        A_(z, j, j, d) = beta;
+        for (size_t i = j + 1; i < d; ++i) A_(z, i, j, d) = 0.0;
+        refl_left(z, d, &rf[j], j, j + 1, q);
+    }
+    double qd[16];
+    memset(qd, 0, sizeof qd);
+    for (size_t i = 0; i < d; ++i) A_(qd, i, i, d) = 1.0;
+    for (size_t j = q; j-- > 0;) refl_left(qd, d, &rf[j], j, 0, d);
+
+    /* wnew = qd^T W qd and the stability test, kernels.cpp:561-575 */
+    double w[16], tmp[16], wn[16];
+    for (size_t j = 0; j < d; ++j)
+        for (size_t i = 0; i < d; ++i) A_(w, i, j, d) = A_(s, pos + i, pos + j, m);
+    memset(tmp, 0, sizeof tmp);
+    memset(wn, 0, sizeof wn);
+    teo_gemm(1, 0, d, d, d, 1.0, qd, d, w, d, tmp, d);
+    teo_gemm(0, 0, d, d, d, 1.0, tmp, d, qd, d, wn, d);
+    double wnorm = 0.0, offnorm = 0.0;
+    for (size_t j = 0; j < d; ++j)
+        for (size_t i = 0; i < d; ++i) {
+            wnorm = fmax(wnorm, fabs(A_(w, i, j, d)));
+            if (i >= q && j < q && i >= j + 1) offnorm = fmax(offnorm, fabs(A_(wn, i, j, d)));
+        }
+    if (offnorm > 32.0 * EPS * fmax(wnorm, SAFMIN)) return 1;
+    for (size_t j = 0; j < q; ++j)
+        for (size_t i = q; i < d; ++i) A_(wn, i, j, d) = 0.0;
+
+    /* commit, kernels.cpp:577-613 */
+    for (size_t j = 0; j < d; ++j)
+        for (size_t i = 0; i < d; ++i) A_(s, pos + i, pos + j, m) = A_(wn, i, j, d);
+    if (pos > 0) {
+        double* top = (double*)malloc(pos * d * sizeof(double));
+        double* topn = (double*)calloc(pos * d, sizeof(double));
+        for (size_t j = 0; j < d; ++j)
+            for (size_t i = 0; i < pos; ++i) top[i + j * pos] = A_(s, i, pos + j, m);
+        teo_gemm(0, 0, pos, d, d, 1.0, top, pos, qd, d, topn, pos);
+        for (size_t j = 0; j < d; ++j)
+            for (size_t i = 0; i < pos; ++i) A_(s, i, pos + j, m) = topn[i + j * pos];
+        free(top);
+        free(topn);
+    }
+    if (pos + d < m) {
+        const size_t rw = m - pos - d;
+        double* rg = (double*)malloc(d * rw * sizeof(double));
+        double* rgn = (double*)calloc(d * rw, sizeof(double));
+        for (size_t j = 0; j < rw; ++j)
+            for (size_t i = 0; i < d; ++i) rg[i + j * d] = A_(s, pos + i, pos + d + j, m);
+        teo_gemm(1, 0, d, rw, d, 1.0, qd, d, rg, d, rgn, d);
+        for (size_t j = 0; j < rw; ++j)
+            for (size_t i = 0; i < d; ++i) A_(s, pos + i, pos + d + j, m) = rgn[i + j * d];
+        free(rg);
+        free(rgn);
+    }
+    {
+        double* av = (double*)malloc(ar * d * sizeof(double));
+        double* avn = (double*)calloc(ar * d, sizeof(double));
+        for (size_t j = 0; j < d; ++j)
+            for (size_t i = 0; i < ar; ++i) av[i + j * ar] = A_(acc, i, pos + j, ar);
+        teo_gemm(0, 0, ar, d, d, 1.0, av, ar, qd, d, avn, ar);
+        for (size_t j = 0; j < d; ++j)
+            for (size_t i = 0; i < ar; ++i) A_(acc, i, pos + j, ar) = avn[i + j * ar];
+        free(av);
+        free(avn);
+    }
+    if (q == 2) restandardize(m, s, ar, acc, pos);
+    if (p == 2) restandardize(m, s, ar, acc, pos + q);
+    return 0;
+}
+
+/* ======================================================================= */
+/* window_reorder, reorder.cpp:124-194                                      */
+
+int teo_window_reorder(size_t d, double* w, size_t nb, const uint8_t* sizes,
+                       const uint8_t* sel, double* acc, uint32_t* order, uint8_t* stuck) {
+    for (size_t j = 0; j < d; ++j)
+        for (size_t i = 0; i < d; ++i) A_(acc, i, j, d) = (i == j) ? 1.0 : 0.0;
+    { /* layout check against the exact-zero subdiagonal, :132-154 */
+        size_t row = 0;
+        for (size_t k = 0; k < nb; ++k) {
+            const size_t sz = sizes[k];
+            if (row + sz > d) return 0;
+            if (sz == 2 && A_(w, row + 1, row, d) == 0.0) return 0;
+            if (row + sz < d && A_(w, row + sz, row + sz - 1, d) != 0.0) return 0;
+            row += sz;
+        }
+        if (row != d) return 0;
+    }
+    uint32_t* arr = order; /* arrangement[slot] = original local block */
+    for (size_t i = 0; i < nb; ++i) {
+        arr[i] = (uint32_t)i;
+        stuck[i] = 0;
+    }
+    size_t dest = 0;
+    for (size_t blk = 0; blk < nb; ++blk) {
+        if (!sel[blk]) continue;
+        size_t slot = 0;
+        while (arr[slot] != blk) ++slot;
+        int st = 0;
+        while (slot > dest) {
+            const uint32_t pred = arr[slot - 1];
+            size_t row = 0;
+            for (size_t i = 0; i + 1 < slot; ++i) row += sizes[arr[i]];
+            if (teo_swap_adjacent_blocks(d, w, d, acc, row, sizes[pred], sizes[blk])) {
+                st = 1;
+                break;
+            }
+            arr[slot - 1] = (uint32_t)blk;
+            arr[slot] = pred;
+            --slot;
+        }
+        if (st) stuck[blk] = 1;
+        dest = slot + 1;
+    }
+    return 1;
+}
+
+/* ======================================================================= */
+/* reorder planner, reorder.cpp:241-324 (iterated assuming success)         */
+
+typedef struct {
+    uint8_t size, selected;
+    uint32_t orig;
+} blockst;
+
+static int plan_push(teo_plan* pl, size_t wtop, size_t wbot, size_t first, size_t count,
+                     size_t group, const blockst* bl) {
+    if (pl->n_windows == pl->cap_windows) {
+        pl->cap_windows = pl->cap_windows ? 2 * pl->cap_windows : 64;
+        pl->windows = (teo_window*)realloc(pl->windows, pl->cap_windows * sizeof(teo_window));
+        if (!pl->windows) return -1;
+    }
+    while (pl->n_entries + count > pl->cap_entries) {
+        pl->cap_entries = pl->cap_entries ? 2 * pl->cap_entries : 1024;
+        pl->sizes = (uint8_t*)realloc(pl->sizes, pl->cap_entries);
+        pl->sel = (uint8_t*)realloc(pl->sel, pl->cap_entries);
+        if (!pl->sizes || !pl->sel) return -1;
+    }
+    teo_window* w = &pl->windows[pl->n_windows++];
+    w->wtop = wtop;
+    w->wbot = wbot;
+    w->first_block = first;
+    w->count = count;
+    w->group = group;
+    w->sizes_off = pl->n_entries;
+    for (size_t i = 0; i < count; ++i) {
+        pl->sizes[pl->n_entries + i] = bl[first + i].size;
+        pl->sel[pl->n_entries + i] = bl[first + i].selected;
+    }
+    pl->n_entries += count;
+    return 0;
+}
+
+/* Plans one group's chain on state bl/starts (mutated as if every window
+ * succeeded).  target/fs/group as in reorder.cpp:243-267. */
+static int plan_chain(blockst* bl, size_t* starts, size_t nbk, size_t target, size_t fs,
+                      size_t gcount, size_t glast0, size_t ws, size_t gid, teo_plan* pl,
+                      long* first_window) {
+    size_t gfirst = fs, glast = glast0;
+    *first_window = (long)pl->n_windows;
+    blockst tmp[4096];
+    (void)nbk;
+    for (;;) {
+        if (gfirst == target) break;
+        const size_t gbot = starts[glast + 1];
+        size_t wtop = gbot > ws ? gbot - ws : 0;
+        if (wtop < starts[target]) wtop = starts[target];
+        /* snap up to a block boundary (first block starting at/after wtop) */
+        size_t bfirst = gfirst;
+        while (bfirst > target && starts[bfirst - 1] >= wtop) --bfirst;
+        wtop = starts[bfirst];
+        const size_t count = glast - bfirst + 1;
+        if (plan_push(pl, wtop, gbot, bfirst, count, gid, bl)) return -1;
+        /* pack: selected to the top in order, then the rest in order */
+        size_t k = 0;
+        for (size_t i = bfirst; i <= glast; ++i)
+            if (bl[i].selected) tmp[k++] = bl[i];
+        for (size_t i = bfirst; i <= glast; ++i)
+            if (!bl[i].selected) tmp[k++] = bl[i];
+        for (size_t i = 0; i < count; ++i) {
+            bl[bfirst + i] = tmp[i];
+            starts[bfirst + i + 1] = starts[bfirst + i] + tmp[i].size;
+        }
+        gfirst = bfirst;
+        glast = bfirst + gcount - 1;
+        if (wtop == starts[target]) break;
+    }
+    return 0;
+}
+
+int teo_plan_reorder(size_t nb, const uint8_t* sizes, const uint8_t* flags, size_t ws,
+                     teo_plan* pl) {
+    memset(pl, 0, sizeof *pl);
+    if (ws < 8) ws = 8;
+    blockst* bl = (blockst*)malloc((nb + 1) * sizeof(blockst));
+    size_t* starts = (size_t*)malloc((nb + 1) * sizeof(size_t));
+    starts[0] = 0;
+    for (size_t i = 0; i < nb; ++i) {
+        bl[i].size = sizes[i];
+        bl[i].selected = flags[i] ? 1 : 0;
+        bl[i].orig = (uint32_t)i;
+        starts[i + 1] = starts[i] + sizes[i];
+    }
+    size_t target = 0, gid = 0;
+    int rc = 0;
+    for (;;) {
+        while (target < nb && bl[target].selected) ++target;
+        size_t fs = target;
+        while (fs < nb && !bl[fs].selected) ++fs;
+        if (fs == nb) break;
+        size_t grows = bl[fs].size, gcount = 1, glast = fs;
+        for (size_t g = fs + 1; g < nb; ++g) {
+            if (!bl[g].selected) continue;
+            const size_t span = starts[g + 1] - starts[fs];
+            if (grows + bl[g].size > ws / 2 || span > ws) break;
+            grows += bl[g].size;
+            ++gcount;
+            glast = g;
+        }
+        long fw;
+        if (plan_chain(bl, starts, nb, target, fs, gcount, glast, ws, gid, pl, &fw)) {
+            rc = -1;
+            break;
+        }
+        ++gid;
+        /* after a successful chain the group's blocks lead at `target`, so
+         * the next iteration's prefix skip moves past them */
+    }
+    pl->n_groups = gid;
+    free(bl);
+    free(starts);
+    return rc;
+}
+
+void teo_plan_free(teo_plan* pl) {
+    free(pl->windows);
+    free(pl->sizes);
+    free(pl->sel);
+    memset(pl, 0, sizeof *pl);
+}
+
+double teo_plan_flops(const teo_plan* pl, size_t n, int with_q) {
+    double f = 0.0;
+    for (size_t i = 0; i < pl->n_windows; ++i) {
+        const double d = (double)(pl->windows[i].wbot - pl->windows[i].wtop);
+        const double a = (double)pl->windows[i].wtop, b = (double)pl->windows[i].wbot;
+        f += 2.0 * d * d * ((double)n - b) + 2.0 * d * d * a + (with_q ? 2.0 * d * d * (double)n : 0.0);
+    }
+    return f;
+}
+
+/* ======================================================================= */
+/* serial reorder_schur, reorder.cpp:215-404                                */
+
+/* left / right panel updates with the window accumulator, window_tasks.cpp:12-30,
+ * applied to the whole panel at once (per element identical to the per-tile
+ * tasks: the k = d accumulation runs in the same order). */
+static void update_left(size_t n, double* s, size_t lds, size_t a, size_t b, const double* acc,
+                        double* scratch) {
+    const size_t d = b - a, m = n - b;
+    if (!m) return;
+    double* g = scratch;
+    double* gn = scratch + d * m;
+    for (size_t j = 0; j < m; ++j)
+        for (size_t i = 0; i < d; ++i) g[i + j * d] = A_(s, a + i, b + j, lds);
+    memset(gn, 0, d * m * sizeof(double));
+    teo_gemm(1, 0, d, m, d, 1.0, acc, d, g, d, gn, d);
+    for (size_t j = 0; j < m; ++j)
+        for (size_t i = 0; i < d; ++i) A_(s, a + i, b + j, lds) = gn[i + j * d];
+}
+
+static void update_right(size_t rows, double* s, size_t lds, size_t a, size_t b,
+                         const double* acc, double* scratch) {
+    const size_t d = b - a;
+    if (!rows) return;
+    double* g = scratch;
+    double* gn = scratch + d * rows;
+    for (size_t j = 0; j < d; ++j)
+        for (size_t i = 0; i < rows; ++i) g[i + j * rows] = A_(s, i, a + j, lds);
+    memset(gn, 0, d * rows * sizeof(double));
+    teo_gemm(0, 0, rows, d, d, 1.0, g, rows, acc, d, gn, rows);
+    for (size_t j = 0; j < d; ++j)
+        for (size_t i = 0; i < rows; ++i) A_(s, i, a + j, lds) = gn[i + j * rows];
+}
+
+long teo_reorder_schur(size_t n, double* s, size_t lds, double* q, size_t ldq, size_t nb,
+                       const uint8_t* sizes, const uint8_t* flags, size_t ws, size_t* perm,
+                       size_t* rejected, size_t* n_rejected, size_t* plan_out, size_t plan_cap,
+                       size_t* n_plan, int* clean, long max_windows) {
+    if (ws == 0) ws = n >= 1000 ? 128 : ((n / 8 > 32 ? n / 8 : 32) + 7) / 8 * 8; /* tile */
+    if (ws < 8) ws = 8;
+    blockst* bl = (blockst*)malloc((nb + 1) * sizeof(blockst));
+    size_t* starts = (size_t*)malloc((nb + 1) * sizeof(size_t));
+    {
+        size_t row = 0;
+        for (size_t i = 0; i < nb; ++i) {
+            bl[i].size = sizes[i];
+            bl[i].selected = flags[i] ? 1 : 0;
+            bl[i].orig = (uint32_t)i;
+            row += sizes[i];
+        }
+        if (row != n) {
+            free(bl);
+            free(starts);
+            return -1;
+        }
+    }
+    *n_rejected = 0;
+    *n_plan = 0;
+    *clean = 1;
+    long executed = 0;
+    double* win = (double*)malloc(ws * ws * sizeof(double));
+    double* acc = (double*)malloc(ws * ws * sizeof(double));
+    double* scratch = (double*)malloc(2 * ws * n * sizeof(double) + 16);
+    uint32_t* order = (uint32_t*)malloc(ws * sizeof(uint32_t));
+    uint8_t* stuck = (uint8_t*)malloc(ws);
+    blockst* slice = (blockst*)malloc(ws * sizeof(blockst));
+    size_t target = 0;
+    teo_plan pl;
+    memset(&pl, 0, sizeof pl);
+    for (;;) {
+        if (max_windows > 0 && executed >= max_windows) break;
+        while (target < nb && bl[target].selected) ++target;
+        size_t fs = target;
+        while (fs < nb && !bl[fs].selected) ++fs;
+        if (fs == nb) break;
+        starts[0] = 0;
+        for (size_t i = 0; i < nb; ++i) starts[i + 1] = starts[i] + bl[i].size;
+        size_t grows = bl[fs].size, gcount = 1, glast = fs;
+        for (size_t g = fs + 1; g < nb; ++g) {
+            if (!bl[g].selected) continue;
+            const size_t span = starts[g + 1] - starts[fs];
+            if (grows + bl[g].size > ws / 2 || span > ws) break;
+            grows += bl[g].size;
+            ++gcount;
+            glast = g;
+        }
+        /* plan the chain on a simulated copy (reorder.cpp:277-324) */
+        blockst* sim = (blockst*)malloc((nb + 1) * sizeof(blockst));
+        size_t* sst = (size_t*)malloc((nb + 1) * sizeof(size_t));
+        memcpy(sim, bl, nb * sizeof(blockst));
+        memcpy(sst, starts, (nb + 1) * sizeof(size_t));
+        pl.n_windows = 0;
+        pl.n_entries = 0;
+        long fw;
+        plan_chain(sim, sst, nb, target, fs, gcount, glast, ws, 0, &pl, &fw);
+        free(sim);
+        free(sst);
+        if (pl.n_windows == 0) continue;
+        /* execute every planned window of the chain, in order (the task
+         * graph's serial semantics, runtime.hpp:79-82) */
+        typedef struct {
+            int executed;
+            uint32_t order[256];
+            uint8_t stuck[256];
+        } outcome;
+        outcome* oc = (outcome*)malloc(pl.n_windows * sizeof(outcome));
+        for (size_t wi = 0; wi < pl.n_windows; ++wi) {
+            const teo_window* w = &pl.windows[wi];
+            const size_t a = w->wtop, b = w->wbot, d = b - a;
+            for (size_t j = 0; j < d; ++j)
+                for (size_t i = 0; i < d; ++i) win[i + j * d] = A_(s, a + i, a + j, lds);
+            oc[wi].executed = teo_window_reorder(d, win, w->count, pl.sizes + w->sizes_off,
+                                                 pl.sel + w->sizes_off, acc, oc[wi].order,
+                                                 oc[wi].stuck);
+            if (oc[wi].executed)
+                for (size_t j = 0; j < d; ++j)
+                    for (size_t i = 0; i < d; ++i) A_(s, a + i, a + j, lds) = win[i + j * d];
+            update_left(n, s, lds, a, b, acc, scratch);
+            update_right(a, s, lds, a, b, acc, scratch);
+            if (q) update_right(n, q, ldq, a, b, acc, scratch);
+            ++executed;
+        }
+        /* fold outcomes, reorder.cpp:366-397 */
+        for (size_t wi = 0; wi < pl.n_windows; ++wi) {
+            const teo_window* w = &pl.windows[wi];
+            if (*n_plan < plan_cap) {
+                plan_out[3 * *n_plan] = w->wtop;
+                plan_out[3 * *n_plan + 1] = w->wbot - w->wtop;
+                plan_out[3 * *n_plan + 2] = w->count;
+            }
+            ++*n_plan;
+            if (!oc[wi].executed) break;
+            memcpy(slice, bl + w->first_block, w->count * sizeof(blockst));
+            for (size_t i = 0; i < w->count; ++i) bl[w->first_block + i] = slice[oc[wi].order[i]];
+            int any = 0;
+            for (size_t i = 0; i < w->count; ++i)
+                if (oc[wi].stuck[i]) {
+                    any = 1;
+                    rejected[(*n_rejected)++] = slice[i].orig;
+                    *clean = 0;
+                    for (size_t k = 0; k < nb; ++k)
+                        if (bl[k].orig == slice[i].orig) bl[k].selected = 0;
+                }
+            if (any) break;
+        }
+        free(oc);
+    }
+    for (size_t i = 0; i < nb; ++i) perm[bl[i].orig] = i;
+    teo_plan_free(&pl);
+    free(bl);
+    free(starts);
+    free(win);
+    free(acc);
+    free(scratch);
+    free(order);
+    free(stuck);
+    free(slice);
+    return executed;
+}
+
+/* ======================================================================= */
+/* verification, verify.cpp:17-130                                         */
+
+static double frob(size_t n, const double* a) { return nrm2(n * n, a); }
+
+double teo_similarity_residual(size_t n, const double* a, size_t lda, const double* q,
+                               size_t ldq, const double* s, size_t lds) {
+    /* ||A - Q S Q^T||_F / ||A||_F  (verify.cpp:39-57) */
+    double* qs = (double*)calloc(n * n, sizeof(double));
+    double* r = (double*)malloc(n * n * sizeof(double));
+    double* ad = (double*)malloc(n * n * sizeof(double));
+    for (size_t j = 0; j < n; ++j)
+        for (size_t i = 0; i < n; ++i) ad[i + j * n] = r[i + j * n] = A_(a, i, j, lda);
+    for (size_t k = 0; k < n; ++k)
+        for (size_t j = 0; j < n; ++j) {
+            const double skj = A_(s, k, j, lds);
+            if (skj == 0.0) continue;
+            for (size_t i = 0; i < n; ++i) qs[i + j * n] += A_(q, i, k, ldq) * skj;
+        }
+    for (size_t k = 0; k < n; ++k)
+        for (size_t j = 0; j < n; ++j) {
+            const double qjk = A_(q, j, k, ldq);
+            if (qjk == 0.0) continue;
+            for (size_t i = 0; i < n; ++i) r[i + j * n] -= qs[i + k * n] * qjk;
+        }
+    const double na = frob(n, ad);
+    const double res = frob(n, r) / (na > 0.0 ? na : 1.0);
+    free(qs);
+    free(r);
+    free(ad);
+    return res;
+}
+
+double teo_orthogonality_defect(size_t n, const double* q, size_t ldq) {
+    /* ||Q^T Q - I||_F  (verify.cpp:59-69) */
+    double* g = (double*)calloc(n * n, sizeof(double));
+    for (size_t j = 0; j < n; ++j)
+        for (size_t i = 0; i <= j; ++i) {
+            double acc = 0.0;
+            for (size_t k = 0; k < n; ++k) acc += A_(q, k, i, ldq) * A_(q, k, j, ldq);
+            g[i + j * n] = g[j + i * n] = acc;
+        }
+    for (size_t i = 0; i < n; ++i) g[i + i * n] -= 1.0;
+    const double r = frob(n, g);
+    free(g);
+    return r;
+}
+
+int teo_is_standardized(size_t n, const double* s, size_t ld) {
+    /* verify.cpp:78-102 */
+    for (size_t j = 0; j < n; ++j)
+        for (size_t i = j + 2; i < n; ++i)
+            if (A_(s, i, j, ld) != 0.0) return 0;
+    for (size_t i = 0; i < n;) {
+        if (i + 1 < n && A_(s, i + 1, i, ld) != 0.0) {
+            if (A_(s, i, i, ld) != A_(s, i + 1, i + 1, ld)) return 0;
+            if (!(A_(s, i, i + 1, ld) * A_(s, i + 1, i, ld) < 0.0)) return 0;
+            if (i + 2 < n && A_(s, i + 2, i + 1, ld) != 0.0) return 0;
+            i += 2;
+        } else {
+            i += 1;
+        }
+    }
+    return 1;
+}
+
+void teo_read_eigenvalues(size_t n, const double* s, size_t ld, double* re, double* im) {
+    for (size_t i = 0; i < n;) {
+        if (i + 1 < n && A_(s, i + 1, i, ld) != 0.0) {
+            const double a = A_(s, i, i, ld), b = A_(s, i, i + 1, ld);
+            const double c = A_(s, i + 1, i, ld), d = A_(s, i + 1, i + 1, ld);
+            const double m = 0.5 * (a + d), p = 0.5 * (a - d);
+            const double disc = p * p + b * c;
+            if (disc < 0.0) {
+                re[i] = m; im[i] = sqrt(-disc);
+                re[i + 1] = m; im[i + 1] = -sqrt(-disc);
+            } else {
+                const double r = sqrt(disc);
+                re[i] = m + r; im[i] = 0.0;
+                re[i + 1] = m - r; im[i + 1] = 0.0;
+            }
+            i += 2;
+        } else {
+            re[i] = A_(s, i, i, ld);
+            im[i] = 0.0;
+            i += 1;
+        }
+    }
+}
