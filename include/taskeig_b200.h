@@ -1,0 +1,133 @@
+/*
+ * taskeig_b200.h -- C ABI of the B200-native (sm_100a) window-based
+ * off-diagonal update path of StarNEig / taskeig.
+ *
+ * This is the thin, stream-ordered CUDA layer underneath the C++ drop-in
+ * (include/taskeig/ headers, namespace taskeig).  It takes plain pointers and
+ * sizes -- no C++ or torch types -- so any FFI (ctypes, cgo, JNI) can bind it.
+ *
+ * Conventions:
+ *   * matrices are COLUMN-MAJOR fp64 with an explicit leading dimension
+ *     (element (i,j) at p[i + j*ld]), the orientation of the reference's tiles
+ *     and DenseMatrix (tiled_matrix.hpp:27-35, dense.hpp:33-36), so a
+ *     TiledMatrix <-> device conversion is a tile-wise copy, no transpose;
+ *   * `*_device` entry points take DEVICE pointers and a cudaStream_t (passed
+ *     as void*, NULL = legacy default stream) and are ordered on that stream;
+ *     they return after their host-side bookkeeping completed (the reorder
+ *     driver synchronizes once per planning pass to fold window outcomes);
+ *   * `*_host` entry points take HOST pointers and include the host<->device
+ *     copies;
+ *   * return value: 0 ok; < 0 invalid argument -i (LAPACK `info` style) or an
+ *     internal error (TEIG_ERR_*); > 0 a count of rejected swaps /
+ *     non-converged windows where documented.  teig_last_error() describes
+ *     the last failure of the calling thread.
+ *
+ * Every entry point cites the reference interface it replaces.
+ */
+#ifndef TASKEIG_B200_H
+#define TASKEIG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TEIG_OK 0
+#define TEIG_ERR_CUDA (-1000)
+#define TEIG_ERR_UNSUPPORTED (-1001)
+#define TEIG_ERR_STRICT (-1002)    /* rejected swap in strict mode (reorder.cpp:383-385) */
+#define TEIG_ERR_INTERNAL (-1003)
+
+const char* teig_last_error(void);
+int teig_version(void);
+
+/* ------------------------------------------------------------------------ */
+/* Reordering (replaces taskeig::reorder_schur, reorder.hpp:88-89 /           */
+/* reorder.cpp:215-404).                                                     */
+
+typedef struct teig_reorder_opts {
+    int64_t window_size; /* 0: default_tile_size(n) (reorder.cpp:221-222); <= 128 */
+    int32_t strict;      /* !=0: fail with TEIG_ERR_STRICT on a rejected swap */
+    int32_t overlap_factor; /* !=0 (default 1 via teig_reorder_opts_default): run the
+                               Q-factor updates on a second stream, overlapped */
+} teig_reorder_opts;
+
+typedef struct teig_reorder_info {
+    int64_t n_windows;     /* executed windows (all passes) */
+    int64_t n_levels;      /* wavefronts (all passes) */
+    int64_t n_passes;      /* planning passes (1 for a clean run) */
+    int64_t n_groups;      /* chains planned in the first pass */
+    int64_t n_rejected;    /* blocks whose swap was rejected */
+    int32_t clean;         /* no rejection, selection fully leading (reorder.hpp:80) */
+    int32_t pad;
+    double update_flops;   /* sum over executed windows of 2d^2(n-b) + 2d^2 a (+ 2d^2 n) */
+    double update_bytes;   /* algorithmic panel bytes: 16 d ((n-b) + a (+ n)) per window */
+    double plan_ms;        /* host planning + scheduling time */
+} teig_reorder_info;
+
+void teig_reorder_opts_default(teig_reorder_opts* o);
+
+/* dS: n x n standardized quasi-triangular Schur form (device, ld lds), updated
+ * in place to the reordered form.  dQ: n x n (device, ld ldq) or NULL; updated
+ * to Q * Q3.  sizes/flags: host arrays of nb diagonal-block sizes (1/2) and
+ * selection flags (a Selection: reorder.hpp:22-32).  perm (host, nb): original
+ * block -> final slot; rejected (host, nb): original indices of rejected
+ * blocks, count in info->n_rejected.  plan (host, 3*plan_cap or NULL):
+ * (position, extent, moved_blocks) per executed window, like
+ * ReorderResult::plan.  Returns 0, or < 0 on error. */
+int teig_reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq,
+                              int64_t nb, const uint8_t* sizes, const uint8_t* flags,
+                              const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
+                              int64_t* plan, int64_t plan_cap, teig_reorder_info* info,
+                              void* stream);
+
+/* Same on HOST buffers (column-major, ld); includes H2D/D2H. */
+int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_t ldq, int64_t nb,
+                            const uint8_t* sizes, const uint8_t* flags,
+                            const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
+                            int64_t* plan, int64_t plan_cap, teig_reorder_info* info,
+                            void* stream);
+
+/* Diagonal-block scan by exact-zero subdiagonal (reorder.cpp:21-43) on a
+ * device matrix.  sizes: host array of capacity n.  Returns nb (>= 0). */
+int64_t teig_scan_blocks_device(int64_t n, const double* dS, int64_t lds, uint8_t* sizes,
+                                void* stream);
+
+/* select_fraction (reorder.cpp:80-97): exactly floor(fraction*nb) blocks by a
+ * Philox(seed ^ 0x5e1ec7) Fisher-Yates shuffle.  flags: host, nb. */
+int teig_select_fraction(int64_t nb, double fraction, uint64_t seed, uint8_t* flags);
+
+/* ------------------------------------------------------------------------ */
+/* Window-level kernels (device buffers; synchronous on `stream`).           */
+
+/* window_reorder (reorder.hpp:62-65 / reorder.cpp:124-194) on a d x d window
+ * (d <= 128) at dW (ld ldw, updated in place); dAcc (d x d, ld d) receives the
+ * accumulated orthogonal factor (identity on a layout mismatch).  order /
+ * stuck: host, nb.  *executed = 0 on a layout mismatch. */
+int teig_window_reorder_device(int64_t d, double* dW, int64_t ldw, int64_t nb,
+                               const uint8_t* sizes, const uint8_t* sel, double* dAcc,
+                               uint32_t* order, uint8_t* stuck, int32_t* executed, void* stream);
+
+/* apply_window_updates (window_tasks.hpp:36-38 / window_tasks.cpp:89-102):
+ * S[a:b, b:n] <- Qw^T S[a:b, b:n];  S[0:a, a:b] <- S[0:a, a:b] Qw;
+ * Q[0:n, a:b] <- Q[0:n, a:b] Qw (dQ may be NULL).  dQw: d x d, ld d. */
+int teig_apply_window_updates_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq,
+                                     int64_t a, int64_t d, const double* dQw, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Synthetic inputs directly in HBM (bit-identical to the      */
+/* reference generators).                                                    */
+
+/* default_spectrum + build_quasi_triangular (generate.cpp:68-91, 115-150)
+ * with the strictly-upper fill drawn from Philox(fill_seed). */
+int teig_gen_schur_input_device(int64_t n, double* dS, int64_t lds, uint64_t fill_seed, void* stream);
+/* generate(hessenberg_random, n, seed) (generate.cpp:192-198) */
+int teig_gen_hessenberg_device(int64_t n, double* dH, int64_t ldh, uint64_t seed, void* stream);
+int teig_set_identity_device(int64_t n, double* dQ, int64_t ldq, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,16 @@
+"""B200-native (sm_100a) window-based off-diagonal update path of StarNEig
+(arXiv 2002.05024): Schur-form eigenvalue reordering (and, next, multishift
+QR with AED) behind the reference's ``taskeig`` API.
+
+The compute path is the in-tree CUDA library ``_lib/libtaskeig_b200.so``
+(C ABI: ``include/taskeig_b200.h``); this package is the host-side mirror of
+the reference interface.  There is no CPU fallback.
+"""
+from ._native import TaskeigError, build, lib  # noqa: F401
+from .reorder import (  # noqa: F401
+    Block, PlanWindow, ReorderOptions, ReorderResult, Selection, WindowReorderOutcome,
+    apply_window_updates, colmajor_empty, gen_hessenberg, gen_schur_input, identity,
+    known_spectrum_seed, reorder_schur, scan_blocks, scan_blocks_device, select_by_name,
+    select_eigenvalues, select_fraction, window_reorder)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

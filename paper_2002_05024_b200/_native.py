@@ -1,0 +1,90 @@
+"""ctypes binding of the in-tree C ABI (include/taskeig_b200.h).
+
+The product path is the CUDA library ``_lib/libtaskeig_b200.so``; there is
+no CPU fallback.  Importing this module on a machine without the built
+library raises immediately, and every call that fails on the device raises
+``TaskeigError`` carrying the library's message.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libtaskeig_b200.so")
+CSRC = os.path.join(HERE, "csrc")
+
+
+class TaskeigError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"taskeig_b200 error {code}: {msg}")
+        self.code = code
+
+
+def build(verbose: bool = False) -> str:
+    """Compile the sm_100a library in-tree (nvcc cross-compiles without a GPU)."""
+    cmd = ["make", "-C", CSRC, "-j8"]
+    if not verbose:
+        cmd.insert(1, "-s")
+    subprocess.run(cmd, check=True)
+    return LIB_PATH
+
+
+class ReorderOpts(C.Structure):
+    _fields_ = [("window_size", C.c_int64), ("strict", C.c_int32), ("overlap_factor", C.c_int32)]
+
+
+class ReorderInfo(C.Structure):
+    _fields_ = [("n_windows", C.c_int64), ("n_levels", C.c_int64), ("n_passes", C.c_int64),
+                ("n_groups", C.c_int64), ("n_rejected", C.c_int64), ("clean", C.c_int32),
+                ("pad", C.c_int32), ("update_flops", C.c_double), ("update_bytes", C.c_double),
+                ("plan_ms", C.c_double)]
+
+
+_P = C.c_void_p
+_I64 = C.c_int64
+
+# symbol -> (restype, argtypes); the test suite checks that every symbol
+# declared in include/taskeig_b200.h is exported.
+SIGNATURES = {
+    "teig_last_error": (C.c_char_p, []),
+    "teig_version": (C.c_int, []),
+    "teig_reorder_opts_default": (None, [_P]),
+    "teig_reorder_schur_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P,
+                                            _I64, _P, _P]),
+    "teig_reorder_schur_host": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P,
+                                          _I64, _P, _P]),
+    "teig_scan_blocks_device": (C.c_int64, [_I64, _P, _I64, _P, _P]),
+    "teig_select_fraction": (C.c_int, [_I64, C.c_double, C.c_uint64, _P]),
+    "teig_window_reorder_device": (C.c_int, [_I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P]),
+    "teig_apply_window_updates_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _I64, _P, _P]),
+    "teig_gen_schur_input_device": (C.c_int, [_I64, _P, _I64, C.c_uint64, _P]),
+    "teig_gen_hessenberg_device": (C.c_int, [_I64, _P, _I64, C.c_uint64, _P]),
+    "teig_set_identity_device": (C.c_int, [_I64, _P, _I64, _P]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load the native library (built in-tree).  Raises if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with "
+                "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> int:
+    if rc < 0:
+        raise TaskeigError(rc, lib().teig_last_error().decode(errors="replace"))
+    return rc

@@ -1,0 +1,126 @@
+// generate.cu -- on-device synthetic inputs (product side, used by bench.py
+// and the tests to build the SURVEY.md 8d workloads directly in HBM).
+//
+// Counter-based Philox4x32-10 (the reference's generator, philox.hpp:18-84)
+// lets every element compute its own draw index, so the fill is bit-identical
+// to the reference's sequential row-major stream:
+//   * schur input: `default_spectrum` + `build_quasi_triangular`
+//     (generate.cpp:68-91, 115-150) -- reals on [-10,10] first, then 2x2
+//     blocks [[re, im], [-im, re]], strictly-upper fill uniform [-1, 1];
+//   * random upper Hessenberg (generate.cpp:192-198).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "launch.h"
+
+namespace teig {
+
+namespace {
+
+__device__ __forceinline__ void philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+        const uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0;
+        const uint32_t n1 = (uint32_t)p1;
+        const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+        const uint32_t n3 = (uint32_t)p0;
+        c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+}
+
+// k-th uniform_sym draw of Philox(seed)
+__device__ __forceinline__ double draw_uniform_sym(uint64_t seed, uint64_t k) {
+    const uint64_t blk = k >> 1;
+    uint32_t c[4] = {(uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u};
+    philox10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const int i = (int)(k & 1);
+    const uint64_t u = (((uint64_t)c[2 * i + 1] << 32) | c[2 * i]) >> 11;
+    return __dsub_rn(__dmul_rn((double)u, 2.0 / 9007199254740992.0), 1.0);
+}
+
+__global__ void gen_schur_kernel(double* S, long long lds, long long n, uint64_t seed) {
+    const long long j = blockIdx.y;
+    const long long npairs = n / 4, nreal = n - 2 * npairs;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        auto first_of_pair = [&](long long r) { return r >= nreal && ((r - nreal) & 1) == 0; };
+        if (i == j) {
+            if (i < nreal) {
+                v = (nreal == 1) ? 1.0 : __dadd_rn(-10.0, __ddiv_rn(__dmul_rn(20.0, (double)i), (double)(nreal - 1)));
+            } else {
+                const long long k = (i - nreal) >> 1;
+                v = (npairs == 1) ? 0.5 : __dadd_rn(-9.7, __ddiv_rn(__dmul_rn(19.4, (double)k), (double)(npairs - 1)));
+            }
+        } else if (i == j + 1) {
+            if (first_of_pair(j)) {
+                const long long k = (j - nreal) >> 1;
+                v = -(1.0 + 2.0 * (double)(k % 3));
+            }
+        } else if (j > i) {
+            if (j == i + 1 && first_of_pair(i)) {
+                const long long k = (i - nreal) >> 1;
+                v = 1.0 + 2.0 * (double)(k % 3);
+            } else {
+                // draws consumed by rows < i, then the position inside row i
+                const long long before = i * (n - 1) - i * (i - 1) / 2 - (i > nreal ? (i - nreal + 1) / 2 : 0);
+                long long inrow = j - i - 1;
+                if (first_of_pair(i)) inrow -= 1;  // the in-block entry is not drawn
+                v = draw_uniform_sym(seed, (uint64_t)(before + inrow));
+            }
+        }
+        S[i + j * lds] = v;
+    }
+}
+
+__global__ void identity_kernel(double* Q, long long ldq, long long n) {
+    const long long j = blockIdx.y;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        Q[i + j * ldq] = (i == j) ? 1.0 : 0.0;
+}
+
+__global__ void gen_hess_kernel(double* H, long long ldh, long long n, uint64_t seed) {
+    const long long j = blockIdx.y;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        if (i <= j + 1) {
+            long long before;
+            if (i == 0) before = 0;
+            else before = n + (i - 1) * (n + 1) - (i - 1) * i / 2;
+            const long long inrow = j - (i == 0 ? 0 : i - 1);
+            v = draw_uniform_sym(seed, (uint64_t)(before + inrow));
+        }
+        H[i + j * ldh] = v;
+    }
+}
+
+dim3 grid_for(long long n) {
+    const long long bx = (n + 255) / 256;
+    return dim3((unsigned)(bx < 64 ? bx : 64), (unsigned)n);
+}
+
+}  // namespace
+
+cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64_t fill_seed, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    gen_schur_kernel<<<grid_for(n), 256, 0, stream>>>(S, lds, n, fill_seed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_identity(double* Q, long long ldq, long long n, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    identity_kernel<<<grid_for(n), 256, 0, stream>>>(Q, ldq, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_hessenberg(double* H, long long ldh, long long n, uint64_t seed, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    gen_hess_kernel<<<grid_for(n), 256, 0, stream>>>(H, ldh, n, seed * 0x9E3779B97F4A7C15ull + 4ull);
+    return cudaGetLastError();
+}
+
+}  // namespace teig

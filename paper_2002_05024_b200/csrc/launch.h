@@ -1,0 +1,33 @@
+// launch.h -- host-side launchers of the sm_100a kernels (internal).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_types.h"
+
+namespace teig {
+
+size_t window_reorder_smem_bytes(int dmax);
+
+cudaError_t launch_window_reorder(const WinDesc* wins, int nwin, int dmax, double* S, long long lds,
+                                  double* qw_pool, const uint8_t* sizes_pool, const uint8_t* sel_pool,
+                                  uint8_t* order_pool, uint8_t* stuck_pool, int32_t* status,
+                                  cudaStream_t stream);
+
+cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
+                               double* S, long long lds, int n, cudaStream_t stream);
+
+cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
+                                double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream);
+
+// synthetic inputs (generate.cu)
+cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64_t fill_seed,
+                                   cudaStream_t stream);
+cudaError_t launch_set_identity(double* Q, long long ldq, long long n, cudaStream_t stream);
+cudaError_t launch_gen_hessenberg(double* H, long long ldh, long long n, uint64_t seed, cudaStream_t stream);
+
+constexpr int kLeftBN = 64;   // columns per left-update tile
+constexpr int kRightBM = 64;  // rows per right/factor-update tile
+
+}  // namespace teig

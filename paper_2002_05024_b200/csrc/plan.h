@@ -1,0 +1,51 @@
+// plan.h -- host-side window planner and wavefront scheduler for the
+// GPU reordering pass.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+namespace teig {
+
+// Bookkeeping of one diagonal block (reference reorder.cpp:200-204).
+struct BlockState {
+    uint8_t size;      // 1 or 2
+    uint8_t selected;  // still to be moved to the leading part
+    uint32_t orig;     // index in the caller's Selection
+};
+
+// One planned window (reference reorder.cpp:271-276).
+struct PlannedWindow {
+    int64_t wtop, wbot;          // rows [wtop, wbot)
+    int64_t first_block, count;  // block slots [first_block, first_block + count)
+    int64_t group;               // chain (group) index within the plan
+    int64_t blk_off;             // offset into ReorderPlan::sizes / sel
+    int32_t level;               // wavefront assigned by schedule_levels()
+};
+
+struct ReorderPlan {
+    std::vector<PlannedWindow> windows;  // in reference (plan) order
+    std::vector<uint8_t> sizes, sel;     // per window: `count` entries
+    int64_t n_groups = 0;
+    int32_t n_levels = 0;
+};
+
+// Plans every group's window chain assuming all swaps succeed -- the
+// reference's per-group chain simulation (reorder.cpp:241-324) iterated over
+// all groups.  `blocks` is not modified.  O(sum of window sizes).
+ReorderPlan plan_reorder(const std::vector<BlockState>& blocks, int64_t ws);
+
+// Greedy wavefront levels: a window's level is one more than the deepest
+// earlier window whose diagonal range intersects it.  Windows of one level
+// are pairwise disjoint; disjoint windows commute exactly (their similarity
+// transformations act on disjoint index sets), so level order preserves the
+// reference's per-element update order for every overlapping pair.
+void schedule_levels(ReorderPlan& plan, int64_t n);
+
+// Update flops of a plan: sum 2d^2 (n-b) + 2d^2 a (+ 2d^2 n with Q)
+// (SURVEY.md 8d).
+double plan_update_flops(const ReorderPlan& plan, int64_t n, bool with_q);
+// Algorithmic HBM bytes of the updates: each panel read and written once.
+double plan_update_bytes(const ReorderPlan& plan, int64_t n, bool with_q);
+
+}  // namespace teig

@@ -1,0 +1,501 @@
+// reorder_driver.cpp -- the GPU window scheduler for Schur-form reordering
+// (host C++ over the sm_100a kernels), exported through the C ABI in
+// include/taskeig_b200.h.
+//
+// Replaces the reference's per-group TaskGraph execution
+// (reorder.cpp:241-398, runtime.cpp:47-249):
+//   1. plan every group's window chain up front (plan.cpp), exactly the
+//      windows the reference would run when every swap succeeds;
+//   2. assign wavefront levels -- chains pipeline behind each other instead of
+//      running one group at a time;
+//   3. per level, three stream-ordered launches: the batched window kernel
+//      (one CTA per window), the batched left (row-panel) update, the batched
+//      right (column-panel) update; the Q-factor updates of the level run on a
+//      second stream, overlapped with the next levels' window work;
+//   4. one D2H readback of the window outcomes per pass; fold them in plan
+//      order (reorder.cpp:366-397); replan if anything deviated.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/taskeig_b200.h"
+#include "device_types.h"
+#include "launch.h"
+#include "plan.h"
+
+namespace teig {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define TEIG_CUDA(expr)                                                                          \
+    do {                                                                                         \
+        cudaError_t _e = (expr);                                                                 \
+        if (_e != cudaSuccess)                                                                   \
+            throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(_e) + " at " + \
+                                     __FILE__ + ":" + std::to_string(__LINE__));                 \
+    } while (0)
+
+int64_t default_tile_size(int64_t n) {
+    // reference tiled_matrix.cpp:168-172
+    if (n >= 1000) return 128;
+    const int64_t base = std::max<int64_t>(32, n / 8);
+    return ((base + 7) / 8) * 8;
+}
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t bytes, cudaStream_t st) : s(st) {
+        if (bytes) TEIG_CUDA(cudaMallocAsync(&p, bytes, st));
+    }
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, s);
+    }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct PassResult {
+    int64_t windows = 0, levels = 0;
+    bool deviated = false;
+};
+
+// Executes one planned pass on the device and folds the outcomes into `blocks`.
+PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq,
+                    std::vector<BlockState>& blocks, std::vector<int64_t>& rejected,
+                    std::vector<int64_t>& plan_log, bool strict, bool overlap,
+                    cudaStream_t stream, cudaStream_t stream2, cudaEvent_t ev) {
+    PassResult pr;
+    const int64_t nw = (int64_t)plan.windows.size();
+    schedule_levels(plan, n);
+    const int32_t nl = plan.n_levels;
+    // order windows by level (stable: plan order inside a level)
+    std::vector<int64_t> idx(nw);
+    for (int64_t i = 0; i < nw; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](int64_t x, int64_t y) { return plan.windows[x].level < plan.windows[y].level; });
+    std::vector<WinDesc> descs(nw);
+    std::vector<int64_t> lvl_off(nl + 1, 0), tl(nl, 0), tr(nl, 0), tq(nl, 0);
+    int dmax = 0;
+    int64_t qw_total = 0;
+    for (int64_t k = 0; k < nw; ++k) {
+        const PlannedWindow& w = plan.windows[idx[k]];
+        WinDesc& dsc = descs[k];
+        const int L = w.level;
+        dsc.a = (int32_t)w.wtop;
+        dsc.d = (int32_t)(w.wbot - w.wtop);
+        dsc.nb = (int32_t)w.count;
+        dsc.flags = 0;
+        dsc.qw_off = qw_total;
+        qw_total += (int64_t)dsc.d * dsc.d;
+        dsc.blk_off = w.blk_off;
+        dsc.tl_pref = (int32_t)tl[L];
+        dsc.tr_pref = (int32_t)tr[L];
+        dsc.tq_pref = (int32_t)tq[L];
+        dsc.pad = 0;
+        tl[L] += (n - w.wbot + kLeftBN - 1) / kLeftBN;
+        tr[L] += (w.wtop + kRightBM - 1) / kRightBM;
+        if (dQ) tq[L] += (n + kRightBM - 1) / kRightBM;
+        lvl_off[L + 1]++;
+        dmax = std::max(dmax, dsc.d);
+    }
+    for (int L = 0; L < nl; ++L) lvl_off[L + 1] += lvl_off[L];
+    const int dmax_k = dmax <= 64 ? 64 : 128;
+
+    const size_t ne = plan.sizes.size();
+    DevBuf d_desc(sizeof(WinDesc) * nw, stream), d_qw(sizeof(double) * std::max<int64_t>(qw_total, 1), stream),
+        d_sizes(ne + 1, stream), d_sel(ne + 1, stream), d_order(ne + 1, stream), d_stuck(ne + 1, stream),
+        d_status(sizeof(int32_t) * nw, stream);
+    TEIG_CUDA(cudaMemcpyAsync(d_desc.p, descs.data(), sizeof(WinDesc) * nw, cudaMemcpyHostToDevice, stream));
+    TEIG_CUDA(cudaMemcpyAsync(d_sizes.p, plan.sizes.data(), ne, cudaMemcpyHostToDevice, stream));
+    TEIG_CUDA(cudaMemcpyAsync(d_sel.p, plan.sel.data(), ne, cudaMemcpyHostToDevice, stream));
+
+    const WinDesc* dd = d_desc.as<WinDesc>();
+    for (int L = 0; L < nl; ++L) {
+        const int64_t o = lvl_off[L], cnt = lvl_off[L + 1] - lvl_off[L];
+        TEIG_CUDA(launch_window_reorder(dd + o, (int)cnt, dmax_k, dS, lds, d_qw.as<double>(), d_sizes.as<uint8_t>(),
+                                        d_sel.as<uint8_t>(), d_order.as<uint8_t>(), d_stuck.as<uint8_t>(),
+                                        d_status.as<int32_t>() + o, stream));
+        if (dQ && overlap) {
+            TEIG_CUDA(cudaEventRecord(ev, stream));
+            TEIG_CUDA(cudaStreamWaitEvent(stream2, ev, 0));
+            TEIG_CUDA(launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
+                                          true, stream2));
+        }
+        TEIG_CUDA(launch_update_left(dd + o, (int)cnt, (int)tl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n, stream));
+        TEIG_CUDA(launch_update_right(dd + o, (int)cnt, (int)tr[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
+                                      false, stream));
+        if (dQ && !overlap)
+            TEIG_CUDA(launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
+                                          true, stream));
+    }
+    if (dQ && overlap) {
+        TEIG_CUDA(cudaEventRecord(ev, stream2));
+        TEIG_CUDA(cudaStreamWaitEvent(stream, ev, 0));
+    }
+    // one readback of all window outcomes
+    std::vector<int32_t> status(nw);
+    std::vector<uint8_t> order(ne + 1), stuck(ne + 1);
+    TEIG_CUDA(cudaMemcpyAsync(status.data(), d_status.p, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost, stream));
+    TEIG_CUDA(cudaMemcpyAsync(order.data(), d_order.p, ne, cudaMemcpyDeviceToHost, stream));
+    TEIG_CUDA(cudaMemcpyAsync(stuck.data(), d_stuck.p, ne, cudaMemcpyDeviceToHost, stream));
+    TEIG_CUDA(cudaStreamSynchronize(stream));
+    std::vector<int32_t> st_by_plan(nw);
+    for (int64_t k = 0; k < nw; ++k) st_by_plan[idx[k]] = status[k];
+
+    // fold in plan order (reorder.cpp:366-397), validating the bookkeeping
+    std::vector<int64_t> start(blocks.size() + 1, 0);
+    for (size_t i = 0; i < blocks.size(); ++i) start[i + 1] = start[i] + blocks[i].size;
+    std::vector<BlockState> slice;
+    for (int64_t wi = 0; wi < nw; ++wi) {
+        const PlannedWindow& w = plan.windows[wi];
+        plan_log.push_back(w.wtop);
+        plan_log.push_back(w.wbot - w.wtop);
+        plan_log.push_back(w.count);
+        const int32_t st = st_by_plan[wi];
+        if (!(st & kWinExecuted)) {
+            pr.deviated = true;
+            continue;
+        }
+        bool consistent = start[w.first_block] == w.wtop &&
+                          w.first_block + w.count <= (int64_t)blocks.size();
+        for (int64_t i = 0; consistent && i < w.count; ++i)
+            consistent = blocks[w.first_block + i].size == plan.sizes[w.blk_off + i];
+        if (!consistent)
+            throw std::runtime_error("reorder: block bookkeeping diverged from the device layout");
+        slice.assign(blocks.begin() + w.first_block, blocks.begin() + w.first_block + w.count);
+        for (int64_t i = 0; i < w.count; ++i) blocks[w.first_block + i] = slice[order[w.blk_off + i]];
+        for (int64_t i = 0; i < w.count; ++i) start[w.first_block + i + 1] = start[w.first_block + i] + blocks[w.first_block + i].size;
+        if (st & kWinStuck) {
+            pr.deviated = true;
+            for (int64_t i = 0; i < w.count; ++i)
+                if (stuck[w.blk_off + i]) {
+                    if (strict) throw std::domain_error("reorder_schur: swap rejected in strict mode");
+                    rejected.push_back(slice[i].orig);
+                    for (auto& b : blocks)
+                        if (b.orig == slice[i].orig) b.selected = 0;
+                }
+        }
+    }
+    pr.windows = nw;
+    pr.levels = nl;
+    return pr;
+}
+
+struct StreamPair {
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev = nullptr;
+    StreamPair() {
+        TEIG_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        TEIG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    }
+    ~StreamPair() {
+        if (ev) cudaEventDestroy(ev);
+        if (s2) cudaStreamDestroy(s2);
+    }
+};
+
+}  // namespace
+
+int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq, int64_t nb,
+                         const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
+                         int64_t* perm, int64_t* rejected_out, int64_t* plan_out, int64_t plan_cap,
+                         teig_reorder_info* info, cudaStream_t stream) {
+    if (n < 1) return set_error(-1, "n must be >= 1");
+    if (!dS) return set_error(-2, "S is null");
+    if (lds < n) return set_error(-3, "lds < n");
+    if (dQ && ldq < n) return set_error(-5, "ldq < n");
+    if (nb < 0 || (nb > 0 && (!sizes || !flags))) return set_error(-6, "malformed selection");
+    teig_reorder_opts o;
+    teig_reorder_opts_default(&o);
+    if (opts) o = *opts;
+    int64_t ws = std::max<int64_t>(o.window_size ? o.window_size : default_tile_size(n), 8);
+    if (ws > 128) return set_error(TEIG_ERR_UNSUPPORTED, "window_size > 128 is not supported by the single-CTA window kernel");
+    if (n > (int64_t)2147483647) return set_error(TEIG_ERR_UNSUPPORTED, "n too large");
+
+    std::vector<BlockState> blocks(nb);
+    int64_t rows = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+        if (sizes[i] != 1 && sizes[i] != 2) return set_error(-8, "block sizes must be 1 or 2");
+        blocks[i] = BlockState{sizes[i], (uint8_t)(flags[i] ? 1 : 0), (uint32_t)i};
+        rows += sizes[i];
+    }
+    if (rows != n) return set_error(-8, "reorder_schur: selection does not match s");
+
+    teig_reorder_info inf{};
+    inf.clean = 1;
+    std::vector<int64_t> rejected, plan_log;
+    try {
+        StreamPair sp;
+        double plan_ms = 0.0;
+        for (int pass = 0; pass < 64; ++pass) {
+            const auto t0 = std::chrono::steady_clock::now();
+            ReorderPlan plan = plan_reorder(blocks, ws);
+            const auto t1 = std::chrono::steady_clock::now();
+            plan_ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+            if (plan.windows.empty()) break;
+            if (pass == 0) inf.n_groups = plan.n_groups;
+            inf.update_flops += plan_update_flops(plan, n, dQ != nullptr);
+            inf.update_bytes += plan_update_bytes(plan, n, dQ != nullptr);
+            PassResult pr = run_pass(plan, n, dS, lds, dQ, ldq, blocks, rejected, plan_log, o.strict != 0,
+                                     o.overlap_factor != 0, stream, sp.s2, sp.ev);
+            inf.n_windows += pr.windows;
+            inf.n_levels += pr.levels;
+            inf.n_passes += 1;
+            if (!pr.deviated) break;
+        }
+        inf.plan_ms = plan_ms;
+    } catch (const std::domain_error& e) {
+        return set_error(TEIG_ERR_STRICT, e.what());
+    } catch (const std::exception& e) {
+        return set_error(TEIG_ERR_CUDA, e.what());
+    }
+    // clean: no rejection and every still-selected block leads
+    bool leading = true;
+    {
+        bool seen_unsel = false;
+        for (const auto& b : blocks) {
+            if (!b.selected) seen_unsel = true;
+            else if (seen_unsel) leading = false;
+        }
+    }
+    inf.n_rejected = (int64_t)rejected.size();
+    inf.clean = (rejected.empty() && leading) ? 1 : 0;
+    if (perm)
+        for (int64_t i = 0; i < nb; ++i) perm[blocks[i].orig] = i;
+    if (rejected_out)
+        for (size_t i = 0; i < rejected.size(); ++i) rejected_out[i] = rejected[i];
+    if (plan_out)
+        for (int64_t i = 0; i < (int64_t)plan_log.size() / 3 && i < plan_cap; ++i)
+            for (int k = 0; k < 3; ++k) plan_out[3 * i + k] = plan_log[3 * i + k];
+    if (info) *info = inf;
+    return 0;
+}
+
+}  // namespace teig
+
+// ============================================================================
+// C ABI
+// ============================================================================
+using namespace teig;
+
+extern "C" {
+
+const char* teig_last_error(void) { return g_last_error.c_str(); }
+int teig_version(void) { return 1; }
+
+void teig_reorder_opts_default(teig_reorder_opts* o) {
+    o->window_size = 0;
+    o->strict = 0;
+    o->overlap_factor = 1;
+}
+
+int teig_reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq, int64_t nb,
+                              const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
+                              int64_t* perm, int64_t* rejected, int64_t* plan, int64_t plan_cap,
+                              teig_reorder_info* info, void* stream) {
+    return reorder_schur_device(n, dS, lds, dQ, ldq, nb, sizes, flags, opts, perm, rejected, plan, plan_cap, info,
+                                (cudaStream_t)stream);
+}
+
+int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_t ldq, int64_t nb,
+                            const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
+                            int64_t* perm, int64_t* rejected, int64_t* plan, int64_t plan_cap,
+                            teig_reorder_info* info, void* stream_v) {
+    if (n < 1) return set_error(-1, "n must be >= 1");
+    if (!S) return set_error(-2, "S is null");
+    if (lds < n) return set_error(-3, "lds < n");
+    if (Q && ldq < n) return set_error(-5, "ldq < n");
+    cudaStream_t stream = (cudaStream_t)stream_v;
+    try {
+        const size_t pitch = (size_t)n * sizeof(double);
+        DevBuf dS(pitch * n, stream), dQ(Q ? pitch * n : 0, stream);
+        TEIG_CUDA(cudaMemcpy2DAsync(dS.p, pitch, S, lds * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
+        if (Q)
+            TEIG_CUDA(cudaMemcpy2DAsync(dQ.p, pitch, Q, ldq * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
+        const int rc = reorder_schur_device(n, dS.as<double>(), n, Q ? dQ.as<double>() : nullptr, n, nb, sizes, flags,
+                                            opts, perm, rejected, plan, plan_cap, info, stream);
+        if (rc != 0) return rc;
+        TEIG_CUDA(cudaMemcpy2DAsync(S, lds * sizeof(double), dS.p, pitch, pitch, n, cudaMemcpyDeviceToHost, stream));
+        if (Q)
+            TEIG_CUDA(cudaMemcpy2DAsync(Q, ldq * sizeof(double), dQ.p, pitch, pitch, n, cudaMemcpyDeviceToHost, stream));
+        TEIG_CUDA(cudaStreamSynchronize(stream));
+    } catch (const std::exception& e) {
+        return set_error(TEIG_ERR_CUDA, e.what());
+    }
+    return 0;
+}
+
+int64_t teig_scan_blocks_device(int64_t n, const double* dS, int64_t lds, uint8_t* sizes, void* stream_v) {
+    if (n < 1) return set_error(-1, "n must be >= 1");
+    cudaStream_t stream = (cudaStream_t)stream_v;
+    std::vector<double> sub(n > 1 ? n - 1 : 1, 0.0);
+    try {
+        if (n > 1) {
+            TEIG_CUDA(cudaMemcpy2DAsync(sub.data(), sizeof(double), dS + 1, (lds + 1) * sizeof(double), sizeof(double),
+                                        n - 1, cudaMemcpyDeviceToHost, stream));
+            TEIG_CUDA(cudaStreamSynchronize(stream));
+        }
+    } catch (const std::exception& e) {
+        return set_error(TEIG_ERR_CUDA, e.what());
+    }
+    int64_t nb = 0;
+    for (int64_t i = 0; i < n;) {
+        if (i + 1 < n && sub[i] != 0.0) {
+            sizes[nb++] = 2;
+            i += 2;
+        } else {
+            sizes[nb++] = 1;
+            i += 1;
+        }
+    }
+    return nb;
+}
+
+int teig_select_fraction(int64_t nb, double fraction, uint64_t seed, uint8_t* flags) {
+    if (fraction < 0.0 || fraction > 1.0) return set_error(-2, "selection fraction must be in [0, 1]");
+    // Philox4x32-10 stream (philox.hpp), Fisher-Yates over block indices
+    struct Stream {
+        uint32_t k0, k1;
+        uint64_t ctr = 0;
+        uint32_t buf[4];
+        int have = 0;
+        uint64_t next() {
+            if (!have) {
+                uint32_t c[4] = {(uint32_t)ctr, (uint32_t)(ctr >> 32), 0u, 0u};
+                uint32_t a = k0, b = k1;
+                for (int r = 0; r < 10; ++r) {
+                    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+                    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ a, n1 = (uint32_t)p1;
+                    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ b, n3 = (uint32_t)p0;
+                    c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+                    a += 0x9E3779B9u;
+                    b += 0xBB67AE85u;
+                }
+                std::memcpy(buf, c, sizeof c);
+                ++ctr;
+                have = 2;
+            }
+            const int i = 2 - have;
+            --have;
+            return ((uint64_t)buf[2 * i + 1] << 32) | buf[2 * i];
+        }
+    };
+    const uint64_t s = seed ^ 0x5e1ec7u;
+    Stream rng{(uint32_t)s, (uint32_t)(s >> 32)};
+    const int64_t want = (int64_t)(fraction * (double)nb);
+    std::vector<int64_t> idx(nb);
+    for (int64_t i = 0; i < nb; ++i) idx[i] = i;
+    for (int64_t i = 0; i < want && i + 1 < nb; ++i) {
+        const int64_t j = i + (int64_t)(rng.next() % (uint64_t)(nb - i));
+        std::swap(idx[i], idx[j]);
+    }
+    std::memset(flags, 0, (size_t)nb);
+    for (int64_t i = 0; i < want; ++i) flags[idx[i]] = 1;
+    return 0;
+}
+
+int teig_window_reorder_device(int64_t d, double* dW, int64_t ldw, int64_t nb, const uint8_t* sizes,
+                               const uint8_t* sel, double* dAcc, uint32_t* order, uint8_t* stuck,
+                               int32_t* executed, void* stream_v) {
+    if (d < 1 || d > 128) return set_error(d < 1 ? -1 : TEIG_ERR_UNSUPPORTED, "window order must be in [1, 128]");
+    if (ldw < d) return set_error(-3, "ldw < d");
+    if (nb < 1 || nb > d) return set_error(-4, "bad block count");
+    cudaStream_t stream = (cudaStream_t)stream_v;
+    try {
+        WinDesc wd{};
+        wd.a = 0;
+        wd.d = (int32_t)d;
+        wd.nb = (int32_t)nb;
+        wd.qw_off = 0;
+        wd.blk_off = 0;
+        DevBuf ddesc(sizeof(WinDesc), stream), dsz(nb, stream), dsel(nb, stream), dord(nb, stream), dstk(nb, stream),
+            dst(sizeof(int32_t), stream);
+        TEIG_CUDA(cudaMemcpyAsync(ddesc.p, &wd, sizeof wd, cudaMemcpyHostToDevice, stream));
+        TEIG_CUDA(cudaMemcpyAsync(dsz.p, sizes, nb, cudaMemcpyHostToDevice, stream));
+        TEIG_CUDA(cudaMemcpyAsync(dsel.p, sel, nb, cudaMemcpyHostToDevice, stream));
+        TEIG_CUDA(launch_window_reorder(ddesc.as<WinDesc>(), 1, d <= 64 ? 64 : 128, dW, ldw, dAcc, dsz.as<uint8_t>(),
+                                        dsel.as<uint8_t>(), dord.as<uint8_t>(), dstk.as<uint8_t>(), dst.as<int32_t>(),
+                                        stream));
+        std::vector<uint8_t> o(nb), s(nb);
+        int32_t st = 0;
+        TEIG_CUDA(cudaMemcpyAsync(o.data(), dord.p, nb, cudaMemcpyDeviceToHost, stream));
+        TEIG_CUDA(cudaMemcpyAsync(s.data(), dstk.p, nb, cudaMemcpyDeviceToHost, stream));
+        TEIG_CUDA(cudaMemcpyAsync(&st, dst.p, sizeof st, cudaMemcpyDeviceToHost, stream));
+        TEIG_CUDA(cudaStreamSynchronize(stream));
+        *executed = (st & kWinExecuted) ? 1 : 0;
+        for (int64_t i = 0; i < nb; ++i) {
+            if (order) order[i] = *executed ? o[i] : (uint32_t)i;
+            if (stuck) stuck[i] = *executed ? s[i] : 0;
+        }
+    } catch (const std::exception& e) {
+        return set_error(TEIG_ERR_CUDA, e.what());
+    }
+    return 0;
+}
+
+int teig_apply_window_updates_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq, int64_t a,
+                                     int64_t d, const double* dQw, void* stream_v) {
+    if (n < 1) return set_error(-1, "n must be >= 1");
+    if (lds < n) return set_error(-3, "lds < n");
+    if (dQ && ldq < n) return set_error(-5, "ldq < n");
+    if (a < 0 || d < 1 || a + d > n) return set_error(-6, "window out of range");
+    if (d > 128) return set_error(TEIG_ERR_UNSUPPORTED, "window order must be <= 128");
+    cudaStream_t stream = (cudaStream_t)stream_v;
+    try {
+        WinDesc wd{};
+        wd.a = (int32_t)a;
+        wd.d = (int32_t)d;
+        wd.nb = 0;
+        wd.qw_off = 0;
+        DevBuf ddesc(sizeof(WinDesc), stream);
+        TEIG_CUDA(cudaMemcpyAsync(ddesc.p, &wd, sizeof wd, cudaMemcpyHostToDevice, stream));
+        const int dm = d <= 64 ? 64 : 128;
+        const int tl = (int)((n - a - d + kLeftBN - 1) / kLeftBN);
+        const int tr = (int)((a + kRightBM - 1) / kRightBM);
+        const int tq = (int)((n + kRightBM - 1) / kRightBM);
+        TEIG_CUDA(launch_update_left(ddesc.as<WinDesc>(), 1, tl, dm, dQw, dS, lds, (int)n, stream));
+        TEIG_CUDA(launch_update_right(ddesc.as<WinDesc>(), 1, tr, dm, dQw, dS, lds, (int)n, false, stream));
+        if (dQ) TEIG_CUDA(launch_update_right(ddesc.as<WinDesc>(), 1, tq, dm, dQw, dQ, ldq, (int)n, true, stream));
+        TEIG_CUDA(cudaStreamSynchronize(stream));
+    } catch (const std::exception& e) {
+        return set_error(TEIG_ERR_CUDA, e.what());
+    }
+    return 0;
+}
+
+int teig_gen_schur_input_device(int64_t n, double* dS, int64_t lds, uint64_t fill_seed, void* stream) {
+    if (n < 1 || lds < n) return set_error(-1, "bad shape");
+    cudaError_t e = launch_gen_schur_input(dS, lds, n, fill_seed, (cudaStream_t)stream);
+    return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+int teig_gen_hessenberg_device(int64_t n, double* dH, int64_t ldh, uint64_t seed, void* stream) {
+    if (n < 1 || ldh < n) return set_error(-1, "bad shape");
+    cudaError_t e = launch_gen_hessenberg(dH, ldh, n, seed, (cudaStream_t)stream);
+    return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+int teig_set_identity_device(int64_t n, double* dQ, int64_t ldq, void* stream) {
+    if (n < 1 || ldq < n) return set_error(-1, "bad shape");
+    cudaError_t e = launch_set_identity(dQ, ldq, n, (cudaStream_t)stream);
+    return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+}  // extern "C"
