@@ -52,6 +52,9 @@ typedef struct teig_reorder_opts {
     int32_t strict;      /* !=0: fail with TEIG_ERR_STRICT on a rejected swap */
     int32_t overlap_factor; /* !=0 (default 1 via teig_reorder_opts_default): run the
                                Q-factor updates on a second stream, overlapped */
+    int32_t profile;     /* !=0: bracket every launch with CUDA events and report
+                            per-kernel-class device time in teig_reorder_info */
+    int32_t pad;
 } teig_reorder_opts;
 
 typedef struct teig_reorder_info {
@@ -65,6 +68,12 @@ typedef struct teig_reorder_info {
     double update_flops;   /* sum over executed windows of 2d^2(n-b) + 2d^2 a (+ 2d^2 n) */
     double update_bytes;   /* algorithmic panel bytes: 16 d ((n-b) + a (+ n)) per window */
     double plan_ms;        /* host planning + scheduling time */
+    int64_t n_launches;    /* kernels launched by the call */
+    double ms_window;      /* profile only: summed device time of the window kernels */
+    double ms_left;        /*   ... of the left (row-panel) update kernels */
+    double ms_right;       /*   ... of the right (column-panel) update kernels */
+    double ms_factor;      /*   ... of the Q-factor update kernels */
+    double flops_left, flops_right, flops_factor; /* update flops per kernel class */
 } teig_reorder_info;
 
 void teig_reorder_opts_default(teig_reorder_opts* o);
@@ -98,6 +107,15 @@ int64_t teig_scan_blocks_device(int64_t n, const double* dS, int64_t lds, uint8_
 /* select_fraction (reorder.cpp:80-97): exactly floor(fraction*nb) blocks by a
  * Philox(seed ^ 0x5e1ec7) Fisher-Yates shuffle.  flags: host, nb. */
 int teig_select_fraction(int64_t nb, double fraction, uint64_t seed, uint8_t* flags);
+
+/* Planner only (host, no device work): the windows reorder_schur would run
+ * on a clean pass -- the reference's per-group chains (reorder.cpp:241-324)
+ * -- with their wavefront levels.  win (host, 5*cap int64 or NULL):
+ * (wtop, wbot, count, group, level) per window.  Returns the window count;
+ * *n_levels, *n_groups, *flops (update flops with Q) when non-NULL. */
+int64_t teig_plan_reorder(int64_t n, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
+                          int64_t window_size, int64_t* win, int64_t cap, int64_t* n_levels,
+                          int64_t* n_groups, double* flops);
 
 /* ------------------------------------------------------------------------ */
 /* Window-level kernels (device buffers; synchronous on `stream`).           */

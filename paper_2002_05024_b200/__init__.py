@@ -10,7 +10,7 @@ from ._native import TaskeigError, build, lib  # noqa: F401
 from .reorder import (  # noqa: F401
     Block, PlanWindow, ReorderOptions, ReorderResult, Selection, WindowReorderOutcome,
     apply_window_updates, colmajor_empty, gen_hessenberg, gen_schur_input, identity,
-    known_spectrum_seed, reorder_schur, scan_blocks, scan_blocks_device, select_by_name,
+    known_spectrum_seed, plan_reorder, reorder_schur, scan_blocks, scan_blocks_device, select_by_name,
     select_eigenvalues, select_fraction, window_reorder)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -32,14 +32,17 @@ def build(verbose: bool = False) -> str:
 
 
 class ReorderOpts(C.Structure):
-    _fields_ = [("window_size", C.c_int64), ("strict", C.c_int32), ("overlap_factor", C.c_int32)]
+    _fields_ = [("window_size", C.c_int64), ("strict", C.c_int32), ("overlap_factor", C.c_int32),
+                ("profile", C.c_int32), ("pad", C.c_int32)]
 
 
 class ReorderInfo(C.Structure):
     _fields_ = [("n_windows", C.c_int64), ("n_levels", C.c_int64), ("n_passes", C.c_int64),
                 ("n_groups", C.c_int64), ("n_rejected", C.c_int64), ("clean", C.c_int32),
                 ("pad", C.c_int32), ("update_flops", C.c_double), ("update_bytes", C.c_double),
-                ("plan_ms", C.c_double)]
+                ("plan_ms", C.c_double), ("n_launches", C.c_int64), ("ms_window", C.c_double),
+                ("ms_left", C.c_double), ("ms_right", C.c_double), ("ms_factor", C.c_double),
+                ("flops_left", C.c_double), ("flops_right", C.c_double), ("flops_factor", C.c_double)]
 
 
 _P = C.c_void_p
@@ -57,6 +60,7 @@ SIGNATURES = {
                                           _I64, _P, _P]),
     "teig_scan_blocks_device": (C.c_int64, [_I64, _P, _I64, _P, _P]),
     "teig_select_fraction": (C.c_int, [_I64, C.c_double, C.c_uint64, _P]),
+    "teig_plan_reorder": (C.c_int64, [_I64, _I64, _P, _P, _I64, _P, _I64, _P, _P, _P]),
     "teig_window_reorder_device": (C.c_int, [_I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "teig_apply_window_updates_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _I64, _P, _P]),
     "teig_gen_schur_input_device": (C.c_int, [_I64, _P, _I64, C.c_uint64, _P]),

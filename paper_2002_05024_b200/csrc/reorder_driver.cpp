@@ -72,16 +72,45 @@ struct DevBuf {
 };
 
 struct PassResult {
-    int64_t windows = 0, levels = 0;
+    int64_t windows = 0, levels = 0, launches = 0;
     bool deviated = false;
+    double ms_window = 0, ms_left = 0, ms_right = 0, ms_factor = 0;
+};
+
+// Event pairs bracketing launches when profiling is on.
+struct EventLog {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;
+    std::vector<std::pair<int, int>> spans[4];  // (start idx, end idx) per class
+    int record(cudaStream_t s) {
+        cudaEvent_t e;
+        TEIG_CUDA(cudaEventCreate(&e));
+        TEIG_CUDA(cudaEventRecord(e, s));
+        ev.push_back(e);
+        return (int)ev.size() - 1;
+    }
+    double total(int cls) {
+        double t = 0;
+        for (auto& sp : spans[cls]) {
+            float ms = 0;
+            TEIG_CUDA(cudaEventElapsedTime(&ms, ev[sp.first], ev[sp.second]));
+            t += ms;
+        }
+        return t;
+    }
+    ~EventLog() {
+        for (auto e : ev) cudaEventDestroy(e);
+    }
 };
 
 // Executes one planned pass on the device and folds the outcomes into `blocks`.
 PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq,
                     std::vector<BlockState>& blocks, std::vector<int64_t>& rejected,
-                    std::vector<int64_t>& plan_log, bool strict, bool overlap,
+                    std::vector<int64_t>& plan_log, bool strict, bool overlap, bool profile,
                     cudaStream_t stream, cudaStream_t stream2, cudaEvent_t ev) {
     PassResult pr;
+    EventLog lg;
+    lg.on = profile;
     const int64_t nw = (int64_t)plan.windows.size();
     schedule_levels(plan, n);
     const int32_t nl = plan.n_levels;
@@ -127,23 +156,42 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     TEIG_CUDA(cudaMemcpyAsync(d_sel.p, plan.sel.data(), ne, cudaMemcpyHostToDevice, stream));
 
     const WinDesc* dd = d_desc.as<WinDesc>();
+    int64_t launches = 0;
+    // runs `f` on stream `st`, bracketed by events of class `cls` when profiling
+    auto timed = [&](int cls, cudaStream_t st, int64_t ntiles, auto&& f) {
+        if (ntiles <= 0) return;
+        int e0 = lg.on ? lg.record(st) : -1;
+        TEIG_CUDA(f());
+        ++launches;
+        if (lg.on) lg.spans[cls].push_back({e0, lg.record(st)});
+    };
     for (int L = 0; L < nl; ++L) {
         const int64_t o = lvl_off[L], cnt = lvl_off[L + 1] - lvl_off[L];
-        TEIG_CUDA(launch_window_reorder(dd + o, (int)cnt, dmax_k, dS, lds, d_qw.as<double>(), d_sizes.as<uint8_t>(),
-                                        d_sel.as<uint8_t>(), d_order.as<uint8_t>(), d_stuck.as<uint8_t>(),
-                                        d_status.as<int32_t>() + o, stream));
+        timed(0, stream, cnt, [&] {
+            return launch_window_reorder(dd + o, (int)cnt, dmax_k, dS, lds, d_qw.as<double>(), d_sizes.as<uint8_t>(),
+                                         d_sel.as<uint8_t>(), d_order.as<uint8_t>(), d_stuck.as<uint8_t>(),
+                                         d_status.as<int32_t>() + o, stream);
+        });
         if (dQ && overlap) {
             TEIG_CUDA(cudaEventRecord(ev, stream));
             TEIG_CUDA(cudaStreamWaitEvent(stream2, ev, 0));
-            TEIG_CUDA(launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
-                                          true, stream2));
+            timed(3, stream2, tq[L], [&] {
+                return launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
+                                           true, stream2);
+            });
         }
-        TEIG_CUDA(launch_update_left(dd + o, (int)cnt, (int)tl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n, stream));
-        TEIG_CUDA(launch_update_right(dd + o, (int)cnt, (int)tr[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
-                                      false, stream));
+        timed(1, stream, tl[L], [&] {
+            return launch_update_left(dd + o, (int)cnt, (int)tl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n, stream);
+        });
+        timed(2, stream, tr[L], [&] {
+            return launch_update_right(dd + o, (int)cnt, (int)tr[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n, false,
+                                       stream);
+        });
         if (dQ && !overlap)
-            TEIG_CUDA(launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
-                                          true, stream));
+            timed(3, stream, tq[L], [&] {
+                return launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
+                                           true, stream);
+            });
     }
     if (dQ && overlap) {
         TEIG_CUDA(cudaEventRecord(ev, stream2));
@@ -195,6 +243,13 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     }
     pr.windows = nw;
     pr.levels = nl;
+    pr.launches = launches;
+    if (lg.on) {
+        pr.ms_window = lg.total(0);
+        pr.ms_left = lg.total(1);
+        pr.ms_right = lg.total(2);
+        pr.ms_factor = lg.total(3);
+    }
     return pr;
 }
 
@@ -253,10 +308,21 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
             if (pass == 0) inf.n_groups = plan.n_groups;
             inf.update_flops += plan_update_flops(plan, n, dQ != nullptr);
             inf.update_bytes += plan_update_bytes(plan, n, dQ != nullptr);
+            for (const auto& w : plan.windows) {
+                const double d = double(w.wbot - w.wtop);
+                inf.flops_left += 2.0 * d * d * double(n - w.wbot);
+                inf.flops_right += 2.0 * d * d * double(w.wtop);
+                if (dQ) inf.flops_factor += 2.0 * d * d * double(n);
+            }
             PassResult pr = run_pass(plan, n, dS, lds, dQ, ldq, blocks, rejected, plan_log, o.strict != 0,
-                                     o.overlap_factor != 0, stream, sp.s2, sp.ev);
+                                     o.overlap_factor != 0, o.profile != 0, stream, sp.s2, sp.ev);
             inf.n_windows += pr.windows;
             inf.n_levels += pr.levels;
+            inf.n_launches += pr.launches;
+            inf.ms_window += pr.ms_window;
+            inf.ms_left += pr.ms_left;
+            inf.ms_right += pr.ms_right;
+            inf.ms_factor += pr.ms_factor;
             inf.n_passes += 1;
             if (!pr.deviated) break;
         }
@@ -304,6 +370,8 @@ void teig_reorder_opts_default(teig_reorder_opts* o) {
     o->window_size = 0;
     o->strict = 0;
     o->overlap_factor = 1;
+    o->profile = 0;
+    o->pad = 0;
 }
 
 int teig_reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq, int64_t nb,
@@ -366,6 +434,35 @@ int64_t teig_scan_blocks_device(int64_t n, const double* dS, int64_t lds, uint8_
         }
     }
     return nb;
+}
+
+int64_t teig_plan_reorder(int64_t n, int64_t nb, const uint8_t* sizes, const uint8_t* flags, int64_t window_size,
+                          int64_t* win, int64_t cap, int64_t* n_levels, int64_t* n_groups, double* flops) {
+    if (n < 1) return set_error(-1, "n must be >= 1");
+    std::vector<BlockState> blocks(nb);
+    int64_t rows = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+        if (sizes[i] != 1 && sizes[i] != 2) return set_error(-3, "block sizes must be 1 or 2");
+        blocks[i] = BlockState{sizes[i], (uint8_t)(flags[i] ? 1 : 0), (uint32_t)i};
+        rows += sizes[i];
+    }
+    if (rows != n) return set_error(-3, "selection does not match n");
+    const int64_t ws = std::max<int64_t>(window_size ? window_size : default_tile_size(n), 8);
+    ReorderPlan plan = plan_reorder(blocks, ws);
+    schedule_levels(plan, n);
+    if (win)
+        for (int64_t i = 0; i < (int64_t)plan.windows.size() && i < cap; ++i) {
+            const auto& w = plan.windows[i];
+            win[5 * i] = w.wtop;
+            win[5 * i + 1] = w.wbot;
+            win[5 * i + 2] = w.count;
+            win[5 * i + 3] = w.group;
+            win[5 * i + 4] = w.level;
+        }
+    if (n_levels) *n_levels = plan.n_levels;
+    if (n_groups) *n_groups = plan.n_groups;
+    if (flops) *flops = plan_update_flops(plan, n, true);
+    return (int64_t)plan.windows.size();
 }
 
 int teig_select_fraction(int64_t nb, double fraction, uint64_t seed, uint8_t* flags) {

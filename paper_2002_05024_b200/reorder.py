@@ -170,6 +170,7 @@ class ReorderOptions:
     seed: int = 0             # accepted for API parity (scheduler perturbation only)
     strict: bool = False      # raise on rejected swaps instead of recording
     overlap_factor: bool = True
+    profile: bool = False     # per-kernel-class CUDA-event timing in ReorderResult.info
 
 
 @dataclass
@@ -247,6 +248,7 @@ def reorder_schur(s, q, sel: Selection, opts: Optional[ReorderOptions] = None,
     o.window_size = int(opts.window_size)
     o.strict = int(bool(opts.strict))
     o.overlap_factor = int(bool(opts.overlap_factor))
+    o.profile = int(bool(opts.profile))
     vp = lambda a: a.ctypes.data_as(C.c_void_p)
     if torch is not None and isinstance(s, torch.Tensor):
         _need_torch_cuda(s)
@@ -283,6 +285,30 @@ def reorder_schur(s, q, sel: Selection, opts: Optional[ReorderOptions] = None,
     inf = {f: getattr(info, f) for f, _ in N.ReorderInfo._fields_ if f != "pad"}
     return ReorderResult(s_out, q_out, [int(x) for x in perm[:nb]],
                          [int(x) for x in rej[:info.n_rejected]], pl, bool(info.clean), inf)
+
+
+def reorder_schur_host_buffers(s_buf: np.ndarray, q_buf: Optional[np.ndarray], n: int, sel: Selection,
+                               opts: Optional[ReorderOptions] = None) -> dict:
+    """Reorders HOST buffers holding S and Q COLUMN-MAJOR with ld = n (e.g. a
+    C-ordered array of S^T, or pinned memory) in place through the C ABI's
+    host entry point; host<->device copies happen inside the call."""
+    opts = opts or ReorderOptions()
+    assert s_buf.dtype == np.float64 and s_buf.size == n * n and s_buf.flags.contiguous
+    nb = len(sel.blocks)
+    sizes, flags = sel.sizes_array(), sel.flags_array()
+    perm = np.zeros(max(nb, 1), dtype=np.int64)
+    rej = np.zeros(max(nb, 1), dtype=np.int64)
+    info = N.ReorderInfo()
+    o = N.ReorderOpts()
+    N.lib().teig_reorder_opts_default(C.byref(o))
+    o.window_size = int(opts.window_size)
+    o.strict = int(bool(opts.strict))
+    o.overlap_factor = int(bool(opts.overlap_factor))
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)
+    N.check(N.lib().teig_reorder_schur_host(n, vp(s_buf), n, vp(q_buf) if q_buf is not None else None, n, nb,
+                                            vp(sizes), vp(flags), C.byref(o), vp(perm), vp(rej), None, 0,
+                                            C.byref(info), None))
+    return {f: getattr(info, f) for f, _ in N.ReorderInfo._fields_ if f != "pad"}
 
 
 def apply_window_updates(s, q, a: int, qw, stream=None) -> None:
@@ -337,3 +363,22 @@ def scan_blocks_device(s, stream=None) -> np.ndarray:
     nb = N.check(N.lib().teig_scan_blocks_device(n, sw.data_ptr(), lds, sizes.ctypes.data_as(C.c_void_p),
                                                  _stream_ptr(stream, s)))
     return sizes[:nb].copy()
+
+
+def plan_reorder(n: int, sel: Selection, window_size: int = 0):
+    """Host planner of the GPU scheduler (no device work).  Returns
+    (windows int64[k, 5] of (wtop, wbot, count, group, level), n_levels,
+    n_groups, update flops with Q)."""
+    sizes, flags = sel.sizes_array(), sel.flags_array()
+    nb = len(sizes)
+    cap = max(64, 2 * nb)
+    while True:
+        win = np.zeros(5 * cap, dtype=np.int64)
+        nl, ng, fl = C.c_int64(0), C.c_int64(0), C.c_double(0)
+        k = N.check(N.lib().teig_plan_reorder(n, nb, sizes.ctypes.data_as(C.c_void_p),
+                                              flags.ctypes.data_as(C.c_void_p), window_size,
+                                              win.ctypes.data_as(C.c_void_p), cap, C.byref(nl),
+                                              C.byref(ng), C.byref(fl)))
+        if k <= cap:
+            return win[:5 * k].reshape(k, 5), nl.value, ng.value, fl.value
+        cap = k
