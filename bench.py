@@ -50,8 +50,6 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-sample-groups", type=int, default=0,
-                    help="groups in the bounded CPU sample (0: auto, ~10-20 s of CPU work)")
     return ap.parse_args()
 
 
@@ -262,7 +260,7 @@ def run_ours(args, rank, world, local):
         "step_ms": [round(x, 3) for x in step_ms],
     }
     if rank == 0 and not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(args, n, sample_groups=args.cpu_sample_groups)
+        out["cpu_baseline"] = cpu_baseline(args, n)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
@@ -281,45 +279,56 @@ def _cpu_problem(n):
     return O, S, sizes, flags
 
 
-def _sample_flags(O, sizes, flags, ws, n, groups):
-    """Keep only the first `groups` groups of the plan selected: the
-    reference then runs exactly those groups' chains of the full problem."""
-    plan, F_total, ng = O.plan_reorder(sizes, flags, ws, n)
-    groups = min(groups, ng)
-    keep = np.zeros_like(flags)
-    # the first `groups` groups are formed from the first selected blocks in order
-    sel_idx = np.nonzero(flags)[0]
-    # count selected blocks per group from the plan: group g's first window has
-    # count - (#unselected) ... simpler: replay group formation
+def _group_members(sizes, flags, ws):
+    """Selected blocks of each group, in order (reorder.cpp:259-267); group
+    membership only depends on the original arrangement because earlier groups
+    move up from above later ones."""
     starts = np.concatenate([[0], np.cumsum(sizes.astype(np.int64))])
-    i = 0
-    taken = 0
-    g = 0
-    while g < groups and i < len(sel_idx):
+    sel_idx = np.nonzero(flags)[0]
+    groups, i = [], 0
+    while i < len(sel_idx):
         fs = sel_idx[i]
         rows = int(sizes[fs])
-        keep[fs] = 1
+        g = [fs]
         i += 1
         while i < len(sel_idx):
             gi = sel_idx[i]
-            span = starts[gi + 1] - starts[fs]
-            if rows + sizes[gi] > ws // 2 or span > ws:
+            if rows + sizes[gi] > ws // 2 or starts[gi + 1] - starts[fs] > ws:
                 break
             rows += int(sizes[gi])
-            keep[gi] = 1
+            g.append(gi)
             i += 1
-        g += 1
-    _, F_sample, ng2 = O.plan_reorder(sizes, keep, ws, n)
-    return keep, F_total, F_sample, groups, ng
+        groups.append(g)
+    return groups
 
 
-def cpu_baseline(args, n, sample_groups=0, steps=1, kind_pref="reference"):
+def _sample_flags(O, sizes, flags, ws, n, frac_target):
+    """Keep the first G groups selected (G: smallest with >= frac_target of
+    the update flops); the reference then runs exactly those groups' chains of
+    the full problem."""
+    plan, F_total, ng = O.plan_reorder(sizes, flags, ws, n)
+    d = (plan[:, 1] - plan[:, 0]).astype(np.float64)
+    a = plan[:, 0].astype(np.float64)
+    b = plan[:, 1].astype(np.float64)
+    fw = 2 * d * d * (n - b) + 2 * d * d * a + 2 * d * d * n
+    per_group = np.bincount(plan[:, 4], weights=fw, minlength=ng)
+    cum = np.cumsum(per_group) / F_total
+    G = int(np.searchsorted(cum, frac_target) + 1)
+    G = max(1, min(G, ng))
+    groups = _group_members(sizes, flags, ws)
+    keep = np.zeros_like(flags)
+    for g in groups[:G]:
+        keep[g] = 1
+    _, F_sample, _ = O.plan_reorder(sizes, keep, ws, n)
+    return keep, F_total, F_sample, G, ng
+
+
+def cpu_baseline(args, n, steps=1, frac_target=0.06):
     O, S, sizes, flags = _cpu_problem(n)
     ws = args.ws or 128
-    use_ref = kind_pref == "reference" and O.ref_available()
+    use_ref = O.ref_available()
     cores = os.cpu_count() or 1
-    groups = sample_groups or max(4, int(0.08 * len(flags) / max(1, ws // 4)))
-    keep, F_total, F_sample, groups, ng = _sample_flags(O, sizes, flags, ws, n, groups)
+    keep, F_total, F_sample, groups, ng = _sample_flags(O, sizes, flags, ws, n, frac_target)
     times = []
     for _ in range(steps):
         if use_ref:
@@ -338,9 +347,9 @@ def cpu_baseline(args, n, sample_groups=0, steps=1, kind_pref="reference"):
     return {"value": round(t_full, 3), "unit": "s", "cores": cores if use_ref else 1,
             "kind": "reference" if use_ref else "port",
             "sample": f"first {groups} of {ng} window chains (groups) of the same n={n} workload "
-                      f"({100 * F_sample / F_total:.1f}% of its update flops) timed in {t_sample:.2f} s, "
-                      f"extrapolated to the full workload by update flops",
-            "sample_seconds": round(t_sample, 3), "flops_fraction": F_sample / F_total}
+                      f"({100 * F_sample / F_total:.1f}% of its update flops) timed in {t_sample:.2f} s "
+                      f"with {cores if use_ref else 1} threads, extrapolated to the full workload by update flops",
+            "sample_seconds": round(t_sample, 3), "flops_fraction": round(F_sample / F_total, 5)}
 
 
 def run_reference(args, rank, world, local):
@@ -350,7 +359,7 @@ def run_reference(args, rank, world, local):
     t = []
     res = None
     for k in range(args.warmup + args.steps):
-        res = cpu_baseline(args, n, sample_groups=args.cpu_sample_groups)
+        res = cpu_baseline(args, n)
         if k >= args.warmup:
             t.append(res["value"])
     v = statistics.mean(t)

@@ -139,99 +139,121 @@ __device__ __forceinline__ double reflector(const double (&x)[L], double (&v)[L]
     return beta;
 }
 
-// Complete-pivoting elimination on a K x K system (reference
-// kernels.cpp:419-464).  m row-major m[i][j].  rhs overwritten by the
-// solution.  Row/column interchanges are predicated selects so everything
-// stays in registers.
+// Complete-pivoting LU of a K x K system (reference kernels.cpp:419-464),
+// kept so that the refinement solve (kernels.cpp:501-504, which refactors the
+// same matrix) replays the identical elimination on the new right-hand side
+// instead of factoring twice.  m row-major m[i][j].  Row/column interchanges
+// are predicated selects so everything stays in registers.
 template <int K>
-__device__ __forceinline__ bool gecp(const double (&m_in)[K][K], double (&rhs)[K], double& rcond) {
-    double m[K][K];
-    int cp[K];
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-        cp[i] = i;
-#pragma unroll
-        for (int j = 0; j < K; ++j) m[i][j] = m_in[i][j];
-    }
-    double amax = 0.0, smin = 0.0;
-#pragma unroll
-    for (int s = 0; s < K; ++s) {
-        int pi = s, pj = s;
-        double pv = 0.0;
-#pragma unroll
-        for (int i = s; i < K; ++i)
-#pragma unroll
-            for (int j = s; j < K; ++j)
-                if (fabs(m[i][j]) > pv) {
-                    pv = fabs(m[i][j]);
-                    pi = i;
-                    pj = j;
-                }
-        if (s == 0) amax = pv;
-        smin = pv;
-        if (pv == 0.0) {
-            rcond = 0.0;
-            return false;
-        }
-        // row interchange s <-> pi
-#pragma unroll
-        for (int i = s + 1; i < K; ++i) {
-            if (pi == i) {
-#pragma unroll
-                for (int j = 0; j < K; ++j) {
-                    const double t = m[s][j];
-                    m[s][j] = m[i][j];
-                    m[i][j] = t;
-                }
-                const double t = rhs[s];
-                rhs[s] = rhs[i];
-                rhs[i] = t;
-            }
-        }
-        // column interchange s <-> pj
-#pragma unroll
-        for (int j = s + 1; j < K; ++j) {
-            if (pj == j) {
-#pragma unroll
-                for (int i = 0; i < K; ++i) {
-                    const double t = m[i][s];
-                    m[i][s] = m[i][j];
-                    m[i][j] = t;
-                }
-                const int t = cp[s];
-                cp[s] = cp[j];
-                cp[j] = t;
-            }
-        }
-#pragma unroll
-        for (int i = s + 1; i < K; ++i) {
-            const double f = m[i][s] / m[s][s];
-            m[i][s] = 0.0;
-#pragma unroll
-            for (int j = s + 1; j < K; ++j) m[i][j] -= f * m[s][j];
-            rhs[i] -= f * rhs[s];
-        }
-    }
-    double x[K];
-#pragma unroll
-    for (int kk = K - 1; kk >= 0; --kk) {
-        double acc = rhs[kk];
-#pragma unroll
-        for (int j = kk + 1; j < K; ++j) acc -= m[kk][j] * x[j];
-        x[kk] = acc / m[kk][kk];
-    }
-    // rhs[cp[i]] = x[i] with predicated scatter
-#pragma unroll
-    for (int t = 0; t < K; ++t) {
-        double v = 0.0;
+struct GecpLU {
+    double u[K][K];     // upper factor (after interchanges)
+    double f[K][K];     // elimination multipliers f[i][s], i > s
+    int pi[K], pj[K];   // row / column pivot of step s
+    double rcond;
+    bool ok;
+
+    __device__ __forceinline__ void factor(const double (&m_in)[K][K]) {
 #pragma unroll
         for (int i = 0; i < K; ++i)
-            if (cp[i] == t) v = x[i];
-        rhs[t] = v;
+#pragma unroll
+            for (int j = 0; j < K; ++j) u[i][j] = m_in[i][j];
+        double amax = 0.0, smin = 0.0;
+        ok = true;
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            int bi = s, bj = s;
+            double pv = 0.0;
+#pragma unroll
+            for (int i = s; i < K; ++i)
+#pragma unroll
+                for (int j = s; j < K; ++j)
+                    if (fabs(u[i][j]) > pv) {
+                        pv = fabs(u[i][j]);
+                        bi = i;
+                        bj = j;
+                    }
+            pi[s] = bi;
+            pj[s] = bj;
+            if (s == 0) amax = pv;
+            smin = pv;
+            if (pv == 0.0) ok = false;
+#pragma unroll
+            for (int i = s + 1; i < K; ++i)
+                if (bi == i) {
+#pragma unroll
+                    for (int j = 0; j < K; ++j) {
+                        const double t = u[s][j];
+                        u[s][j] = u[i][j];
+                        u[i][j] = t;
+                    }
+                }
+#pragma unroll
+            for (int j = s + 1; j < K; ++j)
+                if (bj == j) {
+#pragma unroll
+                    for (int i = 0; i < K; ++i) {
+                        const double t = u[i][s];
+                        u[i][s] = u[i][j];
+                        u[i][j] = t;
+                    }
+                }
+#pragma unroll
+            for (int i = s + 1; i < K; ++i) {
+                const double fm = u[i][s] / u[s][s];
+                f[i][s] = fm;
+                u[i][s] = 0.0;
+#pragma unroll
+                for (int j = s + 1; j < K; ++j) u[i][j] -= fm * u[s][j];
+            }
+        }
+        rcond = ok ? ((amax > 0.0) ? smin / amax : 0.0) : 0.0;
     }
-    rcond = (amax > 0.0) ? smin / amax : 0.0;
-    return true;
-}
+
+    // rhs <- solution, replaying the interchanges and multipliers
+    __device__ __forceinline__ void solve(double (&rhs)[K]) const {
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+#pragma unroll
+            for (int i = s + 1; i < K; ++i)
+                if (pi[s] == i) {
+                    const double t = rhs[s];
+                    rhs[s] = rhs[i];
+                    rhs[i] = t;
+                }
+#pragma unroll
+            for (int i = s + 1; i < K; ++i) rhs[i] -= f[i][s] * rhs[s];
+        }
+        double x[K];
+#pragma unroll
+        for (int kk = K - 1; kk >= 0; --kk) {
+            double acc = rhs[kk];
+#pragma unroll
+            for (int j = kk + 1; j < K; ++j) acc -= u[kk][j] * x[j];
+            x[kk] = acc / u[kk][kk];
+        }
+        // undo the column interchanges: cp = product of the transpositions
+        int cp[K];
+#pragma unroll
+        for (int i = 0; i < K; ++i) cp[i] = i;
+#pragma unroll
+        for (int s = 0; s < K; ++s)
+#pragma unroll
+            for (int j = s + 1; j < K; ++j)
+                if (pj[s] == j) {
+                    const int t = cp[s];
+                    cp[s] = cp[j];
+                    cp[j] = t;
+                }
+#pragma unroll
+        for (int t = 0; t < K; ++t) {
+            double v = 0.0;
+#pragma unroll
+            for (int i = 0; i < K; ++i)
+                if (cp[i] == t) v = x[i];
+            rhs[t] = v;
+        }
+    }
+};
 
 // Direct swap of the adjacent P x P (upper) and Q x Q (lower) blocks held in
 // blk (row-major, D = P+Q).  On success: M (row-major D x D, window <- M^T W M)
@@ -259,8 +281,11 @@ __device__ __forceinline__ bool direct_swap(const double (&blk)[P + Q][P + Q], d
                 }
             rhs[row] = blk[i][P + j];
         }
-    double rcond;
-    if (!gecp<K>(Km, rhs, rcond)) return false;
+    GecpLU<K> lu;
+    lu.factor(Km);
+    if (!lu.ok) return false;
+    const double rcond = lu.rcond;
+    lu.solve(rhs);
     double x[K];
 #pragma unroll
     for (int i = 0; i < K; ++i) x[i] = rhs[i];
@@ -283,11 +308,9 @@ __device__ __forceinline__ bool direct_swap(const double (&blk)[P + Q][P + Q], d
             }
             r[j * P + i] = acc;
         }
-    double rc2;
-    if (gecp<K>(Km, r, rc2)) {
+    lu.solve(r);  // same matrix: the reference's second factorization is identical
 #pragma unroll
-        for (int i = 0; i < K; ++i) x[i] += r[i];
-    }
+    for (int i = 0; i < K; ++i) x[i] += r[i];
     if (rcond < 1.8189894035458565e-12) return false;  // eps^(3/4) = 2^-39 (kernels.cpp:540)
 
     // Householder QR of Z = [-X; I] (D x Q) (kernels.cpp:542-559)
