@@ -13,7 +13,8 @@ size_t window_reorder_smem_bytes(int dmax);
 cudaError_t launch_window_reorder(const WinDesc* wins, int nwin, int dmax, double* S, long long lds,
                                   double* qw_pool, const uint8_t* sizes_pool, const uint8_t* sel_pool,
                                   uint8_t* order_pool, uint8_t* stuck_pool, int32_t* status,
-                                  cudaStream_t stream);
+                                  cudaStream_t stream, unsigned long long* prof = nullptr);
+constexpr int kWindowThreads = 256;  // threads of the window kernel (8 warps)
 
 cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
                                double* S, long long lds, int n, cudaStream_t stream);

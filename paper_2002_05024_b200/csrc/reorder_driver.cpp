@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -157,6 +158,10 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
 
     const WinDesc* dd = d_desc.as<WinDesc>();
     int64_t launches = 0;
+    // TEIG_WINDOW_PROF=1: per-warp phase timing of every window CTA (diagnostics)
+    static const bool wprof = getenv("TEIG_WINDOW_PROF") && atoi(getenv("TEIG_WINDOW_PROF")) != 0;
+    DevBuf d_prof(wprof ? sizeof(unsigned long long) * nw * kWindowThreads / 32 * 4 : 0, stream);
+    if (wprof) TEIG_CUDA(cudaMemsetAsync(d_prof.p, 0, sizeof(unsigned long long) * nw * kWindowThreads / 32 * 4, stream));
     // runs `f` on stream `st`, bracketed by events of class `cls` when profiling
     auto timed = [&](int cls, cudaStream_t st, int64_t ntiles, auto&& f) {
         if (ntiles <= 0) return;
@@ -170,7 +175,8 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         timed(0, stream, cnt, [&] {
             return launch_window_reorder(dd + o, (int)cnt, dmax_k, dS, lds, d_qw.as<double>(), d_sizes.as<uint8_t>(),
                                          d_sel.as<uint8_t>(), d_order.as<uint8_t>(), d_stuck.as<uint8_t>(),
-                                         d_status.as<int32_t>() + o, stream);
+                                         d_status.as<int32_t>() + o, stream,
+                                         wprof ? d_prof.as<unsigned long long>() + o * (kWindowThreads / 32) * 4 : nullptr);
         });
         if (dQ && overlap) {
             TEIG_CUDA(cudaEventRecord(ev, stream));
@@ -204,6 +210,27 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     TEIG_CUDA(cudaMemcpyAsync(order.data(), d_order.p, ne, cudaMemcpyDeviceToHost, stream));
     TEIG_CUDA(cudaMemcpyAsync(stuck.data(), d_stuck.p, ne, cudaMemcpyDeviceToHost, stream));
     TEIG_CUDA(cudaStreamSynchronize(stream));
+    if (wprof) {
+        const int NW = kWindowThreads / 32;
+        std::vector<unsigned long long> pf((size_t)nw * NW * 4);
+        TEIG_CUDA(cudaMemcpy(pf.data(), d_prof.p, pf.size() * 8, cudaMemcpyDeviceToHost));
+        double p1[8] = {0}, p2[8] = {0}, steps = 0, kc = 0, kmax = 0;
+        for (int64_t k = 0; k < nw; ++k) {
+            for (int w = 0; w < NW; ++w) {
+                p1[w] += pf[(k * NW + w) * 4 + 0];
+                p2[w] += pf[(k * NW + w) * 4 + 1];
+            }
+            steps += pf[(k * NW) * 4 + 2];
+            kc += pf[(k * NW) * 4 + 3];
+            kmax = std::max(kmax, (double)pf[(k * NW) * 4 + 3]);
+        }
+        fprintf(stderr, "[teig window prof] windows=%lld levels=%d steps/window=%.1f kernel cycles/window=%.0f\n",
+                (long long)nw, nl, steps / nw, kc / nw);
+        for (int w = 0; w < NW; ++w)
+            fprintf(stderr, "  warp %d: phase1 cycles/step=%.0f phase2 cycles/step=%.0f\n", w, p1[w] / steps,
+                    p2[w] / steps);
+        fprintf(stderr, "  kernel cycles per step (window avg) = %.0f\n", kc / steps);
+    }
     std::vector<int32_t> st_by_plan(nw);
     for (int64_t k = 0; k < nw; ++k) st_by_plan[idx[k]] = status[k];
 

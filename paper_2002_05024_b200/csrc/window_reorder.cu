@@ -57,13 +57,16 @@ struct WinShared {
     uint8_t bsz[kMaxBlocks];     // block id -> size
     uint8_t bsel[kMaxBlocks];    // block id -> selected
     uint8_t bstuck[kMaxBlocks];  // block id -> rejected (stops moving)
-    int8_t owner[2][kMaxBlocks]; // row/col index -> pair owning it (-1: none), per buffer
+    int8_t owner[3][kMaxBlocks]; // row/col index -> pair owning it (-1: none), per buffer
+    int16_t acc_lo[kMaxBlocks];  // nonzero row range of each ACC column
+    int16_t acc_hi[kMaxBlocks];
     int16_t srow[kMaxBlocks + 1];
-    PairRec pairs[2][kMaxPairs];
-    int16_t type_list[2][4][kMaxPairs];
-    int type_cnt[2][4];
-    int npairs[2];
+    PairRec pairs[3][kMaxPairs];   // pair state of steps t-1, t, t+1 (index step % 3)
+    int16_t type_list[3][4][kMaxPairs];
+    int type_cnt[3][4];
+    int npairs[3];
     int status;
+    int redo;
     double M[2][kMaxPairs][16];  // row-major D x D, window <- M^T W M
     double B[kMaxPairs][16];     // new diagonal block, row-major D x D
 };
@@ -199,124 +202,111 @@ __device__ __forceinline__ void matT_vec(const double* M, const double* x, doubl
     }
 }
 
-// ACC[:, pos:pos+D] <- ACC[:, pos:pos+D] M for the pairs of buffer `buf`,
-// threads [t0, t0+nt) of the CTA
-__device__ __forceinline__ void acc_update(const WinShared& sh, double* acc, int d, int buf, int t0, int nt, int tid) {
+// ACC[:, pos:pos+D] <- ACC[:, pos:pos+D] M for the pairs of buffer `buf`.
+// One warp per pair (warp-uniform D, M in registers), lanes over the rows of
+// the union of the columns' nonzero row ranges (ACC starts as I; a column's
+// support only grows by mixing with its pair partner).
+template <int D>
+__device__ __forceinline__ void acc_pair(WinShared& sh, double* acc, int d, const double* Ms, int pos, int lane) {
+    double M[D * D];
+#pragma unroll
+    for (int i = 0; i < D * D; ++i) M[i] = Ms[i];
+    int lo = sh.acc_lo[pos], hi = sh.acc_hi[pos];
+#pragma unroll
+    for (int j = 1; j < D; ++j) {
+        lo = min(lo, (int)sh.acc_lo[pos + j]);
+        hi = max(hi, (int)sh.acc_hi[pos + j]);
+    }
+    double* c0 = acc + pos * d;
+    for (int r = lo + lane; r <= hi; r += 32) {
+        double x[D], y[D];
+#pragma unroll
+        for (int j = 0; j < D; ++j) x[j] = c0[r + j * d];
+        vec_mat<D>(x, M, y);
+#pragma unroll
+        for (int j = 0; j < D; ++j) c0[r + j * d] = y[j];
+    }
+    __syncwarp();
+    if (lane < D) {
+        sh.acc_lo[pos + lane] = (int16_t)lo;
+        sh.acc_hi[pos + lane] = (int16_t)hi;
+    }
+}
+
+__device__ __forceinline__ void acc_update(WinShared& sh, double* acc, int d, int buf, int mbuf, int w0, int nw, int warp, int lane) {
     const int np = sh.npairs[buf];
-    for (int item = tid - t0; item < np * d; item += nt) {
-        const int pi = item / d, r = item - pi * d;
+    for (int pi = warp - w0; pi < np; pi += nw) {
         const PairRec pr = sh.pairs[buf][pi];
         if (!pr.ok) continue;
         const int D = pr.p + pr.q;
-        double* c0 = acc + r + pr.pos * d;
-        double x[4], y[4];
-        const double* M = sh.M[buf][pi];
-        if (D == 2) {
-            x[0] = c0[0]; x[1] = c0[d];
-            vec_mat<2>(x, M, y);
-            c0[0] = y[0]; c0[d] = y[1];
-        } else if (D == 3) {
-            x[0] = c0[0]; x[1] = c0[d]; x[2] = c0[2 * d];
-            vec_mat<3>(x, M, y);
-            c0[0] = y[0]; c0[d] = y[1]; c0[2 * d] = y[2];
-        } else {
-            x[0] = c0[0]; x[1] = c0[d]; x[2] = c0[2 * d]; x[3] = c0[3 * d];
-            vec_mat<4>(x, M, y);
-            c0[0] = y[0]; c0[d] = y[1]; c0[2 * d] = y[2]; c0[3 * d] = y[3];
-        }
+        const double* M = sh.M[mbuf][pi];
+        if (D == 2) acc_pair<2>(sh, acc, d, M, pr.pos, lane);
+        else if (D == 3) acc_pair<3>(sh, acc, d, M, pr.pos, lane);
+        else acc_pair<4>(sh, acc, d, M, pr.pos, lane);
     }
 }
 
-// W[r, A] <- W[r, A] M_A for one row r above A's block
+// Rows of pair A: W[A, c] <- M_A^T W[A, c] for every column c right of A's
+// block (lanes over columns).
 template <int DA>
-__device__ __forceinline__ void upd_row(double* w, int r, int posA, const double* MA) {
-    double x[DA], y[DA];
+__device__ __forceinline__ void rows_pair(double* w, int d, int posA, const double* MAs, int lane) {
+    double MA[DA * DA];
 #pragma unroll
-    for (int j = 0; j < DA; ++j) x[j] = w[pk(r, posA + j)];
-    vec_mat<DA>(x, MA, y);
+    for (int i = 0; i < DA * DA; ++i) MA[i] = MAs[i];
+    for (int c = posA + DA + lane; c < d; c += 32) {
+        double* col = w + pk(posA, c);
+        double x[DA], y[DA];
 #pragma unroll
-    for (int j = 0; j < DA; ++j) w[pk(r, posA + j)] = y[j];
-}
-// W[A, c] <- M_A^T W[A, c] for one column c right of A's block
-template <int DA>
-__device__ __forceinline__ void upd_col(double* w, int c, int posA, const double* MA) {
-    double* col = w + pk(0, c) + posA;
-    double x[DA], y[DA];
+        for (int i = 0; i < DA; ++i) x[i] = col[i];
+        matT_vec<DA>(MA, x, y);
 #pragma unroll
-    for (int i = 0; i < DA; ++i) x[i] = col[i];
-    matT_vec<DA>(MA, x, y);
-#pragma unroll
-    for (int i = 0; i < DA; ++i) col[i] = y[i];
-}
-// joint cell W[A, B] <- M_A^T W[A, B] M_B
-template <int DA, int DB>
-__device__ __forceinline__ void upd_joint(double* w, int posA, int posB, const double* MA, const double* MB) {
-    double t[DA][DB];
-#pragma unroll
-    for (int j = 0; j < DB; ++j) {
-        double cx[DA], cy[DA];
-        const double* col = w + pk(0, posB + j) + posA;
-#pragma unroll
-        for (int i = 0; i < DA; ++i) cx[i] = col[i];
-        matT_vec<DA>(MA, cx, cy);
-#pragma unroll
-        for (int i = 0; i < DA; ++i) t[i][j] = cy[i];
-    }
-#pragma unroll
-    for (int i = 0; i < DA; ++i) {
-        double ry[DB];
-        vec_mat<DB>(t[i], MB, ry);
-#pragma unroll
-        for (int j = 0; j < DB; ++j) w[pk(posA + i, posB + j)] = ry[j];
+        for (int i = 0; i < DA; ++i) col[i] = y[i];
     }
 }
-template <int DA>
-__device__ __forceinline__ void upd_joint_a(double* w, int posA, int posB, int DB, const double* MA, const double* MB) {
-    if (DB == 2) upd_joint<DA, 2>(w, posA, posB, MA, MB);
-    else if (DB == 3) upd_joint<DA, 3>(w, posA, posB, MA, MB);
-    else upd_joint<DA, 4>(w, posA, posB, MA, MB);
+// Columns of pair B: W[r, B] <- W[r, B] M_B for every row r above B's block
+// (lanes over rows), then B's new diagonal block.
+template <int DB>
+__device__ __forceinline__ void cols_pair(double* w, int posB, const double* MBs, const double* Bblk, int lane) {
+    double MB[DB * DB];
+#pragma unroll
+    for (int i = 0; i < DB * DB; ++i) MB[i] = MBs[i];
+    for (int r = lane; r < posB; r += 32) {
+        double x[DB], y[DB];
+#pragma unroll
+        for (int j = 0; j < DB; ++j) x[j] = w[pk(r, posB + j)];
+        vec_mat<DB>(x, MB, y);
+#pragma unroll
+        for (int j = 0; j < DB; ++j) w[pk(r, posB + j)] = y[j];
+    }
+    if (lane < DB * DB) {
+        const int i = lane / DB, j = lane % DB;
+        if (i <= j + 1) w[pk(posB + i, posB + j)] = Bblk[i * DB + j];
+    }
 }
 
-// Window update of one step (see the header): warps [1, NW) of the CTA.
-__device__ __forceinline__ void window_update(WinShared& sh, double* w, int d, int buf, int warp, int lane, int nwarps) {
+__device__ __forceinline__ void rows_phase(WinShared& sh, double* w, int d, int buf, int mbuf, int warp, int lane, int nw) {
     const int np = sh.npairs[buf];
-    for (int pi = warp - 1; pi < np; pi += nwarps - 1) {
+    for (int pi = warp; pi < np; pi += nw) {
         const PairRec pa = sh.pairs[buf][pi];
         if (!pa.ok) continue;
-        const int DA = pa.p + pa.q, posA = pa.pos;
-        const double* MA = sh.M[buf][pi];
-        const int nitems = d - DA;  // rows [0, posA) then columns [posA+DA, d)
-        for (int k = lane; k < nitems; k += 32) {
-            if (k < posA) {
-                // row k, columns of A (a row owned by another swapping pair is
-                // handled there as a joint cell)
-                const int ow = sh.owner[buf][k];
-                if (ow >= 0 && sh.pairs[buf][ow].ok) continue;
-                if (DA == 2) upd_row<2>(w, k, posA, MA);
-                else if (DA == 3) upd_row<3>(w, k, posA, MA);
-                else upd_row<4>(w, k, posA, MA);
-            } else {
-                const int c = k + DA;  // column right of A's block
-                const int ob = sh.owner[buf][c];
-                if (ob >= 0 && sh.pairs[buf][ob].ok) {
-                    const PairRec pb = sh.pairs[buf][ob];
-                    if (c != pb.pos) continue;  // the cell is handled at B's first column
-                    const int DB = pb.p + pb.q;
-                    const double* MB = sh.M[buf][ob];
-                    if (DA == 2) upd_joint_a<2>(w, posA, c, DB, MA, MB);
-                    else if (DA == 3) upd_joint_a<3>(w, posA, c, DB, MA, MB);
-                    else upd_joint_a<4>(w, posA, c, DB, MA, MB);
-                } else {
-                    if (DA == 2) upd_col<2>(w, c, posA, MA);
-                    else if (DA == 3) upd_col<3>(w, c, posA, MA);
-                    else upd_col<4>(w, c, posA, MA);
-                }
-            }
-        }
-        if (lane < DA * DA) {
-            const int i = lane / DA, j = lane % DA;
-            if (i <= j + 1) w[pk(posA + i, posA + j)] = sh.B[pi][i * DA + j];
-        }
+        const int D = pa.p + pa.q;
+        const double* M = sh.M[mbuf][pi];
+        if (D == 2) rows_pair<2>(w, d, pa.pos, M, lane);
+        else if (D == 3) rows_pair<3>(w, d, pa.pos, M, lane);
+        else rows_pair<4>(w, d, pa.pos, M, lane);
+    }
+}
+
+__device__ __forceinline__ void cols_phase(WinShared& sh, double* w, int buf, int mbuf, int warp, int lane, int nw) {
+    const int np = sh.npairs[buf];
+    for (int pi = warp; pi < np; pi += nw) {
+        const PairRec pb = sh.pairs[buf][pi];
+        if (!pb.ok) continue;
+        const int D = pb.p + pb.q;
+        const double* M = sh.M[mbuf][pi];
+        if (D == 2) cols_pair<2>(w, pb.pos, M, sh.B[pi], lane);
+        else if (D == 3) cols_pair<3>(w, pb.pos, M, sh.B[pi], lane);
+        else cols_pair<4>(w, pb.pos, M, sh.B[pi], lane);
     }
 }
 
@@ -324,8 +314,13 @@ __global__ void __launch_bounds__(kWinThreads, 1)
 window_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S, long long lds,
                       double* __restrict__ qw_pool, const uint8_t* __restrict__ sizes_pool,
                       const uint8_t* __restrict__ sel_pool, uint8_t* __restrict__ order_pool,
-                      uint8_t* __restrict__ stuck_pool, int32_t* __restrict__ status) {
+                      uint8_t* __restrict__ stuck_pool, int32_t* __restrict__ status,
+                      unsigned long long* __restrict__ prof) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // optional per-warp phase timing (prof != nullptr): [warp][0] phase-1
+    // busy cycles, [1] phase-2 busy cycles, [2] steps, [3] kernel cycles
+    unsigned long long t_p1 = 0, t_p2 = 0, n_steps = 0;
+    const unsigned long long t_k0 = clock64();
     WinShared& sh = *reinterpret_cast<WinShared*>(smem_raw);
     double* w = reinterpret_cast<double*>(smem_raw + ((sizeof(WinShared) + 15) & ~size_t(15)));
     const WinDesc wd = wins[blockIdx.x];
@@ -344,13 +339,17 @@ window_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S, 
         for (int i = lane; i < len; i += 32) dst[i] = src[i];
     }
     for (int idx = tid; idx < d * d; idx += kWinThreads) acc[idx] = ((idx % d) == (idx / d)) ? 1.0 : 0.0;
+    for (int k = tid; k < d; k += kWinThreads) {
+        sh.acc_lo[k] = (int16_t)k;
+        sh.acc_hi[k] = (int16_t)k;
+    }
     for (int k = tid; k < nb; k += kWinThreads) {
         sh.arr[k] = (uint8_t)k;
         sh.bsz[k] = sizes_pool[wd.blk_off + k];
         sh.bsel[k] = sel_pool[wd.blk_off + k];
         sh.bstuck[k] = 0;
     }
-    if (tid == 0) sh.npairs[0] = sh.npairs[1] = 0;
+    if (tid == 0) sh.npairs[0] = sh.npairs[1] = sh.npairs[2] = 0;
     __syncthreads();
     if (warp == 0) {
         // layout check against the exact-zero subdiagonal (reorder.cpp:132-154)
@@ -374,53 +373,83 @@ window_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S, 
     const bool executed = sh.status & kWinExecuted;
 
     if (executed) {
-        int cur = 0;
+        int cur = 0, mb = 0;  // pair-state buffer (step % 3), M buffer (step % 2)
         bool have_prev = false;
+        if (tid == 0) sh.redo = 0;
+        __syncthreads();
         for (;;) {
             const int np = sh.npairs[cur];
-            // ---- phase 1: decisions of this step || accumulator of the previous step ----
+            const int nxt = (cur + 1) % 3, prv = (cur + 2) % 3;
+            const unsigned long long c0 = clock64();
+            // ---- phase 1: decisions of this step || accumulator of the previous
+            // step; warp 0 also commits the arrangement assuming every swap of
+            // the step succeeds and finds the next step's pairs from it ----
             if (warp < 4) {
                 const int cnt = sh.type_cnt[cur][warp];
                 for (int k = lane; k < cnt; k += 32) {
                     const int pi = sh.type_list[cur][warp][k];
                     PairRec& pr = sh.pairs[cur][pi];
-                    if (warp == 0) decide_givens(w, pr, sh.M[cur][pi], sh.B[pi]);
-                    else if (warp == 1) decide_direct<1, 2>(w, pr, sh.M[cur][pi], sh.B[pi]);
-                    else if (warp == 2) decide_direct<2, 1>(w, pr, sh.M[cur][pi], sh.B[pi]);
-                    else decide_direct<2, 2>(w, pr, sh.M[cur][pi], sh.B[pi]);
+                    if (warp == 0) decide_givens(w, pr, sh.M[mb][pi], sh.B[pi]);
+                    else if (warp == 1) decide_direct<1, 2>(w, pr, sh.M[mb][pi], sh.B[pi]);
+                    else if (warp == 2) decide_direct<2, 1>(w, pr, sh.M[mb][pi], sh.B[pi]);
+                    else decide_direct<2, 2>(w, pr, sh.M[mb][pi], sh.B[pi]);
+                }
+                if (warp == 0) {
+                    for (int pi = lane; pi < np; pi += 32) {
+                        const int s = sh.pairs[cur][pi].slot;
+                        const uint8_t t = sh.arr[s];
+                        sh.arr[s] = sh.arr[s + 1];
+                        sh.arr[s + 1] = t;
+                    }
+                    __syncwarp();
+                    find_pairs(sh, nb, d, nxt, lane);
                 }
             } else if (have_prev) {
-                acc_update(sh, acc, d, cur ^ 1, 4 * 32, kWinThreads - 4 * 32, tid);
+                acc_update(sh, acc, d, prv, mb ^ 1, 4, NW - 4, warp, lane);
+            }
+            const unsigned long long c1 = clock64();
+            __syncthreads();
+            const unsigned long long c2 = clock64();
+            // ---- phase 2a: rows of every accepted pair ----
+            rows_phase(sh, w, d, cur, mb, warp, lane, NW);
+            if (lane == 0) {
+                for (int pi = warp; pi < np; pi += NW)
+                    if (!sh.pairs[cur][pi].ok) sh.redo = 1;
             }
             __syncthreads();
-            // ---- phase 2: window update || commit arrangement + next pairs ----
-            if (warp == 0) {
+            // ---- phase 2b: columns + new diagonal blocks; rare fix-up of a
+            // rejected swap (undo it in the arrangement, stop the block, redo
+            // the next step's pairs) ----
+            cols_phase(sh, w, cur, mb, warp, lane, NW);
+            if (sh.redo && warp == 0) {
                 if (lane == 0) {
                     for (int pi = 0; pi < np; ++pi) {
                         const PairRec pr = sh.pairs[cur][pi];
+                        if (pr.ok) continue;
                         const int s = pr.slot;
-                        if (pr.ok) {
-                            const uint8_t t = sh.arr[s];
-                            sh.arr[s] = sh.arr[s + 1];
-                            sh.arr[s + 1] = t;
-                        } else {
-                            sh.bstuck[sh.arr[s + 1]] = 1;
-                            sh.status |= kWinStuck;
-                        }
+                        const uint8_t t = sh.arr[s];  // undo the optimistic swap
+                        sh.arr[s] = sh.arr[s + 1];
+                        sh.arr[s + 1] = t;
+                        sh.bstuck[sh.arr[s + 1]] = 1;
+                        sh.status |= kWinStuck;
                     }
+                    sh.redo = 0;
                 }
                 __syncwarp();
-                find_pairs(sh, nb, d, cur ^ 1, lane);
-            } else {
-                window_update(sh, w, d, cur, warp, lane, NW);
+                find_pairs(sh, nb, d, nxt, lane);
             }
+            const unsigned long long c3 = clock64();
             __syncthreads();
+            t_p1 += c1 - c0;
+            t_p2 += c3 - c2;
+            ++n_steps;
             have_prev = true;
-            cur ^= 1;
+            cur = nxt;
+            mb ^= 1;
             if (sh.npairs[cur] == 0) break;
         }
         // accumulator of the last step
-        acc_update(sh, acc, d, cur ^ 1, 0, kWinThreads, tid);
+        acc_update(sh, acc, d, (cur + 2) % 3, mb ^ 1, 0, NW, warp, lane);
         __syncthreads();
     }
 
@@ -441,6 +470,13 @@ window_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S, 
     double* qw = qw_pool + wd.qw_off;
     for (int idx = tid; idx < d * d; idx += kWinThreads) qw[idx] = acc[idx];
     if (tid == 0) status[blockIdx.x] = st;
+    if (prof && lane == 0) {
+        unsigned long long* pw = prof + (blockIdx.x * (size_t)NW + warp) * 4;
+        pw[0] = t_p1;
+        pw[1] = t_p2;
+        pw[2] = n_steps;
+        pw[3] = clock64() - t_k0;
+    }
 }
 
 size_t window_reorder_smem_bytes(int dmax) {
@@ -451,7 +487,7 @@ size_t window_reorder_smem_bytes(int dmax) {
 cudaError_t launch_window_reorder(const WinDesc* wins, int nwin, int dmax, double* S, long long lds,
                                   double* qw_pool, const uint8_t* sizes_pool, const uint8_t* sel_pool,
                                   uint8_t* order_pool, uint8_t* stuck_pool, int32_t* status,
-                                  cudaStream_t stream) {
+                                  cudaStream_t stream, unsigned long long* prof) {
     if (nwin <= 0) return cudaSuccess;
     const size_t smem = window_reorder_smem_bytes(dmax);
     static size_t configured = 0;
@@ -462,7 +498,7 @@ cudaError_t launch_window_reorder(const WinDesc* wins, int nwin, int dmax, doubl
         configured = smem;
     }
     window_reorder_kernel<<<nwin, kWinThreads, smem, stream>>>(wins, S, lds, qw_pool, sizes_pool, sel_pool,
-                                                               order_pool, stuck_pool, status);
+                                                               order_pool, stuck_pool, status, prof);
     return cudaGetLastError();
 }
 
