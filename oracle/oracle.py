@@ -91,8 +91,37 @@ def lib():
         L.teo_plan_free.restype = None
         L.teo_plan_flops.argtypes = [_P, _SZ, C.c_int]
         L.teo_plan_flops.restype = _D
+        L.teo_small_schur.argtypes = [_SZ, _P, _P, _P]
+        L.teo_small_schur.restype = C.c_int
+        L.teo_deflation_check.argtypes = [_D, _D, C.c_int, _D]
+        L.teo_deflation_check.restype = C.c_int
+        L.teo_aed_step.argtypes = [_SZ, _P, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _P, _P, _P]
+        L.teo_aed_step.restype = C.c_int
+        L.teo_sweep.argtypes = [_SZ, _P, _SZ, _P, _SZ, _SZ, _SZ, _SZ, _P, _SZ]
+        L.teo_sweep.restype = C.c_int
+        L.teo_schur_reduce.argtypes = [_SZ, _P, _SZ, _P, _SZ, _SZ, _P, _P, _P]
+        L.teo_schur_reduce.restype = C.c_int
         _lib = L
     return _lib
+
+
+class SchurOpts(C.Structure):
+    """teo_schur_opts == SchurOptions (schur.hpp:20-29)."""
+    _fields_ = [("deflation", C.c_int), ("shift_count", _SZ), ("aed_window", _SZ),
+                ("iteration_limit", _SZ), ("small_threshold", _SZ)]
+
+
+class AedOut(C.Structure):
+    _fields_ = [("window", _SZ), ("deflated", _SZ), ("nshifts", _SZ), ("spike_eliminated", C.c_int),
+                ("converged", C.c_int), ("swap_rejected", C.c_int), ("newbeta", _D)]
+
+
+class SchurInfo(C.Structure):
+    _fields_ = [("sweeps", _SZ), ("rounds", _SZ), ("converged_trailing", _SZ), ("converged", C.c_int)]
+
+
+def schur_opts(deflation=1, shift_count=0, aed_window=0, iteration_limit=0, small_threshold=64):
+    return SchurOpts(deflation, shift_count, aed_window, iteration_limit, small_threshold)
 
 
 def ref_available() -> bool:
@@ -469,3 +498,58 @@ def ref_similarity_residual(a_rm, q_rm, s_rm) -> float:
 def ref_orthogonality_defect(q_rm) -> float:
     q_rm = np.ascontiguousarray(q_rm)
     return ref().ref_orthogonality_defect(q_rm.shape[0], _ptr(q_rm))
+
+
+# --------------------------------------------------------------------------
+# Schur reduction path (restatement of schur.cpp / kernels.cpp:223-381)
+
+def small_schur(h: np.ndarray):
+    """small_schur on a Fortran k x k array in place; returns (ok, q, sweeps)."""
+    assert h.flags.f_contiguous
+    k = h.shape[0]
+    q = np.zeros((k, k), order="F")
+    sw = _SZ(0)
+    ok = lib().teo_small_schur(k, _ptr(h), _ptr(q), C.byref(sw))
+    return bool(ok), q, sw.value
+
+
+def deflation_check(spike, diag_sum, norm_stable, wnorm) -> bool:
+    return bool(lib().teo_deflation_check(spike, diag_sum, int(norm_stable), wnorm))
+
+
+def aed_step(h: np.ndarray, q, l, ihi, window, **opts):
+    """aed_step (schur.cpp:599-609) on Fortran arrays in place."""
+    n = h.shape[0]
+    assert h.flags.f_contiguous and (q is None or q.flags.f_contiguous)
+    o = schur_opts(**opts)
+    r = AedOut()
+    sh = np.zeros(2 * n + 4)
+    rc = lib().teo_aed_step(n, _ptr(h), n, _ptr(q), n, l, ihi, window, C.byref(o), C.byref(r), _ptr(sh))
+    if rc:
+        raise ValueError("aed_step: bad arguments")
+    ns = r.nshifts
+    return dict(window=r.window, deflated=r.deflated, spike_eliminated=bool(r.spike_eliminated),
+                converged=bool(r.converged), swap_rejected=bool(r.swap_rejected),
+                shifts=sh[0:2 * ns:2] + 1j * sh[1:2 * ns:2])
+
+
+def sweep(h: np.ndarray, q, l, ihi, shifts, window_size):
+    """introduce_bulges + chase_bulges (schur.cpp:611-669) in place."""
+    n = h.shape[0]
+    sh = np.zeros(2 * len(shifts))
+    sh[0::2] = np.real(shifts)
+    sh[1::2] = np.imag(shifts)
+    if lib().teo_sweep(n, _ptr(h), n, _ptr(q), n, l, ihi, len(shifts), _ptr(sh), window_size):
+        raise ValueError("sweep: bad arguments")
+
+
+def schur_reduce(h: np.ndarray, q=None, tile=0, **opts):
+    """Serial schur_reduce (schur.cpp:671-906) in place on Fortran arrays."""
+    n = h.shape[0]
+    assert h.flags.f_contiguous and (q is None or q.flags.f_contiguous)
+    o = schur_opts(**opts)
+    info = SchurInfo()
+    eig = np.zeros(2 * n)
+    lib().teo_schur_reduce(n, _ptr(h), n, _ptr(q), n, tile, C.byref(o), _ptr(eig), C.byref(info))
+    return dict(eigenvalues=eig[:n] + 1j * eig[n:], sweeps=info.sweeps, converged=bool(info.converged),
+                converged_trailing=info.converged_trailing)

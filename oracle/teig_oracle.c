@@ -1045,3 +1045,816 @@ void teo_read_eigenvalues(size_t n, const double* s, size_t ld, double* re, doub
         }
     }
 }
+
+/* ======================================================================= */
+/* Schur reduction path: small_schur (kernels.cpp:223-381), multishift QR   */
+/* with AED (schur.cpp:29-399), the tiled driver (schur.cpp:406-906).       */
+/* The reference's task graphs have serial semantics (runtime.hpp:79-82):   */
+/* every window op is followed by its L/R/Q updates in insertion order,     */
+/* which is what the serial restatement below executes.                     */
+
+/* general-length make_reflector (kernels.cpp:24-58); v[len], returns beta */
+static double make_refl_n(const double* x, size_t len, double* v, double* tau) {
+    *tau = 0.0;
+    for (size_t i = 0; i < len; ++i) v[i] = 0.0;
+    if (len == 0) return 0.0;
+    v[0] = 1.0;
+    if (len == 1) return x[0];
+    const double alpha = x[0];
+    const double tail = nrm2(len - 1, x + 1);
+    if (tail == 0.0) return alpha == 0.0 ? 0.0 : alpha;
+    double beta = -sgn(alpha) * hypot(alpha, tail);
+    double* tl = (double*)malloc((len - 1) * sizeof(double));
+    for (size_t i = 1; i < len; ++i) tl[i - 1] = x[i];
+    double a = alpha, t;
+    int rescale = 0;
+    while (fabs(beta) < SAFMIN / EPS && rescale < 20) {
+        const double big = 1.0 / (SAFMIN / EPS);
+        for (size_t i = 0; i + 1 < len; ++i) tl[i] *= big;
+        a *= big;
+        t = nrm2(len - 1, tl);
+        beta = -sgn(a) * hypot(a, t);
+        ++rescale;
+    }
+    *tau = (beta - a) / beta;
+    const double inv = 1.0 / (a - beta);
+    for (size_t i = 1; i < len; ++i) v[i] = tl[i - 1] * inv;
+    for (int r = 0; r < rescale; ++r) beta *= SAFMIN / EPS;
+    free(tl);
+    return beta;
+}
+
+/* apply_reflector_left / _right (kernels.cpp:60-82) for general length */
+static void rl_n(double* a, size_t ld, const double* v, double tau, size_t len, size_t r0,
+                 size_t c0, size_t c1) {
+    if (tau == 0.0) return;
+    for (size_t j = c0; j < c1; ++j) {
+        double w = 0.0;
+        for (size_t i = 0; i < len; ++i) w += v[i] * A_(a, r0 + i, j, ld);
+        w *= tau;
+        for (size_t i = 0; i < len; ++i) A_(a, r0 + i, j, ld) -= w * v[i];
+    }
+}
+static void rr_n(double* a, size_t ld, const double* v, double tau, size_t len, size_t c0,
+                 size_t r0, size_t r1) {
+    if (tau == 0.0) return;
+    for (size_t i = r0; i < r1; ++i) {
+        double w = 0.0;
+        for (size_t j = 0; j < len; ++j) w += A_(a, i, c0 + j, ld) * v[j];
+        w *= tau;
+        for (size_t j = 0; j < len; ++j) A_(a, i, c0 + j, ld) -= w * v[j];
+    }
+}
+
+static void set_identity(size_t n, double* q, size_t ld) {
+    for (size_t j = 0; j < n; ++j)
+        for (size_t i = 0; i < n; ++i) A_(q, i, j, ld) = (i == j) ? 1.0 : 0.0;
+}
+
+/* standardize_block_at (kernels.cpp:245-256) == standardize_block_dense
+ * (schur.cpp:82-94): h n x n (ld), q qr x n (ld ldq) */
+static void std_block(size_t n, double* h, size_t ld, size_t qr, double* q, size_t ldq,
+                      size_t p) {
+    double st[10];
+    teo_standardize_2x2(A_(h, p, p, ld), A_(h, p, p + 1, ld), A_(h, p + 1, p, ld),
+                        A_(h, p + 1, p + 1, ld), st);
+    rot_rows(h, ld, st[0], st[1], p, p + 1, p + 2, n);
+    rot_cols(h, ld, st[0], st[1], p, p + 1, 0, p);
+    A_(h, p, p, ld) = st[2];
+    A_(h, p, p + 1, ld) = st[3];
+    A_(h, p + 1, p, ld) = st[4];
+    A_(h, p + 1, p + 1, ld) = st[5];
+    rot_cols(q, ldq, st[0], st[1], p, p + 1, 0, qr);
+}
+
+static size_t scan_active(size_t n, double* h, size_t ld, size_t ihi, double hnorm) {
+    const double smlnum = SAFMIN * ((double)n / EPS);
+    size_t l = ihi - 1;
+    while (l > 0) {
+        double tst = fabs(A_(h, l - 1, l - 1, ld)) + fabs(A_(h, l, l, ld));
+        if (tst == 0.0) tst = hnorm;
+        if (fabs(A_(h, l, l - 1, ld)) <= fmax(EPS * tst, smlnum)) {
+            A_(h, l, l - 1, ld) = 0.0;
+            break;
+        }
+        --l;
+    }
+    return l;
+}
+
+static double hess_norm(size_t n, const double* h, size_t ld) {
+    double hn = 0.0;
+    for (size_t j = 0; j < n; ++j)
+        for (size_t i = 0; i <= (j + 1 < n - 1 ? j + 1 : n - 1); ++i) hn = fmax(hn, fabs(A_(h, i, j, ld)));
+    return hn;
+}
+
+int teo_small_schur(size_t n, double* h, double* q, size_t* sweeps_out) {
+    set_identity(n, q, n);
+    size_t sweeps = 0;
+    if (sweeps_out) *sweeps_out = 0;
+    if (n <= 1) return 1;
+    const double hnorm = hess_norm(n, h, n);
+    if (hnorm == 0.0) return 1;
+    const size_t max_sweeps = 30 * n;
+    size_t ihi = n, its = 0;
+    while (ihi > 0) {
+        if (ihi == 1) {
+            ihi = 0;
+            its = 0;
+            continue;
+        }
+        const size_t l = scan_active(n, h, n, ihi, hnorm);
+        if (l == ihi - 1) {
+            ihi = l;
+            its = 0;
+            continue;
+        }
+        if (l == ihi - 2) {
+            std_block(n, h, n, n, q, n, l);
+            ihi = l;
+            its = 0;
+            continue;
+        }
+        ++its;
+        ++sweeps;
+        if (sweeps_out) *sweeps_out = sweeps;
+        if (sweeps > max_sweeps) return 0;
+        double s11, s12, s21, s22;
+        if (its % 10 == 0) {
+            const double sp = fabs(A_(h, ihi - 1, ihi - 2, n)) +
+                              ((ihi >= l + 3) ? fabs(A_(h, ihi - 2, ihi - 3, n)) : 0.0);
+            s11 = 0.75 * sp + A_(h, ihi - 1, ihi - 1, n);
+            s12 = -0.4375 * sp;
+            s21 = sp;
+            s22 = s11;
+        } else {
+            s11 = A_(h, ihi - 2, ihi - 2, n);
+            s12 = A_(h, ihi - 2, ihi - 1, n);
+            s21 = A_(h, ihi - 1, ihi - 2, n);
+            s22 = A_(h, ihi - 1, ihi - 1, n);
+        }
+        const double ssum = s11 + s22, sprod = s11 * s22 - s12 * s21;
+        double v[3];
+        {
+            const double a11 = A_(h, l, l, n), a12 = A_(h, l, l + 1, n);
+            const double a21 = A_(h, l + 1, l, n), a22 = A_(h, l + 1, l + 1, n);
+            const double a32 = A_(h, l + 2, l + 1, n);
+            v[0] = a11 * a11 + a12 * a21 - ssum * a11 + sprod;
+            v[1] = a21 * (a11 + a22 - ssum);
+            v[2] = a21 * a32;
+            const double vm = fmax(fabs(v[0]), fmax(fabs(v[1]), fabs(v[2])));
+            if (vm != 0.0) {
+                v[0] /= vm;
+                v[1] /= vm;
+                v[2] /= vm;
+            }
+        }
+        for (size_t i = l; i + 3 <= ihi; ++i) {
+            double w[3], rv[3], tau;
+            if (i == l) {
+                w[0] = v[0];
+                w[1] = v[1];
+                w[2] = v[2];
+            } else {
+                w[0] = A_(h, i, i - 1, n);
+                w[1] = A_(h, i + 1, i - 1, n);
+                w[2] = A_(h, i + 2, i - 1, n);
+            }
+            const double beta = make_refl_n(w, 3, rv, &tau);
+            if (i > l) {
+                A_(h, i, i - 1, n) = beta;
+                A_(h, i + 1, i - 1, n) = 0.0;
+                A_(h, i + 2, i - 1, n) = 0.0;
+            }
+            rl_n(h, n, rv, tau, 3, i, i, n);
+            rr_n(h, n, rv, tau, 3, i, 0, (i + 4 < ihi ? i + 4 : ihi));
+            rr_n(q, n, rv, tau, 3, i, 0, n);
+        }
+        {
+            const size_t i = ihi - 2;
+            double w[2] = {A_(h, i, i - 1, n), A_(h, i + 1, i - 1, n)}, rv[2], tau;
+            const double beta = make_refl_n(w, 2, rv, &tau);
+            A_(h, i, i - 1, n) = beta;
+            A_(h, i + 1, i - 1, n) = 0.0;
+            rl_n(h, n, rv, tau, 2, i, i, n);
+            rr_n(h, n, rv, tau, 2, i, 0, ihi);
+            rr_n(q, n, rv, tau, 2, i, 0, n);
+        }
+    }
+    return 1;
+}
+
+/* shift_vector (schur.cpp:29-43) on the window whose (0,0) is h(o,o) */
+static void shift_vec(const double* w, size_t ld, size_t rows, size_t o, double ssum, double sprod,
+                      double v[3]) {
+    const double a11 = A_(w, o, o, ld), a12 = A_(w, o, o + 1, ld);
+    const double a21 = A_(w, o + 1, o, ld), a22 = A_(w, o + 1, o + 1, ld);
+    const double a32 = (rows > 2) ? A_(w, o + 2, o + 1, ld) : 0.0;
+    v[0] = a11 * a11 + a12 * a21 - ssum * a11 + sprod;
+    v[1] = a21 * (a11 + a22 - ssum);
+    v[2] = a21 * a32;
+    const double vm = fmax(fabs(v[0]), fmax(fabs(v[1]), fabs(v[2])));
+    if (vm != 0.0) {
+        v[0] /= vm;
+        v[1] /= vm;
+        v[2] /= vm;
+    }
+}
+
+/* chase_one_step (schur.cpp:48-63): w d x d (ld d) spans [a, b); acc d x d */
+static size_t chase_step(double* w, double* acc, size_t a, size_t b, size_t ihi, size_t r) {
+    const size_t d = b - a;
+    const size_t len = (ihi - r < 3) ? ihi - r : 3;
+    if (len < 2 || r + 1 >= ihi) return ihi - 1;
+    const size_t ri = r - a;
+    double col[3], v[3], tau;
+    for (size_t i = 0; i < len; ++i) col[i] = A_(w, ri + i, ri - 1, d);
+    const double beta = make_refl_n(col, len, v, &tau);
+    A_(w, ri, ri - 1, d) = beta;
+    for (size_t i = 1; i < len; ++i) A_(w, ri + i, ri - 1, d) = 0.0;
+    rl_n(w, d, v, tau, len, ri, ri, d);
+    rr_n(w, d, v, tau, len, ri, 0, (ri + len + 1 < d ? ri + len + 1 : d));
+    rr_n(acc, d, v, tau, len, ri, 0, d);
+    return r + 1;
+}
+
+/* introduce_one_bulge (schur.cpp:67-78) */
+static void intro_bulge(double* w, double* acc, size_t d, double ssum, double sprod) {
+    double sv[3], v[3], tau;
+    shift_vec(w, d, d, 0, ssum, sprod, sv);
+    const size_t len = d < 3 ? d : 3;
+    (void)make_refl_n(sv, len, v, &tau);
+    rl_n(w, d, v, tau, len, 0, 0, d);
+    rr_n(w, d, v, tau, len, 0, 0, (len + 1 < d ? len + 1 : d));
+    rr_n(acc, d, v, tau, len, 0, 0, d);
+}
+
+static size_t default_shift_count(size_t active) { /* schur.cpp:119-129 */
+    size_t m = (active / 16) & ~(size_t)1;
+    if (m < 4) m = 4;
+    if (m > 64) m = 64;
+    if (3 * (m / 2) + 2 > active) {
+        const size_t nb = (active >= 6) ? (active - 2) / 3 : 1;
+        m = 2 * nb;
+        if (m < 2) m = 2;
+        if (m > 64) m = 64;
+    }
+    return m;
+}
+
+/* pick_shifts (schur.cpp:97-117); sh/out: (re, im) pairs */
+static size_t pick_shifts(const double* sh, size_t nh, size_t m_max, double* out) {
+    size_t no = 0, nr = 0;
+    double* reals = (double*)malloc((nh + 1) * sizeof(double));
+    for (size_t i = 0; i < nh && no + 1 < m_max + 1; ++i) {
+        const double re = sh[2 * i], im = sh[2 * i + 1];
+        if (im > 0.0) {
+            if (no + 2 <= m_max) {
+                out[2 * no] = re;
+                out[2 * no + 1] = im;
+                out[2 * no + 2] = re;
+                out[2 * no + 3] = -im;
+                no += 2;
+            }
+        } else if (im == 0.0) {
+            reals[nr++] = re;
+        }
+    }
+    for (size_t i = 0; i + 1 < nr && no + 2 <= m_max; i += 2) {
+        out[2 * no] = reals[i];
+        out[2 * no + 1] = 0.0;
+        out[2 * no + 2] = reals[i + 1];
+        out[2 * no + 3] = 0.0;
+        no += 2;
+    }
+    free(reals);
+    return no;
+}
+
+int teo_deflation_check(double spike, double diag_sum, int norm_stable, double wnorm) {
+    if (!norm_stable) return spike <= fmax(EPS * diag_sum, SAFMIN); /* schur.cpp:406-411 */
+    return spike <= EPS * wnorm;
+}
+
+/* apply_similarity_dense (schur.cpp:252-282): h n x n, q n x n (or NULL) */
+static void similarity_dense(size_t n, double* h, size_t ldh, size_t qr, double* q, size_t ldq,
+                             size_t a, size_t b, const double* acc) {
+    const size_t d = b - a;
+    double* scratch = (double*)malloc(2 * d * (n > qr ? n : qr) * sizeof(double) + 16);
+    if (b < n) update_left(n, h, ldh, a, b, acc, scratch);
+    if (a > 0) update_right(a, h, ldh, a, b, acc, scratch);
+    if (q) update_right(qr, q, ldq, a, b, acc, scratch);
+    free(scratch);
+}
+
+static int mshift_dense(size_t n, double* h, double* q, const teo_schur_opts* o, int depth);
+
+/* aed_process_window (schur.cpp:147-248): s (w x w, ld w) is transformed in
+ * place; qw (w x w) receives the window similarity. */
+static void aed_core(size_t w, double* s, double* qw, double beta, const teo_schur_opts* o,
+                     int depth, teo_aed_out* r, double* shifts) {
+    memset(r, 0, sizeof *r);
+    r->converged = 1;
+    const double wnorm = nrm2(w * w, s);
+    if (w <= o->small_threshold || depth >= 8) {
+        size_t sw;
+        r->converged = teo_small_schur(w, s, qw, &sw);
+    } else {
+        set_identity(w, qw, w);
+        r->converged = mshift_dense(w, s, qw, o, depth + 1);
+    }
+    if (!r->converged) return;
+    if (beta == 0.0) {
+        r->deflated = w;
+        r->newbeta = 0.0;
+        r->spike_eliminated = 1;
+        return;
+    }
+    size_t ktop = 0, ns = w;
+    while (ns > ktop) {
+        const size_t bsize = (ns >= 2 && ns - 2 >= ktop && A_(s, ns - 1, ns - 2, w) != 0.0) ? 2 : 1;
+        const size_t bs = ns - bsize;
+        double spike = 0.0, dsum = 0.0;
+        for (size_t rr = bs; rr < ns; ++rr) {
+            spike = fmax(spike, fabs(beta * A_(qw, 0, rr, w)));
+            dsum += fabs(A_(s, rr, rr, w));
+        }
+        if (teo_deflation_check(spike, dsum, o->deflation, wnorm)) {
+            ns = bs;
+        } else {
+            size_t cur = bs;
+            int stuck = 0;
+            while (cur > ktop) {
+                const size_t psize =
+                    (cur >= 2 && cur - 2 >= ktop && A_(s, cur - 1, cur - 2, w) != 0.0) ? 2 : 1;
+                const size_t ps = cur - psize;
+                if (teo_swap_adjacent_blocks(w, s, w, qw, ps, psize, bsize)) {
+                    stuck = 1;
+                    break;
+                }
+                cur = ps;
+            }
+            if (stuck) {
+                r->swap_rejected = 1;
+                break;
+            }
+            ktop += bsize;
+        }
+    }
+    r->deflated = w - ns;
+    size_t nsh = 0;
+    for (size_t i = 0; i < ns;) {
+        if (i + 1 < ns && A_(s, i + 1, i, w) != 0.0) {
+            const double a = A_(s, i, i, w), b = A_(s, i, i + 1, w), c = A_(s, i + 1, i, w);
+            const double im = sqrt(fabs(b)) * sqrt(fabs(c));
+            shifts[2 * nsh] = a;
+            shifts[2 * nsh + 1] = im;
+            shifts[2 * nsh + 2] = a;
+            shifts[2 * nsh + 3] = -im;
+            nsh += 2;
+            i += 2;
+        } else {
+            shifts[2 * nsh] = A_(s, i, i, w);
+            shifts[2 * nsh + 1] = 0.0;
+            nsh += 1;
+            i += 1;
+        }
+    }
+    r->nshifts = nsh;
+    if (ns == 0) {
+        r->newbeta = 0.0;
+    } else if (ns == 1) {
+        r->newbeta = beta * A_(qw, 0, 0, w);
+    } else {
+        double* spk = (double*)malloc(ns * sizeof(double));
+        double* v = (double*)malloc(ns * sizeof(double));
+        double tau;
+        for (size_t i = 0; i < ns; ++i) spk[i] = beta * A_(qw, 0, i, w);
+        r->newbeta = make_refl_n(spk, ns, v, &tau);
+        rl_n(s, w, v, tau, ns, 0, 0, w);
+        rr_n(s, w, v, tau, ns, 0, 0, ns);
+        rr_n(qw, w, v, tau, ns, 0, 0, w);
+        for (size_t j = 0; j + 2 < ns; ++j) {
+            const size_t len = ns - j - 1;
+            double hb;
+            for (size_t i = j + 1; i < ns; ++i) spk[i - j - 1] = A_(s, i, j, w);
+            hb = make_refl_n(spk, len, v, &tau);
+            if (tau == 0.0) continue;
+            A_(s, j + 1, j, w) = hb;
+            for (size_t i = j + 2; i < ns; ++i) A_(s, i, j, w) = 0.0;
+            rl_n(s, w, v, tau, len, j + 1, j + 1, w);
+            rr_n(s, w, v, tau, len, j + 1, 0, ns);
+            rr_n(qw, w, v, tau, len, j + 1, 0, w);
+        }
+        free(spk);
+        free(v);
+    }
+    r->spike_eliminated = 1;
+}
+
+static void gather(const double* h, size_t ld, size_t r0, size_t c0, size_t m, double* w) {
+    for (size_t j = 0; j < m; ++j)
+        for (size_t i = 0; i < m; ++i) A_(w, i, j, m) = A_(h, r0 + i, c0 + j, ld);
+}
+static void scatter(double* h, size_t ld, size_t r0, size_t c0, size_t m, const double* w) {
+    for (size_t j = 0; j < m; ++j)
+        for (size_t i = 0; i < m; ++i) A_(h, r0 + i, c0 + j, ld) = A_(w, i, j, m);
+}
+
+/* multishift_schur_dense (schur.cpp:304-399): h, q n x n (ld n) */
+static int mshift_dense(size_t n, double* h, double* q, const teo_schur_opts* o, int depth) {
+    if (n <= 1) return 1;
+    const double hnorm = hess_norm(n, h, n);
+    const size_t limit = 30 * n;
+    size_t sweeps = 0, stagnation = 0, ihi = n;
+    int ok = 1;
+    double* win = (double*)malloc(n * n * sizeof(double));
+    double* qw = (double*)malloc(n * n * sizeof(double));
+    double* sh = (double*)malloc(2 * (n + 2) * sizeof(double));
+    double* picked = (double*)malloc(2 * (n + 70) * sizeof(double));
+    while (ihi > 0) {
+        if (ihi == 1) {
+            ihi = 0;
+            continue;
+        }
+        const size_t l = scan_active(n, h, n, ihi, hnorm);
+        const size_t active = ihi - l;
+        if (active == 1) {
+            ihi = l;
+            continue;
+        }
+        if (active == 2) {
+            std_block(n, h, n, n, q, n, l);
+            ihi = l;
+            continue;
+        }
+        if (active <= o->small_threshold || depth >= 8) {
+            gather(h, n, l, l, active, win);
+            if (!teo_small_schur(active, win, qw, NULL)) {
+                ok = 0;
+                break;
+            }
+            scatter(h, n, l, l, active, win);
+            similarity_dense(n, h, n, n, q, n, l, ihi, qw);
+            ihi = l;
+            continue;
+        }
+        const size_t m = o->shift_count ? o->shift_count : default_shift_count(active);
+        size_t w = o->aed_window ? o->aed_window : (3 * m) / 2;
+        if (w < 4) w = 4;
+        if (w > active) w = active;
+        const size_t e = ihi - w;
+        gather(h, n, e, e, w, win);
+        const double beta = (e > l) ? A_(h, e, e - 1, n) : 0.0;
+        teo_aed_out core;
+        aed_core(w, win, qw, beta, o, depth + 1, &core, sh);
+        if (!core.converged) {
+            ok = 0;
+            break;
+        }
+        scatter(h, n, e, e, w, win);
+        if (e > l) A_(h, e, e - 1, n) = core.newbeta;
+        similarity_dense(n, h, n, n, q, n, e, ihi, qw);
+        stagnation = (core.deflated == 0) ? stagnation + 1 : 0;
+        ihi -= core.deflated;
+        if (core.deflated > 0 && 100 * core.deflated >= 14 * w) continue;
+        if (ihi - l < 4) continue;
+        size_t np = pick_shifts(sh, core.nshifts, m, picked);
+        if (stagnation >= 6 || np < 2) {
+            const double sp = fabs(A_(h, ihi - 1, ihi - 2, n)) +
+                              ((ihi >= l + 3) ? fabs(A_(h, ihi - 2, ihi - 3, n)) : 0.0);
+            const double h11 = 0.75 * sp + A_(h, ihi - 1, ihi - 1, n);
+            double st[10];
+            teo_standardize_2x2(h11, -0.4375 * sp, sp, h11, st);
+            picked[0] = st[6];
+            picked[1] = st[7];
+            picked[2] = st[8];
+            picked[3] = st[9];
+            np = 2;
+            stagnation = 0;
+        }
+        if (++sweeps > limit) {
+            ok = 0;
+            break;
+        }
+        const size_t nb = (np / 2 < (ihi - l - 2) / 3) ? np / 2 : (ihi - l - 2) / 3;
+        if (nb == 0) continue;
+        const size_t aw = ihi - l;
+        gather(h, n, l, l, aw, win);
+        set_identity(aw, qw, aw);
+        size_t* pos = (size_t*)malloc(nb * sizeof(size_t));
+        for (size_t j = 0; j < nb; ++j) {
+            /* (s1 + s2).real(), (s1 * s2).real() */
+            const double ssum = picked[4 * j] + picked[4 * j + 2];
+            const double sprod = picked[4 * j] * picked[4 * j + 2] - picked[4 * j + 1] * picked[4 * j + 3];
+            intro_bulge(win, qw, aw, ssum, sprod);
+            size_t r = l + 1;
+            const size_t target = l + 1 + 3 * (nb - 1 - j);
+            while (r < target) r = chase_step(win, qw, l, ihi, ihi, r);
+            pos[j] = target;
+        }
+        for (size_t j = 0; j < nb; ++j) {
+            size_t r = pos[j];
+            while (r < ihi - 1) r = chase_step(win, qw, l, ihi, ihi, r);
+        }
+        free(pos);
+        scatter(h, n, l, l, aw, win);
+        similarity_dense(n, h, n, n, q, n, l, ihi, qw);
+    }
+    free(win);
+    free(qw);
+    free(sh);
+    free(picked);
+    return ok;
+}
+
+/* ---- tiled driver, serial semantics ------------------------------------ */
+
+typedef struct {
+    size_t n;
+    double* h;
+    size_t ldh;
+    double* q;
+    size_t ldq;
+    double* scratch;
+} teo_mat;
+
+/* apply_window_updates (window_tasks.cpp:89-102) */
+static void win_updates(teo_mat* M, size_t a, size_t b, const double* acc) {
+    if (b < M->n) update_left(M->n, M->h, M->ldh, a, b, acc, M->scratch);
+    if (a > 0) update_right(a, M->h, M->ldh, a, b, acc, M->scratch);
+    if (M->q) update_right(M->n, M->q, M->ldq, a, b, acc, M->scratch);
+}
+
+/* insert_aed_tasks' window task + updates (schur.cpp:421-459) */
+static void aed_round(teo_mat* M, size_t l, size_t ihi, size_t w, const teo_schur_opts* o,
+                      teo_aed_out* r, double* shifts) {
+    const size_t e = ihi - w;
+    double* win = (double*)malloc(w * w * sizeof(double));
+    double* qw = (double*)malloc(w * w * sizeof(double));
+    gather(M->h, M->ldh, e, e, w, win);
+    const double beta = (e > l) ? A_(M->h, e, e - 1, M->ldh) : 0.0;
+    aed_core(w, win, qw, beta, o, 0, r, shifts);
+    r->window = w;
+    if (!r->converged) {
+        set_identity(w, qw, w);
+    } else {
+        scatter(M->h, M->ldh, e, e, w, win);
+        if (e > l) A_(M->h, e, e - 1, M->ldh) = r->newbeta;
+    }
+    win_updates(M, e, ihi, qw);
+    free(win);
+    free(qw);
+}
+
+int teo_aed_step(size_t n, double* h, size_t ldh, double* q, size_t ldq, size_t l, size_t ihi,
+                 size_t window, const teo_schur_opts* o, teo_aed_out* r, double* shifts) {
+    if (window < 4 || ihi > n || l >= ihi) return -1;
+    if (window > ihi - l) window = ihi - l;
+    teo_mat M = {n, h, ldh, q, ldq, (double*)malloc(2 * window * n * sizeof(double) + 16)};
+    aed_round(&M, l, ihi, window, o, r, shifts);
+    free(M.scratch);
+    return 0;
+}
+
+/* plan_chase + run_chase_window (schur.cpp:484-523), executed in order */
+static int chase_chain(teo_mat* M, size_t* positions, size_t npos, size_t ihi, size_t cw) {
+    double* w = (double*)malloc(cw * cw * sizeof(double));
+    double* acc = (double*)malloc(cw * cw * sizeof(double));
+    while (npos) {
+        const size_t p_top = positions[npos - 1], p_bot = positions[0];
+        const size_t a = p_top - 1;
+        const size_t b = (a + cw < ihi) ? a + cw : ihi;
+        const int final = (b == ihi);
+        size_t hop = 0;
+        if (!final) {
+            hop = (b >= p_bot + 4) ? (b - 4 - p_bot) : 0;
+            if (hop == 0) {
+                free(w);
+                free(acc);
+                return -1;
+            }
+        }
+        const size_t d = b - a;
+        gather(M->h, M->ldh, a, a, d, w);
+        set_identity(d, acc, d);
+        for (size_t j = 0; j < npos; ++j) {
+            size_t r = positions[j];
+            if (final) {
+                while (r < ihi - 1) r = chase_step(w, acc, a, b, ihi, r);
+            } else {
+                for (size_t s = 0; s < hop; ++s) r = chase_step(w, acc, a, b, ihi, r);
+            }
+        }
+        scatter(M->h, M->ldh, a, a, d, w);
+        win_updates(M, a, b, acc);
+        if (final) npos = 0;
+        else
+            for (size_t j = 0; j < npos; ++j) positions[j] += hop;
+    }
+    free(w);
+    free(acc);
+    return 0;
+}
+
+/* introduce_bulges' window (schur.cpp:628-647 / 851-866); positions out,
+ * bottom first */
+static void intro_window(teo_mat* M, size_t l, size_t ihi, size_t nb, const double* sh,
+                         size_t* positions) {
+    const size_t wi = (l + 3 * nb + 2 < ihi) ? l + 3 * nb + 2 : ihi;
+    const size_t d = wi - l;
+    double* w = (double*)malloc(d * d * sizeof(double));
+    double* acc = (double*)malloc(d * d * sizeof(double));
+    gather(M->h, M->ldh, l, l, d, w);
+    set_identity(d, acc, d);
+    for (size_t j = 0; j < nb; ++j) {
+        const double ssum = sh[4 * j] + sh[4 * j + 2];
+        const double sprod = sh[4 * j] * sh[4 * j + 2] - sh[4 * j + 1] * sh[4 * j + 3];
+        intro_bulge(w, acc, d, ssum, sprod);
+        size_t r = l + 1;
+        const size_t target = l + 1 + 3 * (nb - 1 - j);
+        while (r < target) r = chase_step(w, acc, l, wi, ihi, r);
+        positions[j] = target; /* decreasing in j: already bottom first */
+    }
+    scatter(M->h, M->ldh, l, l, d, w);
+    win_updates(M, l, wi, acc);
+    free(w);
+    free(acc);
+}
+
+int teo_sweep(size_t n, double* h, size_t ldh, double* q, size_t ldq, size_t l, size_t ihi,
+              size_t nshifts, const double* shifts, size_t window_size) {
+    if (nshifts < 2 || nshifts % 2 || l + 3 * (nshifts / 2) + 2 > ihi || ihi > n) return -1;
+    const size_t nb = nshifts / 2;
+    size_t cw = window_size > 3 * nb + 6 ? window_size : 3 * nb + 6;
+    teo_mat M = {n, h, ldh, q, ldq, (double*)malloc(2 * cw * n * sizeof(double) + 16)};
+    size_t* pos = (size_t*)malloc(nb * sizeof(size_t));
+    intro_window(&M, l, ihi, nb, shifts, pos);
+    const int rc = chase_chain(&M, pos, nb, ihi, cw);
+    free(pos);
+    free(M.scratch);
+    return rc;
+}
+
+/* schur_reduce (schur.cpp:671-906), serial semantics */
+int teo_schur_reduce(size_t n, double* h, size_t ldh, double* q, size_t ldq, size_t tile,
+                     const teo_schur_opts* o, double* eig, teo_schur_info* info) {
+    memset(info, 0, sizeof *info);
+    if (!tile) tile = n >= 1000 ? 128 : ((n / 8 > 32 ? n / 8 : 32) + 7) / 8 * 8;
+    const size_t limit = o->iteration_limit ? o->iteration_limit : 30 * n;
+    const double hnorm = hess_norm(n, h, ldh);
+    const size_t cwmax = tile > 3 * 32 + 6 ? tile : 3 * 32 + 6;
+    size_t smax = cwmax > 256 ? cwmax : 256;
+    teo_mat M = {n, h, ldh, q, ldq, (double*)malloc(2 * smax * n * sizeof(double) + 16)};
+    double* shifts = (double*)malloc(2 * 512 * sizeof(double));
+    double* picked = (double*)malloc(2 * 520 * sizeof(double));
+    size_t* pos = (size_t*)malloc(64 * sizeof(size_t));
+    size_t ihi = n, stagnation = 0;
+    int have_pending = 0, hard_fail = 0;
+    teo_aed_out pend;
+    memset(&pend, 0, sizeof pend);
+    while (ihi > 0 && !hard_fail) {
+        teo_aed_out res;
+        int have_aed = 0;
+        size_t l = 0;
+        memset(&res, 0, sizeof res);
+        if (have_pending) {
+            res = pend;
+            have_pending = 0;
+            have_aed = 1;
+            if (!res.converged) {
+                const size_t w2 = res.window / 2 > 4 ? res.window / 2 : 4;
+                l = scan_active(n, h, ldh, ihi, hnorm);
+                if (w2 < res.window && ihi - l >= w2) aed_round(&M, l, ihi, w2, o, &res, shifts);
+                if (!res.converged) {
+                    hard_fail = 1;
+                    break;
+                }
+            }
+            ihi -= res.deflated;
+            stagnation = (res.deflated == 0) ? stagnation + 1 : 0;
+            if (ihi == 0) break;
+        }
+        l = scan_active(n, h, ldh, ihi, hnorm);
+        size_t active = ihi - l;
+        if (active == 1) {
+            ihi = l;
+            have_pending = 0;
+            continue;
+        }
+        if (active == 2) {
+            double w[4], qw[4];
+            gather(h, ldh, l, l, 2, w);
+            set_identity(2, qw, 2);
+            std_block(2, w, 2, 2, qw, 2, 0);
+            scatter(h, ldh, l, l, 2, w);
+            win_updates(&M, l, ihi, qw);
+            info->rounds++;
+            ihi = l;
+            continue;
+        }
+        if (active <= o->small_threshold) {
+            double* w = (double*)malloc(active * active * sizeof(double));
+            double* qw = (double*)malloc(active * active * sizeof(double));
+            gather(h, ldh, l, l, active, w);
+            const int ok = teo_small_schur(active, w, qw, NULL);
+            scatter(h, ldh, l, l, active, w);
+            win_updates(&M, l, ihi, qw);
+            free(w);
+            free(qw);
+            info->rounds++;
+            if (!ok) {
+                hard_fail = 1;
+                break;
+            }
+            ihi = l;
+            continue;
+        }
+        if (!have_aed) {
+            const size_t m = o->shift_count ? o->shift_count : default_shift_count(active);
+            size_t w = o->aed_window ? o->aed_window : (3 * m) / 2;
+            if (w < 4) w = 4;
+            if (w > active) w = active;
+            aed_round(&M, l, ihi, w, o, &res, shifts);
+            info->rounds++;
+            if (!res.converged) {
+                const size_t w2 = w / 2 > 4 ? w / 2 : 4;
+                if (w2 < w) aed_round(&M, l, ihi, w2 < ihi - l ? w2 : ihi - l, o, &res, shifts);
+                if (!res.converged) {
+                    hard_fail = 1;
+                    break;
+                }
+            }
+            ihi -= res.deflated;
+            stagnation = (res.deflated == 0) ? stagnation + 1 : 0;
+            if (ihi == 0) break;
+            l = scan_active(n, h, ldh, ihi, hnorm);
+            active = ihi - l;
+            if (active < 4) continue;
+        }
+        if (res.deflated > 0 && 100 * res.deflated >= 14 * res.window) continue;
+        if (active <= o->small_threshold) continue;
+        if (info->sweeps >= limit) {
+            hard_fail = 1;
+            break;
+        }
+        info->sweeps++;
+        const size_t m_want = o->shift_count ? o->shift_count : default_shift_count(active);
+        size_t np = pick_shifts(shifts, res.nshifts, m_want, picked);
+        if (stagnation >= 6 || np < 2) {
+            const double sp = fabs(A_(h, ihi - 1, ihi - 2, ldh)) +
+                              ((ihi >= l + 3) ? fabs(A_(h, ihi - 2, ihi - 3, ldh)) : 0.0);
+            const double h11 = 0.75 * sp + A_(h, ihi - 1, ihi - 1, ldh);
+            double st[10];
+            teo_standardize_2x2(h11, -0.4375 * sp, sp, h11, st);
+            picked[0] = st[6];
+            picked[1] = st[7];
+            picked[2] = st[8];
+            picked[3] = st[9];
+            np = 2;
+            stagnation = 0;
+        }
+        size_t nb = np / 2 < (active - 2) / 3 ? np / 2 : (active - 2) / 3;
+        if (nb == 0) continue;
+        info->rounds++;
+        intro_window(&M, l, ihi, nb, picked, pos);
+        const size_t cw = tile > 3 * nb + 6 ? tile : 3 * nb + 6;
+        if (chase_chain(&M, pos, nb, ihi, cw)) {
+            hard_fail = 1;
+            break;
+        }
+        {
+            const size_t m2 = o->shift_count ? o->shift_count : default_shift_count(active);
+            size_t w2 = o->aed_window ? o->aed_window : (3 * m2) / 2;
+            if (w2 < 4) w2 = 4;
+            if (w2 > active) w2 = active;
+            aed_round(&M, l, ihi, w2, o, &pend, shifts);
+            have_pending = 1;
+        }
+    }
+    info->converged = !hard_fail;
+    info->converged_trailing = n - ihi;
+    if (!hard_fail && eig) { /* eigenvalue read-off, schur.cpp:888-904 */
+        for (size_t i = 0; i < n;) {
+            if (i + 1 < n && A_(h, i + 1, i, ldh) != 0.0) {
+                const double a = A_(h, i, i, ldh), b = A_(h, i, i + 1, ldh), c = A_(h, i + 1, i, ldh);
+                const double im = sqrt(fabs(b)) * sqrt(fabs(c));
+                eig[i] = a;
+                eig[n + i] = im;
+                eig[i + 1] = a;
+                eig[n + i + 1] = -im;
+                i += 2;
+            } else {
+                eig[i] = A_(h, i, i, ldh);
+                eig[n + i] = 0.0;
+                i += 1;
+            }
+        }
+    }
+    free(M.scratch);
+    free(shifts);
+    free(picked);
+    free(pos);
+    return 0;
+}

@@ -112,6 +112,42 @@ long teo_reorder_schur(size_t n, double* s, size_t lds, double* q, size_t ldq, s
 void teo_gemm(int ta, int tb, size_t m, size_t n, size_t k, double alpha, const double* a,
               size_t lda, const double* b, size_t ldb, double* c, size_t ldc);
 
+
+/* ---- Schur reduction path (schur.cpp, kernels.cpp:223-381) ------------- */
+typedef struct {
+    int deflation;          /* 0 classic, 1 norm-stable (SchurOptions, schur.hpp:20-29) */
+    size_t shift_count;     /* 0: default_shift_count */
+    size_t aed_window;      /* 0: 3m/2 */
+    size_t iteration_limit; /* 0: 30 n */
+    size_t small_threshold; /* 64 */
+} teo_schur_opts;
+
+typedef struct { /* AedResult (schur.hpp:32-39) + the window's new spike */
+    size_t window, deflated, nshifts;
+    int spike_eliminated, converged, swap_rejected;
+    double newbeta;
+} teo_aed_out;
+
+typedef struct {
+    size_t sweeps, rounds, converged_trailing;
+    int converged;
+} teo_schur_info;
+
+/* small_schur (kernels.cpp:260-381): h k x k (ld k) in place, q (k x k) out.
+ * Returns 1 converged. */
+int teo_small_schur(size_t k, double* h, double* q, size_t* sweeps);
+int teo_deflation_check(double spike, double diag_sum, int norm_stable, double wnorm);
+/* aed_step (schur.cpp:599-609); shifts: 2*window doubles (re, im) out */
+int teo_aed_step(size_t n, double* h, size_t ldh, double* q, size_t ldq, size_t l, size_t ihi,
+                 size_t window, const teo_schur_opts* o, teo_aed_out* r, double* shifts);
+/* introduce_bulges + chase_bulges (schur.cpp:611-669); shifts: (re, im) */
+int teo_sweep(size_t n, double* h, size_t ldh, double* q, size_t ldq, size_t l, size_t ihi,
+              size_t nshifts, const double* shifts, size_t window_size);
+/* schur_reduce (schur.cpp:671-906), serial semantics; tile 0: default_tile_size(n).
+ * eig: re[n] then im[n] (or NULL). */
+int teo_schur_reduce(size_t n, double* h, size_t ldh, double* q, size_t ldq, size_t tile,
+                     const teo_schur_opts* o, double* eig, teo_schur_info* info);
+
 /* ---- verification (verify.cpp) ----------------------------------------- */
 double teo_similarity_residual(size_t n, const double* a, size_t lda, const double* q,
                                size_t ldq, const double* s, size_t lds);
