@@ -135,6 +135,85 @@ int teig_apply_window_updates_device(int64_t n, double* dS, int64_t lds, double*
                                      int64_t a, int64_t d, const double* dQw, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Schur reduction: multishift QR with aggressive early deflation           */
+/* (replaces taskeig::schur_reduce, schur.hpp:94-95 / schur.cpp:671-906,     */
+/* and the per-step ops aed_step, introduce_bulges, chase_bulges,            */
+/* deflation_check, kernels::small_schur: schur.hpp:63-89, kernels.hpp:93).  */
+
+typedef struct teig_schur_opts {  /* SchurOptions, schur.hpp:20-29 */
+    int32_t deflation;        /* 0 classic, 1 norm-stable (default) */
+    int32_t shift_count;      /* 0: max(4, round-to-even(active/16)), cap 64 */
+    int32_t aed_window;       /* 0: 3m/2; <= 112 (single-CTA AED window) */
+    int32_t small_threshold;  /* direct small_schur at or below (default 64, <= 112) */
+    int64_t iteration_limit;  /* 0: 30 n sweeps */
+    int64_t tile_size;        /* chase window: 0 = default_tile_size(n) (128 for n >= 1000); <= 128 */
+    int32_t profile;          /* !=0: CUDA-event time per kernel class in teig_schur_info */
+    int32_t pad;
+} teig_schur_opts;
+
+typedef struct teig_schur_info {  /* SchurDecomposition's scalars, schur.hpp:50-58 */
+    int64_t sweeps;
+    int64_t rounds;             /* executed rounds (one readback each) */
+    int64_t aed_windows;
+    int64_t chase_windows;      /* intro + chase windows */
+    int64_t converged_trailing; /* meaningful when !converged */
+    int64_t n_launches;
+    int32_t converged;
+    int32_t pad;
+    double update_flops;        /* sum over windows of 2d^2(n-b) + 2d^2 a (+ 2d^2 n) */
+    double ms_window;           /* profile only: device time of window kernels */
+    double ms_update;           /* profile only: device time of update kernels (both streams) */
+    double ms_total_host;       /* host wall time of the call */
+} teig_schur_info;
+
+typedef struct teig_aed_result {  /* AedResult, schur.hpp:32-39 */
+    int64_t window, deflated, nshifts;
+    int32_t spike_eliminated, converged, swap_rejected, pad;
+} teig_aed_result;
+
+void teig_schur_opts_default(teig_schur_opts* o);
+
+/* schur_reduce: dH (n x n upper Hessenberg, device, ld ldh) -> standardized
+ * real Schur form in place; dQ (device, ld ldq) or NULL: Q <- Q * Z.
+ * eig_re/eig_im (host, n, or NULL): eigenvalues read off the diagonal as the
+ * reference does (schur.cpp:888-904).  Returns 0 (check info->converged), < 0
+ * on bad arguments, TEIG_ERR_* otherwise. */
+int teig_schur_reduce_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t ldq,
+                             const teig_schur_opts* opts, double* eig_re, double* eig_im,
+                             teig_schur_info* info, void* stream);
+/* Same on HOST buffers (column-major, ld); includes H2D/D2H. */
+int teig_schur_reduce_host(int64_t n, double* H, int64_t ldh, double* Q, int64_t ldq,
+                           const teig_schur_opts* opts, double* eig_re, double* eig_im,
+                           teig_schur_info* info, void* stream);
+
+/* aed_step (schur.hpp:68-69): one AED window of the active range [l, ihi)
+ * with its off-window updates.  shifts (host, 2*window doubles): (re, im). */
+int teig_aed_step_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t ldq, int64_t l,
+                         int64_t ihi, int64_t window, const teig_schur_opts* opts,
+                         teig_aed_result* result, double* shifts, void* stream);
+
+/* introduce_bulges (schur.hpp:73-75): shifts (host) as nshifts (re, im)
+ * pairs; positions (host, nshifts/2) receives the bulge rows, bottom first. */
+int teig_introduce_bulges_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t ldq,
+                                 int64_t l, int64_t ihi, int64_t nshifts, const double* shifts,
+                                 int64_t* positions, void* stream);
+
+/* chase_bulges (schur.hpp:87-89): chases the chain (positions bottom first,
+ * as returned by teig_introduce_bulges_device) off the bottom of [., chain_end)
+ * with windows of max(window_size, 3nb+6) rows. */
+int teig_chase_bulges_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t ldq,
+                             int64_t chain_end, int64_t nb, const int64_t* positions,
+                             int64_t window_size, int64_t* n_windows, void* stream);
+
+/* kernels::small_schur (kernels.hpp:93): dH k x k (ld ldh) in place, dQ
+ * (k x k, ld k) receives the similarity.  k <= 112. */
+int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int32_t* converged,
+                            void* stream);
+
+/* deflation_check (schur.hpp:63-64); host only. */
+int teig_deflation_check(double spike, double diag_sum, int32_t deflation, double wnorm);
+
+/* ------------------------------------------------------------------------ */
 /* Synthetic inputs directly in HBM (bit-identical to the      */
 /* reference generators).                                                    */
 

@@ -553,3 +553,10 @@ def schur_reduce(h: np.ndarray, q=None, tile=0, **opts):
     lib().teo_schur_reduce(n, _ptr(h), n, _ptr(q), n, tile, C.byref(o), _ptr(eig), C.byref(info))
     return dict(eigenvalues=eig[:n] + 1j * eig[n:], sweeps=info.sweeps, converged=bool(info.converged),
                 converged_trailing=info.converged_trailing)
+
+
+def ref_default_spectrum(n: int, seed: int) -> np.ndarray:
+    """default_spectrum (generate.cpp:68-91) from the reference."""
+    out = np.zeros(2 * n)
+    ref().ref_default_spectrum(n, seed, _ptr(out))
+    return out[0::2] + 1j * out[1::2]

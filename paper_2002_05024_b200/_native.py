@@ -45,6 +45,25 @@ class ReorderInfo(C.Structure):
                 ("flops_left", C.c_double), ("flops_right", C.c_double), ("flops_factor", C.c_double)]
 
 
+class SchurOpts(C.Structure):
+    _fields_ = [("deflation", C.c_int32), ("shift_count", C.c_int32), ("aed_window", C.c_int32),
+                ("small_threshold", C.c_int32), ("iteration_limit", C.c_int64), ("tile_size", C.c_int64),
+                ("profile", C.c_int32), ("pad", C.c_int32)]
+
+
+class SchurInfo(C.Structure):
+    _fields_ = [("sweeps", C.c_int64), ("rounds", C.c_int64), ("aed_windows", C.c_int64),
+                ("chase_windows", C.c_int64), ("converged_trailing", C.c_int64), ("n_launches", C.c_int64),
+                ("converged", C.c_int32), ("pad", C.c_int32), ("update_flops", C.c_double),
+                ("ms_window", C.c_double), ("ms_update", C.c_double), ("ms_total_host", C.c_double)]
+
+
+class AedResultC(C.Structure):
+    _fields_ = [("window", C.c_int64), ("deflated", C.c_int64), ("nshifts", C.c_int64),
+                ("spike_eliminated", C.c_int32), ("converged", C.c_int32), ("swap_rejected", C.c_int32),
+                ("pad", C.c_int32)]
+
+
 _P = C.c_void_p
 _I64 = C.c_int64
 
@@ -66,6 +85,14 @@ SIGNATURES = {
     "teig_gen_schur_input_device": (C.c_int, [_I64, _P, _I64, C.c_uint64, _P]),
     "teig_gen_hessenberg_device": (C.c_int, [_I64, _P, _I64, C.c_uint64, _P]),
     "teig_set_identity_device": (C.c_int, [_I64, _P, _I64, _P]),
+    "teig_schur_opts_default": (None, [_P]),
+    "teig_schur_reduce_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P]),
+    "teig_schur_reduce_host": (C.c_int, [_I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _P]),
+    "teig_aed_step_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P, _P]),
+    "teig_introduce_bulges_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P, _P]),
+    "teig_chase_bulges_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _I64, _P, _I64, _P, _P]),
+    "teig_small_schur_device": (C.c_int, [_I64, _P, _I64, _P, _P, _P]),
+    "teig_deflation_check": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.c_double]),
 }
 
 _lib = None

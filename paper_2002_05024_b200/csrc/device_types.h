@@ -29,4 +29,44 @@ enum : int32_t {
     kWinStuck = 2,        // at least one swap was rejected
 };
 
+// ---- Schur reduction (schur_window.cu) --------------------------------------
+
+// SchurOptions (reference schur.hpp:20-29) as seen by the window kernels
+struct SchurDevOpts {
+    int32_t deflation;        // 0 classic, 1 norm-stable
+    int32_t shift_count;      // 0: default_shift_count
+    int32_t aed_window;       // 0: 3m/2
+    int32_t small_threshold;  // direct small_schur below this active size
+};
+
+// outcome of one AED / small-solve window (AedResult, schur.hpp:32-39)
+struct AedDevOut {
+    int32_t deflated;
+    int32_t converged;
+    int32_t swap_rejected;
+    int32_t spike_eliminated;
+    int32_t nshifts;
+    int32_t pad;
+    double newbeta;
+};
+
+enum : int32_t { kSchurModeAed = 0, kSchurModeSmall = 1, kSchurModeStd2 = 2 };
+enum : int32_t { kChaseHop = 0, kChaseFinal = 1, kChaseIntro = 2 };
+
+// one window of a bulge chain (intro window or a chase window of plan_chase,
+// reference schur.cpp:484-505); bulge k (k = 0 bottom-most) enters at row
+// p_bot - 3k (bulges stay exactly 3 rows apart)
+struct ChaseWin {
+    int32_t a, d;        // window rows/cols [a, a+d)
+    int32_t ihi;         // end of the active range
+    int32_t mode;        // kChaseHop / kChaseFinal / kChaseIntro
+    int32_t nb;          // bulges in the window
+    int32_t hop;         // steps per bulge (kChaseHop)
+    int32_t p_bot;       // entering position of the bottom-most bulge
+    int32_t shift_off;   // intro: offset of the (re, im) x 2 shift pairs
+    int64_t qw_off;      // offset (doubles) of the window's Q_w
+    int32_t packed_len;  // doubles of the packed window band
+    int32_t pad;
+};
+
 }  // namespace teig

@@ -28,6 +28,22 @@ cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64
 cudaError_t launch_set_identity(double* Q, long long ldq, long long n, cudaStream_t stream);
 cudaError_t launch_gen_hessenberg(double* H, long long ldh, long long n, uint64_t seed, cudaStream_t stream);
 
+// Schur reduction window kernels (schur_window.cu)
+constexpr int kAedThreads = 256;
+constexpr int kChaseThreads = 512;
+constexpr int kAedMaxWindow = 112;   // AED / small-solve window order limit (shared memory)
+constexpr int kChaseMaxWindow = 128; // chase window order limit
+size_t aed_window_smem_bytes(int w);
+size_t chase_window_smem_bytes(int d);
+int chase_window_packed_len(int d);
+cudaError_t launch_aed_window(double* H, long long ldh, int mode, int l, int e, int w, const SchurDevOpts& o,
+                              double* qw_out, AedDevOut* out, double* shifts_out, cudaStream_t stream);
+cudaError_t launch_chase_window(double* H, long long ldh, const ChaseWin* wins_dev, int idx, int d,
+                                const double* shift_pairs, double* qw_pool, cudaStream_t stream);
+cudaError_t launch_hess_norm(const double* H, long long ldh, int n, unsigned long long* out, cudaStream_t stream);
+cudaError_t launch_scan_active(double* H, long long ldh, int n, int ihi, double hnorm, int* out,
+                               cudaStream_t stream);
+
 constexpr int kLeftBN = 64;   // columns per left-update tile
 constexpr int kRightBM = 64;  // rows per right/factor-update tile
 

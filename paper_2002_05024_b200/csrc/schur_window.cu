@@ -1,0 +1,1238 @@
+// schur_window.cu -- single-CTA window kernels of the multishift-QR Schur
+// reduction (sm_100a).
+//
+// Two kernels, each owning ONE diagonal window of H in shared memory and
+// accumulating the window's orthogonal similarity Q_w for the DMMA update
+// kernels (update_dmma.cu), which apply it to the row panel right of the
+// window, the column panel above it and the Schur-vector factor -- the
+// reference's L/R/Q tasks (window_tasks.cpp:12-102).
+//
+// aed_window_kernel -- the AED window task (reference schur.cpp:421-459,
+//   aed_process_window :147-248), the direct small-block solve (:554-579,
+//   kernels.cpp:260-381) and the 2x2 standardization round (:728-757).
+//   The reference gathers every nested window (recursive multishift QR,
+//   :304-399, down to small_schur) into fresh dense matrices and propagates
+//   their similarities with dense GEMMs.  Here everything happens IN PLACE on
+//   the one shared-memory copy of the top window: every reflector/rotation is
+//   applied to the full rows right of and the full columns above the
+//   affected indices (which is what gather + apply_similarity_dense compute),
+//   to Q_w, and to the first row of every enclosing nested AED window's
+//   accumulator -- the only part of a nested accumulator the algorithm ever
+//   reads (the spike beta*q(0,:)).  Nested levels therefore cost no extra
+//   storage and no GEMMs.  Control flow is uniform: every decision is taken
+//   by all threads from the same shared-memory values.
+//
+// chase_window_kernel -- one window of a bulge chain (intro window
+//   :833-867 / introduce_bulges :611-648, chase windows run_chase_window
+//   :507-523).  The reference moves the bulges one after the other (the
+//   bottom bulge over the whole hop, then the next).  Bulges sit exactly 3
+//   rows apart, so a step of bulge k and the same step of its neighbours act
+//   on disjoint index sets; the kernel advances ALL bulges of the window one
+//   position per step (three barrier-separated phases: reflectors, left
+//   applications + accumulator, right applications), which reorders only
+//   commuting left/right multiplications of the reference's sequence.  The
+//   window lives packed in shared memory (column j keeps rows 0..j+3: the
+//   Hessenberg band plus the bulges' fill), Q_w densely.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <type_traits>
+
+#include "device_types.h"
+#include "launch.h"
+#include "swap_math.cuh"
+
+namespace teig {
+
+namespace {
+
+constexpr int NT = kAedThreads;      // threads of the AED / small-solve kernel
+constexpr int NTC = kChaseThreads;   // threads of the chase kernel
+constexpr int kMaxSpk = 5;           // nested AED levels (depth 0, 2, 4, 6, 8)
+
+__device__ __forceinline__ int tid() { return (int)threadIdx.x; }
+
+struct Mat {
+    double* p;
+    int ld;
+    __device__ __forceinline__ double& operator()(int i, int j) const { return p[i + j * ld]; }
+};
+
+// first row of a nested AED window's accumulator (window starts at `off`)
+struct Spk {
+    double* p;
+    int off;
+};
+
+struct Ctx {
+    Mat H;        // the top window, N x N
+    int N;
+    Mat Q;        // its accumulator, N x N
+    Spk spk[kMaxSpk];
+    int nspk;
+    double* red;  // >= 32 doubles: block reductions
+    double* scr;  // >= N + 8 doubles: reflector broadcast
+    int* iscr;    // >= 8 ints
+    double* shb;  // harvested shifts, per level 2*N doubles
+    double* pkb;  // picked shifts, per level 2*(N+4) doubles
+    double* spkb; // spike rows, per level N doubles
+    int* nsh;     // harvested shift count per level
+    SchurDevOpts o;
+};
+
+__device__ double block_max(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if ((tid() & 31) == 0) red[tid() >> 5] = v;
+    __syncthreads();
+    double r = red[0];
+    for (int i = 1; i < NT / 32; ++i) r = fmax(r, red[i]);
+    return r;
+}
+
+__device__ double block_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((tid() & 31) == 0) red[tid() >> 5] = v;
+    __syncthreads();
+    double r = 0.0;
+    for (int i = 0; i < NT / 32; ++i) r += red[i];
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// in-place similarity primitives (all threads call; no barrier inside)
+
+// rows r0..r0+L-1 of H <- (I - tau v v^T) rows, columns [c0, N)
+template <int L>
+__device__ __forceinline__ void left_apply(const Ctx& c, int r0, const double (&v)[L], double tau, int c0) {
+    if (tau == 0.0) return;
+    for (int j = c0 + tid(); j < c.N; j += NT) {
+        double* col = &c.H(r0, j);
+        double w = 0.0;
+#pragma unroll
+        for (int i = 0; i < L; ++i) w += v[i] * col[i];
+        w *= tau;
+#pragma unroll
+        for (int i = 0; i < L; ++i) col[i] -= w * v[i];
+    }
+}
+
+// the row vector starting at p (column stride cs) <- row (I - tau v v^T)
+template <int L>
+__device__ __forceinline__ void row_apply(double* p, int cs, const double (&v)[L], double tau) {
+    double w = 0.0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) w += p[j * cs] * v[j];
+    w *= tau;
+#pragma unroll
+    for (int j = 0; j < L; ++j) p[j * cs] -= w * v[j];
+}
+
+// columns c0..c0+L-1: H rows [0, r1), all rows of Q, every spike row
+template <int L>
+__device__ __forceinline__ void right_apply(const Ctx& c, int c0, const double (&v)[L], double tau, int r1) {
+    if (tau == 0.0) return;
+    const int total = r1 + c.N + c.nspk;
+    for (int t = tid(); t < total; t += NT) {
+        if (t < r1) row_apply<L>(&c.H(t, c0), c.H.ld, v, tau);
+        else if (t < r1 + c.N) row_apply<L>(&c.Q(t - r1, c0), c.Q.ld, v, tau);
+        else {
+            const Spk& s = c.spk[t - r1 - c.N];
+            row_apply<L>(s.p + (c0 - s.off), 1, v, tau);
+        }
+    }
+}
+
+// general-length reflector held in c.scr[0..len) (v), c.scr[len] = tau
+__device__ void left_apply_n(const Ctx& c, int r0, int len, int c0) {
+    const double tau = c.scr[len];
+    if (tau == 0.0) return;
+    for (int j = c0 + tid(); j < c.N; j += NT) {
+        double* col = &c.H(r0, j);
+        double w = 0.0;
+        for (int i = 0; i < len; ++i) w += c.scr[i] * col[i];
+        w *= tau;
+        for (int i = 0; i < len; ++i) col[i] -= w * c.scr[i];
+    }
+}
+
+__device__ void right_apply_n(const Ctx& c, int c0, int len, int r1) {
+    const double tau = c.scr[len];
+    if (tau == 0.0) return;
+    const int total = r1 + c.N + c.nspk;
+    for (int t = tid(); t < total; t += NT) {
+        double* p;
+        int cs;
+        if (t < r1) {
+            p = &c.H(t, c0);
+            cs = c.H.ld;
+        } else if (t < r1 + c.N) {
+            p = &c.Q(t - r1, c0);
+            cs = c.Q.ld;
+        } else {
+            const Spk& s = c.spk[t - r1 - c.N];
+            p = s.p + (c0 - s.off);
+            cs = 1;
+        }
+        double w = 0.0;
+        for (int j = 0; j < len; ++j) w += p[j * cs] * c.scr[j];
+        w *= tau;
+        for (int j = 0; j < len; ++j) p[j * cs] -= w * c.scr[j];
+    }
+}
+
+// make_reflector (kernels.cpp:24-58) of x = c.scr[0..len), in place: on return
+// (after a barrier) c.scr[0..len) = v, c.scr[len] = tau, c.scr[len+1] = beta.
+__device__ void make_refl_block(const Ctx& c, int len) {
+    __syncthreads();  // x written by the caller
+    if (tid() < 32) {
+        const int lane = tid();
+        double* x = c.scr;
+        double tau = 0.0, beta;
+        if (len == 1) {
+            beta = x[0];
+        } else {
+            const double alpha = x[0];
+            auto tailnorm = [&]() {
+                double mx = 0.0;
+                for (int i = 1 + lane; i < len; i += 32) mx = fmax(mx, fabs(x[i]));
+#pragma unroll
+                for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+                if (mx == 0.0) return 0.0;
+                double acc = 0.0;
+                for (int i = 1 + lane; i < len; i += 32) {
+                    const double t = x[i] / mx;
+                    acc += t * t;
+                }
+#pragma unroll
+                for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                return mx * sqrt(acc);
+            };
+            const double tail = tailnorm();
+            if (tail == 0.0) {
+                beta = (alpha == 0.0) ? 0.0 : alpha;
+                __syncwarp();
+                for (int i = 1 + lane; i < len; i += 32) x[i] = 0.0;
+            } else {
+                beta = -sgnd(alpha) * hypot(alpha, tail);
+                double a = alpha;
+                int rescale = 0;
+                while (fabs(beta) < kSafeMinD / kEpsD && rescale < 20) {
+                    const double big = 1.0 / (kSafeMinD / kEpsD);
+                    __syncwarp();
+                    for (int i = 1 + lane; i < len; i += 32) x[i] *= big;
+                    __syncwarp();
+                    a *= big;
+                    beta = -sgnd(a) * hypot(a, tailnorm());
+                    ++rescale;
+                }
+                tau = (beta - a) / beta;
+                const double inv = 1.0 / (a - beta);
+                __syncwarp();
+                for (int i = 1 + lane; i < len; i += 32) x[i] *= inv;
+                for (int r = 0; r < rescale; ++r) beta *= kSafeMinD / kEpsD;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            x[0] = 1.0;
+            x[len] = tau;
+            x[len + 1] = beta;
+        }
+    }
+    __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// negligible-subdiagonal scan of the block [lo, lo+ihi) (schur.cpp:286-300,
+// kernels.cpp:283-292): largest l in (0, ihi) with a negligible H(l, l-1),
+// zeroed; 0 if none.
+__device__ int scan_block(const Ctx& c, int lo, int ihi, double hnorm, double smlnum) {
+    __syncthreads();
+    if (tid() == 0) c.iscr[0] = 0;
+    __syncthreads();
+    for (int l = ihi - 1 - tid(); l > 0; l -= NT) {
+        double tst = fabs(c.H(lo + l - 1, lo + l - 1)) + fabs(c.H(lo + l, lo + l));
+        if (tst == 0.0) tst = hnorm;
+        if (fabs(c.H(lo + l, lo + l - 1)) <= fmax(kEpsD * tst, smlnum)) atomicMax(c.iscr, l);
+    }
+    __syncthreads();
+    const int l = c.iscr[0];
+    __syncthreads();
+    if (l > 0 && tid() == 0) c.H(lo + l, lo + l - 1) = 0.0;
+    __syncthreads();
+    return l;
+}
+
+__device__ double hess_norm_block(const Ctx& c, int lo, int n) {
+    double m = 0.0;
+    for (int idx = tid(); idx < n * n; idx += NT) {
+        const int j = idx / n, i = idx - j * n;
+        if (i <= min(j + 1, n - 1)) m = fmax(m, fabs(c.H(lo + i, lo + j)));
+    }
+    return block_max(m, c.red);
+}
+
+// standardize the 2x2 block at p (kernels.cpp:245-256 / schur.cpp:82-94)
+__device__ void std_block_dev(const Ctx& c, int p) {
+    double st[6];
+    std2x2(c.H(p, p), c.H(p, p + 1), c.H(p + 1, p), c.H(p + 1, p + 1), st);
+    __syncthreads();
+    const double cs = st[0], sn = st[1];
+    const int ncol = c.N - p - 2;
+    const int total = ncol + p + c.N + c.nspk;
+    for (int t = tid(); t < total; t += NT) {
+        if (t < ncol) {
+            const int k = p + 2 + t;
+            const double x = c.H(p, k), y = c.H(p + 1, k);
+            c.H(p, k) = cs * x + sn * y;
+            c.H(p + 1, k) = -sn * x + cs * y;
+        } else {
+            double* a;
+            int s;
+            const int u = t - ncol;
+            if (u < p) {
+                a = &c.H(u, p);
+                s = c.H.ld;
+            } else if (u < p + c.N) {
+                a = &c.Q(u - p, p);
+                s = c.Q.ld;
+            } else {
+                const Spk& sp = c.spk[u - p - c.N];
+                a = sp.p + (p - sp.off);
+                s = 1;
+            }
+            const double x = a[0], y = a[s];
+            a[0] = cs * x + sn * y;
+            a[s] = -sn * x + cs * y;
+        }
+    }
+    if (tid() == 0) {
+        c.H(p, p) = st[2];
+        c.H(p, p + 1) = st[3];
+        c.H(p + 1, p) = st[4];
+        c.H(p + 1, p + 1) = st[5];
+    }
+    __syncthreads();
+}
+
+// one similarity step with a length-L reflector at index k0: left on rows
+// k0.. for columns [k0, N), right on columns k0.. for rows [0, r1).  When
+// annih >= 0, column annih (rows k0..k0+L-1) is set to (beta, 0, ..).
+template <int L>
+__device__ __forceinline__ void sim_step(const Ctx& c, int k0, const double (&v)[L], double tau, double beta,
+                                         int annih, int r1) {
+    left_apply<L>(c, k0, v, tau, k0);
+    __syncthreads();
+    if (annih >= 0 && tid() == 0) {
+        c.H(k0, annih) = beta;
+#pragma unroll
+        for (int i = 1; i < L; ++i) c.H(k0 + i, annih) = 0.0;
+    }
+    right_apply<L>(c, k0, v, tau, r1);
+    __syncthreads();
+}
+
+// small_schur (kernels.cpp:260-381) on the block [lo, lo+n), in place
+__device__ bool small_schur_dev(const Ctx& c, int lo, int n) {
+    if (n <= 1) return true;
+    const double hnorm = hess_norm_block(c, lo, n);
+    if (hnorm == 0.0) return true;
+    const double smlnum = kSafeMinD * ((double)n / kEpsD);
+    const int max_sweeps = 30 * n;
+    int ihi = n, its = 0, sweeps = 0;
+    while (ihi > 0) {
+        if (ihi == 1) {
+            ihi = 0;
+            its = 0;
+            continue;
+        }
+        const int l = scan_block(c, lo, ihi, hnorm, smlnum);
+        if (l == ihi - 1) {
+            ihi = l;
+            its = 0;
+            continue;
+        }
+        if (l == ihi - 2) {
+            std_block_dev(c, lo + l);
+            ihi = l;
+            its = 0;
+            continue;
+        }
+        ++its;
+        ++sweeps;
+        if (sweeps > max_sweeps) return false;
+        double s11, s12, s21, s22;
+        if (its % 10 == 0) {
+            const double sp = fabs(c.H(lo + ihi - 1, lo + ihi - 2)) +
+                              ((ihi >= l + 3) ? fabs(c.H(lo + ihi - 2, lo + ihi - 3)) : 0.0);
+            s11 = 0.75 * sp + c.H(lo + ihi - 1, lo + ihi - 1);
+            s12 = -0.4375 * sp;
+            s21 = sp;
+            s22 = s11;
+        } else {
+            s11 = c.H(lo + ihi - 2, lo + ihi - 2);
+            s12 = c.H(lo + ihi - 2, lo + ihi - 1);
+            s21 = c.H(lo + ihi - 1, lo + ihi - 2);
+            s22 = c.H(lo + ihi - 1, lo + ihi - 1);
+        }
+        const double ssum = s11 + s22, sprod = s11 * s22 - s12 * s21;
+        double v0[3];
+        {
+            const int b = lo + l;
+            const double a11 = c.H(b, b), a12 = c.H(b, b + 1), a21 = c.H(b + 1, b), a22 = c.H(b + 1, b + 1);
+            const double a32 = c.H(b + 2, b + 1);
+            v0[0] = a11 * a11 + a12 * a21 - ssum * a11 + sprod;
+            v0[1] = a21 * (a11 + a22 - ssum);
+            v0[2] = a21 * a32;
+            const double vm = fmax(fabs(v0[0]), fmax(fabs(v0[1]), fabs(v0[2])));
+            if (vm != 0.0) {
+                v0[0] /= vm;
+                v0[1] /= vm;
+                v0[2] /= vm;
+            }
+        }
+        for (int i = l; i + 3 <= ihi; ++i) {
+            double x[3];
+            if (i == l) {
+                x[0] = v0[0];
+                x[1] = v0[1];
+                x[2] = v0[2];
+            } else {
+                x[0] = c.H(lo + i, lo + i - 1);
+                x[1] = c.H(lo + i + 1, lo + i - 1);
+                x[2] = c.H(lo + i + 2, lo + i - 1);
+            }
+            double v[3], tau;
+            const double beta = reflector<3>(x, v, tau);
+            sim_step<3>(c, lo + i, v, tau, beta, i > l ? lo + i - 1 : -1, lo + min(i + 4, ihi));
+        }
+        {
+            const int i = ihi - 2;
+            double x[2] = {c.H(lo + i, lo + i - 1), c.H(lo + i + 1, lo + i - 1)};
+            double v[2], tau;
+            const double beta = reflector<2>(x, v, tau);
+            sim_step<2>(c, lo + i, v, tau, beta, lo + i - 1, lo + ihi);
+        }
+    }
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// adjacent block swap (kernels.cpp:510-631) at absolute index pos, applied to
+// the rows right of / columns above the block, to Q and the spike rows.
+__device__ __noinline__ bool swap_dev(const Ctx& c, int pos, int p, int q) {
+    __syncthreads();
+    double* M = c.scr;        // row-major D x D
+    double* NB = c.scr + 16;  // new block, row-major
+    if (tid() == 0) {
+        int st = 1;
+        if (p == 1 && q == 1) {
+            const double t11 = c.H(pos, pos), t12 = c.H(pos, pos + 1), t22 = c.H(pos + 1, pos + 1);
+            double cs = 1.0, sn = 0.0;
+            const double bb = t22 - t11;
+            if (bb == 0.0) {
+                cs = 1.0;
+                sn = 0.0;
+            } else if (t12 == 0.0) {
+                cs = 0.0;
+                sn = 1.0;
+            } else {
+                const double r = hypot(t12, bb);
+                cs = t12 / r;
+                sn = bb / r;
+            }
+            if (t12 == 0.0 && bb == 0.0) {
+                st = 2;  // equal values: no-op (kernels.cpp:517)
+            } else {
+                M[0] = cs;
+                M[1] = -sn;
+                M[2] = sn;
+                M[3] = cs;
+                NB[0] = t22;
+                NB[1] = t12;
+                NB[2] = 0.0;
+                NB[3] = t11;
+            }
+        } else {
+            auto run = [&](auto P_, auto Q_) {
+                constexpr int P = decltype(P_)::value, Qn = decltype(Q_)::value, D = P + Qn;
+                double blk[D][D], Mm[D][D], nb[D][D];
+#pragma unroll
+                for (int i = 0; i < D; ++i)
+#pragma unroll
+                    for (int j = 0; j < D; ++j) blk[i][j] = c.H(pos + i, pos + j);
+                const bool ok = direct_swap<P, Qn>(blk, Mm, nb);
+                if (ok) {
+#pragma unroll
+                    for (int i = 0; i < D; ++i)
+#pragma unroll
+                        for (int j = 0; j < D; ++j) {
+                            M[i * D + j] = Mm[i][j];
+                            NB[i * D + j] = nb[i][j];
+                        }
+                }
+                return ok;
+            };
+            bool ok;
+            if (p == 1) ok = run(std::integral_constant<int, 1>(), std::integral_constant<int, 2>());
+            else if (q == 1) ok = run(std::integral_constant<int, 2>(), std::integral_constant<int, 1>());
+            else ok = run(std::integral_constant<int, 2>(), std::integral_constant<int, 2>());
+            st = ok ? 1 : 0;
+        }
+        c.iscr[1] = st;
+    }
+    __syncthreads();
+    const int st = c.iscr[1];
+    if (st != 1) return st == 2;
+    const int D = p + q;
+    const int ncol = c.N - pos - D;
+    const int total = ncol + pos + c.N + c.nspk;
+    for (int t = tid(); t < total; t += NT) {
+        double x[4], y[4];
+        if (t < ncol) {  // rows pos.. of column k <- M^T rows
+            const int k = pos + D + t;
+            for (int r = 0; r < D; ++r) x[r] = c.H(pos + r, k);
+            for (int i = 0; i < D; ++i) {
+                double a = 0.0;
+                for (int r = 0; r < D; ++r) a += M[r * D + i] * x[r];
+                y[i] = a;
+            }
+            for (int i = 0; i < D; ++i) c.H(pos + i, k) = y[i];
+        } else {  // a row segment over columns pos..pos+D-1 <- row M
+            const int u = t - ncol;
+            double* a;
+            int s;
+            if (u < pos) {
+                a = &c.H(u, pos);
+                s = c.H.ld;
+            } else if (u < pos + c.N) {
+                a = &c.Q(u - pos, pos);
+                s = c.Q.ld;
+            } else {
+                const Spk& sp = c.spk[u - pos - c.N];
+                a = sp.p + (pos - sp.off);
+                s = 1;
+            }
+            for (int r = 0; r < D; ++r) x[r] = a[r * s];
+            for (int j = 0; j < D; ++j) {
+                double acc = 0.0;
+                for (int r = 0; r < D; ++r) acc += x[r] * M[r * D + j];
+                y[j] = acc;
+            }
+            for (int j = 0; j < D; ++j) a[j * s] = y[j];
+        }
+    }
+    if (tid() == 0)
+        for (int i = 0; i < D; ++i)
+            for (int j = 0; j < D; ++j) c.H(pos + i, pos + j) = NB[i * D + j];
+    __syncthreads();
+    return true;
+}
+
+__device__ __forceinline__ int default_shift_count_dev(int active) {  // schur.cpp:119-129
+    int m = (active / 16) & ~1;
+    m = max(m, 4);
+    m = min(m, 64);
+    if (3 * (m / 2) + 2 > active) {
+        const int nb = (active >= 6) ? (active - 2) / 3 : 1;
+        m = min(max(2, 2 * nb), 64);
+    }
+    return m;
+}
+
+__device__ __forceinline__ bool deflation_check_dev(double spike, double dsum, int norm_stable, double wnorm) {
+    if (!norm_stable) return spike <= fmax(kEpsD * dsum, kSafeMinD);  // schur.cpp:406-411
+    return spike <= kEpsD * wnorm;
+}
+
+struct AedCoreDev {
+    int deflated;
+    int converged;
+    int swap_rejected;
+    int spike_eliminated;
+    double newbeta;
+};
+
+template <int D>
+__device__ AedCoreDev aed_dev(Ctx& c, int e, int w, double beta);
+
+// shift_vector (schur.cpp:29-43) at the top of the window starting at b
+__device__ __forceinline__ void shift_vec_dev(const Ctx& c, int b, int rows, double ssum, double sprod,
+                                              double (&v)[3]) {
+    const double a11 = c.H(b, b), a12 = c.H(b, b + 1), a21 = c.H(b + 1, b), a22 = c.H(b + 1, b + 1);
+    const double a32 = rows > 2 ? c.H(b + 2, b + 1) : 0.0;
+    v[0] = a11 * a11 + a12 * a21 - ssum * a11 + sprod;
+    v[1] = a21 * (a11 + a22 - ssum);
+    v[2] = a21 * a32;
+    const double vm = fmax(fabs(v[0]), fmax(fabs(v[1]), fabs(v[2])));
+    if (vm != 0.0) {
+        v[0] /= vm;
+        v[1] /= vm;
+        v[2] /= vm;
+    }
+}
+
+// chase_one_step (schur.cpp:48-63) in place: the window is [lo+l, lo+ihi);
+// r is in block coordinates.  Returns the new r.
+__device__ int chase_step_dev(const Ctx& c, int lo, int ihi, int r) {
+    const int len = min(3, ihi - r);
+    if (len < 2 || r + 1 >= ihi) return ihi - 1;
+    const int g = lo + r;
+    const int r1 = lo + min(r + len + 1, ihi);
+    if (len == 3) {
+        double x[3] = {c.H(g, g - 1), c.H(g + 1, g - 1), c.H(g + 2, g - 1)}, v[3], tau;
+        const double beta = reflector<3>(x, v, tau);
+        sim_step<3>(c, g, v, tau, beta, g - 1, r1);
+    } else {
+        double x[2] = {c.H(g, g - 1), c.H(g + 1, g - 1)}, v[2], tau;
+        const double beta = reflector<2>(x, v, tau);
+        sim_step<2>(c, g, v, tau, beta, g - 1, r1);
+    }
+    return r + 1;
+}
+
+// multishift_schur_dense (schur.cpp:304-399) on the block [lo, lo+n), in place
+template <int D>
+__device__ bool mshift_dev(Ctx& c, int lo, int n) {
+    if (n <= 1) return true;
+    const double hnorm = hess_norm_block(c, lo, n);
+    const double smlnum = kSafeMinD * ((double)n / kEpsD);
+    const int limit = 30 * n;
+    int sweeps = 0, stagnation = 0, ihi = n;
+    const int lvl = (D + 1) / 2;  // level of the AED windows this call opens
+    while (ihi > 0) {
+        if (ihi == 1) {
+            ihi = 0;
+            continue;
+        }
+        const int l = scan_block(c, lo, ihi, hnorm, smlnum);
+        const int active = ihi - l;
+        if (active == 1) {
+            ihi = l;
+            continue;
+        }
+        if (active == 2) {
+            std_block_dev(c, lo + l);
+            ihi = l;
+            continue;
+        }
+        if (active <= c.o.small_threshold || D >= 8) {
+            if (!small_schur_dev(c, lo + l, active)) return false;
+            ihi = l;
+            continue;
+        }
+        const int m = c.o.shift_count ? c.o.shift_count : default_shift_count_dev(active);
+        int w = c.o.aed_window ? c.o.aed_window : (3 * m) / 2;
+        w = min(max(w, 4), active);
+        const int e = ihi - w;
+        const double beta = (e > l) ? c.H(lo + e, lo + e - 1) : 0.0;
+        AedCoreDev core{0, 0, 0, 0, 0.0};
+        if constexpr (D < 8) core = aed_dev<D + 1>(c, lo + e, w, beta);
+        if (!core.converged) return false;
+        if (e > l && tid() == 0) c.H(lo + e, lo + e - 1) = core.newbeta;
+        __syncthreads();
+        stagnation = (core.deflated == 0) ? stagnation + 1 : 0;
+        ihi -= core.deflated;
+        if (core.deflated > 0 && 100 * core.deflated >= 14 * w) continue;
+        if (ihi - l < 4) continue;
+        // pick_shifts (schur.cpp:97-117) by thread 0 into the level's buffer
+        double* sh = c.shb + lvl * 2 * c.N;
+        double* pk = c.pkb + lvl * 2 * (c.N + 4);
+        if (tid() == 0) {
+            int no = 0;
+            const int nh = c.nsh[lvl];
+            for (int i = 0; i < nh && no + 1 < m + 1; ++i) {
+                const double re = sh[2 * i], im = sh[2 * i + 1];
+                if (im > 0.0) {
+                    if (no + 2 <= m) {
+                        pk[2 * no] = re;
+                        pk[2 * no + 1] = im;
+                        pk[2 * no + 2] = re;
+                        pk[2 * no + 3] = -im;
+                        no += 2;
+                    }
+                }
+            }
+            // reals in harvest order, taken in pairs
+            int nr = 0;
+            double r0 = 0.0;
+            for (int i = 0; i < nh; ++i) {
+                if (sh[2 * i + 1] != 0.0) continue;
+                if (nr % 2 == 0) {
+                    r0 = sh[2 * i];
+                } else if (no + 2 <= m) {
+                    pk[2 * no] = r0;
+                    pk[2 * no + 1] = 0.0;
+                    pk[2 * no + 2] = sh[2 * i];
+                    pk[2 * no + 3] = 0.0;
+                    no += 2;
+                }
+                ++nr;
+            }
+            c.iscr[2] = no;
+        }
+        __syncthreads();
+        int np = c.iscr[2];
+        double ex[4];
+        const bool exc = (stagnation >= 6 || np < 2);
+        if (exc) {
+            const double sp = fabs(c.H(lo + ihi - 1, lo + ihi - 2)) +
+                              ((ihi >= l + 3) ? fabs(c.H(lo + ihi - 2, lo + ihi - 3)) : 0.0);
+            const double h11 = 0.75 * sp + c.H(lo + ihi - 1, lo + ihi - 1);
+            double st[6];
+            std2x2(h11, -0.4375 * sp, sp, h11, st);
+            // eigenvalues of the standardized block (kernels.cpp:210-217)
+            if (st[4] == 0.0) {
+                ex[0] = st[2];
+                ex[1] = 0.0;
+                ex[2] = st[5];
+                ex[3] = 0.0;
+            } else {
+                const double bt = sqrt(fabs(st[3])) * sqrt(fabs(st[4]));
+                ex[0] = st[2];
+                ex[1] = bt;
+                ex[2] = st[2];
+                ex[3] = -bt;
+            }
+            np = 2;
+            stagnation = 0;
+        }
+        if (++sweeps > limit) return false;
+        const int nb = min(np / 2, (ihi - l - 2) / 3);
+        if (nb == 0) continue;
+        const int aw = ihi - l;
+        // intro + chase of nb bulges over the active block, in place
+        for (int j = 0; j < nb; ++j) {
+            double re1, im1, re2, im2;
+            if (exc) {
+                re1 = ex[0]; im1 = ex[1]; re2 = ex[2]; im2 = ex[3];
+            } else {
+                re1 = pk[4 * j]; im1 = pk[4 * j + 1]; re2 = pk[4 * j + 2]; im2 = pk[4 * j + 3];
+            }
+            const double ssum = re1 + re2, sprod = re1 * re2 - im1 * im2;
+            double sv[3], v[3], tau;
+            shift_vec_dev(c, lo + l, aw, ssum, sprod, sv);
+            (void)reflector<3>(sv, v, tau);
+            sim_step<3>(c, lo + l, v, tau, 0.0, -1, lo + l + min(4, aw));
+            int r = l + 1;
+            const int target = l + 1 + 3 * (nb - 1 - j);
+            while (r < target) r = chase_step_dev(c, lo, ihi, r);
+        }
+        for (int j = 0; j < nb; ++j) {
+            int r = l + 1 + 3 * (nb - 1 - j);
+            while (r < ihi - 1) r = chase_step_dev(c, lo, ihi, r);
+        }
+    }
+    return true;
+}
+
+// aed_process_window (schur.cpp:147-248) on the window [e, e+w), in place.
+template <int D>
+__device__ AedCoreDev aed_dev(Ctx& c, int e, int w, double beta) {
+    AedCoreDev core{0, 1, 0, 0, 0.0};
+    const int lvl = D / 2;
+    // window Frobenius norm (frobenius_norm: scaled two-pass nrm2)
+    double mx = 0.0;
+    for (int idx = tid(); idx < w * w; idx += NT) mx = fmax(mx, fabs(c.H(e + idx % w, e + idx / w)));
+    mx = block_max(mx, c.red);
+    double wnorm = 0.0;
+    if (mx != 0.0) {
+        double acc = 0.0;
+        for (int idx = tid(); idx < w * w; idx += NT) {
+            const double t = c.H(e + idx % w, e + idx / w) / mx;
+            acc += t * t;
+        }
+        wnorm = mx * sqrt(block_sum(acc, c.red));
+    }
+    // spike row: Q row 0 at the top level (Q is the window accumulator), a
+    // tracked row for nested windows
+    double* sp;
+    int sps;
+    if (D == 0) {
+        sp = &c.Q(0, 0);
+        sps = c.Q.ld;
+    } else {
+        sp = c.spkb + lvl * c.N;
+        sps = 1;
+        for (int i = tid(); i < w; i += NT) sp[i] = (i == 0) ? 1.0 : 0.0;
+        c.spk[c.nspk] = Spk{sp, e};
+        c.nspk++;
+    }
+    __syncthreads();
+    bool conv;
+    if (w <= c.o.small_threshold || D >= 8) conv = small_schur_dev(c, e, w);
+    else {
+        if constexpr (D < 8) conv = mshift_dev<D + 1>(c, e, w);
+        else conv = small_schur_dev(c, e, w);
+    }
+    core.converged = conv ? 1 : 0;
+    if (conv && beta == 0.0) {
+        core.deflated = w;
+        core.newbeta = 0.0;
+        core.spike_eliminated = 1;
+    } else if (conv) {
+        int ktop = 0, ns = w;
+        while (ns > ktop) {
+            const int bsize = (ns >= 2 && ns - 2 >= ktop && c.H(e + ns - 1, e + ns - 2) != 0.0) ? 2 : 1;
+            const int bs = ns - bsize;
+            double spike = 0.0, dsum = 0.0;
+            for (int r = bs; r < ns; ++r) {
+                spike = fmax(spike, fabs(beta * sp[r * sps]));
+                dsum += fabs(c.H(e + r, e + r));
+            }
+            if (deflation_check_dev(spike, dsum, c.o.deflation, wnorm)) {
+                ns = bs;
+            } else {
+                int cur = bs;
+                bool stuck = false;
+                while (cur > ktop) {
+                    const int psize = (cur >= 2 && cur - 2 >= ktop && c.H(e + cur - 1, e + cur - 2) != 0.0) ? 2 : 1;
+                    const int ps = cur - psize;
+                    if (!swap_dev(c, e + ps, psize, bsize)) {
+                        stuck = true;
+                        break;
+                    }
+                    cur = ps;
+                }
+                if (stuck) {
+                    core.swap_rejected = 1;
+                    break;
+                }
+                ktop += bsize;
+            }
+        }
+        core.deflated = w - ns;
+        // harvest the shifts of the undeflated part (schur.cpp:206-219)
+        __syncthreads();
+        if (tid() == 0) {
+            double* sh = c.shb + lvl * 2 * c.N;
+            int nsh = 0;
+            for (int i = 0; i < ns;) {
+                if (i + 1 < ns && c.H(e + i + 1, e + i) != 0.0) {
+                    const double a = c.H(e + i, e + i), b = c.H(e + i, e + i + 1), cc = c.H(e + i + 1, e + i);
+                    const double im = sqrt(fabs(b)) * sqrt(fabs(cc));
+                    sh[2 * nsh] = a;
+                    sh[2 * nsh + 1] = im;
+                    sh[2 * nsh + 2] = a;
+                    sh[2 * nsh + 3] = -im;
+                    nsh += 2;
+                    i += 2;
+                } else {
+                    sh[2 * nsh] = c.H(e + i, e + i);
+                    sh[2 * nsh + 1] = 0.0;
+                    nsh += 1;
+                    i += 1;
+                }
+            }
+            c.nsh[lvl] = nsh;
+        }
+        // spike elimination and Hessenberg restore (schur.cpp:222-245)
+        if (ns == 0) {
+            core.newbeta = 0.0;
+        } else if (ns == 1) {
+            core.newbeta = beta * sp[0];
+        } else {
+            for (int i = tid(); i < ns; i += NT) c.scr[i] = beta * sp[i * sps];
+            make_refl_block(c, ns);
+            core.newbeta = c.scr[ns + 1];
+            left_apply_n(c, e, ns, e);
+            __syncthreads();
+            right_apply_n(c, e, ns, e + ns);
+            __syncthreads();
+            for (int j = 0; j + 2 < ns; ++j) {
+                const int len = ns - j - 1;
+                for (int i = tid(); i < len; i += NT) c.scr[i] = c.H(e + j + 1 + i, e + j);
+                make_refl_block(c, len);
+                if (c.scr[len] == 0.0) continue;
+                const double hb = c.scr[len + 1];
+                left_apply_n(c, e + j + 1, len, e + j + 1);
+                for (int i = tid(); i < len; i += NT) c.H(e + j + 1 + i, e + j) = (i == 0) ? hb : 0.0;
+                __syncthreads();
+                right_apply_n(c, e + j + 1, len, e + ns);
+                __syncthreads();
+            }
+        }
+        core.spike_eliminated = 1;
+    }
+    __syncthreads();
+    if (D != 0) c.nspk--;
+    __syncthreads();
+    return core;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// AED / small-solve / 2x2 window kernel (one CTA)
+__global__ void __launch_bounds__(NT) aed_window_kernel(double* __restrict__ Hg, long long ldh, int mode, int l,
+                                                        int e, int w, SchurDevOpts o, double* __restrict__ qw_out,
+                                                        AedDevOut* __restrict__ out, double* __restrict__ shifts_out) {
+    extern __shared__ __align__(16) double sm[];
+    const int ld = w | 1;
+    double* base = sm;
+    Ctx c;
+    c.H = Mat{base, ld};
+    base += (size_t)ld * w;
+    c.Q = Mat{base, ld};
+    base += (size_t)ld * w;
+    c.N = w;
+    c.nspk = 0;
+    c.red = base;
+    base += 32;
+    c.scr = base;
+    base += w + 40;
+    c.shb = base;
+    base += (size_t)kMaxSpk * 2 * w;
+    c.pkb = base;
+    base += (size_t)kMaxSpk * 2 * (w + 4);
+    c.spkb = base;
+    base += (size_t)kMaxSpk * w;
+    c.iscr = reinterpret_cast<int*>(base);
+    c.nsh = c.iscr + 8;
+    c.o = o;
+    for (int idx = tid(); idx < w * w; idx += NT) {
+        const int j = idx / w, i = idx - j * w;
+        c.H(i, j) = Hg[(long long)(e + i) + (long long)(e + j) * ldh];
+        c.Q(i, j) = (i == j) ? 1.0 : 0.0;
+    }
+    const double beta = (e > l) ? Hg[(long long)e + (long long)(e - 1) * ldh] : 0.0;
+    __syncthreads();
+    AedCoreDev core{0, 1, 0, 0, 0.0};
+    if (mode == kSchurModeAed) {
+        core = aed_dev<0>(c, 0, w, beta);
+    } else if (mode == kSchurModeSmall) {
+        core.converged = small_schur_dev(c, 0, w) ? 1 : 0;
+    } else {
+        std_block_dev(c, 0);
+    }
+    __syncthreads();
+    const bool keep = !(mode == kSchurModeAed && !core.converged);
+    for (int idx = tid(); idx < w * w; idx += NT) {
+        const int j = idx / w, i = idx - j * w;
+        if (keep) Hg[(long long)(e + i) + (long long)(e + j) * ldh] = c.H(i, j);
+        qw_out[i + (long long)j * w] = keep ? c.Q(i, j) : (i == j ? 1.0 : 0.0);
+    }
+    if (tid() == 0) {
+        if (mode == kSchurModeAed && core.converged && e > l) Hg[(long long)e + (long long)(e - 1) * ldh] = core.newbeta;
+        out->deflated = core.deflated;
+        out->converged = core.converged;
+        out->swap_rejected = core.swap_rejected;
+        out->spike_eliminated = core.spike_eliminated;
+        out->newbeta = core.newbeta;
+        out->nshifts = (mode == kSchurModeAed && core.converged && beta != 0.0) ? c.nsh[0] : 0;
+    }
+    if (mode == kSchurModeAed && core.converged && beta != 0.0)
+        for (int i = tid(); i < 2 * c.nsh[0]; i += NT) shifts_out[i] = c.shb[i];
+}
+
+size_t aed_window_smem_bytes(int w) {
+    const size_t ld = (size_t)(w | 1);
+    const size_t dbl = 2 * ld * w + 32 + w + 40 + kMaxSpk * 2 * w + kMaxSpk * 2 * (w + 4) + kMaxSpk * w;
+    return dbl * sizeof(double) + 32 * sizeof(int);
+}
+
+cudaError_t launch_aed_window(double* H, long long ldh, int mode, int l, int e, int w, const SchurDevOpts& o,
+                              double* qw_out, AedDevOut* out, double* shifts_out, cudaStream_t stream) {
+    const size_t smem = aed_window_smem_bytes(w);
+    static size_t configured = 0;
+    if (smem > configured) {
+        cudaError_t err = cudaFuncSetAttribute(aed_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)aed_window_smem_bytes(kAedMaxWindow));
+        if (err != cudaSuccess) return err;
+        configured = aed_window_smem_bytes(kAedMaxWindow);
+    }
+    aed_window_kernel<<<1, NT, smem, stream>>>(H, ldh, mode, l, e, w, o, qw_out, out, shifts_out);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// chase window kernel (one CTA per window, all bulges advance together)
+
+namespace {
+
+struct BulgeRefl {
+    double v1, v2, tau, beta;
+    int ri, len, kind, pad;  // kind: 0 inactive, 1 chase step, 2 intro
+};
+
+// packed column-major window: column j holds rows 0..min(j+3, d-1)
+struct Packed {
+    double* p;
+    const int* off;
+    __device__ __forceinline__ double& operator()(int i, int j) const { return p[off[j] + i]; }
+};
+
+}  // namespace
+
+__global__ void __launch_bounds__(NTC) chase_window_kernel(double* __restrict__ Hg, long long ldh,
+                                                           const ChaseWin* __restrict__ wins,
+                                                           const double* __restrict__ shift_pairs,
+                                                           double* __restrict__ qw_pool) {
+    const ChaseWin cw = wins[blockIdx.x];
+    const int a = cw.a, d = cw.d;
+    extern __shared__ __align__(16) double sm[];
+    const int lda = d | 1;
+    double* acc = sm;
+    double* win = acc + (size_t)lda * d;
+    int* off = reinterpret_cast<int*>(win + cw.packed_len);
+    BulgeRefl* br = reinterpret_cast<BulgeRefl*>(off + d + 2);
+    // column offsets of the packed layout
+    if (tid() == 0) {
+        int o = 0;
+        for (int j = 0; j < d; ++j) {
+            off[j] = o;
+            o += min(j + 4, d);
+        }
+        off[d] = o;
+    }
+    __syncthreads();
+    Packed W{win, off};
+    for (int j = threadIdx.x >> 5; j < d; j += NTC / 32) {
+        const int rows = min(j + 4, d);
+        for (int i = threadIdx.x & 31; i < rows; i += 32) W(i, j) = Hg[(long long)(a + i) + (long long)(a + j) * ldh];
+    }
+    for (int idx = tid(); idx < d * d; idx += NTC) {
+        const int j = idx / d, i = idx - j * d;
+        acc[i + j * lda] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+
+    const int nb = cw.nb;
+    const int ihi_l = cw.ihi - a;  // local end of the active range
+    // schedule: bulge k (k = 0 bottom-most) -- first step time t0[k], step count
+    // cnt[k], local row of its first reflector r0[k]:
+    //   intro (mode 2): k = nb-1-j for bulge j: t0 = 3j, cnt = 3(nb-1-j)+1 (intro + chase)
+    //   chase (mode 0): t0 = 0, cnt = hop, r0 = p_k - a
+    //   final (mode 1): t0 = 0, cnt = ihi-1-p_k
+    int T;
+    if (cw.mode == kChaseIntro) T = 3 * nb - 2;
+    else if (cw.mode == kChaseHop) T = cw.hop;
+    else T = cw.ihi - 1 - (cw.p_bot - 3 * (nb - 1));
+    const int lane = tid() & 31, warp = tid() >> 5;
+    constexpr int NW = NTC / 32;
+    for (int t = 0; t < T; ++t) {
+        // phase R: reflectors (thread k for bulge k)
+        if (tid() < nb) {
+            const int k = tid();
+            BulgeRefl b{0, 0, 0, 0, 0, 0, 0, 0};
+            int ri = -1;
+            bool intro = false;
+            if (cw.mode == kChaseIntro) {
+                const int j = nb - 1 - k;
+                const int s = t - 3 * j;  // step index of bulge j
+                if (s >= 0 && s <= 3 * (nb - 1 - j)) {
+                    if (s == 0) intro = true;
+                    ri = s;  // intro at local row 0, then chase from row 1
+                }
+            } else {
+                const int p = cw.p_bot - 3 * k;
+                const int cnt = (cw.mode == kChaseHop) ? cw.hop : (cw.ihi - 1 - p);
+                if (t < cnt) ri = p + t - a;
+            }
+            if (ri >= 0) {
+                if (intro) {
+                    const int j = nb - 1 - k;
+                    const double re1 = shift_pairs[cw.shift_off + 4 * j], im1 = shift_pairs[cw.shift_off + 4 * j + 1];
+                    const double re2 = shift_pairs[cw.shift_off + 4 * j + 2], im2 = shift_pairs[cw.shift_off + 4 * j + 3];
+                    const double ssum = re1 + re2, sprod = re1 * re2 - im1 * im2;
+                    const double a11 = W(0, 0), a12 = W(0, 1), a21 = W(1, 0), a22 = W(1, 1);
+                    const double a32 = d > 2 ? W(2, 1) : 0.0;
+                    double sv[3] = {a11 * a11 + a12 * a21 - ssum * a11 + sprod, a21 * (a11 + a22 - ssum), a21 * a32};
+                    const double vm = fmax(fabs(sv[0]), fmax(fabs(sv[1]), fabs(sv[2])));
+                    if (vm != 0.0) {
+                        sv[0] /= vm;
+                        sv[1] /= vm;
+                        sv[2] /= vm;
+                    }
+                    double v[3], tau;
+                    b.beta = reflector<3>(sv, v, tau);
+                    b.v1 = v[1];
+                    b.v2 = v[2];
+                    b.tau = tau;
+                    b.ri = 0;
+                    b.len = 3;
+                    b.kind = 2;
+                } else {
+                    const int len = min(3, ihi_l - ri);
+                    if (len >= 2 && ri + 1 < ihi_l) {
+                        if (len == 3) {
+                            double x[3] = {W(ri, ri - 1), W(ri + 1, ri - 1), W(ri + 2, ri - 1)}, v[3], tau;
+                            b.beta = reflector<3>(x, v, tau);
+                            b.v1 = v[1];
+                            b.v2 = v[2];
+                            b.tau = tau;
+                        } else {
+                            double x[2] = {W(ri, ri - 1), W(ri + 1, ri - 1)}, v[2], tau;
+                            b.beta = reflector<2>(x, v, tau);
+                            b.v1 = v[1];
+                            b.v2 = 0.0;
+                            b.tau = tau;
+                        }
+                        b.ri = ri;
+                        b.len = len;
+                        b.kind = 1;
+                    }
+                }
+            }
+            br[k] = b;
+        }
+        __syncthreads();
+        // phase L: annihilated columns, left applications, accumulator
+        for (int k = warp; k < nb; k += NW) {
+            const BulgeRefl b = br[k];
+            if (!b.kind) continue;
+            const int ri = b.ri;
+            if (b.kind == 1 && lane < b.len) W(ri + lane, ri - 1) = (lane == 0) ? b.beta : 0.0;
+            if (b.tau == 0.0) continue;
+            const double v1 = b.v1, v2 = b.v2, tau = b.tau;
+            if (b.len == 3) {
+                for (int j = ri + lane; j < d; j += 32) {
+                    double* col = &W(ri, j);
+                    double w = (col[0] + v1 * col[1] + v2 * col[2]) * tau;
+                    col[0] -= w;
+                    col[1] -= w * v1;
+                    col[2] -= w * v2;
+                }
+                for (int i = lane; i < d; i += 32) {
+                    double* r = acc + i + ri * lda;
+                    double w = (r[0] + r[lda] * v1 + r[2 * lda] * v2) * tau;
+                    r[0] -= w;
+                    r[lda] -= w * v1;
+                    r[2 * lda] -= w * v2;
+                }
+            } else {
+                for (int j = ri + lane; j < d; j += 32) {
+                    double* col = &W(ri, j);
+                    double w = (col[0] + v1 * col[1]) * tau;
+                    col[0] -= w;
+                    col[1] -= w * v1;
+                }
+                for (int i = lane; i < d; i += 32) {
+                    double* r = acc + i + ri * lda;
+                    double w = (r[0] + r[lda] * v1) * tau;
+                    r[0] -= w;
+                    r[lda] -= w * v1;
+                }
+            }
+        }
+        __syncthreads();
+        // phase Rt: right applications on the window rows above each bulge
+        for (int k = warp; k < nb; k += NW) {
+            const BulgeRefl b = br[k];
+            if (!b.kind || b.tau == 0.0) continue;
+            const int ri = b.ri;
+            const int r1 = min(ri + b.len + 1, d);
+            const double v1 = b.v1, v2 = b.v2, tau = b.tau;
+            double* c0 = win + off[ri];
+            double* c1 = win + off[ri + 1];
+            if (b.len == 3) {
+                double* c2 = win + off[ri + 2];
+                for (int i = lane; i < r1; i += 32) {
+                    double w = (c0[i] + c1[i] * v1 + c2[i] * v2) * tau;
+                    c0[i] -= w;
+                    c1[i] -= w * v1;
+                    c2[i] -= w * v2;
+                }
+            } else {
+                for (int i = lane; i < r1; i += 32) {
+                    double w = (c0[i] + c1[i] * v1) * tau;
+                    c0[i] -= w;
+                    c1[i] -= w * v1;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // scatter the window band and publish Q_w
+    for (int j = threadIdx.x >> 5; j < d; j += NTC / 32) {
+        const int rows = min(j + 4, d);
+        for (int i = threadIdx.x & 31; i < rows; i += 32) Hg[(long long)(a + i) + (long long)(a + j) * ldh] = W(i, j);
+    }
+    double* qw = qw_pool + cw.qw_off;
+    for (int idx = tid(); idx < d * d; idx += NTC) {
+        const int j = idx / d, i = idx - j * d;
+        qw[idx] = acc[i + j * lda];
+    }
+}
+
+size_t chase_window_smem_bytes(int d) {
+    const size_t lda = (size_t)(d | 1);
+    size_t packed = 0;
+    for (int j = 0; j < d; ++j) packed += (size_t)std::min(j + 4, d);
+    return (lda * d + packed) * sizeof(double) + (size_t)(d + 2) * sizeof(int) + 64 * sizeof(BulgeRefl) + 64;
+}
+
+int chase_window_packed_len(int d) {
+    int o = 0;
+    for (int j = 0; j < d; ++j) o += std::min(j + 4, d);
+    return o;
+}
+
+cudaError_t launch_chase_window(double* H, long long ldh, const ChaseWin* wins_dev, int idx, int d,
+                                const double* shift_pairs, double* qw_pool, cudaStream_t stream) {
+    static bool init = false;
+    if (!init) {
+        cudaError_t err = cudaFuncSetAttribute(chase_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)chase_window_smem_bytes(kChaseMaxWindow));
+        if (err != cudaSuccess) return err;
+        init = true;
+    }
+    chase_window_kernel<<<1, NTC, chase_window_smem_bytes(d), stream>>>(H, ldh, wins_dev + idx, shift_pairs, qw_pool);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// whole-matrix helpers of the driver
+
+// max |h_ij| over the Hessenberg part (schur.cpp:682-685)
+__global__ void hess_norm_kernel(const double* __restrict__ H, long long ldh, int n,
+                                 unsigned long long* __restrict__ out) {
+    double m = 0.0;
+    for (long long j = blockIdx.x; j < n; j += gridDim.x) {
+        const int rows = min((int)j + 2, n);
+        for (int i = threadIdx.x; i < rows; i += blockDim.x) m = fmax(m, fabs(H[i + j * ldh]));
+    }
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+// scan_active_start_tiled (schur.cpp:581-595): largest l in (0, ihi) with a
+// negligible subdiagonal, zeroed; *out = l (0 if none)
+__global__ void scan_active_kernel(double* __restrict__ H, long long ldh, int n, int ihi, double hnorm,
+                                   int* __restrict__ out) {
+    __shared__ int best;
+    if (threadIdx.x == 0) best = 0;
+    __syncthreads();
+    const double smlnum = kSafeMinD * ((double)n / kEpsD);
+    for (int l = ihi - 1 - (int)threadIdx.x; l > 0; l -= blockDim.x) {
+        double tst = fabs(H[(l - 1) + (long long)(l - 1) * ldh]) + fabs(H[l + (long long)l * ldh]);
+        if (tst == 0.0) tst = hnorm;
+        if (fabs(H[l + (long long)(l - 1) * ldh]) <= fmax(kEpsD * tst, smlnum)) atomicMax(&best, l);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int l = best;
+        if (l > 0) H[l + (long long)(l - 1) * ldh] = 0.0;
+        *out = l;
+    }
+}
+
+cudaError_t launch_hess_norm(const double* H, long long ldh, int n, unsigned long long* out, cudaStream_t stream) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+    hess_norm_kernel<<<std::min(n, 2048), 256, 0, stream>>>(H, ldh, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scan_active(double* H, long long ldh, int n, int ihi, double hnorm, int* out,
+                               cudaStream_t stream) {
+    scan_active_kernel<<<1, 1024, 0, stream>>>(H, ldh, n, ihi, hnorm, out);
+    return cudaGetLastError();
+}
+
+}  // namespace teig

@@ -13,6 +13,11 @@ Contents (all from the reference itself):
     n=300 ws=64, with Q: S, Q, permutation, plan
   * select_fraction flags of the n=2000 synthetic input (seed 99)
   * schur_reduce of generate(hessenberg_random, n=80, seed=3): eigenvalues
+  * the Schur path: small_schur (k=30), aed_step (n=100, w=16, both
+    deflation conditions), a windowed sweep (n=64, 6 shifts, window 16),
+    the perfect-shift problem (n=24) and the known-spectrum pipeline
+    (n=150: A, hessenberg_reduce's H and Q, true spectrum, eigenvalues),
+    schur_reduce eigenvalues of generate(hessenberg_random, 300, 1)
 """
 import os
 import sys
@@ -115,6 +120,50 @@ def main():
     r = O.ref_schur_reduce(hh, None, workers=1)
     g["hess80_eig"] = r["eigenvalues"]
     g["hess80_s"] = hh
+    # Schur path (schur.cpp / kernels.cpp:260-381), all from the reference
+    h = np.asfortranarray(O.ref_generate(4, 30, 5))
+    g["ss30_in"] = h.copy()
+    ok, q, sw = O.ref_small_schur(h)
+    g["ss30_s"], g["ss30_q"], g["ss30_sweeps"] = h, q, np.array(sw)
+    h = O.ref_generate(4, 100, 13)
+    g["aed100_in"] = h.copy()
+    for cond in (0, 1):
+        hh, qq = h.copy(), np.eye(100)
+        r = O.ref_aed_step(hh, qq, 0, 100, 16, deflation=cond, tile=32)
+        g[f"aed100_c{cond}_s"], g[f"aed100_c{cond}_q"] = hh, qq
+        g[f"aed100_c{cond}_deflated"] = np.array(r["deflated"])
+        g[f"aed100_c{cond}_shifts"] = np.asarray(r["shifts"], dtype=complex)
+    h = O.ref_generate(4, 64, 37)
+    g["sw64_in"] = h.copy()
+    sh = np.array([0.2 * j + 1j * (1.0 + j) for j in range(3) for _ in (0,)])
+    shifts = []
+    for z in sh:
+        shifts += [z, np.conj(z)]
+    hh, qq = h.copy(), np.eye(64)
+    O.ref_sweep(hh, qq, 0, 64, shifts, 16, tile=8)
+    g["sw64_shifts"] = np.asarray(shifts)
+    g["sw64_s"], g["sw64_q"] = hh, qq
+    # perfect-shift problem (test_schur.cpp:238-257): Hessenberg form + shifts
+    a = O.ref_generate(3, 24, 3)
+    hr, _ = O.ref_hessenberg_reduce(a)
+    sp = O.ref_default_spectrum(24, 3)
+    z = next(x for x in sp if x.imag > 0)
+    g["ps24_a"], g["ps24_h"], g["ps24_shifts"] = a, hr, np.array([z, np.conj(z)])
+    # known-spectrum pipeline n=150 (test_schur.cpp:281-301): A, its
+    # Hessenberg form and Q, the true spectrum, the reference's eigenvalues
+    a = O.ref_generate(1, 150, 17)
+    hr, qr = O.ref_hessenberg_reduce(a)
+    g["ks150_a"], g["ks150_h"], g["ks150_q"] = a, hr, qr
+    g["ks150_true"] = O.ref_default_spectrum(150, 17)
+    hh, qq = hr.copy(), qr.copy()
+    r = O.ref_schur_reduce(hh, qq, workers=1)
+    g["ks150_eig"] = r["eigenvalues"]
+    # schur_reduce of random Hessenberg n=300 (seed 1): eigenvalues
+    h = O.ref_generate(4, 300, 1)
+    hh = h.copy()
+    r = O.ref_schur_reduce(hh, None, workers=1)
+    g["hess300_eig"] = r["eigenvalues"]
+    g["hess300_sweeps"] = np.array(r["sweeps"])
     np.savez_compressed(os.path.join(HERE, "reference_golden.npz"), **g)
     print("wrote", os.path.join(HERE, "reference_golden.npz"), sorted(g))
 
