@@ -23,6 +23,8 @@
 #include <chrono>
 #include <cmath>
 #include <complex>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -180,8 +182,22 @@ class SchurRunner {
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_out_), sizeof(AedDevOut), s_));
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_int_), sizeof(unsigned long long) * 2, s_));
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_sh_), sizeof(double) * 2 * kAedMaxWindow, s_));
+        if (getenv("TEIG_AED_PROF") && atoi(getenv("TEIG_AED_PROF"))) {
+            TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_prof_), sizeof(unsigned long long) * 8, s_));
+            TEIG_CUDA(cudaMemsetAsync(d_prof_, 0, sizeof(unsigned long long) * 8, s_));
+        }
     }
     ~SchurRunner() {
+        if (d_prof_) {
+            unsigned long long pf[8] = {0};
+            cudaMemcpy(pf, d_prof_, sizeof pf, cudaMemcpyDeviceToHost);
+            fprintf(stderr,
+                    "[teig aed prof] windows(aed)=%lld chase=%lld | Mcycles: total %.1f small %.1f swap %.1f (n=%llu) "
+                    "sweep %.1f spike %.1f | sim_steps %llu small_sweeps %llu\n",
+                    (long long)aed_windows_, (long long)chase_windows_, pf[0] / 1e6, pf[1] / 1e6, pf[2] / 1e6, pf[3],
+                    pf[4] / 1e6, pf[5] / 1e6, pf[6], pf[7]);
+            cudaFree(d_prof_);
+        }
         qw_.release(s_);
         descs_.release(s_);
         cwins_.release(s_);
@@ -264,7 +280,7 @@ class SchurRunner {
             if (w.kind == 0) {
                 last0 = (int)k;
                 TEIG_CUDA(launch_aed_window(dH_, ldh_, w.mode, (int)w.l, (int)w.a, (int)w.d, dopts_,
-                                            qw_.p + k * kSlot, d_out_, d_sh_, s_));
+                                            qw_.p + k * kSlot, d_out_, d_sh_, s_, d_prof_));
                 if (w.mode == kSchurModeAed) {
                     last_aed = (int)k;
                     ++aed_windows_;
@@ -454,6 +470,7 @@ class SchurRunner {
     AedDevOut* d_out_ = nullptr;
     int* d_int_ = nullptr;
     double* d_sh_ = nullptr;
+    unsigned long long* d_prof_ = nullptr;
     std::vector<Win> wins_;
     std::vector<ChaseWin> hchase_;
     std::vector<double> hpairs_;
