@@ -50,6 +50,10 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--workload", default="reorder", choices=["reorder", "schur"],
+                    help="reorder: C2 (headline); schur: C3 multishift QR + AED of random Hessenberg")
+    ap.add_argument("--no-schur", action="store_true", help="skip the C3 section of the default line")
+    ap.add_argument("--schur-n", type=int, default=10000)
     return ap.parse_args()
 
 
@@ -261,10 +265,111 @@ def run_ours(args, rank, world, local):
     }
     if rank == 0 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args, n)
+    if not args.no_schur:
+        out["schur_c3"] = run_schur(args, dev, with_cpu=(rank == 0 and not args.no_cpu), with_e2e=not args.no_e2e)
+        out["schur_c3"]["gpu_launches_counted_in_line"] = False
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# C3: Schur reduction (multishift QR + AED) of a random upper Hessenberg matrix
+
+SCHUR_SEED = 1
+SCHUR_CPU_N = 0     # 0: the full C3 matrix (~30 s of the reference on 16 host threads)
+
+
+def run_schur(args, dev, steps=2, warmup=1, with_cpu=True, with_e2e=True):
+    """One step = one full schur_reduce (Q accumulated, Q_in = I) of
+    generate(hessenberg_random, n, seed 1), generated in HBM (bit-identical
+    to the reference generator), restored before every step."""
+    import torch
+    import paper_2002_05024_b200 as T
+    n = args.schur_n
+    H0 = T.gen_hessenberg(n, SCHUR_SEED, device=dev)
+    H = T.colmajor_empty(n, dev)
+    Q = T.colmajor_empty(n, dev)
+    Q0 = T.identity(n, dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(warmup):
+        H.copy_(H0)
+        Q.copy_(Q0)
+        T.schur_reduce(H, Q)
+    torch.cuda.synchronize()
+    ms, infos = [], []
+    for _ in range(steps):
+        H.copy_(H0)
+        Q.copy_(Q0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = T.schur_reduce(H, Q, T.SchurOptions(profile=True))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        infos.append(res.info)
+    info = infos[-1]
+    back = float(torch.linalg.norm(H0 - Q @ H @ Q.t()) / torch.linalg.norm(H0))
+    orth = float(torch.linalg.norm(Q.t() @ Q - torch.eye(n, dtype=torch.float64, device=dev)))
+    from oracle import oracle as O
+    std = bool(O.is_standardized(H.cpu().numpy())) if n <= 12000 else None
+    t = statistics.mean(ms) / 1e3
+    tol = 10 * n * 2.220446049250313e-16
+    upd_ms = sum(i["ms_update"] for i in infos) / len(infos)
+    win_ms = sum(i["ms_window"] for i in infos) / len(infos)
+    ach = info["update_flops"] / (upd_ms * 1e-3) / 1e12 if upd_ms > 0 else 0.0
+    out = {"workload": f"C3: schur_reduce of generate(hessenberg_random, n={n}, seed {SCHUR_SEED}), Q accumulated, "
+                       f"SchurOptions defaults (norm-stable, 64 shifts, AED window 96, chase window 128)",
+           "value": round(t, 4), "unit": "s", "steps": steps, "warmup": warmup,
+           "step_ms": [round(x, 2) for x in ms], "converged": bool(info["converged"]), "sweeps": info["sweeps"],
+           "rounds": info["rounds"], "aed_windows": info["aed_windows"], "chase_windows": info["chase_windows"],
+           "update_flops": info["update_flops"], "gpu_launches": info["n_launches"],
+           "parity": {"backward_error": back, "orthogonality": orth, "tol_10neps": tol, "standardized": std,
+                      "pass": back <= tol and orth <= tol and std is not False},
+           "time_split_ms": {"window_kernels": round(win_ms, 2), "update_kernels_both_streams": round(upd_ms, 2)},
+           "roofline": {"bound": "tensor", "kernel": "update_left/right DMMA kernels of the Schur rounds",
+                        "achieved": round(ach, 3), "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                        "frac": round(ach / FP64_DMMA_PEAK_TFLOPS, 4), "traffic": None,
+                        "note": "the step is bound by the single-CTA AED window kernel (latency, no roofline): "
+                                "see time_split_ms"}}
+    if with_e2e:
+        Hh = H0.t().contiguous().cpu().numpy().copy()  # row-major of H^T == column-major of H
+        Qh = np.eye(n)
+        e2e = []
+        for _ in range(2):
+            hh, qh = Hh.copy(), Qh.copy()
+            t0 = time.perf_counter()
+            T.schur.schur_reduce_host_buffers(hh, qh, n)
+            e2e.append(time.perf_counter() - t0)
+        out["e2e"] = {"value": round(min(e2e), 4), "unit": "s", "h2d_bytes_per_step": 2 * n * n * 8,
+                      "d2h_bytes_per_step": 2 * n * n * 8, "api": "teig_schur_reduce_host (C ABI, host H,Q)"}
+    if with_cpu:
+        out["cpu_baseline"] = schur_cpu_baseline()
+    return out
+
+
+def schur_cpu_baseline(n_sample=SCHUR_CPU_N, n_full=None):
+    from oracle import oracle as O
+    n_full = n_full or 10000
+    n_sample = n_sample or n_full
+    cores = os.cpu_count() or 1
+    h = O.hessenberg_random(n_sample, SCHUR_SEED)
+    if O.ref_available():
+        r = O.ref_schur_reduce(np.ascontiguousarray(h), np.eye(n_sample), workers=cores)
+        secs, kind = r["seconds"], "reference"
+    else:
+        hf, qf = np.asfortranarray(h.copy()), np.asfortranarray(np.eye(n_sample))
+        t0 = time.perf_counter()
+        O.schur_reduce(hf, qf)
+        secs, kind, cores = time.perf_counter() - t0, "port", 1
+    full = secs * (n_full / n_sample) ** 3
+    return {"value": round(full, 2), "unit": "s", "cores": cores, "kind": kind,
+            "sample": (f"the full workload: schur_reduce of generate(hessenberg_random, n={n_sample}, seed {SCHUR_SEED}) "
+                       f"with Q, {cores} threads" if n_sample == n_full else
+                       f"schur_reduce of generate(hessenberg_random, n={n_sample}, seed {SCHUR_SEED}) with Q timed in "
+                       f"{secs:.2f} s with {cores} threads, extrapolated to n={n_full} by (n/{n_sample})^3"),
+            "sample_seconds": round(secs, 3)}
 
 
 # ---------------------------------------------------------------------------
@@ -375,10 +480,47 @@ def run_reference(args, rank, world, local):
     print(json.dumps(out), flush=True)
 
 
+def run_schur_line(args, rank, world, local):
+    """--workload schur: the C3 measurement as the line's headline."""
+    import torch
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        vals = [schur_cpu_baseline(n_full=args.schur_n) for _ in range(max(1, args.steps))]
+        v = statistics.mean(x["value"] for x in vals)
+        out = {"metric": METRIC, "impl": "reference", "value": round(v, 3), "unit": "s", "n_gpus": world,
+               "steps": args.steps, "warmup": 0, "higher_is_better": False, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference hessenberg_random generator)",
+               "config": {"workload": f"C3: schur_reduce n={args.schur_n}"}, "cpu_baseline": vals[-1],
+               "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return
+    sampler = ClockSampler(local)
+    sampler.start()
+    r = run_schur(args, dev, steps=args.steps, warmup=max(args.warmup, 1), with_cpu=(rank == 0 and not args.no_cpu),
+                  with_e2e=not args.no_e2e)
+    clocks = sampler.stop()
+    if rank != 0:
+        return
+    out = {"metric": METRIC, "value": r["value"], "unit": "s", "n_gpus": world, "steps": args.steps,
+           "warmup": max(args.warmup, 1), "ms_per_step": round(r["value"] * 1e3, 2), "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (reference hessenberg_random generator, in HBM)",
+           "config": {"workload": r["workload"], "n": args.schur_n, "parallelism": "single-gpu",
+                      "l2": "H + Q = 1.6 GB > 126 MB L2"},
+           "roofline": r["roofline"], "e2e": r.get("e2e"), "gpu_launches": r["gpu_launches"], "clocks": clocks,
+           "parity": r["parity"], "cpu_baseline": r.get("cpu_baseline"), "schur": r}
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
-    if args.impl == "reference":
+    if args.workload == "schur":
+        run_schur_line(args, rank, world, local)
+    elif args.impl == "reference":
         run_reference(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)

@@ -12,7 +12,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libtaskeig_b200.so")
+LIB_PATH = os.environ.get("TEIG_LIB_PATH") or os.path.join(HERE, "_lib", "libtaskeig_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 
 

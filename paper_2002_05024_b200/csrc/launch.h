@@ -29,7 +29,10 @@ cudaError_t launch_set_identity(double* Q, long long ldq, long long n, cudaStrea
 cudaError_t launch_gen_hessenberg(double* H, long long ldh, long long n, uint64_t seed, cudaStream_t stream);
 
 // Schur reduction window kernels (schur_window.cu)
-constexpr int kAedThreads = 256;
+#ifndef TEIG_AED_THREADS
+#define TEIG_AED_THREADS 256
+#endif
+constexpr int kAedThreads = TEIG_AED_THREADS;
 constexpr int kChaseThreads = 512;
 constexpr int kAedMaxWindow = 112;   // AED / small-solve window order limit (shared memory)
 constexpr int kChaseMaxWindow = 128; // chase window order limit

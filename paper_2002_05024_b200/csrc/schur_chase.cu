@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(NTC) chase_window_kernel(double* __restrict__ 
                         sv[2] /= vm;
                     }
                     double v[3], tau;
-                    b.beta = reflector<3>(sv, v, tau);
+                    b.beta = reflector_fast<3>(sv, v, tau);
                     b.v1 = v[1];
                     b.v2 = v[2];
                     b.tau = tau;
@@ -141,13 +141,13 @@ __global__ void __launch_bounds__(NTC) chase_window_kernel(double* __restrict__ 
                     if (len >= 2 && ri + 1 < ihi_l) {
                         if (len == 3) {
                             double x[3] = {W(ri, ri - 1), W(ri + 1, ri - 1), W(ri + 2, ri - 1)}, v[3], tau;
-                            b.beta = reflector<3>(x, v, tau);
+                            b.beta = reflector_fast<3>(x, v, tau);
                             b.v1 = v[1];
                             b.v2 = v[2];
                             b.tau = tau;
                         } else {
                             double x[2] = {W(ri, ri - 1), W(ri + 1, ri - 1)}, v[2], tau;
-                            b.beta = reflector<2>(x, v, tau);
+                            b.beta = reflector_fast<2>(x, v, tau);
                             b.v1 = v[1];
                             b.v2 = 0.0;
                             b.tau = tau;

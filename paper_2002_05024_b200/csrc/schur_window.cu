@@ -69,6 +69,7 @@ struct Ctx {
     int* nsh;     // harvested shift count per level
     SchurDevOpts o;
     unsigned long long* prof;  // shared-memory cycle counters (nullptr: off)
+    double* brf;  // per-bulge reflector table of the pipelined sweeps (64 entries)
 };
 
 // diagnostics (TEIG_AED_PROF=1): cycle counters kept by thread 0
@@ -413,14 +414,14 @@ __device__ bool small_schur_body(const Ctx& c, int lo, int n) {
                 x[2] = c.H(lo + i + 2, lo + i - 1);
             }
             double v[3], tau;
-            const double beta = reflector<3>(x, v, tau);
+            const double beta = reflector_fast<3>(x, v, tau);
             sim_step<3>(c, lo + i, v, tau, beta, i > l ? lo + i - 1 : -1, lo + min(i + 4, ihi));
         }
         {
             const int i = ihi - 2;
             double x[2] = {c.H(lo + i, lo + i - 1), c.H(lo + i + 1, lo + i - 1)};
             double v[2], tau;
-            const double beta = reflector<2>(x, v, tau);
+            const double beta = reflector_fast<2>(x, v, tau);
             sim_step<2>(c, lo + i, v, tau, beta, lo + i - 1, lo + ihi);
         }
     }
@@ -591,14 +592,123 @@ __device__ int chase_step_dev(const Ctx& c, int lo, int ihi, int r) {
     const int r1 = lo + min(r + len + 1, ihi);
     if (len == 3) {
         double x[3] = {c.H(g, g - 1), c.H(g + 1, g - 1), c.H(g + 2, g - 1)}, v[3], tau;
-        const double beta = reflector<3>(x, v, tau);
+        const double beta = reflector_fast<3>(x, v, tau);
         sim_step<3>(c, g, v, tau, beta, g - 1, r1);
     } else {
         double x[2] = {c.H(g, g - 1), c.H(g + 1, g - 1)}, v[2], tau;
-        const double beta = reflector<2>(x, v, tau);
+        const double beta = reflector_fast<2>(x, v, tau);
         sim_step<2>(c, g, v, tau, beta, g - 1, r1);
     }
     return r + 1;
+}
+
+// one bulge's reflector at one step of a pipelined sweep
+struct BRf {
+    double v1, v2, tau, beta;
+    int g, len, kind, r1;  // kind: 0 idle, 1 chase step, 2 intro
+};
+
+// The multishift sweep of multishift_schur_dense (schur.cpp:374-393) on the
+// active block [l, ihi) of the block at lo, in place, with the nb bulges
+// PIPELINED: bulge j is introduced at time 3j and then moves one row per time
+// step (the reference introduces and partially chases them one by one, then
+// chases each to the end).  At every position the lower bulge still acts
+// first, and bulges 3 rows apart act on disjoint index sets, so this only
+// reorders commuting left/right multiplications; depth 3nb + active instead
+// of ~nb * active.  pairs: (re1, im1, re2, im2) per bulge.
+__device__ void sweep_pipelined(const Ctx& c, int lo, int l, int ihi, int nb, const double* pairs) {
+    BRf* tb = reinterpret_cast<BRf*>(c.brf);
+    const int aw = ihi - l;
+    const int T = 3 * (nb - 1) + (ihi - 1 - l);
+    const int M = 2 * c.N + c.nspk;
+    for (int t = 0; t < T; ++t) {
+        if (tid() < nb) {
+            const int j = tid(), s = t - 3 * j;
+            BRf b{0.0, 0.0, 0.0, 0.0, 0, 0, 0, 0};
+            if (s == 0) {
+                const double re1 = pairs[4 * j], im1 = pairs[4 * j + 1], re2 = pairs[4 * j + 2], im2 = pairs[4 * j + 3];
+                double sv[3], v[3], tau;
+                shift_vec_dev(c, lo + l, aw, re1 + re2, re1 * re2 - im1 * im2, sv);
+                b.beta = reflector_fast<3>(sv, v, tau);
+                b.v1 = v[1];
+                b.v2 = v[2];
+                b.tau = tau;
+                b.g = lo + l;
+                b.len = 3;
+                b.kind = 2;
+                b.r1 = lo + l + min(4, aw);
+            } else if (s > 0 && l + s < ihi - 1) {
+                const int r = l + s, len = min(3, ihi - r), g = lo + r;
+                if (len == 3) {
+                    double x[3] = {c.H(g, g - 1), c.H(g + 1, g - 1), c.H(g + 2, g - 1)}, v[3], tau;
+                    b.beta = reflector_fast<3>(x, v, tau);
+                    b.v1 = v[1];
+                    b.v2 = v[2];
+                    b.tau = tau;
+                } else {
+                    double x[2] = {c.H(g, g - 1), c.H(g + 1, g - 1)}, v[2], tau;
+                    b.beta = reflector_fast<2>(x, v, tau);
+                    b.v1 = v[1];
+                    b.tau = tau;
+                }
+                b.g = g;
+                b.len = len;
+                b.kind = 1;
+                b.r1 = lo + min(r + len + 1, ihi);
+            }
+            tb[j] = b;
+        }
+        __syncthreads();
+        for (int it = tid(); it < nb * c.N; it += NT) {
+            const int j = it / c.N, col = it - j * c.N;
+            const BRf b = tb[j];
+            if (!b.kind) continue;
+            if (b.kind == 1 && col < b.len) c.H(b.g + col, b.g - 1) = (col == 0) ? b.beta : 0.0;
+            if (b.tau == 0.0 || col < b.g) continue;
+            double* p = &c.H(b.g, col);
+            if (b.len == 3) {
+                const double w = (p[0] + b.v1 * p[1] + b.v2 * p[2]) * b.tau;
+                p[0] -= w;
+                p[1] -= w * b.v1;
+                p[2] -= w * b.v2;
+            } else {
+                const double w = (p[0] + b.v1 * p[1]) * b.tau;
+                p[0] -= w;
+                p[1] -= w * b.v1;
+            }
+        }
+        __syncthreads();
+        for (int it = tid(); it < nb * M; it += NT) {
+            const int j = it / M, k = it - j * M;
+            const BRf b = tb[j];
+            if (!b.kind || b.tau == 0.0) continue;
+            double* p;
+            int cs;
+            if (k < c.N) {
+                if (k >= b.r1) continue;
+                p = &c.H(k, b.g);
+                cs = c.H.ld;
+            } else if (k < 2 * c.N) {
+                p = &c.Q(k - c.N, b.g);
+                cs = c.Q.ld;
+            } else {
+                const Spk& sp = c.spk[k - 2 * c.N];
+                p = sp.p + (b.g - sp.off);
+                cs = 1;
+            }
+            if (b.len == 3) {
+                const double w = (p[0] + p[cs] * b.v1 + p[2 * cs] * b.v2) * b.tau;
+                p[0] -= w;
+                p[cs] -= w * b.v1;
+                p[2 * cs] -= w * b.v2;
+            } else {
+                const double w = (p[0] + p[cs] * b.v1) * b.tau;
+                p[0] -= w;
+                p[cs] -= w * b.v1;
+            }
+        }
+        __syncthreads();
+    }
 }
 
 // multishift_schur_dense (schur.cpp:304-399) on the block [lo, lo+n), in place
@@ -712,27 +822,12 @@ __device__ bool mshift_dev(Ctx& c, int lo, int n) {
         if (nb == 0) continue;
         const int aw = ihi - l;
         PF_T0();
-        // intro + chase of nb bulges over the active block, in place
-        for (int j = 0; j < nb; ++j) {
-            double re1, im1, re2, im2;
-            if (exc) {
-                re1 = ex[0]; im1 = ex[1]; re2 = ex[2]; im2 = ex[3];
-            } else {
-                re1 = pk[4 * j]; im1 = pk[4 * j + 1]; re2 = pk[4 * j + 2]; im2 = pk[4 * j + 3];
-            }
-            const double ssum = re1 + re2, sprod = re1 * re2 - im1 * im2;
-            double sv[3], v[3], tau;
-            shift_vec_dev(c, lo + l, aw, ssum, sprod, sv);
-            (void)reflector<3>(sv, v, tau);
-            sim_step<3>(c, lo + l, v, tau, 0.0, -1, lo + l + min(4, aw));
-            int r = l + 1;
-            const int target = l + 1 + 3 * (nb - 1 - j);
-            while (r < target) r = chase_step_dev(c, lo, ihi, r);
+        if (exc) {
+            if (tid() == 0)
+                for (int q = 0; q < 4; ++q) pk[q] = ex[q];
+            __syncthreads();
         }
-        for (int j = 0; j < nb; ++j) {
-            int r = l + 1 + 3 * (nb - 1 - j);
-            while (r < ihi - 1) r = chase_step_dev(c, lo, ihi, r);
-        }
+        sweep_pipelined(c, lo, l, ihi, nb, pk);
         PF_ADD(kPfSweep);
     }
     return true;
@@ -909,6 +1004,8 @@ __global__ void __launch_bounds__(NT) aed_window_kernel(double* __restrict__ Hg,
     base += (size_t)kMaxSpk * 2 * (w + 4);
     c.spkb = base;
     base += (size_t)kMaxSpk * w;
+    c.brf = base;
+    base += 64 * 6;
     c.iscr = reinterpret_cast<int*>(base);
     c.nsh = c.iscr + 8;
     c.o = o;
@@ -954,7 +1051,7 @@ __global__ void __launch_bounds__(NT) aed_window_kernel(double* __restrict__ Hg,
 
 size_t aed_window_smem_bytes(int w) {
     const size_t ld = (size_t)(w | 1);
-    const size_t dbl = 2 * ld * w + 32 + w + 40 + kMaxSpk * 2 * w + kMaxSpk * 2 * (w + 4) + kMaxSpk * w;
+    const size_t dbl = 2 * ld * w + 32 + w + 40 + kMaxSpk * 2 * w + kMaxSpk * 2 * (w + 4) + kMaxSpk * w + 64 * 6;
     return dbl * sizeof(double) + 32 * sizeof(int);
 }
 

@@ -139,6 +139,34 @@ __device__ __forceinline__ double reflector(const double (&x)[L], double (&v)[L]
     return beta;
 }
 
+// Householder reflector of a length-L (2 or 3) vector with the reference's
+// conventions (beta = -sign(x0)||x||, v[0] = 1, zero tail -> tau = 0;
+// kernels.cpp:24-58) in one square root and one division: mathematically the
+// same reflector as reflector<L> (the reference's scaled two-pass norm and
+// rescale loop are kept for the out-of-range cases only), used on the bulge
+// chase critical path.
+template <int L>
+__device__ __forceinline__ double reflector_fast(const double (&x)[L], double (&v)[L], double& tau) {
+    const double alpha = x[0];
+    double mx = 0.0;
+#pragma unroll
+    for (int i = 1; i < L; ++i) mx = fmax(mx, fabs(x[i]));
+    const double s = fmax(mx, fabs(alpha));
+    if (mx == 0.0 || !(s > 1e-140 && s < 1e140)) return reflector<L>(x, v, tau);
+    double ss = alpha * alpha;
+#pragma unroll
+    for (int i = 1; i < L; ++i) ss = fma(x[i], x[i], ss);
+    const double beta = -sgnd(alpha) * sqrt(ss);
+    const double u = beta - alpha;           // |u| = |alpha| + ||x|| > 0
+    const double r = 1.0 / (beta * u);
+    tau = u * u * r;                         // (beta - alpha) / beta
+    const double inv = -beta * r;            // 1 / (alpha - beta)
+    v[0] = 1.0;
+#pragma unroll
+    for (int i = 1; i < L; ++i) v[i] = x[i] * inv;
+    return beta;
+}
+
 // Complete-pivoting LU of a K x K system (reference kernels.cpp:419-464),
 // kept so that the refinement solve (kernels.cpp:501-504, which refactors the
 // same matrix) replays the identical elimination on the new right-hand side

@@ -231,3 +231,16 @@ def small_schur(h, stream=None):
     if cb_h:
         h.copy_(hw)
     return bool(conv.value), qt.t()
+
+
+def schur_reduce_host_buffers(h_buf: np.ndarray, q_buf: Optional[np.ndarray], n: int,
+                              opts: Optional[SchurOptions] = None) -> dict:
+    """Reduces HOST buffers holding H and Q COLUMN-MAJOR with ld = n (e.g. a
+    C-ordered array of H^T) in place through the C ABI's host entry point;
+    host<->device copies happen inside the call."""
+    assert h_buf.dtype == np.float64 and h_buf.size == n * n and h_buf.flags.contiguous
+    o = _opts(opts)
+    info = N.SchurInfo()
+    N.check(N.lib().teig_schur_reduce_host(n, _vp(h_buf), n, _vp(q_buf) if q_buf is not None else None, n,
+                                           C.byref(o), None, None, C.byref(info), None))
+    return {f: getattr(info, f) for f, _ in N.SchurInfo._fields_ if f != "pad"}
