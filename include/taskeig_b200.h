@@ -224,6 +224,55 @@ int teig_gen_schur_input_device(int64_t n, double* dS, int64_t lds, uint64_t fil
 int teig_gen_hessenberg_device(int64_t n, double* dH, int64_t ldh, uint64_t seed, void* stream);
 int teig_set_identity_device(int64_t n, double* dQ, int64_t ldq, void* stream);
 
+
+/* ------------------------------------------------------------------------ */
+/* Multi-GPU reordering: S in column slabs, Q in   */
+/* row slabs, one NCCL all-reduce of the packed Q_w per wavefront, halo      */
+/* transfers for windows straddling a slab boundary.  Same result, bit for   */
+/* bit, as teig_reorder_schur_device (replaces the reference's distributed   */
+/* execution of reorder_schur's window tasks, reorder.cpp:330-364 /          */
+/* window_tasks.cpp:31-87, which StarNEig runs over MPI+StarPU).             */
+
+/* Balanced slab boundaries (world+1 each): column slabs with equal left +
+ * right update flops (from the planner), >= 256 columns each; equal Q row
+ * slabs. */
+int teig_dist_balance(int64_t n, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
+                      int64_t window_size, int32_t world, int64_t* col_bounds, int64_t* row_bounds);
+
+/* Host-side communication schedule of the first pass (no device work): per
+ * transfer 8 int64 (level, phase, src, dst, r0, r1, c0, c1); phase 0 window
+ * halo in, 1 panel halo in, 2 halo back.  Returns the transfer count. */
+int64_t teig_dist_schedule(int64_t n, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
+                           int64_t window_size, int32_t world, const int64_t* col_bounds, int64_t* out,
+                           int64_t cap);
+
+/* One rank of the distributed reorder.  nccl_comm: from teig_nccl_comm_init
+ * (one process per GPU: dS_slabs/dQ_slabs hold THIS rank's slab), or NULL for
+ * the loopback mode (all `world` ranks in this process on the current device:
+ * dS_slabs/dQ_slabs hold every rank's slab, rank ignored).  S slab of rank r:
+ * n x (C[r+1]-C[r]+128) column-major, ld lds (>= n), columns [C[r], C[r+1])
+ * plus a 128-column halo; Q slab of rank r: (R[r+1]-R[r]) x n column-major,
+ * ld R[r+1]-R[r], rows [R[r], R[r+1]) (dQ_slabs NULL: no Q).  Arguments as
+ * teig_reorder_schur_device otherwise. */
+int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_comm,
+                            double* const* dS_slabs, int64_t lds, double* const* dQ_slabs,
+                            const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb,
+                            const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
+                            int64_t* perm, int64_t* rejected, teig_reorder_info* info, void* stream);
+
+/* NCCL plumbing (libnccl.so.2 resolved at run time). */
+int teig_nccl_available(void);
+int teig_nccl_unique_id(uint8_t* id128);
+int teig_nccl_comm_init(int32_t world, int32_t rank, const uint8_t* id128, void** comm);
+int teig_nccl_comm_destroy(void* comm);
+
+/* Slab generators: columns [c0, c1) of the synthetic Schur form into dS
+ * (ld lds, column c0 first); rows [r0, r1) of the identity into dQ (ld ldq). */
+int teig_gen_schur_input_cols_device(int64_t n, double* dS, int64_t lds, int64_t c0, int64_t c1,
+                                     uint64_t fill_seed, void* stream);
+int teig_set_identity_rows_device(int64_t n, double* dQ, int64_t ldq, int64_t r0, int64_t r1,
+                                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -93,6 +93,16 @@ SIGNATURES = {
     "teig_chase_bulges_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _I64, _P, _I64, _P, _P]),
     "teig_small_schur_device": (C.c_int, [_I64, _P, _I64, _P, _P, _P]),
     "teig_deflation_check": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.c_double]),
+    "teig_dist_balance": (C.c_int, [_I64, _I64, _P, _P, _I64, C.c_int32, _P, _P]),
+    "teig_dist_schedule": (C.c_int64, [_I64, _I64, _P, _P, _I64, C.c_int32, _P, _P, _I64]),
+    "teig_dist_reorder_schur": (C.c_int, [_I64, C.c_int32, C.c_int32, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P,
+                                          _P, _P, _P, _P]),
+    "teig_nccl_available": (C.c_int, []),
+    "teig_nccl_unique_id": (C.c_int, [_P]),
+    "teig_nccl_comm_init": (C.c_int, [C.c_int32, C.c_int32, _P, _P]),
+    "teig_nccl_comm_destroy": (C.c_int, [_P]),
+    "teig_gen_schur_input_cols_device": (C.c_int, [_I64, _P, _I64, _I64, _I64, C.c_uint64, _P]),
+    "teig_set_identity_rows_device": (C.c_int, [_I64, _P, _I64, _I64, _I64, _P]),
 }
 
 _lib = None

@@ -21,6 +21,13 @@ struct WinDesc {
     int32_t tr_pref;   // exclusive prefix of right-update tiles (S) within the level
     int32_t tq_pref;   // exclusive prefix of factor-update tiles (Q) within the level
     int32_t pad;
+    // index ranges the update kernels cover (absolute matrix coordinates; the
+    // matrix pointers passed to the kernels are bases such that absolute
+    // (i, j) lives at base[i + j*ld] -- for a column slab / row slab of a
+    // distributed matrix the base is offset accordingly):
+    int32_t lc0, lc1;  // left update:   S[a:b, lc0:lc1]   (single GPU: b, n)
+    int32_t rr0, rr1;  // right update:  S[rr0:rr1, a:b]   (single GPU: 0, a)
+    int32_t qr0, qr1;  // factor update: Q[qr0:qr1, a:b]   (single GPU: 0, n)
 };
 
 // Per-window outcome flags written by the window kernel.

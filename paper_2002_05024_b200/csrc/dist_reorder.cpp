@@ -1,0 +1,738 @@
+// dist_reorder.cpp -- multi-GPU Schur-form reordering (SURVEY.md 8e, config
+// C4): S distributed over the ranks in COLUMN SLABS, Q in ROW SLABS, one
+// NCCL all-reduce of the packed Q_w of every wavefront, point-to-point
+// transfers only for windows that straddle a slab boundary.
+//
+// Why this layout (reference: the per-window L/R/Q tasks of
+// window_tasks.cpp:12-102, scheduled by reorder.cpp:330-364):
+//   * the LEFT update S[a:b, b:n] <- Q_w^T S[a:b, b:n] acts column by column,
+//     so with column slabs every rank updates its own columns of every
+//     window's row panel -- no data exchange, only Q_w;
+//   * the RIGHT update S[0:a, a:b] <- S[0:a, a:b] Q_w and the window kernel
+//     need whole columns [a, b): they run on the rank owning column a; when
+//     the window straddles into the next slab, the neighbour ships the missing
+//     columns into a 128-column halo of the owner's slab and takes them back
+//     afterwards ("gather/scatter windows that straddle blocks via
+//     ncclSend/ncclRecv");
+//   * the Q update Q[:, a:b] <- Q[:, a:b] Q_w acts row by row: Q in row slabs
+//     spreads that half of all flops evenly over the ranks.
+// Slab boundaries are chosen from the plan's per-column work profile so
+// every rank gets the same S-update flops (teig_dist_balance).
+//
+// Per wavefront level (windows pairwise disjoint), on every rank:
+//   P1 halo-in  (window rows)   neighbour -> owner, for straddling windows
+//   P2 window kernels of the windows this rank owns
+//   P3 all-reduce(sum) of the level's Q_w slots (owners wrote theirs, the
+//      other ranks' slots are zero: the sum is exact)
+//   P4 left updates of all windows, this rank's columns
+//   P5 halo-in  (rows above the window, after P4 -- the neighbour's left
+//      updates of the level touched them)
+//   P6 right updates of the owned windows (slab + halo)
+//   P7 halo-out (rows 0..b of the halo columns) owner -> neighbour
+//   P8 Q updates of all windows, this rank's Q rows
+// Every matrix element receives exactly the single-GPU sequence of updates
+// (same kernels, same per-element k order): the distributed result is
+// bitwise identical to teig_reorder_schur_device.
+//
+// Communication is behind `Comm`: NCCL (one rank per process, one GPU per
+// rank) or a loopback that runs all ranks inside one process on one device
+// (peer copies) -- used to test the distributed algorithm on a single GPU.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/taskeig_b200.h"
+#include "device_types.h"
+#include "launch.h"
+#include "plan.h"
+
+namespace teig {
+
+int set_error(int code, const std::string& msg);
+int64_t default_tile_size(int64_t n);
+
+namespace {
+
+#define TEIG_CUDA(expr)                                                                          \
+    do {                                                                                         \
+        cudaError_t _e = (expr);                                                                 \
+        if (_e != cudaSuccess)                                                                   \
+            throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(_e) + " at " + \
+                                     __FILE__ + ":" + std::to_string(__LINE__));                 \
+    } while (0)
+
+constexpr int64_t kHalo = 128;  // halo columns right of every S slab
+
+// ---------------------------------------------------------------------------
+// NCCL, resolved at run time (no link-time dependency of the library)
+
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (tried) return api;
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the one torch already loaded, if any
+    if (!h) {
+        const char* env = getenv("TEIG_NCCL_LIB");
+        h = dlopen(env && *env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    }
+    if (!h) return api;
+    auto sym = [&](const char* name) { return dlsym(h, name); };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Send && api.Recv &&
+             api.GroupStart && api.GroupEnd && api.GetErrorString;
+    return api;
+}
+
+#define TEIG_NCCL(expr)                                                                              \
+    do {                                                                                             \
+        ncclResult_t _r = (expr);                                                                    \
+        if (_r != ncclSuccess)                                                                       \
+            throw std::runtime_error(std::string("NCCL error ") + nccl().GetErrorString(_r) + " at " + \
+                                     __FILE__ + ":" + std::to_string(__LINE__));                     \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// per-rank state
+
+struct RankBufs {
+    int rank = 0;
+    double* S = nullptr;  // virtual base: absolute (i, j) at S[i + j*lds]
+    double* Q = nullptr;  // virtual base: absolute (i, j) at Q[i + j*ldq]
+    int64_t ldq = 0;
+    double* qw = nullptr;       // Q_w slots of the pass (all windows)
+    WinDesc* descs = nullptr;   // per-level descriptor arrays of this rank
+    uint8_t *sizes = nullptr, *sel = nullptr, *order = nullptr, *stuck = nullptr;
+    int32_t* status = nullptr;
+    double* stage = nullptr;    // contiguous staging for NCCL transfers
+    size_t stage_cap = 0;
+};
+
+// a submatrix move between two ranks' slabs (absolute coordinates)
+struct Xfer {
+    int src, dst;
+    int64_t r0, r1, c0, c1;
+};
+
+class Comm {
+   public:
+    virtual ~Comm() = default;
+    virtual bool local(int r) const = 0;
+    // sum-all-reduce of `count` elements at byte offset `off` of every local
+    // rank's buffer (ptrs[r] indexes local ranks' buffers by rank)
+    virtual void allreduce(const std::vector<void*>& bufs, size_t count, ncclDataType_t t, cudaStream_t s) = 0;
+    virtual void transfer(std::vector<RankBufs>& R, const std::vector<Xfer>& xs, int64_t lds, cudaStream_t s) = 0;
+};
+
+size_t dtype_size(ncclDataType_t t) {
+    switch (t) {
+        case ncclFloat64: return 8;
+        case ncclInt32: return 4;
+        default: return 1;
+    }
+}
+
+// all ranks in this process, one device: collectives are peer copies
+class LoopbackComm : public Comm {
+   public:
+    explicit LoopbackComm(int world) : world_(world) {}
+    bool local(int) const override { return true; }
+    void allreduce(const std::vector<void*>& bufs, size_t count, ncclDataType_t t, cudaStream_t s) override;
+    void transfer(std::vector<RankBufs>& R, const std::vector<Xfer>& xs, int64_t lds, cudaStream_t s) override {
+        for (const auto& x : xs) {
+            const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
+            if (rows <= 0 || cols <= 0) continue;
+            TEIG_CUDA(cudaMemcpy2DAsync(R[x.dst].S + x.r0 + x.c0 * lds, lds * 8, R[x.src].S + x.r0 + x.c0 * lds,
+                                        lds * 8, rows * 8, cols, cudaMemcpyDeviceToDevice, s));
+        }
+    }
+
+   private:
+    int world_;
+};
+
+void LoopbackComm::allreduce(const std::vector<void*>& bufs, size_t count, ncclDataType_t t, cudaStream_t s) {
+    // element-wise sum of every rank's buffer, written back to all of them
+    TEIG_CUDA(launch_sum_buffers(bufs.data(), (int)bufs.size(), count, (int)dtype_size(t), s));
+}
+
+class NcclComm : public Comm {
+   public:
+    NcclComm(ncclComm_t c, int rank) : c_(c), rank_(rank) {}
+    bool local(int r) const override { return r == rank_; }
+    void allreduce(const std::vector<void*>& bufs, size_t count, ncclDataType_t t, cudaStream_t s) override {
+        void* b = bufs[rank_];
+        TEIG_NCCL(nccl().AllReduce(b, b, count, t, ncclSum, c_, s));
+    }
+    void transfer(std::vector<RankBufs>& R, const std::vector<Xfer>& xs, int64_t lds, cudaStream_t s) override {
+        // pack every outgoing piece, exchange in one group, unpack
+        RankBufs& me = R[rank_];
+        size_t need = 0;
+        for (const auto& x : xs)
+            if (x.src == rank_ || x.dst == rank_) need += (size_t)std::max<int64_t>(0, x.r1 - x.r0) * std::max<int64_t>(0, x.c1 - x.c0);
+        if (need == 0) return;
+        if (need > me.stage_cap) {
+            if (me.stage) TEIG_CUDA(cudaFreeAsync(me.stage, s));
+            me.stage_cap = std::max(need, me.stage_cap * 2);
+            TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&me.stage), me.stage_cap * 8, s));
+        }
+        size_t off = 0;
+        std::vector<size_t> offs(xs.size());
+        for (size_t i = 0; i < xs.size(); ++i) {
+            const auto& x = xs[i];
+            offs[i] = off;
+            if (x.src != rank_ && x.dst != rank_) continue;
+            const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
+            if (rows <= 0 || cols <= 0) continue;
+            if (x.src == rank_)
+                TEIG_CUDA(cudaMemcpy2DAsync(me.stage + off, rows * 8, me.S + x.r0 + x.c0 * lds, lds * 8, rows * 8, cols,
+                                            cudaMemcpyDeviceToDevice, s));
+            off += (size_t)rows * cols;
+        }
+        TEIG_NCCL(nccl().GroupStart());
+        for (size_t i = 0; i < xs.size(); ++i) {
+            const auto& x = xs[i];
+            const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
+            if (rows <= 0 || cols <= 0) continue;
+            if (x.src == rank_) TEIG_NCCL(nccl().Send(me.stage + offs[i], (size_t)rows * cols, ncclFloat64, x.dst, c_, s));
+            else if (x.dst == rank_) TEIG_NCCL(nccl().Recv(me.stage + offs[i], (size_t)rows * cols, ncclFloat64, x.src, c_, s));
+        }
+        TEIG_NCCL(nccl().GroupEnd());
+        for (size_t i = 0; i < xs.size(); ++i) {
+            const auto& x = xs[i];
+            const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
+            if (rows <= 0 || cols <= 0 || x.dst != rank_) continue;
+            TEIG_CUDA(cudaMemcpy2DAsync(me.S + x.r0 + x.c0 * lds, lds * 8, me.stage + offs[i], rows * 8, rows * 8, cols,
+                                        cudaMemcpyDeviceToDevice, s));
+        }
+    }
+
+   private:
+    ncclComm_t c_;
+    int rank_;
+};
+
+// ---------------------------------------------------------------------------
+
+struct LevelPlan {
+    // per rank: offsets (into that rank's desc array) and counts
+    struct Part {
+        int64_t w_off = 0, w_cnt = 0;                  // window kernels (owned)
+        int64_t l_off = 0, l_cnt = 0, l_tiles = 0;     // left updates
+        int64_t r_off = 0, r_cnt = 0, r_tiles = 0;     // right updates (owned)
+        int64_t q_off = 0, q_cnt = 0, q_tiles = 0;     // Q updates
+    };
+    std::vector<Part> part;          // [rank]
+    int64_t qw_off = 0, qw_len = 0;  // the level's Q_w slots
+    std::vector<Xfer> halo_win, halo_panel, halo_back;
+    int dmax = 64;
+};
+
+int owner_of(const std::vector<int64_t>& C, int64_t col) {
+    return (int)(std::upper_bound(C.begin(), C.end(), col) - C.begin()) - 1;
+}
+
+struct PassOut {
+    int64_t windows = 0, levels = 0, launches = 0;
+    bool deviated = false;
+};
+
+PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankBufs>& R, Comm& comm, int64_t lds,
+                      const std::vector<int64_t>& C, const std::vector<int64_t>& Rw, bool with_q,
+                      std::vector<BlockState>& blocks, std::vector<int64_t>& rejected, std::vector<int64_t>& plan_log,
+                      bool strict, cudaStream_t s) {
+    PassOut po;
+    const int64_t nw = (int64_t)plan.windows.size();
+    schedule_levels(plan, n);
+    const int nl = plan.n_levels;
+    std::vector<int64_t> idx(nw);
+    for (int64_t i = 0; i < nw; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](int64_t x, int64_t y) { return plan.windows[x].level < plan.windows[y].level; });
+    // Q_w slots in level order; window kernel status in plan order
+    std::vector<int64_t> qw_off(nw);
+    int64_t qw_total = 0;
+    for (int64_t k = 0; k < nw; ++k) {
+        const auto& w = plan.windows[idx[k]];
+        qw_off[idx[k]] = qw_total;
+        qw_total += (w.wbot - w.wtop) * (w.wbot - w.wtop);
+    }
+    // per-rank descriptor arrays, level by level
+    std::vector<std::vector<WinDesc>> D(world);
+    std::vector<std::vector<int64_t>> Dp(world);  // plan index of every descriptor
+    std::vector<LevelPlan> L(nl);
+    int64_t k = 0;
+    for (int lv = 0; lv < nl; ++lv) {
+        LevelPlan& lp = L[lv];
+        lp.part.resize(world);
+        const int64_t k0 = k;
+        while (k < nw && plan.windows[idx[k]].level == lv) ++k;
+        lp.qw_off = qw_off[idx[k0]];
+        lp.qw_len = 0;
+        for (int64_t t = k0; t < k; ++t) {
+            const auto& w = plan.windows[idx[t]];
+            lp.qw_len += (w.wbot - w.wtop) * (w.wbot - w.wtop);
+            lp.dmax = std::max<int>(lp.dmax, (int)(w.wbot - w.wtop));
+        }
+        lp.dmax = lp.dmax <= 64 ? 64 : 128;
+        for (int r = 0; r < world; ++r) {
+            auto& P = lp.part[r];
+            auto base = [&](int64_t t) {
+                const auto& w = plan.windows[idx[t]];
+                WinDesc d{};
+                d.a = (int32_t)w.wtop;
+                d.d = (int32_t)(w.wbot - w.wtop);
+                d.nb = (int32_t)w.count;
+                d.qw_off = qw_off[idx[t]];
+                d.blk_off = w.blk_off;
+                return d;
+            };
+            // window kernels of the owned windows
+            P.w_off = (int64_t)D[r].size();
+            for (int64_t t = k0; t < k; ++t)
+                if (owner_of(C, plan.windows[idx[t]].wtop) == r) D[r].push_back(base(t)), Dp[r].push_back(idx[t]), ++P.w_cnt;
+            // left updates: this rank's columns of every row panel
+            P.l_off = (int64_t)D[r].size();
+            for (int64_t t = k0; t < k; ++t) {
+                const auto& w = plan.windows[idx[t]];
+                const int64_t c0 = std::max<int64_t>(w.wbot, C[r]), c1 = C[r + 1];
+                if (c1 <= c0) continue;
+                WinDesc d = base(t);
+                d.lc0 = (int32_t)c0;
+                d.lc1 = (int32_t)c1;
+                d.tl_pref = (int32_t)P.l_tiles;
+                P.l_tiles += (c1 - c0 + kLeftBN - 1) / kLeftBN;
+                D[r].push_back(d);
+                Dp[r].push_back(-1);
+                ++P.l_cnt;
+            }
+            // right updates of the owned windows
+            P.r_off = (int64_t)D[r].size();
+            for (int64_t t = k0; t < k; ++t) {
+                const auto& w = plan.windows[idx[t]];
+                if (owner_of(C, w.wtop) != r || w.wtop == 0) continue;
+                WinDesc d = base(t);
+                d.rr0 = 0;
+                d.rr1 = (int32_t)w.wtop;
+                d.tr_pref = (int32_t)P.r_tiles;
+                P.r_tiles += (w.wtop + kRightBM - 1) / kRightBM;
+                D[r].push_back(d);
+                Dp[r].push_back(-1);
+                ++P.r_cnt;
+            }
+            // Q updates: this rank's Q rows
+            P.q_off = (int64_t)D[r].size();
+            if (with_q && Rw[r + 1] > Rw[r])
+                for (int64_t t = k0; t < k; ++t) {
+                    WinDesc d = base(t);
+                    d.qr0 = (int32_t)Rw[r];
+                    d.qr1 = (int32_t)Rw[r + 1];
+                    d.tq_pref = (int32_t)P.q_tiles;
+                    P.q_tiles += (Rw[r + 1] - Rw[r] + kRightBM - 1) / kRightBM;
+                    D[r].push_back(d);
+                    Dp[r].push_back(-1);
+                    ++P.q_cnt;
+                }
+        }
+        // straddling windows: halo transfers
+        for (int64_t t = k0; t < k; ++t) {
+            const auto& w = plan.windows[idx[t]];
+            const int o = owner_of(C, w.wtop);
+            if (w.wbot <= C[o + 1]) continue;
+            const int nbr = o + 1;
+            if (nbr >= world || w.wbot > C[nbr + 1] || w.wbot - C[nbr] > kHalo)
+                throw std::runtime_error("distributed reorder: a window spans more than two slabs");
+            lp.halo_win.push_back(Xfer{nbr, o, w.wtop, w.wbot, C[nbr], w.wbot});
+            if (w.wtop > 0) lp.halo_panel.push_back(Xfer{nbr, o, 0, w.wtop, C[nbr], w.wbot});
+            lp.halo_back.push_back(Xfer{o, nbr, 0, w.wbot, C[nbr], w.wbot});
+        }
+    }
+    // device buffers of the pass, per local rank
+    const size_t ne = plan.sizes.size();
+    std::vector<void*> qw_bufs(world, nullptr), ord_bufs(world, nullptr), stk_bufs(world, nullptr);
+    for (int r = 0; r < world; ++r) {
+        if (!comm.local(r)) continue;
+        RankBufs& B = R[r];
+        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.qw), sizeof(double) * std::max<int64_t>(qw_total, 1), s));
+        TEIG_CUDA(cudaMemsetAsync(B.qw, 0, sizeof(double) * std::max<int64_t>(qw_total, 1), s));
+        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.descs), sizeof(WinDesc) * std::max<size_t>(D[r].size(), 1), s));
+        if (!D[r].empty())
+            TEIG_CUDA(cudaMemcpyAsync(B.descs, D[r].data(), sizeof(WinDesc) * D[r].size(), cudaMemcpyHostToDevice, s));
+        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.sizes), ne + 1, s));
+        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.sel), ne + 1, s));
+        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.order), ne + 1, s));
+        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.stuck), ne + 1, s));
+        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.status), sizeof(int32_t) * std::max<size_t>(D[r].size(), 1), s));
+        TEIG_CUDA(cudaMemsetAsync(B.order, 0, ne + 1, s));
+        TEIG_CUDA(cudaMemsetAsync(B.stuck, 0, ne + 1, s));
+        TEIG_CUDA(cudaMemsetAsync(B.status, 0, sizeof(int32_t) * std::max<size_t>(D[r].size(), 1), s));
+        TEIG_CUDA(cudaMemcpyAsync(B.sizes, plan.sizes.data(), ne, cudaMemcpyHostToDevice, s));
+        TEIG_CUDA(cudaMemcpyAsync(B.sel, plan.sel.data(), ne, cudaMemcpyHostToDevice, s));
+        qw_bufs[r] = B.qw;
+        ord_bufs[r] = B.order;
+        stk_bufs[r] = B.stuck;
+    }
+    int64_t launches = 0;
+    for (int lv = 0; lv < nl; ++lv) {
+        LevelPlan& lp = L[lv];
+        if (!lp.halo_win.empty()) comm.transfer(R, lp.halo_win, lds, s);  // P1
+        for (int r = 0; r < world; ++r) {  // P2
+            if (!comm.local(r)) continue;
+            const auto& P = lp.part[r];
+            if (P.w_cnt) {
+                TEIG_CUDA(launch_window_reorder(R[r].descs + P.w_off, (int)P.w_cnt, lp.dmax, R[r].S, lds, R[r].qw,
+                                                R[r].sizes, R[r].sel, R[r].order, R[r].stuck, R[r].status + P.w_off,
+                                                s));
+                ++launches;
+            }
+        }
+        {  // P3
+            std::vector<void*> b(world, nullptr);
+            for (int r = 0; r < world; ++r)
+                if (comm.local(r)) b[r] = R[r].qw + lp.qw_off;
+            comm.allreduce(b, (size_t)lp.qw_len, ncclFloat64, s);
+        }
+        for (int r = 0; r < world; ++r) {  // P4
+            if (!comm.local(r)) continue;
+            const auto& P = lp.part[r];
+            if (P.l_tiles) {
+                TEIG_CUDA(launch_update_left(R[r].descs + P.l_off, (int)P.l_cnt, (int)P.l_tiles, lp.dmax, R[r].qw,
+                                             R[r].S, lds, (int)n, s));
+                ++launches;
+            }
+        }
+        if (!lp.halo_panel.empty()) comm.transfer(R, lp.halo_panel, lds, s);  // P5
+        for (int r = 0; r < world; ++r) {  // P6
+            if (!comm.local(r)) continue;
+            const auto& P = lp.part[r];
+            if (P.r_tiles) {
+                TEIG_CUDA(launch_update_right(R[r].descs + P.r_off, (int)P.r_cnt, (int)P.r_tiles, lp.dmax, R[r].qw,
+                                              R[r].S, lds, (int)n, false, s));
+                ++launches;
+            }
+        }
+        if (!lp.halo_back.empty()) comm.transfer(R, lp.halo_back, lds, s);  // P7
+        for (int r = 0; r < world; ++r) {  // P8
+            if (!comm.local(r)) continue;
+            const auto& P = lp.part[r];
+            if (P.q_tiles) {
+                TEIG_CUDA(launch_update_right(R[r].descs + P.q_off, (int)P.q_cnt, (int)P.q_tiles, lp.dmax, R[r].qw,
+                                              R[r].Q, R[r].ldq, (int)n, true, s));
+                ++launches;
+            }
+        }
+    }
+    // share the window outcomes (each written by its owner only), fold
+    comm.allreduce(ord_bufs, ne + 1, ncclUint8, s);
+    comm.allreduce(stk_bufs, ne + 1, ncclUint8, s);
+    int me = 0;
+    while (!comm.local(me)) ++me;
+    std::vector<int32_t> status(std::max<int64_t>(nw, 1), 0);
+    std::vector<uint8_t> order(ne + 1), stuck(ne + 1);
+    TEIG_CUDA(cudaMemcpyAsync(order.data(), R[me].order, ne + 1, cudaMemcpyDeviceToHost, s));
+    TEIG_CUDA(cudaMemcpyAsync(stuck.data(), R[me].stuck, ne + 1, cudaMemcpyDeviceToHost, s));
+    for (int r = 0; r < world; ++r) {
+        if (!comm.local(r) || D[r].empty()) continue;
+        std::vector<int32_t> st(D[r].size());
+        TEIG_CUDA(cudaMemcpyAsync(st.data(), R[r].status, sizeof(int32_t) * st.size(), cudaMemcpyDeviceToHost, s));
+        TEIG_CUDA(cudaStreamSynchronize(s));
+        for (size_t i = 0; i < st.size(); ++i)
+            if (Dp[r][i] >= 0) status[Dp[r][i]] |= st[i];
+    }
+    if (!comm.local((me + 1) % world) && world > 1) {  // NCCL: combine the ranks' statuses
+        int32_t* dst = nullptr;
+        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dst), sizeof(int32_t) * status.size(), s));
+        TEIG_CUDA(cudaMemcpyAsync(dst, status.data(), sizeof(int32_t) * status.size(), cudaMemcpyHostToDevice, s));
+        std::vector<void*> b(world, nullptr);
+        b[me] = dst;
+        comm.allreduce(b, status.size(), ncclInt32, s);
+        TEIG_CUDA(cudaMemcpyAsync(status.data(), dst, sizeof(int32_t) * status.size(), cudaMemcpyDeviceToHost, s));
+        TEIG_CUDA(cudaFreeAsync(dst, s));
+    }
+    TEIG_CUDA(cudaStreamSynchronize(s));
+    for (int r = 0; r < world; ++r) {
+        if (!comm.local(r)) continue;
+        RankBufs& B = R[r];
+        cudaFreeAsync(B.qw, s);
+        cudaFreeAsync(B.descs, s);
+        cudaFreeAsync(B.sizes, s);
+        cudaFreeAsync(B.sel, s);
+        cudaFreeAsync(B.order, s);
+        cudaFreeAsync(B.stuck, s);
+        cudaFreeAsync(B.status, s);
+        B.qw = nullptr;
+    }
+    status.resize(nw);
+    po.deviated = fold_outcomes(plan, blocks, status, order, stuck, rejected, plan_log, strict);
+    po.windows = nw;
+    po.levels = nl;
+    po.launches = launches;
+    return po;
+}
+
+}  // namespace
+
+// balanced column slabs: equal left+right update flops per rank (from the
+// first-pass plan), widths >= 2*kHalo; Q row slabs: equal rows.
+int dist_balance(int64_t n, int64_t nb, const uint8_t* sizes, const uint8_t* flags, int64_t window_size, int world,
+                 int64_t* col_bounds, int64_t* row_bounds) {
+    if (world < 1) return set_error(-6, "world must be >= 1");
+    if (n < 2 * kHalo * world) return set_error(-1, "n too small for this many slabs (>= 256 columns per rank)");
+    std::vector<BlockState> blocks(nb);
+    int64_t rows = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+        if (sizes[i] != 1 && sizes[i] != 2) return set_error(-3, "block sizes must be 1 or 2");
+        blocks[i] = BlockState{sizes[i], (uint8_t)(flags[i] ? 1 : 0), (uint32_t)i};
+        rows += sizes[i];
+    }
+    if (rows != n) return set_error(-3, "selection does not match n");
+    const int64_t ws = std::max<int64_t>(window_size ? window_size : default_tile_size(n), 8);
+    ReorderPlan plan = plan_reorder(blocks, ws);
+    std::vector<double> dens(n + 1, 0.0);
+    for (const auto& w : plan.windows) {
+        const double d = double(w.wbot - w.wtop);
+        dens[w.wbot] += 2.0 * d * d;  // left: 2d^2 per column >= b
+    }
+    for (int64_t j = 1; j <= n; ++j) dens[j] += dens[j - 1];
+    std::vector<double> right(n + 1, 0.0);
+    for (const auto& w : plan.windows) {
+        const double d = double(w.wbot - w.wtop);
+        right[w.wtop] += 2.0 * d * double(w.wtop);  // right: 2d^2 a spread over [a, b)
+        right[w.wbot] -= 2.0 * d * double(w.wtop);
+    }
+    std::vector<double> cum(n + 1, 0.0);
+    double run = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        run += right[j];
+        cum[j + 1] = cum[j] + dens[j] + run;
+    }
+    const double tot = cum[n];
+    col_bounds[0] = 0;
+    for (int g = 1; g < world; ++g) {
+        const double target = tot * g / world;
+        int64_t c = (int64_t)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+        c = std::max<int64_t>(c, col_bounds[g - 1] + 2 * kHalo);
+        c = std::min<int64_t>(c, n - (int64_t)(world - g) * 2 * kHalo);
+        col_bounds[g] = c;
+    }
+    col_bounds[world] = n;
+    for (int g = 0; g <= world; ++g) row_bounds[g] = n * g / world;
+    return 0;
+}
+
+}  // namespace teig
+
+using namespace teig;
+
+extern "C" {
+
+int teig_dist_balance(int64_t n, int64_t nb, const uint8_t* sizes, const uint8_t* flags, int64_t window_size,
+                      int32_t world, int64_t* col_bounds, int64_t* row_bounds) {
+    try {
+        return dist_balance(n, nb, sizes, flags, window_size, world, col_bounds, row_bounds);
+    } catch (const std::exception& e) {
+        return set_error(TEIG_ERR_INTERNAL, e.what());
+    }
+}
+
+int64_t teig_dist_schedule(int64_t n, int64_t nb, const uint8_t* sizes, const uint8_t* flags, int64_t window_size,
+                           int32_t world, const int64_t* col_bounds, int64_t* out, int64_t cap) {
+    if (n < 1 || world < 1 || !col_bounds) return set_error(-1, "bad arguments");
+    std::vector<BlockState> blocks(nb);
+    int64_t rows = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+        if (sizes[i] != 1 && sizes[i] != 2) return set_error(-3, "block sizes must be 1 or 2");
+        blocks[i] = BlockState{sizes[i], (uint8_t)(flags[i] ? 1 : 0), (uint32_t)i};
+        rows += sizes[i];
+    }
+    if (rows != n) return set_error(-3, "selection does not match n");
+    try {
+        const int64_t ws = std::max<int64_t>(window_size ? window_size : default_tile_size(n), 8);
+        ReorderPlan plan = plan_reorder(blocks, ws);
+        schedule_levels(plan, n);
+        std::vector<int64_t> C(col_bounds, col_bounds + world + 1);
+        std::vector<int64_t> idx(plan.windows.size());
+        for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int64_t)i;
+        std::stable_sort(idx.begin(), idx.end(),
+                         [&](int64_t x, int64_t y) { return plan.windows[x].level < plan.windows[y].level; });
+        int64_t k = 0;
+        auto put = [&](int64_t lv, int64_t ph, const Xfer& x) {
+            if (out && k < cap) {
+                int64_t* o = out + 8 * k;
+                o[0] = lv; o[1] = ph; o[2] = x.src; o[3] = x.dst; o[4] = x.r0; o[5] = x.r1; o[6] = x.c0; o[7] = x.c1;
+            }
+            ++k;
+        };
+        for (int64_t t : idx) {
+            const auto& w = plan.windows[t];
+            const int o = owner_of(C, w.wtop);
+            if (w.wbot <= C[o + 1]) continue;
+            const int nbr = o + 1;
+            if (nbr >= world || w.wbot > C[nbr + 1] || w.wbot - C[nbr] > kHalo)
+                return set_error(-7, "a window spans more than two slabs");
+            put(w.level, 0, Xfer{nbr, o, w.wtop, w.wbot, C[nbr], w.wbot});
+            if (w.wtop > 0) put(w.level, 1, Xfer{nbr, o, 0, w.wtop, C[nbr], w.wbot});
+            put(w.level, 2, Xfer{o, nbr, 0, w.wbot, C[nbr], w.wbot});
+        }
+        return k;
+    } catch (const std::exception& e) {
+        return set_error(TEIG_ERR_INTERNAL, e.what());
+    }
+}
+
+int teig_nccl_available(void) { return nccl().ok ? 1 : 0; }
+
+int teig_nccl_unique_id(uint8_t* id128) {
+    if (!nccl().ok) return set_error(TEIG_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    const ncclResult_t r = nccl().GetUniqueId(&id);
+    if (r != ncclSuccess) return set_error(TEIG_ERR_INTERNAL, nccl().GetErrorString(r));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    std::memcpy(id128, &id, 128);
+    return 0;
+}
+
+int teig_nccl_comm_init(int32_t world, int32_t rank, const uint8_t* id128, void** comm) {
+    if (!nccl().ok) return set_error(TEIG_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    std::memcpy(&id, id128, 128);
+    ncclComm_t c;
+    const ncclResult_t r = nccl().CommInitRank(&c, world, id, rank);
+    if (r != ncclSuccess) return set_error(TEIG_ERR_INTERNAL, nccl().GetErrorString(r));
+    *comm = c;
+    return 0;
+}
+
+int teig_nccl_comm_destroy(void* comm) {
+    if (!comm || !nccl().ok) return 0;
+    nccl().CommDestroy(static_cast<ncclComm_t>(comm));
+    return 0;
+}
+
+int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_comm, double* const* dS_slabs,
+                            int64_t lds, double* const* dQ_slabs, const int64_t* col_bounds,
+                            const int64_t* row_bounds, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
+                            const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected_out,
+                            teig_reorder_info* info, void* stream_v) {
+    if (n < 1) return set_error(-1, "n must be >= 1");
+    if (world < 1) return set_error(-2, "world must be >= 1");
+    const bool loop = nccl_comm == nullptr;
+    if (!loop && (rank < 0 || rank >= world)) return set_error(-3, "rank out of range");
+    if (!dS_slabs || !col_bounds || !row_bounds) return set_error(-5, "null slabs/bounds");
+    if (lds < n) return set_error(-6, "lds < n");
+    if (col_bounds[0] != 0 || col_bounds[world] != n || row_bounds[0] != 0 || row_bounds[world] != n)
+        return set_error(-9, "bounds must start at 0 and end at n");
+    for (int g = 0; g < world; ++g) {
+        if (col_bounds[g + 1] - col_bounds[g] < kHalo) return set_error(-9, "column slabs must be >= 128 wide");
+        if (row_bounds[g + 1] < row_bounds[g]) return set_error(-9, "row bounds must be nondecreasing");
+    }
+    teig_reorder_opts o;
+    teig_reorder_opts_default(&o);
+    if (opts) o = *opts;
+    const int64_t ws = std::max<int64_t>(o.window_size ? o.window_size : default_tile_size(n), 8);
+    if (ws > 128) return set_error(TEIG_ERR_UNSUPPORTED, "window_size > 128");
+    std::vector<BlockState> blocks(nb);
+    int64_t rows = 0;
+    for (int64_t i = 0; i < nb; ++i) {
+        if (sizes[i] != 1 && sizes[i] != 2) return set_error(-12, "block sizes must be 1 or 2");
+        blocks[i] = BlockState{sizes[i], (uint8_t)(flags[i] ? 1 : 0), (uint32_t)i};
+        rows += sizes[i];
+    }
+    if (rows != n) return set_error(-12, "reorder_schur: selection does not match s");
+    cudaStream_t s = (cudaStream_t)stream_v;
+    std::vector<int64_t> C(col_bounds, col_bounds + world + 1), Rw(row_bounds, row_bounds + world + 1);
+    teig_reorder_info inf{};
+    std::vector<int64_t> rejected, plan_log;
+    try {
+        std::vector<RankBufs> R(world);
+        for (int r = 0; r < world; ++r) {
+            R[r].rank = r;
+            const int li = loop ? r : (r == rank ? 0 : -1);
+            if (li < 0) continue;
+            R[r].S = dS_slabs[li] - C[r] * lds;
+            R[r].ldq = std::max<int64_t>(Rw[r + 1] - Rw[r], 1);
+            R[r].Q = (dQ_slabs && dQ_slabs[li]) ? dQ_slabs[li] - Rw[r] : nullptr;
+        }
+        const bool with_q = dQ_slabs != nullptr;
+        LoopbackComm lb(world);
+        if (!loop && !nccl().ok) return set_error(TEIG_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
+        NcclComm nc(static_cast<ncclComm_t>(nccl_comm), rank);
+        Comm& comm = loop ? static_cast<Comm&>(lb) : static_cast<Comm&>(nc);
+        for (int pass = 0; pass < 64; ++pass) {
+            ReorderPlan plan = plan_reorder(blocks, ws);
+            if (plan.windows.empty()) break;
+            if (pass == 0) inf.n_groups = plan.n_groups;
+            inf.update_flops += plan_update_flops(plan, n, with_q);
+            inf.update_bytes += plan_update_bytes(plan, n, with_q);
+            PassOut po = run_dist_pass(plan, n, world, R, comm, lds, C, Rw, with_q, blocks, rejected, plan_log,
+                                       o.strict != 0, s);
+            inf.n_windows += po.windows;
+            inf.n_levels += po.levels;
+            inf.n_launches += po.launches;
+            inf.n_passes += 1;
+            if (!po.deviated) break;
+        }
+        for (auto& B : R)
+            if (B.stage) cudaFreeAsync(B.stage, s);
+        TEIG_CUDA(cudaStreamSynchronize(s));
+    } catch (const std::domain_error& e) {
+        return set_error(TEIG_ERR_STRICT, e.what());
+    } catch (const std::exception& e) {
+        return set_error(TEIG_ERR_CUDA, e.what());
+    }
+    bool leading = true, seen_unsel = false;
+    for (const auto& b : blocks) {
+        if (!b.selected) seen_unsel = true;
+        else if (seen_unsel) leading = false;
+    }
+    inf.n_rejected = (int64_t)rejected.size();
+    inf.clean = (rejected.empty() && leading) ? 1 : 0;
+    if (perm)
+        for (int64_t i = 0; i < nb; ++i) perm[blocks[i].orig] = i;
+    if (rejected_out)
+        for (size_t i = 0; i < rejected.size(); ++i) rejected_out[i] = rejected[i];
+    if (info) *info = inf;
+    return 0;
+}
+
+int teig_gen_schur_input_cols_device(int64_t n, double* dS, int64_t lds, int64_t c0, int64_t c1, uint64_t fill_seed,
+                                     void* stream) {
+    if (n < 1 || lds < n || c0 < 0 || c1 > n || c1 < c0) return set_error(-1, "bad shape");
+    cudaError_t e = launch_gen_schur_cols(dS, lds, n, fill_seed, c0, c1, (cudaStream_t)stream);
+    return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+int teig_set_identity_rows_device(int64_t n, double* dQ, int64_t ldq, int64_t r0, int64_t r1, void* stream) {
+    if (n < 1 || r0 < 0 || r1 > n || r1 < r0 || ldq < r1 - r0) return set_error(-1, "bad shape");
+    cudaError_t e = launch_identity_rows(dQ, ldq, n, r0, r1, (cudaStream_t)stream);
+    return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));
+}
+
+}  // extern "C"

@@ -43,8 +43,8 @@ __device__ __forceinline__ double draw_uniform_sym(uint64_t seed, uint64_t k) {
     return __dsub_rn(__dmul_rn((double)u, 2.0 / 9007199254740992.0), 1.0);
 }
 
-__global__ void gen_schur_kernel(double* S, long long lds, long long n, uint64_t seed) {
-    const long long j = blockIdx.y;
+__global__ void gen_schur_kernel(double* S, long long lds, long long n, uint64_t seed, long long c0) {
+    const long long j = c0 + blockIdx.y;  // columns [c0, c0 + gridDim.y) into S[:, 0..)
     const long long npairs = n / 4, nreal = n - 2 * npairs;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         double v = 0.0;
@@ -73,8 +73,15 @@ __global__ void gen_schur_kernel(double* S, long long lds, long long n, uint64_t
                 v = draw_uniform_sym(seed, (uint64_t)(before + inrow));
             }
         }
-        S[i + j * lds] = v;
+        S[i + (j - c0) * lds] = v;
     }
+}
+
+// rows [r0, r1) of the n x n identity into Q (ld ldq): Q[i - r0, j]
+__global__ void identity_rows_kernel(double* Q, long long ldq, long long r0, long long r1) {
+    const long long j = blockIdx.y;
+    for (long long i = r0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < r1; i += (long long)gridDim.x * blockDim.x)
+        Q[(i - r0) + j * ldq] = (i == j) ? 1.0 : 0.0;
 }
 
 __global__ void identity_kernel(double* Q, long long ldq, long long n) {
@@ -107,7 +114,25 @@ dim3 grid_for(long long n) {
 
 cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64_t fill_seed, cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
-    gen_schur_kernel<<<grid_for(n), 256, 0, stream>>>(S, lds, n, fill_seed);
+    gen_schur_kernel<<<grid_for(n), 256, 0, stream>>>(S, lds, n, fill_seed, 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_schur_cols(double* S, long long lds, long long n, uint64_t fill_seed, long long c0,
+                                  long long c1, cudaStream_t stream) {
+    if (n <= 0 || c1 <= c0) return cudaSuccess;
+    dim3 g = grid_for(n);
+    g.y = (unsigned)(c1 - c0);
+    gen_schur_kernel<<<g, 256, 0, stream>>>(S, lds, n, fill_seed, c0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_identity_rows(double* Q, long long ldq, long long n, long long r0, long long r1,
+                                 cudaStream_t stream) {
+    if (n <= 0 || r1 <= r0) return cudaSuccess;
+    dim3 g = grid_for(r1 - r0);
+    g.y = (unsigned)n;
+    identity_rows_kernel<<<g, 256, 0, stream>>>(Q, ldq, r0, r1);
     return cudaGetLastError();
 }
 

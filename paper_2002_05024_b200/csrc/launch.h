@@ -27,6 +27,10 @@ cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64
                                    cudaStream_t stream);
 cudaError_t launch_set_identity(double* Q, long long ldq, long long n, cudaStream_t stream);
 cudaError_t launch_gen_hessenberg(double* H, long long ldh, long long n, uint64_t seed, cudaStream_t stream);
+cudaError_t launch_gen_schur_cols(double* S, long long lds, long long n, uint64_t fill_seed, long long c0,
+                                  long long c1, cudaStream_t stream);
+cudaError_t launch_identity_rows(double* Q, long long ldq, long long n, long long r0, long long r1,
+                                 cudaStream_t stream);
 
 // Schur reduction window kernels (schur_window.cu)
 #ifndef TEIG_AED_THREADS
@@ -47,6 +51,9 @@ cudaError_t launch_chase_window(double* H, long long ldh, const ChaseWin* wins_d
 cudaError_t launch_hess_norm(const double* H, long long ldh, int n, unsigned long long* out, cudaStream_t stream);
 cudaError_t launch_scan_active(double* H, long long ldh, int n, int ihi, double hnorm, int* out,
                                cudaStream_t stream);
+
+// element-wise sum of nbuf device buffers into all of them (loopback all-reduce)
+cudaError_t launch_sum_buffers(void* const* bufs, int nbuf, size_t count, int elem_bytes, cudaStream_t s);
 
 constexpr int kLeftBN = 64;   // columns per left-update tile
 constexpr int kRightBM = 64;  // rows per right/factor-update tile

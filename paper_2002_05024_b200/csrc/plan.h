@@ -48,4 +48,10 @@ double plan_update_flops(const ReorderPlan& plan, int64_t n, bool with_q);
 // Algorithmic HBM bytes of the updates: each panel read and written once.
 double plan_update_bytes(const ReorderPlan& plan, int64_t n, bool with_q);
 
+// Folds one executed pass's window outcomes into `blocks` in plan order
+// (reference reorder.cpp:366-397); returns true when a replan is needed.
+bool fold_outcomes(const ReorderPlan& plan, std::vector<BlockState>& blocks, const std::vector<int32_t>& st_by_plan,
+                   const std::vector<uint8_t>& order, const std::vector<uint8_t>& stuck,
+                   std::vector<int64_t>& rejected, std::vector<int64_t>& plan_log, bool strict);
+
 }  // namespace teig

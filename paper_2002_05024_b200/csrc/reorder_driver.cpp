@@ -54,6 +54,52 @@ int64_t default_tile_size(int64_t n) {
     return ((base + 7) / 8) * 8;
 }
 
+// Folds the window outcomes of one executed pass into the block bookkeeping,
+// in plan order (reference reorder.cpp:366-397).  st_by_plan: status per
+// window in plan order; order/stuck: per-block pools (WinDesc::blk_off).
+// Returns true when a window deviated from the plan (rejection or layout
+// mismatch), i.e. a replanning pass is needed.
+bool fold_outcomes(const ReorderPlan& plan, std::vector<BlockState>& blocks, const std::vector<int32_t>& st_by_plan,
+                   const std::vector<uint8_t>& order, const std::vector<uint8_t>& stuck,
+                   std::vector<int64_t>& rejected, std::vector<int64_t>& plan_log, bool strict) {
+    bool deviated = false;
+    const int64_t nw = (int64_t)plan.windows.size();
+    std::vector<int64_t> start(blocks.size() + 1, 0);
+    for (size_t i = 0; i < blocks.size(); ++i) start[i + 1] = start[i] + blocks[i].size;
+    std::vector<BlockState> slice;
+    for (int64_t wi = 0; wi < nw; ++wi) {
+        const PlannedWindow& w = plan.windows[wi];
+        plan_log.push_back(w.wtop);
+        plan_log.push_back(w.wbot - w.wtop);
+        plan_log.push_back(w.count);
+        const int32_t st = st_by_plan[wi];
+        if (!(st & kWinExecuted)) {
+            deviated = true;
+            continue;
+        }
+        bool consistent = start[w.first_block] == w.wtop &&
+                          w.first_block + w.count <= (int64_t)blocks.size();
+        for (int64_t i = 0; consistent && i < w.count; ++i)
+            consistent = blocks[w.first_block + i].size == plan.sizes[w.blk_off + i];
+        if (!consistent)
+            throw std::runtime_error("reorder: block bookkeeping diverged from the device layout");
+        slice.assign(blocks.begin() + w.first_block, blocks.begin() + w.first_block + w.count);
+        for (int64_t i = 0; i < w.count; ++i) blocks[w.first_block + i] = slice[order[w.blk_off + i]];
+        for (int64_t i = 0; i < w.count; ++i) start[w.first_block + i + 1] = start[w.first_block + i] + blocks[w.first_block + i].size;
+        if (st & kWinStuck) {
+            deviated = true;
+            for (int64_t i = 0; i < w.count; ++i)
+                if (stuck[w.blk_off + i]) {
+                    if (strict) throw std::domain_error("reorder_schur: swap rejected in strict mode");
+                    rejected.push_back(slice[i].orig);
+                    for (auto& b : blocks)
+                        if (b.orig == slice[i].orig) b.selected = 0;
+                }
+        }
+    }
+    return deviated;
+}
+
 namespace {
 
 struct DevBuf {
@@ -139,6 +185,12 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         dsc.tr_pref = (int32_t)tr[L];
         dsc.tq_pref = (int32_t)tq[L];
         dsc.pad = 0;
+        dsc.lc0 = (int32_t)w.wbot;
+        dsc.lc1 = (int32_t)n;
+        dsc.rr0 = 0;
+        dsc.rr1 = (int32_t)w.wtop;
+        dsc.qr0 = 0;
+        dsc.qr1 = (int32_t)n;
         tl[L] += (n - w.wbot + kLeftBN - 1) / kLeftBN;
         tr[L] += (w.wtop + kRightBM - 1) / kRightBM;
         if (dQ) tq[L] += (n + kRightBM - 1) / kRightBM;
@@ -233,41 +285,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     }
     std::vector<int32_t> st_by_plan(nw);
     for (int64_t k = 0; k < nw; ++k) st_by_plan[idx[k]] = status[k];
-
-    // fold in plan order (reorder.cpp:366-397), validating the bookkeeping
-    std::vector<int64_t> start(blocks.size() + 1, 0);
-    for (size_t i = 0; i < blocks.size(); ++i) start[i + 1] = start[i] + blocks[i].size;
-    std::vector<BlockState> slice;
-    for (int64_t wi = 0; wi < nw; ++wi) {
-        const PlannedWindow& w = plan.windows[wi];
-        plan_log.push_back(w.wtop);
-        plan_log.push_back(w.wbot - w.wtop);
-        plan_log.push_back(w.count);
-        const int32_t st = st_by_plan[wi];
-        if (!(st & kWinExecuted)) {
-            pr.deviated = true;
-            continue;
-        }
-        bool consistent = start[w.first_block] == w.wtop &&
-                          w.first_block + w.count <= (int64_t)blocks.size();
-        for (int64_t i = 0; consistent && i < w.count; ++i)
-            consistent = blocks[w.first_block + i].size == plan.sizes[w.blk_off + i];
-        if (!consistent)
-            throw std::runtime_error("reorder: block bookkeeping diverged from the device layout");
-        slice.assign(blocks.begin() + w.first_block, blocks.begin() + w.first_block + w.count);
-        for (int64_t i = 0; i < w.count; ++i) blocks[w.first_block + i] = slice[order[w.blk_off + i]];
-        for (int64_t i = 0; i < w.count; ++i) start[w.first_block + i + 1] = start[w.first_block + i] + blocks[w.first_block + i].size;
-        if (st & kWinStuck) {
-            pr.deviated = true;
-            for (int64_t i = 0; i < w.count; ++i)
-                if (stuck[w.blk_off + i]) {
-                    if (strict) throw std::domain_error("reorder_schur: swap rejected in strict mode");
-                    rejected.push_back(slice[i].orig);
-                    for (auto& b : blocks)
-                        if (b.orig == slice[i].orig) b.selected = 0;
-                }
-        }
-    }
+    pr.deviated = fold_outcomes(plan, blocks, st_by_plan, order, stuck, rejected, plan_log, strict);
     pr.windows = nw;
     pr.levels = nl;
     pr.launches = launches;
@@ -588,6 +606,12 @@ int teig_apply_window_updates_device(int64_t n, double* dS, int64_t lds, double*
         wd.d = (int32_t)d;
         wd.nb = 0;
         wd.qw_off = 0;
+        wd.lc0 = (int32_t)(a + d);
+        wd.lc1 = (int32_t)n;
+        wd.rr0 = 0;
+        wd.rr1 = (int32_t)a;
+        wd.qr0 = 0;
+        wd.qr1 = (int32_t)n;
         DevBuf ddesc(sizeof(WinDesc), stream);
         TEIG_CUDA(cudaMemcpyAsync(ddesc.p, &wd, sizeof wd, cudaMemcpyHostToDevice, stream));
         const int dm = d <= 64 ? 64 : 128;

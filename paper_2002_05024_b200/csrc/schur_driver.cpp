@@ -259,6 +259,12 @@ class SchurRunner {
             w.a = (int32_t)wins_[k].a;
             w.d = (int32_t)wins_[k].d;
             w.qw_off = k * kSlot;
+            w.lc0 = (int32_t)(wins_[k].a + wins_[k].d);
+            w.lc1 = (int32_t)n_;
+            w.rr0 = 0;
+            w.rr1 = (int32_t)wins_[k].a;
+            w.qr0 = 0;
+            w.qr1 = (int32_t)n_;
             if (wins_[k].kind == 1) hchase_[wins_[k].cw_idx].qw_off = k * kSlot;
         }
         descs_.need(nw, s_);

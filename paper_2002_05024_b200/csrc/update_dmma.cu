@@ -6,7 +6,9 @@
 //   right (column panel): S[0:a, a:b]  <- S[0:a, a:b] Q_w          (window_tasks.cpp:22-30)
 //   factor:               Q[0:n, a:b]  <- Q[0:n, a:b] Q_w          (window_tasks.cpp:72-86)
 // Every CTA owns one in-place output tile and the full K = d extent of its
-// panel tile, so no other CTA reads what it overwrites.  One launch covers
+// panel tile, so no other CTA reads what it overwrites.  The index ranges
+// come from WinDesc (lc0/lc1, rr0/rr1, qr0/qr1) so the same kernels update a
+// column slab or row slab of a distributed matrix.  One launch covers
 // all windows of a wavefront: the CTA locates its window by binary search
 // over the per-level tile prefix sums carried in WinDesc.
 //
@@ -80,9 +82,9 @@ update_left_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __r
     const int t = blockIdx.x;
     const int wi = find_window<0>(wins, nwin, t);
     const WinDesc wd = wins[wi];
-    const int d = wd.d, a = wd.a, b = a + d;
-    const int c = b + (t - wd.tl_pref) * BN;
-    const int ncols = min(BN, n - c);
+    const int d = wd.d, a = wd.a;
+    const int c = wd.lc0 + (t - wd.tl_pref) * BN;
+    const int ncols = min(BN, wd.lc1 - c);
     const double* Qw = qw_pool + wd.qw_off;
     double* P = S + (long long)a + (long long)c * lds;
 
@@ -185,8 +187,8 @@ update_right_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __
     const WinDesc wd = wins[wi];
     const int d = wd.d, a = wd.a;
     const int pref = (Field == 1) ? wd.tr_pref : wd.tq_pref;
-    const int r0 = (t - pref) * BM;
-    const int row_end = (Field == 1) ? a : nrows_total;
+    const int r0 = ((Field == 1) ? wd.rr0 : wd.qr0) + (t - pref) * BM;
+    const int row_end = (Field == 1) ? wd.rr1 : wd.qr1;
     const int nrows = min(BM, row_end - r0);
     const double* Qw = qw_pool + wd.qw_off;
     double* P = M + (long long)r0 + (long long)a * ldm;
