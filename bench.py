@@ -1,21 +1,25 @@
 #!/usr/bin/env python3
 """bench.py -- B200 benchmark of the window-based off-diagonal update path.
 
-Workload (BASELINE.json configs[1], "C2"): eigenvalue reordering of the
-synthetic standardized Schur form of SURVEY.md 8d, n = 10000 fp64, 35 % of
-the diagonal blocks selected (select_fraction seed 99), Q accumulated
+Workload: the configuration BASELINE.json's metric is quoted on --
+eigenvalue reordering of the synthetic standardized Schur form of SURVEY.md
+8d at n = 40000 fp64 (configs[3], "C4"; it fits one B200: S + Q = 25.6 GB),
+35 % of the diagonal blocks selected (select_fraction seed 99), Q accumulated
 (Q_in = I), window size = the reference default (tile size 128).  One step =
 one full ``reorder_schur`` of that matrix.  Inputs are generated directly in
 HBM by the library's Philox generator (bit-identical to the reference's
 generator) and restored from a pristine device copy before every step
-(outside the per-step events).  S + Q = 1.6 GB > L2 (126 MB), so no L2 flush
-is needed between steps.
+(outside the per-step events).  Inputs >> L2 (126 MB): no flush needed.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 10000] [--ws 0]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--n 40000] [--ws 0]
   python bench.py --impl reference ...   # the reference CPU path, host cores
 
-Under torchrun (N > 1) every rank reorders its own replica (the multi-GPU
-2D distribution is not built yet): "scaling": "weak", value = max over ranks.
+N = 1: the single-GPU path.  N > 1 (torchrun, one rank per GPU): the
+distributed path (S column slabs, Q row slabs, NCCL all-reduce of the
+packed Q_w per wavefront, halo transfers; csrc/dist_reorder.cpp) on the SAME
+n = 40000 problem: "scaling": "strong", value = max time over ranks.  The
+line also carries C2 (n = 10000, configs[1]) and C3 (Schur reduction,
+configs[2]) sections at N = 1.
 """
 from __future__ import annotations
 
@@ -45,7 +49,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--n", type=int, default=10000)
+    ap.add_argument("--n", type=int, default=40000)
+    ap.add_argument("--c2-n", type=int, default=10000, help="size of the C2 section (0: skip)")
     ap.add_argument("--ws", type=int, default=0, help="window size (0: reference default = tile 128)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -54,6 +59,7 @@ def parse():
                     help="reorder: C2 (headline); schur: C3 multishift QR + AED of random Hessenberg")
     ap.add_argument("--no-schur", action="store_true", help="skip the C3 section of the default line")
     ap.add_argument("--schur-n", type=int, default=10000)
+    ap.add_argument("--force-dist", action="store_true", help="use the NCCL distributed path even at N=1 (plumbing test)")
     return ap.parse_args()
 
 
@@ -125,15 +131,30 @@ def make_problem(T, n, dev):
     return S0, sel
 
 
+def synthetic_selection(T, n):
+    """select_fraction on the synthetic Schur form's block pattern (reals
+    first, then floor(n/4) 2x2 blocks: generate.cpp:68-91, 115-150) without
+    materialising the matrix -- what every rank of the distributed run uses."""
+    import ctypes as C
+    npairs = n // 4
+    nreal = n - 2 * npairs
+    sizes = np.array([1] * nreal + [2] * npairs, dtype=np.uint8)
+    flags = np.zeros(len(sizes), dtype=np.uint8)
+    T._native.check(T._native.lib().teig_select_fraction(len(sizes), FRACTION, SEL_SEED,
+                                                         flags.ctypes.data_as(C.c_void_p)))
+    starts = np.concatenate([[0], np.cumsum(sizes.astype(np.int64))])
+    blocks = [T.Block(int(starts[i]), int(sizes[i]), 0j) for i in range(len(sizes))]
+    return T.Selection(blocks, [bool(f) for f in flags])
+
+
 def run_ours(args, rank, world, local):
     import torch
     import paper_2002_05024_b200 as T
 
+    if world > 1 or args.force_dist:
+        return run_ours_dist(args, rank, world, local)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
     n = args.n
     S0, sel = make_problem(T, n, dev)
     S = T.colmajor_empty(n, dev)
@@ -195,25 +216,7 @@ def run_ours(args, rank, world, local):
     # ---------------- e2e: host buffers through the C ABI, copies inside ----------------
     e2e = None
     if not args.no_e2e:
-        Sh = torch.empty((n, n), dtype=torch.float64).pin_memory()
-        Qh = torch.empty((n, n), dtype=torch.float64).pin_memory()
-        S0h = S0.t().contiguous().cpu()  # row-major of S^T == column-major of S
-        I_h = torch.eye(n, dtype=torch.float64)
-        e2e_ms = []
-        for k in range(max(1, min(args.steps, 3)) + 1):
-            Sh.copy_(S0h)
-            Qh.copy_(I_h)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            T.reorder.reorder_schur_host_buffers(Sh.numpy(), Qh.numpy(), n, sel, opts)
-            dt = (time.perf_counter() - t0) * 1e3
-            if k > 0:  # first call is a warm-up of the pinned path
-                e2e_ms.append(dt)
-        ok = np.allclose(Sh.numpy().T, S.cpu().numpy(), rtol=0, atol=1e-9)
-        e2e = {"value": round(statistics.mean(e2e_ms) / 1e3, 6), "unit": "s",
-               "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": 2 * n * n * 8,
-               "steps": len(e2e_ms), "matches_device_result": bool(ok),
-               "api": "teig_reorder_schur_host (C ABI, pinned host S,Q column-major)"}
+        e2e = e2e_reorder(T, S0, S, sel, opts, n, min(args.steps, 3))
 
     # ---------------- roofline of the dominant kernel class ----------------
     k_ms = prof["ms_left"] + prof["ms_right"] + prof["ms_factor"]
@@ -241,15 +244,15 @@ def run_ours(args, rank, world, local):
         "warmup": args.warmup,
         "ms_per_step": round(ms_step, 3),
         "higher_is_better": False,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (SURVEY.md 8d Schur form generated in HBM by the library's Philox generator)",
-        "config": {"workload": f"C2: reorder_schur n={n}, 35% selected (select_fraction seed {SEL_SEED}), "
-                               f"Q accumulated, window {info and (args.ws or 128)}",
+        "config": {"workload": f"{workload_name(n)}: reorder_schur n={n}, 35% selected (select_fraction seed "
+                               f"{SEL_SEED}), Q accumulated, window {args.ws or 128}",
                    "n": n, "window_size": args.ws or 128, "fraction": FRACTION,
-                   "parallelism": "replicas" if world > 1 else "single-gpu",
-                   "l2": "inputs 1.6 GB > 126 MB L2, no flush needed"},
+                   "parallelism": "single-gpu",
+                   "l2": f"inputs {2 * n * n * 8 / 1e9:.1f} GB > 126 MB L2, no flush needed"},
         "update_tflops": round(info["update_flops"] / (ms_step * 1e-3) / 1e12, 3),
         "update_flops": info["update_flops"],
         "windows": info["n_windows"], "levels": info["n_levels"], "groups": info["n_groups"],
@@ -265,6 +268,10 @@ def run_ours(args, rank, world, local):
     }
     if rank == 0 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(args, n)
+    del S0, S, Q, Q0
+    torch.cuda.empty_cache()
+    if args.c2_n:
+        out["c2_n10000"] = run_c2(args, dev)
     if not args.no_schur:
         out["schur_c3"] = run_schur(args, dev, with_cpu=(rank == 0 and not args.no_cpu), with_e2e=not args.no_e2e)
         out["schur_c3"]["gpu_launches_counted_in_line"] = False
@@ -273,6 +280,186 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.destroy_process_group()
 
+
+
+def workload_name(n):
+    return {10000: "C2", 40000: "C4"}.get(n, "reorder")
+
+
+def e2e_reorder(T, S0, S_dev_result, sel, opts, n, steps):
+    """The same reorder through the C ABI's host entry point: pinned host S,Q
+    (column-major), H2D + D2H inside the timed call."""
+    import torch
+    try:
+        Sh = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        Qh = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    except RuntimeError as e:  # host RAM
+        return {"value": None, "unit": "s", "skipped": f"pinned host buffers: {e}"[:200]}
+    e2e_ms = []
+    for k in range(max(1, steps) + 1):
+        Sh.copy_(S0.t())  # row-major of S^T == column-major of S
+        Qh.zero_()
+        Qh.diagonal().fill_(1.0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        T.reorder.reorder_schur_host_buffers(Sh.numpy(), Qh.numpy(), n, sel, opts)
+        dt = (time.perf_counter() - t0) * 1e3
+        if k > 0:  # first call warms the pinned path
+            e2e_ms.append(dt)
+    ok = bool(torch.equal(Sh.cuda().t(), S_dev_result))
+    del Sh, Qh
+    return {"value": round(statistics.mean(e2e_ms) / 1e3, 6), "unit": "s",
+            "h2d_bytes_per_step": 2 * n * n * 8, "d2h_bytes_per_step": 2 * n * n * 8,
+            "steps": len(e2e_ms), "matches_device_result": ok,
+            "api": "teig_reorder_schur_host (C ABI, pinned host S,Q column-major)"}
+
+
+def run_c2(args, dev, steps=3, warmup=2):
+    """C2 (configs[1]): reorder n=10000 on one GPU, device time + parity + the
+    CPU reference sample (kept for continuity with the round-1 profiles)."""
+    import torch
+    import paper_2002_05024_b200 as T
+    n = args.c2_n
+    S0, sel = make_problem(T, n, dev)
+    S, Q = T.colmajor_empty(n, dev), T.colmajor_empty(n, dev)
+    Q0 = T.identity(n, dev)
+    opts = T.ReorderOptions(window_size=args.ws)
+    for _ in range(warmup):
+        S.copy_(S0)
+        Q.copy_(Q0)
+        T.reorder_schur(S, Q, sel, opts)
+    ms = []
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(steps):
+        S.copy_(S0)
+        Q.copy_(Q0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = T.reorder_schur(S, Q, sel, opts)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    back = float(torch.linalg.norm(S0 - Q @ S @ Q.t()) / torch.linalg.norm(S0))
+    orth = float(torch.linalg.norm(Q.t() @ Q - torch.eye(n, dtype=torch.float64, device=dev)))
+    tol = 10 * n * 2.220446049250313e-16
+    out = {"workload": f"C2: reorder_schur n={n}, 35% selected (seed {SEL_SEED}), Q accumulated, window "
+                       f"{args.ws or 128}", "value": round(statistics.mean(ms) / 1e3, 5), "unit": "s",
+           "step_ms": [round(x, 2) for x in ms], "update_tflops": round(res.info["update_flops"] / (statistics.mean(ms) * 1e-3) / 1e12, 3),
+           "windows": res.info["n_windows"], "levels": res.info["n_levels"], "clean": res.clean,
+           "parity": {"backward_error": back, "orthogonality": orth, "tol_10neps": tol,
+                      "pass": back <= tol and orth <= tol}}
+    if not args.no_e2e:
+        out["e2e"] = e2e_reorder(T, S0, S, sel, opts, n, 2)
+    if not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(args, n)
+    return out
+
+
+def run_ours_dist(args, rank, world, local):
+    """N > 1: one rank per GPU, the distributed path on the same n problem."""
+    import torch
+    import torch.distributed as dist
+    import paper_2002_05024_b200 as T
+    from paper_2002_05024_b200 import dist as D
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+    n = args.n
+    sel = synthetic_selection(T, n)
+    cb, rb = D.balance(n, sel, world, args.ws)
+    c0, c1, r0, r1 = int(cb[rank]), int(cb[rank + 1]), int(rb[rank]), int(rb[rank + 1])
+    comm = D.nccl_comm(rank, world)
+    seed = T.known_spectrum_seed(FILL_SEED_BASE)
+    S0 = D.gen_schur_input_slab(n, seed, c0, c1, dev)
+    Q0 = D.identity_rows_slab(n, r0, r1, dev)
+    S = D.s_slab_empty(n, c0, c1, dev)
+    Q = D.q_slab_empty(n, r0, r1, dev)
+    opts = T.ReorderOptions(window_size=args.ws)
+
+    def reset():
+        S.copy_(S0)
+        Q.copy_(Q0)
+
+    for _ in range(max(args.warmup, 0)):
+        reset()
+        res = D.reorder_schur_dist(S, Q, sel, cb, rb, rank, world, comm, opts)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        reset()
+        ev[k][0].record(stream)
+        res = D.reorder_schur_dist(S, Q, sel, cb, rb, rank, world, comm, opts)
+        ev[k][1].record(stream)
+    torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t0
+    dist.barrier()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    t = torch.tensor([statistics.mean(step_ms)], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = float(t.item())
+    info = res.info
+    # parity: the distributed result must equal the single-GPU result bit for
+    # bit -- gather both slabs to rank 0, rerun single-GPU there, compare
+    parity = None
+    if n <= 40000:
+        wc = c1 - c0
+        s_loc = S[:, :wc].contiguous()
+        q_loc = Q.contiguous()
+        sizes_s = [int(cb[g + 1] - cb[g]) for g in range(world)]
+        sizes_q = [int(rb[g + 1] - rb[g]) for g in range(world)]
+        if rank == 0:
+            s_parts = [torch.empty((n, w), dtype=torch.float64, device=dev) for w in sizes_s]
+            q_parts = [torch.empty((h, n), dtype=torch.float64, device=dev) for h in sizes_q]
+        for g in range(world):  # point-to-point gather (unequal slab sizes)
+            if rank == 0 and g == 0:
+                s_parts[0].copy_(s_loc)
+                q_parts[0].copy_(q_loc)
+            elif rank == 0:
+                dist.recv(s_parts[g], src=g)
+                dist.recv(q_parts[g], src=g)
+            elif rank == g:
+                dist.send(s_loc, dst=0)
+                dist.send(q_loc, dst=0)
+        del s_loc, q_loc
+        if rank == 0:
+            Sd = torch.cat(s_parts, dim=1)
+            Qd = torch.cat(q_parts, dim=0)
+            del s_parts, q_parts
+            S1 = T.gen_schur_input(n, seed, device=dev)
+            Q1 = T.identity(n, dev)
+            T.reorder_schur(S1, Q1, sel, opts)
+            parity = {"bitwise_equal_to_single_gpu": bool(torch.equal(Sd, S1) and torch.equal(Qd, Q1))}
+            del Sd, Qd, S1, Q1
+        dist.barrier()
+    D.nccl_comm_destroy(comm)
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(ms_step / 1e3, 6), "unit": "s", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": False,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (SURVEY.md 8d Schur form, each rank generates its slabs in HBM)",
+               "config": {"workload": f"{workload_name(n)}: reorder_schur n={n}, 35% selected (select_fraction seed "
+                                      f"{SEL_SEED}), Q accumulated, window {args.ws or 128}", "n": n,
+                          "window_size": args.ws or 128, "fraction": FRACTION,
+                          "parallelism": f"dist{world}: S column slabs {list(map(int, cb))}, Q row slabs, "
+                                         "NCCL all-reduce of Q_w per wavefront + halo send/recv",
+                          "l2": "inputs >> 126 MB L2"},
+               "update_tflops": round(info["update_flops"] / (ms_step * 1e-3) / 1e12, 3),
+               "update_flops": info["update_flops"], "windows": info["n_windows"], "levels": info["n_levels"],
+               "clean": info["clean"] == 1, "parity": parity, "gpu_launches": info["n_launches"],
+               "clocks": clocks, "wall_s_timed_region": round(t_wall, 3), "step_ms": [round(x, 3) for x in step_ms]}
+        print(json.dumps(out), flush=True)
+    dist.destroy_process_group()
 
 # ---------------------------------------------------------------------------
 # C3: Schur reduction (multishift QR + AED) of a random upper Hessenberg matrix
@@ -428,11 +615,15 @@ def _sample_flags(O, sizes, flags, ws, n, frac_target):
     return keep, F_total, F_sample, G, ng
 
 
-def cpu_baseline(args, n, steps=1, frac_target=0.06):
+def cpu_baseline(args, n, steps=1, sample_flops=1.0e12):
+    """~1e12 update flops of the same workload (~20 s of the reference on 16
+    host threads), extrapolated by update flops."""
     O, S, sizes, flags = _cpu_problem(n)
     ws = args.ws or 128
     use_ref = O.ref_available()
     cores = os.cpu_count() or 1
+    plan, F_all, _ = O.plan_reorder(sizes, flags, ws, n)
+    frac_target = min(0.06, sample_flops / F_all)
     keep, F_total, F_sample, groups, ng = _sample_flags(O, sizes, flags, ws, n, frac_target)
     times = []
     for _ in range(steps):
