@@ -143,8 +143,8 @@ int teig_apply_window_updates_device(int64_t n, double* dS, int64_t lds, double*
 typedef struct teig_schur_opts {  /* SchurOptions, schur.hpp:20-29 */
     int32_t deflation;        /* 0 classic, 1 norm-stable (default) */
     int32_t shift_count;      /* 0: max(4, round-to-even(active/16)), cap 64 */
-    int32_t aed_window;       /* 0: 3m/2; <= 112 (single-CTA AED window) */
-    int32_t small_threshold;  /* direct small_schur at or below (default 64, <= 112) */
+    int32_t aed_window;       /* 0: 3m/2; <= 104 (single-CTA AED window) */
+    int32_t small_threshold;  /* direct small_schur at or below (default 64, <= 104) */
     int64_t iteration_limit;  /* 0: 30 n sweeps */
     int64_t tile_size;        /* chase window: 0 = default_tile_size(n) (128 for n >= 1000); <= 128 */
     int32_t profile;          /* !=0: CUDA-event time per kernel class in teig_schur_info */
@@ -206,7 +206,7 @@ int teig_chase_bulges_device(int64_t n, double* dH, int64_t ldh, double* dQ, int
                              int64_t window_size, int64_t* n_windows, void* stream);
 
 /* kernels::small_schur (kernels.hpp:93): dH k x k (ld ldh) in place, dQ
- * (k x k, ld k) receives the similarity.  k <= 112. */
+ * (k x k, ld k) receives the similarity.  k <= 104. */
 int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int32_t* converged,
                             void* stream);
 

@@ -38,14 +38,14 @@ cudaError_t launch_identity_rows(double* Q, long long ldq, long long n, long lon
 #endif
 constexpr int kAedThreads = TEIG_AED_THREADS;
 constexpr int kChaseThreads = 512;
-constexpr int kAedMaxWindow = 112;   // AED / small-solve window order limit (shared memory)
+constexpr int kAedMaxWindow = 104;   // AED / small-solve window order limit (shared memory)
 constexpr int kChaseMaxWindow = 128; // chase window order limit
 size_t aed_window_smem_bytes(int w);
 size_t chase_window_smem_bytes(int d);
 int chase_window_packed_len(int d);
 cudaError_t launch_aed_window(double* H, long long ldh, int mode, int l, int e, int w, const SchurDevOpts& o,
                               double* qw_out, AedDevOut* out, double* shifts_out, cudaStream_t stream,
-                              unsigned long long* prof = nullptr);
+                              unsigned long long* prof = nullptr, double* snap = nullptr);
 cudaError_t launch_chase_window(double* H, long long ldh, const ChaseWin* wins_dev, int idx, int d,
                                 const double* shift_pairs, double* qw_pool, cudaStream_t stream);
 cudaError_t launch_hess_norm(const double* H, long long ldh, int n, unsigned long long* out, cudaStream_t stream);

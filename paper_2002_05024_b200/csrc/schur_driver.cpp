@@ -173,6 +173,7 @@ class SchurRunner {
         dopts_.shift_count = o.shift_count;
         dopts_.aed_window = o.aed_window;
         dopts_.small_threshold = o.small_threshold;
+        dopts_.small_mode = (getenv("TEIG_SMALL_MODE") && atoi(getenv("TEIG_SMALL_MODE")) == 1) ? 1 : 0;
         tile_ = o.tile_size ? o.tile_size : default_tile_size(n);
         TEIG_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
         TEIG_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
@@ -182,20 +183,23 @@ class SchurRunner {
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_out_), sizeof(AedDevOut), s_));
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_int_), sizeof(unsigned long long) * 2, s_));
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_sh_), sizeof(double) * 2 * kAedMaxWindow, s_));
+        if (!(getenv("TEIG_NO_WAVE") && atoi(getenv("TEIG_NO_WAVE"))))
+            TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_snap_),
+                                      sizeof(double) * 2 * kAedMaxWindow * kAedMaxWindow, s_));
         if (getenv("TEIG_AED_PROF") && atoi(getenv("TEIG_AED_PROF"))) {
-            TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_prof_), sizeof(unsigned long long) * 8, s_));
-            TEIG_CUDA(cudaMemsetAsync(d_prof_, 0, sizeof(unsigned long long) * 8, s_));
+            TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_prof_), sizeof(unsigned long long) * 12, s_));
+            TEIG_CUDA(cudaMemsetAsync(d_prof_, 0, sizeof(unsigned long long) * 12, s_));
         }
     }
     ~SchurRunner() {
         if (d_prof_) {
-            unsigned long long pf[8] = {0};
+            unsigned long long pf[12] = {0};
             cudaMemcpy(pf, d_prof_, sizeof pf, cudaMemcpyDeviceToHost);
             fprintf(stderr,
                     "[teig aed prof] windows(aed)=%lld chase=%lld | Mcycles: total %.1f small %.1f swap %.1f (n=%llu) "
-                    "sweep %.1f spike %.1f | sim_steps %llu small_sweeps %llu\n",
+                    "sweep %.1f spike %.1f | sim_steps %llu small_sweeps %llu | wave steps %llu decide %.1f plan %.1f\n",
                     (long long)aed_windows_, (long long)chase_windows_, pf[0] / 1e6, pf[1] / 1e6, pf[2] / 1e6, pf[3],
-                    pf[4] / 1e6, pf[5] / 1e6, pf[6], pf[7]);
+                    pf[4] / 1e6, pf[5] / 1e6, pf[6], pf[7], pf[8], pf[9] / 1e6, pf[10] / 1e6);
             cudaFree(d_prof_);
         }
         qw_.release(s_);
@@ -205,6 +209,7 @@ class SchurRunner {
         if (d_out_) cudaFreeAsync(d_out_, s_);
         if (d_int_) cudaFreeAsync(d_int_, s_);
         if (d_sh_) cudaFreeAsync(d_sh_, s_);
+        if (d_snap_) cudaFreeAsync(d_snap_, s_);
         cudaStreamSynchronize(s_);
         if (h_out_) cudaFreeHost(h_out_);
         for (auto e : evpool_) cudaEventDestroy(e);
@@ -286,7 +291,7 @@ class SchurRunner {
             if (w.kind == 0) {
                 last0 = (int)k;
                 TEIG_CUDA(launch_aed_window(dH_, ldh_, w.mode, (int)w.l, (int)w.a, (int)w.d, dopts_,
-                                            qw_.p + k * kSlot, d_out_, d_sh_, s_, d_prof_));
+                                            qw_.p + k * kSlot, d_out_, d_sh_, s_, d_prof_, d_snap_));
                 if (w.mode == kSchurModeAed) {
                     last_aed = (int)k;
                     ++aed_windows_;
@@ -477,6 +482,7 @@ class SchurRunner {
     int* d_int_ = nullptr;
     double* d_sh_ = nullptr;
     unsigned long long* d_prof_ = nullptr;
+    double* d_snap_ = nullptr;
     std::vector<Win> wins_;
     std::vector<ChaseWin> hchase_;
     std::vector<double> hpairs_;
@@ -495,9 +501,9 @@ int check_opts(const teig_schur_opts& o) {
         return set_error(-7, "negative option");
     if (o.shift_count > 2 * kAedMaxWindow) return set_error(TEIG_ERR_UNSUPPORTED, "shift_count too large");
     if (o.aed_window > kAedMaxWindow)
-        return set_error(TEIG_ERR_UNSUPPORTED, "aed_window > 112 exceeds the single-CTA AED window kernel");
+        return set_error(TEIG_ERR_UNSUPPORTED, "aed_window > 104 exceeds the single-CTA AED window kernel");
     if (o.small_threshold > kAedMaxWindow)
-        return set_error(TEIG_ERR_UNSUPPORTED, "small_threshold > 112 exceeds the single-CTA window kernel");
+        return set_error(TEIG_ERR_UNSUPPORTED, "small_threshold > 104 exceeds the single-CTA window kernel");
     if (o.tile_size > kChaseMaxWindow) return set_error(TEIG_ERR_UNSUPPORTED, "chase window (tile_size) > 128");
     return 0;
 }
@@ -749,7 +755,7 @@ int teig_aed_step_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t
     if (opts) o = *opts;
     if (int rc = check_opts(o)) return rc;
     window = std::min(window, ihi - l);
-    if (window > kAedMaxWindow) return set_error(TEIG_ERR_UNSUPPORTED, "AED window > 112");
+    if (window > kAedMaxWindow) return set_error(TEIG_ERR_UNSUPPORTED, "AED window > 104");
     try {
         SchurRunner R(n, dH, ldh, dQ, ldq, o, (cudaStream_t)stream);
         R.begin_round();
@@ -845,7 +851,7 @@ int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int3
     if (k < 1) return set_error(-1, "k must be >= 1");
     if (!dH || ldh < k) return set_error(-3, "bad H");
     if (!dQ) return set_error(-4, "Q is null");
-    if (k > kAedMaxWindow) return set_error(TEIG_ERR_UNSUPPORTED, "small_schur order > 112");
+    if (k > kAedMaxWindow) return set_error(TEIG_ERR_UNSUPPORTED, "small_schur order > 104");
     teig_schur_opts o;
     teig_schur_opts_default(&o);
     try {
@@ -853,7 +859,7 @@ int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int3
         AedDevOut hout{};
         cudaStream_t s = (cudaStream_t)stream;
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dout), sizeof(AedDevOut), s));
-        SchurDevOpts d{o.deflation, o.shift_count, o.aed_window, o.small_threshold};
+        SchurDevOpts d{o.deflation, o.shift_count, o.aed_window, o.small_threshold, 0};
         TEIG_CUDA(launch_aed_window(dH, ldh, kSchurModeSmall, 0, 0, (int)k, d, dQ, dout, nullptr, s));
         TEIG_CUDA(cudaMemcpyAsync(&hout, dout, sizeof hout, cudaMemcpyDeviceToHost, s));
         TEIG_CUDA(cudaFreeAsync(dout, s));

@@ -70,10 +70,16 @@ struct Ctx {
     SchurDevOpts o;
     unsigned long long* prof;  // shared-memory cycle counters (nullptr: off)
     double* brf;  // per-bulge reflector table of the pipelined sweeps (64 entries)
+    int* wave_i;     // swap-wave bookkeeping (block list, pairs)
+    double* wave_d;  // swap-wave pair transforms (kWaveMaxPairs x 32)
+    double* snap;    // global scratch: H and Q snapshot of the top window (2 N^2)
 };
 
+constexpr int kWaveMaxPairs = 56;
+constexpr int kWaveMinWindow = 24;  // smaller AED windows use the sequential order
+
 // diagnostics (TEIG_AED_PROF=1): cycle counters kept by thread 0
-enum { kPfTotal, kPfSmall, kPfSwap, kPfSwapN, kPfSweep, kPfSpike, kPfSteps, kPfSmallSweeps, kPfN };
+enum { kPfTotal, kPfSmall, kPfSwap, kPfSwapN, kPfSweep, kPfSpike, kPfSteps, kPfSmallSweeps, kPfWaveSteps, kPfWaveDecide, kPfWavePlan, kPfN };
 #define PF_T0() const long long _pf0 = clock64()
 #define PF_ADD(i) do { if (c.prof && tid() == 0) c.prof[i] += (unsigned long long)(clock64() - _pf0); } while (0)
 #define PF_INC(i) do { if (c.prof && tid() == 0) c.prof[i] += 1ull; } while (0)
@@ -335,17 +341,155 @@ __device__ __forceinline__ void sim_step(const Ctx& c, int k0, const double (&v)
     __syncthreads();
 }
 
-// small_schur (kernels.cpp:260-381) on the block [lo, lo+n), in place
-__device__ bool small_schur_body(const Ctx& c, int lo, int n);
-__device__ bool small_schur_dev(const Ctx& c, int lo, int n) {
-    PF_T0();
-    const bool ok = small_schur_body(c, lo, n);
-    PF_ADD(kPfSmall);
-    return ok;
+// ---------------------------------------------------------------------------
+// small_schur (kernels.cpp:260-381) on the block [lo, lo+n), in place, run by
+// ONE WARP: a double-shift sweep is a chain of dependent 3-element reflector
+// steps whose per-step work (<= 96 columns left, <= 2*96 rows right) is a
+// few items per lane, so warp-synchronous steps (__syncwarp) beat CTA-wide
+// barriers.  The other warps wait at the closing barrier.
+
+struct WCtx {  // the fields the warp path touches, held in registers
+    double* H;
+    int ldh, N;
+    double* Q;
+    int ldq, nspk;
+    double* sp[kMaxSpk];
+    int spoff[kMaxSpk];
+    unsigned long long* prof;
+};
+
+__device__ __forceinline__ WCtx wctx(const Ctx& c) {
+    WCtx w;
+    w.H = c.H.p;
+    w.ldh = c.H.ld;
+    w.N = c.N;
+    w.Q = c.Q.p;
+    w.ldq = c.Q.ld;
+    w.nspk = c.nspk;
+#pragma unroll
+    for (int k = 0; k < kMaxSpk; ++k) {
+        w.sp[k] = c.spk[k].p;
+        w.spoff[k] = c.spk[k].off;
+    }
+    w.prof = c.prof;
+    return w;
 }
-__device__ bool small_schur_body(const Ctx& c, int lo, int n) {
+
+#define WH(i, j) W.H[(i) + (j) * W.ldh]
+
+template <int G>
+__device__ __forceinline__ void gsync() {
+    if (G == 32) __syncwarp();
+    else __syncthreads();
+}
+
+template <int L, int G>
+__device__ __forceinline__ void w_step(const WCtx& W, int lane, int k0, const double (&v)[L], double tau,
+                                       double beta, int annih, int r1) {
+    if (W.prof && lane == 0) W.prof[kPfSteps] += 1ull;
+    if (tau != 0.0) {
+        for (int j = k0 + lane; j < W.N; j += G) {
+            double* col = &WH(k0, j);
+            double w = 0.0;
+#pragma unroll
+            for (int i = 0; i < L; ++i) w += v[i] * col[i];
+            w *= tau;
+#pragma unroll
+            for (int i = 0; i < L; ++i) col[i] -= w * v[i];
+        }
+    }
+    gsync<G>();
+    if (annih >= 0 && lane == 0) {
+        WH(k0, annih) = beta;
+#pragma unroll
+        for (int i = 1; i < L; ++i) WH(k0 + i, annih) = 0.0;
+    }
+    if (tau != 0.0) {
+        const int total = r1 + W.N + W.nspk;
+        for (int t = lane; t < total; t += G) {
+            double* p;
+            int cs;
+            if (t < r1) {
+                p = &WH(t, k0);
+                cs = W.ldh;
+            } else if (t < r1 + W.N) {
+                p = W.Q + (t - r1) + (size_t)k0 * W.ldq;
+                cs = W.ldq;
+            } else {
+                const int k = t - r1 - W.N;
+                p = W.sp[k] + (k0 - W.spoff[k]);
+                cs = 1;
+            }
+            double w = 0.0;
+#pragma unroll
+            for (int j = 0; j < L; ++j) w += p[j * cs] * v[j];
+            w *= tau;
+#pragma unroll
+            for (int j = 0; j < L; ++j) p[j * cs] -= w * v[j];
+        }
+    }
+    gsync<G>();
+}
+
+template <int G>
+__device__ void w_std_block(const WCtx& W, int lane, int p) {
+    double st[6];
+    std2x2(WH(p, p), WH(p, p + 1), WH(p + 1, p), WH(p + 1, p + 1), st);
+    gsync<G>();
+    const double cs = st[0], sn = st[1];
+    const int ncol = W.N - p - 2;
+    const int total = ncol + p + W.N + W.nspk;
+    for (int t = lane; t < total; t += G) {
+        if (t < ncol) {
+            const int k = p + 2 + t;
+            const double x = WH(p, k), y = WH(p + 1, k);
+            WH(p, k) = cs * x + sn * y;
+            WH(p + 1, k) = -sn * x + cs * y;
+        } else {
+            double* a;
+            int s;
+            const int u = t - ncol;
+            if (u < p) {
+                a = &WH(u, p);
+                s = W.ldh;
+            } else if (u < p + W.N) {
+                a = W.Q + (u - p) + (size_t)p * W.ldq;
+                s = W.ldq;
+            } else {
+                const int k = u - p - W.N;
+                a = W.sp[k] + (p - W.spoff[k]);
+                s = 1;
+            }
+            const double x = a[0], y = a[s];
+            a[0] = cs * x + sn * y;
+            a[s] = -sn * x + cs * y;
+        }
+    }
+    if (lane == 0) {
+        WH(p, p) = st[2];
+        WH(p, p + 1) = st[3];
+        WH(p + 1, p) = st[4];
+        WH(p + 1, p + 1) = st[5];
+    }
+    gsync<G>();
+}
+
+template <int G>
+__device__ bool small_schur_grp(const WCtx& W, int lane, int lo, int n, double* red, int* iscr) {
     if (n <= 1) return true;
-    const double hnorm = hess_norm_block(c, lo, n);
+    double hm = 0.0;
+    for (int idx = lane; idx < n * n; idx += G) {
+        const int j = idx / n, i = idx - j * n;
+        if (i <= min(j + 1, n - 1)) hm = fmax(hm, fabs(WH(lo + i, lo + j)));
+    }
+    double hnorm;
+    if (G == 32) {
+#pragma unroll
+        for (int o = 16; o; o >>= 1) hm = fmax(hm, __shfl_xor_sync(0xffffffffu, hm, o));
+        hnorm = hm;
+    } else {
+        hnorm = block_max(hm, red);
+    }
     if (hnorm == 0.0) return true;
     const double smlnum = kSafeMinD * ((double)n / kEpsD);
     const int max_sweeps = 30 * n;
@@ -356,42 +500,61 @@ __device__ bool small_schur_body(const Ctx& c, int lo, int n) {
             its = 0;
             continue;
         }
-        const int l = scan_block(c, lo, ihi, hnorm, smlnum);
+        int best = 0;  // negligible-subdiagonal scan (kernels.cpp:283-292)
+        for (int l = ihi - 1 - lane; l > 0; l -= G) {
+            double tst = fabs(WH(lo + l - 1, lo + l - 1)) + fabs(WH(lo + l, lo + l));
+            if (tst == 0.0) tst = hnorm;
+            if (fabs(WH(lo + l, lo + l - 1)) <= fmax(kEpsD * tst, smlnum)) best = max(best, l);
+        }
+        int l;
+        if (G == 32) {
+            l = __reduce_max_sync(0xffffffffu, best);
+        } else {
+            best = __reduce_max_sync(0xffffffffu, best);
+            if (lane == 0) iscr[0] = 0;
+            __syncthreads();
+            if ((lane & 31) == 0 && best > 0) atomicMax(iscr, best);
+            __syncthreads();
+            l = iscr[0];
+            __syncthreads();
+        }
+        if (l > 0 && lane == 0) WH(lo + l, lo + l - 1) = 0.0;
+        gsync<G>();
         if (l == ihi - 1) {
             ihi = l;
             its = 0;
             continue;
         }
         if (l == ihi - 2) {
-            std_block_dev(c, lo + l);
+            w_std_block<G>(W, lane, lo + l);
             ihi = l;
             its = 0;
             continue;
         }
         ++its;
         ++sweeps;
-        PF_INC(kPfSmallSweeps);
+        if (W.prof && lane == 0) W.prof[kPfSmallSweeps] += 1ull;
         if (sweeps > max_sweeps) return false;
         double s11, s12, s21, s22;
         if (its % 10 == 0) {
-            const double sp = fabs(c.H(lo + ihi - 1, lo + ihi - 2)) +
-                              ((ihi >= l + 3) ? fabs(c.H(lo + ihi - 2, lo + ihi - 3)) : 0.0);
-            s11 = 0.75 * sp + c.H(lo + ihi - 1, lo + ihi - 1);
+            const double sp = fabs(WH(lo + ihi - 1, lo + ihi - 2)) +
+                              ((ihi >= l + 3) ? fabs(WH(lo + ihi - 2, lo + ihi - 3)) : 0.0);
+            s11 = 0.75 * sp + WH(lo + ihi - 1, lo + ihi - 1);
             s12 = -0.4375 * sp;
             s21 = sp;
             s22 = s11;
         } else {
-            s11 = c.H(lo + ihi - 2, lo + ihi - 2);
-            s12 = c.H(lo + ihi - 2, lo + ihi - 1);
-            s21 = c.H(lo + ihi - 1, lo + ihi - 2);
-            s22 = c.H(lo + ihi - 1, lo + ihi - 1);
+            s11 = WH(lo + ihi - 2, lo + ihi - 2);
+            s12 = WH(lo + ihi - 2, lo + ihi - 1);
+            s21 = WH(lo + ihi - 1, lo + ihi - 2);
+            s22 = WH(lo + ihi - 1, lo + ihi - 1);
         }
         const double ssum = s11 + s22, sprod = s11 * s22 - s12 * s21;
         double v0[3];
         {
             const int b = lo + l;
-            const double a11 = c.H(b, b), a12 = c.H(b, b + 1), a21 = c.H(b + 1, b), a22 = c.H(b + 1, b + 1);
-            const double a32 = c.H(b + 2, b + 1);
+            const double a11 = WH(b, b), a12 = WH(b, b + 1), a21 = WH(b + 1, b), a22 = WH(b + 1, b + 1);
+            const double a32 = WH(b + 2, b + 1);
             v0[0] = a11 * a11 + a12 * a21 - ssum * a11 + sprod;
             v0[1] = a21 * (a11 + a22 - ssum);
             v0[2] = a21 * a32;
@@ -409,87 +572,112 @@ __device__ bool small_schur_body(const Ctx& c, int lo, int n) {
                 x[1] = v0[1];
                 x[2] = v0[2];
             } else {
-                x[0] = c.H(lo + i, lo + i - 1);
-                x[1] = c.H(lo + i + 1, lo + i - 1);
-                x[2] = c.H(lo + i + 2, lo + i - 1);
+                x[0] = WH(lo + i, lo + i - 1);
+                x[1] = WH(lo + i + 1, lo + i - 1);
+                x[2] = WH(lo + i + 2, lo + i - 1);
             }
             double v[3], tau;
             const double beta = reflector_fast<3>(x, v, tau);
-            sim_step<3>(c, lo + i, v, tau, beta, i > l ? lo + i - 1 : -1, lo + min(i + 4, ihi));
+            w_step<3, G>(W, lane, lo + i, v, tau, beta, i > l ? lo + i - 1 : -1, lo + min(i + 4, ihi));
         }
         {
             const int i = ihi - 2;
-            double x[2] = {c.H(lo + i, lo + i - 1), c.H(lo + i + 1, lo + i - 1)};
+            double x[2] = {WH(lo + i, lo + i - 1), WH(lo + i + 1, lo + i - 1)};
             double v[2], tau;
             const double beta = reflector_fast<2>(x, v, tau);
-            sim_step<2>(c, lo + i, v, tau, beta, lo + i - 1, lo + ihi);
+            w_step<2, G>(W, lane, lo + i, v, tau, beta, lo + i - 1, lo + ihi);
         }
     }
     return true;
 }
 
+#undef WH
+
+__device__ bool small_schur_dev(const Ctx& c, int lo, int n) {
+    PF_T0();
+    __syncthreads();
+    bool ok;
+    if (c.o.small_mode == 1) {  // one warp
+        if (tid() < 32) {
+            const WCtx W = wctx(c);
+            const bool r = small_schur_grp<32>(W, tid(), lo, n, c.red, c.iscr);
+            if (tid() == 0) c.iscr[3] = r ? 1 : 0;
+        }
+        __syncthreads();
+        ok = c.iscr[3] != 0;
+    } else {  // the whole CTA, register-held context
+        const WCtx W = wctx(c);
+        ok = small_schur_grp<NT>(W, tid(), lo, n, c.red, c.iscr);
+    }
+    PF_ADD(kPfSmall);
+    return ok;
+}
+
 // ---------------------------------------------------------------------------
 // adjacent block swap (kernels.cpp:510-631) at absolute index pos, applied to
 // the rows right of / columns above the block, to Q and the spike rows.
+// One thread's swap decision (kernels.cpp:510-631) for the adjacent p x p /
+// q x q blocks at pos of H: M (row-major D x D, window <- M^T W M) and the new
+// block NB.  Returns 0 rejected, 1 ok, 2 no-op (equal 1x1 values).
+__device__ __noinline__ int swap_decide(const double* H, int ldh, int pos, int p, int q, double* M, double* NB) {
+    if (p == 1 && q == 1) {
+        const double t11 = H[pos + pos * ldh], t12 = H[pos + (pos + 1) * ldh], t22 = H[(pos + 1) + (pos + 1) * ldh];
+        double cs = 1.0, sn = 0.0;
+        const double bb = t22 - t11;
+        if (bb == 0.0) {
+            cs = 1.0;
+            sn = 0.0;
+        } else if (t12 == 0.0) {
+            cs = 0.0;
+            sn = 1.0;
+        } else {
+            const double r = hypot(t12, bb);
+            cs = t12 / r;
+            sn = bb / r;
+        }
+        if (t12 == 0.0 && bb == 0.0) return 2;  // equal values: no-op (kernels.cpp:517)
+        M[0] = cs;
+        M[1] = -sn;
+        M[2] = sn;
+        M[3] = cs;
+        NB[0] = t22;
+        NB[1] = t12;
+        NB[2] = 0.0;
+        NB[3] = t11;
+        return 1;
+    }
+    auto run = [&](auto P_, auto Q_) {
+        constexpr int P = decltype(P_)::value, Qn = decltype(Q_)::value, D = P + Qn;
+        double blk[D][D], Mm[D][D], nb[D][D];
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+#pragma unroll
+            for (int j = 0; j < D; ++j) blk[i][j] = H[(pos + i) + (pos + j) * ldh];
+        const bool ok = direct_swap<P, Qn>(blk, Mm, nb);
+        if (ok) {
+#pragma unroll
+            for (int i = 0; i < D; ++i)
+#pragma unroll
+                for (int j = 0; j < D; ++j) {
+                    M[i * D + j] = Mm[i][j];
+                    NB[i * D + j] = nb[i][j];
+                }
+        }
+        return ok;
+    };
+    bool ok;
+    if (p == 1) ok = run(std::integral_constant<int, 1>(), std::integral_constant<int, 2>());
+    else if (q == 1) ok = run(std::integral_constant<int, 2>(), std::integral_constant<int, 1>());
+    else ok = run(std::integral_constant<int, 2>(), std::integral_constant<int, 2>());
+    return ok ? 1 : 0;
+}
+
 __device__ __noinline__ bool swap_dev(const Ctx& c, int pos, int p, int q) {
     __syncthreads();
     double* M = c.scr;        // row-major D x D
     double* NB = c.scr + 16;  // new block, row-major
     if (tid() == 0) {
-        int st = 1;
-        if (p == 1 && q == 1) {
-            const double t11 = c.H(pos, pos), t12 = c.H(pos, pos + 1), t22 = c.H(pos + 1, pos + 1);
-            double cs = 1.0, sn = 0.0;
-            const double bb = t22 - t11;
-            if (bb == 0.0) {
-                cs = 1.0;
-                sn = 0.0;
-            } else if (t12 == 0.0) {
-                cs = 0.0;
-                sn = 1.0;
-            } else {
-                const double r = hypot(t12, bb);
-                cs = t12 / r;
-                sn = bb / r;
-            }
-            if (t12 == 0.0 && bb == 0.0) {
-                st = 2;  // equal values: no-op (kernels.cpp:517)
-            } else {
-                M[0] = cs;
-                M[1] = -sn;
-                M[2] = sn;
-                M[3] = cs;
-                NB[0] = t22;
-                NB[1] = t12;
-                NB[2] = 0.0;
-                NB[3] = t11;
-            }
-        } else {
-            auto run = [&](auto P_, auto Q_) {
-                constexpr int P = decltype(P_)::value, Qn = decltype(Q_)::value, D = P + Qn;
-                double blk[D][D], Mm[D][D], nb[D][D];
-#pragma unroll
-                for (int i = 0; i < D; ++i)
-#pragma unroll
-                    for (int j = 0; j < D; ++j) blk[i][j] = c.H(pos + i, pos + j);
-                const bool ok = direct_swap<P, Qn>(blk, Mm, nb);
-                if (ok) {
-#pragma unroll
-                    for (int i = 0; i < D; ++i)
-#pragma unroll
-                        for (int j = 0; j < D; ++j) {
-                            M[i * D + j] = Mm[i][j];
-                            NB[i * D + j] = nb[i][j];
-                        }
-                }
-                return ok;
-            };
-            bool ok;
-            if (p == 1) ok = run(std::integral_constant<int, 1>(), std::integral_constant<int, 2>());
-            else if (q == 1) ok = run(std::integral_constant<int, 2>(), std::integral_constant<int, 1>());
-            else ok = run(std::integral_constant<int, 2>(), std::integral_constant<int, 2>());
-            st = ok ? 1 : 0;
-        }
+        const int st = swap_decide(c.H.p, c.H.ld, pos, p, q, M, NB);
         c.iscr[1] = st;
     }
     __syncthreads();
@@ -711,6 +899,191 @@ __device__ void sweep_pipelined(const Ctx& c, int lo, int l, int ihi, int nb, co
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// AED deflation as a SWAP WAVE.  The reference (schur.cpp:169-204) tests the
+// bottom block of the undecided range; a failed block is moved to the top of
+// the window by a chain of adjacent swaps before the next block is tested.
+// A block's test only reads its own diagonal and its spike entries
+// beta*q(0, rows), which the failed blocks change only while passing it, so
+// the next block can be tested as soon as the last failed block has passed
+// it.  Here every failed block ("mover") climbs one block per step, movers
+// trail each other, every mover's swap of the step is decided by its own
+// thread and all are applied in one two-phase pass (rows, then columns:
+// disjoint pairs commute).  The final arrangement and every decision are the
+// reference's; the depth drops from #swaps (~800 per 96-window) to
+// ~#blocks + #failures.  A rejected swap (where the reference stops the
+// whole loop) makes the caller restore a snapshot and rerun the reference
+// order.  Returns false on a rejection; ns_out = top of the deflated part.
+__device__ bool deflate_wave(const Ctx& c, int e, int w, double beta, double wnorm, const double* sp, int sps,
+                             int& ns_out) {
+    int* wi = c.wave_i;     // [0] nblk [1] npairs [2] done [3] ns [4] rejected
+    int* bsz = wi + 8;      // block sizes, top to bottom
+    int* bst = bsz + 128;   // 0 undecided, 1 mover, 2 settled (top), 3 deflated (bottom)
+    int* pr = bst + 128;    // per pair: upper block index, pos, p, q
+    double* pm = c.wave_d;  // per pair: M[16], NB[16]
+    const int lane = tid() & 31, warp = tid() >> 5;
+    constexpr int NW = NT / 32;
+    __syncthreads();
+    if (tid() == 0) {
+        int i = 0, k = 0;
+        while (i < w) {
+            const int sz = (i + 1 < w && c.H(e + i + 1, e + i) != 0.0) ? 2 : 1;
+            bsz[k] = sz;
+            bst[k] = 0;
+            i += sz;
+            ++k;
+        }
+        wi[0] = k;
+        wi[3] = w;
+        wi[4] = 0;
+    }
+    __syncthreads();
+    const int nblk = wi[0];
+    for (;;) {
+        long long _pfp = clock64();
+        if (tid() == 0) {
+            // test the bottom undecided block(s) nobody still has to pass
+            for (;;) {
+                int k = nblk - 1;
+                while (k >= 0 && bst[k] == 3) --k;
+                if (k < 0 || bst[k] != 0) break;
+                int pos = 0;
+                for (int t = 0; t < k; ++t) pos += bsz[t];
+                double spike = 0.0, dsum = 0.0;
+                for (int r = pos; r < pos + bsz[k]; ++r) {
+                    spike = fmax(spike, fabs(beta * sp[(e + r) * sps]));
+                    dsum += fabs(c.H(e + r, e + r));
+                }
+                if (deflation_check_dev(spike, dsum, c.o.deflation, wnorm)) {
+                    bst[k] = 3;
+                    wi[3] = pos;
+                } else {
+                    bst[k] = 1;
+                    break;
+                }
+            }
+            // movers: settle at the top or pair with the undecided block above
+            int np = 0, pos = 0;
+            bool any = false;
+            for (int k = 0; k < nblk; ++k) {
+                if (bst[k] == 1) {
+                    if (k == 0 || bst[k - 1] == 2) {
+                        bst[k] = 2;
+                    } else if (bst[k - 1] == 0 && np < kWaveMaxPairs) {
+                        pr[4 * np] = k - 1;
+                        pr[4 * np + 1] = e + pos - bsz[k - 1];
+                        pr[4 * np + 2] = bsz[k - 1];
+                        pr[4 * np + 3] = bsz[k];
+                        ++np;
+                    }
+                }
+                if (bst[k] == 0 || bst[k] == 1) any = true;
+                pos += bsz[k];
+            }
+            wi[1] = np;
+            wi[2] = any ? 0 : 1;
+        }
+        __syncthreads();
+        if (c.prof && tid() == 0) {
+            c.prof[kPfWavePlan] += (unsigned long long)(clock64() - _pfp);
+            c.prof[kPfWaveSteps] += 1ull;
+        }
+        if (wi[2]) break;
+        const int np = wi[1];
+        _pfp = clock64();
+        if (tid() < np) {  // every mover's swap decision on its own thread
+            const int t = tid();
+            double* M = pm + 32 * t;
+            double* NB = M + 16;
+            const int pos = pr[4 * t + 1], p = pr[4 * t + 2], q = pr[4 * t + 3];
+            const int st = swap_decide(c.H.p, c.H.ld, pos, p, q, M, NB);
+            if (st == 0) wi[4] = 1;
+            if (st == 2) {  // equal 1x1 values: the swap is the identity
+                M[0] = 1.0; M[1] = 0.0; M[2] = 0.0; M[3] = 1.0;
+                NB[0] = c.H(pos, pos); NB[1] = c.H(pos, pos + 1); NB[2] = 0.0; NB[3] = c.H(pos + 1, pos + 1);
+            }
+        }
+        __syncthreads();
+        if (c.prof && tid() == 0) c.prof[kPfWaveDecide] += (unsigned long long)(clock64() - _pfp);
+        if (wi[4]) return false;
+        if (c.prof && tid() == 0) c.prof[kPfSwapN] += (unsigned long long)np;
+        for (int q = warp; q < np; q += NW) {  // rows of each pair, columns right of its block
+            const double* M = pm + 32 * q;
+            const int pos = pr[4 * q + 1], D = pr[4 * q + 2] + pr[4 * q + 3];
+            for (int k = pos + D + lane; k < c.N; k += 32) {
+                double x[4], y[4];
+                for (int r = 0; r < D; ++r) x[r] = c.H(pos + r, k);
+                for (int i = 0; i < D; ++i) {
+                    double a = 0.0;
+                    for (int r = 0; r < D; ++r) a += M[r * D + i] * x[r];
+                    y[i] = a;
+                }
+                for (int i = 0; i < D; ++i) c.H(pos + i, k) = y[i];
+            }
+        }
+        __syncthreads();
+        for (int q = warp; q < np; q += NW) {  // columns of each pair: rows above, Q, spikes; the block
+            const double* M = pm + 32 * q;
+            const double* NB = M + 16;
+            const int pos = pr[4 * q + 1], D = pr[4 * q + 2] + pr[4 * q + 3];
+            const int total = pos + c.N + c.nspk;
+            for (int t = lane; t < total; t += 32) {
+                double* a;
+                int st;
+                if (t < pos) {
+                    a = &c.H(t, pos);
+                    st = c.H.ld;
+                } else if (t < pos + c.N) {
+                    a = &c.Q(t - pos, pos);
+                    st = c.Q.ld;
+                } else {
+                    const Spk& sk = c.spk[t - pos - c.N];
+                    a = sk.p + (pos - sk.off);
+                    st = 1;
+                }
+                double x[4], y[4];
+                for (int r = 0; r < D; ++r) x[r] = a[r * st];
+                for (int j = 0; j < D; ++j) {
+                    double acc = 0.0;
+                    for (int r = 0; r < D; ++r) acc += x[r] * M[r * D + j];
+                    y[j] = acc;
+                }
+                for (int j = 0; j < D; ++j) a[j * st] = y[j];
+            }
+            if (lane < D * D) c.H(pos + lane / D, pos + lane % D) = NB[lane];
+        }
+        __syncthreads();
+        if (tid() == 0)
+            for (int q = 0; q < np; ++q) {  // the pair's blocks changed places
+                const int k = pr[4 * q];
+                const int ts = bsz[k], tt = bst[k];
+                bsz[k] = bsz[k + 1];
+                bst[k] = bst[k + 1];
+                bsz[k + 1] = ts;
+                bst[k + 1] = tt;
+            }
+    }
+    ns_out = wi[3] - 0;
+    return true;
+}
+
+// top-window snapshot (H and Q, N x N each) to global scratch and back
+__device__ void snap_copy(const Ctx& c, bool save) {
+    const int N = c.N;
+    for (int idx = tid(); idx < N * N; idx += NT) {
+        const int j = idx / N, i = idx - j * N;
+        if (save) {
+            c.snap[idx] = c.H(i, j);
+            c.snap[N * N + idx] = c.Q(i, j);
+        } else {
+            c.H(i, j) = c.snap[idx];
+            c.Q(i, j) = c.snap[N * N + idx];
+        }
+    }
+    __syncthreads();
+}
+
 // multishift_schur_dense (schur.cpp:304-399) on the block [lo, lo+n), in place
 template <int D>
 __device__ bool mshift_dev(Ctx& c, int lo, int n) {
@@ -879,7 +1252,21 @@ __device__ AedCoreDev aed_dev(Ctx& c, int e, int w, double beta) {
         core.spike_eliminated = 1;
     } else if (conv) {
         int ktop = 0, ns = w;
-        while (ns > ktop) {
+        bool waved = false;
+        if (D == 0 && w >= kWaveMinWindow && c.snap) {
+            PF_T0();
+            snap_copy(c, true);
+            int nsw = w;
+            if (deflate_wave(c, e, w, beta, wnorm, sp, sps, nsw)) {
+                waved = true;
+                ns = nsw;
+                ktop = ns;
+            } else {
+                snap_copy(c, false);  // a rejected swap: rerun in the reference's order
+            }
+            PF_ADD(kPfSwap);
+        }
+        while (!waved && ns > ktop) {
             const int bsize = (ns >= 2 && ns - 2 >= ktop && c.H(e + ns - 1, e + ns - 2) != 0.0) ? 2 : 1;
             const int bs = ns - bsize;
             double spike = 0.0, dsum = 0.0;
@@ -980,7 +1367,8 @@ __device__ AedCoreDev aed_dev(Ctx& c, int e, int w, double beta) {
 __global__ void __launch_bounds__(NT) aed_window_kernel(double* __restrict__ Hg, long long ldh, int mode, int l,
                                                         int e, int w, SchurDevOpts o, double* __restrict__ qw_out,
                                                         AedDevOut* __restrict__ out, double* __restrict__ shifts_out,
-                                                        unsigned long long* __restrict__ prof_out) {
+                                                        unsigned long long* __restrict__ prof_out,
+                                                        double* __restrict__ snap) {
     extern __shared__ __align__(16) double sm[];
     __shared__ unsigned long long pf[kPfN];
     const long long t_start = clock64();
@@ -1006,8 +1394,12 @@ __global__ void __launch_bounds__(NT) aed_window_kernel(double* __restrict__ Hg,
     base += (size_t)kMaxSpk * w;
     c.brf = base;
     base += 64 * 6;
+    c.wave_d = base;
+    base += kWaveMaxPairs * 32;
+    c.snap = snap;
     c.iscr = reinterpret_cast<int*>(base);
     c.nsh = c.iscr + 8;
+    c.wave_i = c.iscr + 32;
     c.o = o;
     c.prof = prof_out ? pf : nullptr;
     for (int idx = tid(); idx < w * w; idx += NT) {
@@ -1051,13 +1443,14 @@ __global__ void __launch_bounds__(NT) aed_window_kernel(double* __restrict__ Hg,
 
 size_t aed_window_smem_bytes(int w) {
     const size_t ld = (size_t)(w | 1);
-    const size_t dbl = 2 * ld * w + 32 + w + 40 + kMaxSpk * 2 * w + kMaxSpk * 2 * (w + 4) + kMaxSpk * w + 64 * 6;
-    return dbl * sizeof(double) + 32 * sizeof(int);
+    const size_t dbl = 2 * ld * w + 32 + w + 40 + kMaxSpk * 2 * w + kMaxSpk * 2 * (w + 4) + kMaxSpk * w + 64 * 6 +
+                       kWaveMaxPairs * 32;
+    return dbl * sizeof(double) + (32 + 8 + 128 + 128 + 4 * kWaveMaxPairs) * sizeof(int);
 }
 
 cudaError_t launch_aed_window(double* H, long long ldh, int mode, int l, int e, int w, const SchurDevOpts& o,
                               double* qw_out, AedDevOut* out, double* shifts_out, cudaStream_t stream,
-                              unsigned long long* prof) {
+                              unsigned long long* prof, double* snap) {
     const size_t smem = aed_window_smem_bytes(w);
     static size_t configured = 0;
     if (smem > configured) {
@@ -1066,7 +1459,7 @@ cudaError_t launch_aed_window(double* H, long long ldh, int mode, int l, int e, 
         if (err != cudaSuccess) return err;
         configured = aed_window_smem_bytes(kAedMaxWindow);
     }
-    aed_window_kernel<<<1, NT, smem, stream>>>(H, ldh, mode, l, e, w, o, qw_out, out, shifts_out, prof);
+    aed_window_kernel<<<1, NT, smem, stream>>>(H, ldh, mode, l, e, w, o, qw_out, out, shifts_out, prof, snap);
     return cudaGetLastError();
 }
 
