@@ -616,6 +616,69 @@ __device__ bool small_schur_dev(const Ctx& c, int lo, int n) {
 // ---------------------------------------------------------------------------
 // adjacent block swap (kernels.cpp:510-631) at absolute index pos, applied to
 // the rows right of / columns above the block, to Q and the spike rows.
+// one swap's transform M (row-major D x D) on the rows of its block, columns
+// right of the block (M^T), by one warp
+template <int D>
+__device__ __forceinline__ void pair_left(const Ctx& c, const double* Mg, int pos, int lane) {
+    double M[D][D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int i = 0; i < D; ++i) M[r][i] = Mg[r * D + i];
+    for (int k = pos + D + lane; k < c.N; k += 32) {
+        double* col = &c.H(pos, k);
+        double x[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) x[r] = col[r];
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+            double a = 0.0;
+#pragma unroll
+            for (int r = 0; r < D; ++r) a += M[r][i] * x[r];
+            col[i] = a;
+        }
+    }
+}
+
+// ... on the columns of its block: H rows above, all Q rows, spike rows (M),
+// and the new block NB
+template <int D>
+__device__ __forceinline__ void pair_right(const Ctx& c, const double* Mg, int pos, int lane) {
+    double M[D][D];
+#pragma unroll
+    for (int r = 0; r < D; ++r)
+#pragma unroll
+        for (int j = 0; j < D; ++j) M[r][j] = Mg[r * D + j];
+    const int total = pos + c.N + c.nspk;
+    for (int t = lane; t < total; t += 32) {
+        double* a;
+        int st;
+        if (t < pos) {
+            a = &c.H(t, pos);
+            st = c.H.ld;
+        } else if (t < pos + c.N) {
+            a = &c.Q(t - pos, pos);
+            st = c.Q.ld;
+        } else {
+            const Spk& sk = c.spk[t - pos - c.N];
+            a = sk.p + (pos - sk.off);
+            st = 1;
+        }
+        double x[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) x[r] = a[r * st];
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int r = 0; r < D; ++r) acc += x[r] * M[r][j];
+            a[j * st] = acc;
+        }
+    }
+    const double* NB = Mg + 16;
+    if (lane < D * D) c.H(pos + lane / D, pos + lane % D) = NB[lane];
+}
+
 // One thread's swap decision (kernels.cpp:510-631) for the adjacent p x p /
 // q x q blocks at pos of H: M (row-major D x D, window <- M^T W M) and the new
 // block NB.  Returns 0 rejected, 1 ok, 2 no-op (equal 1x1 values).
@@ -684,46 +747,17 @@ __device__ __noinline__ bool swap_dev(const Ctx& c, int pos, int p, int q) {
     const int st = c.iscr[1];
     if (st != 1) return st == 2;
     const int D = p + q;
-    const int ncol = c.N - pos - D;
-    const int total = ncol + pos + c.N + c.nspk;
-    for (int t = tid(); t < total; t += NT) {
-        double x[4], y[4];
-        if (t < ncol) {  // rows pos.. of column k <- M^T rows
-            const int k = pos + D + t;
-            for (int r = 0; r < D; ++r) x[r] = c.H(pos + r, k);
-            for (int i = 0; i < D; ++i) {
-                double a = 0.0;
-                for (int r = 0; r < D; ++r) a += M[r * D + i] * x[r];
-                y[i] = a;
-            }
-            for (int i = 0; i < D; ++i) c.H(pos + i, k) = y[i];
-        } else {  // a row segment over columns pos..pos+D-1 <- row M
-            const int u = t - ncol;
-            double* a;
-            int s;
-            if (u < pos) {
-                a = &c.H(u, pos);
-                s = c.H.ld;
-            } else if (u < pos + c.N) {
-                a = &c.Q(u - pos, pos);
-                s = c.Q.ld;
-            } else {
-                const Spk& sp = c.spk[u - pos - c.N];
-                a = sp.p + (pos - sp.off);
-                s = 1;
-            }
-            for (int r = 0; r < D; ++r) x[r] = a[r * s];
-            for (int j = 0; j < D; ++j) {
-                double acc = 0.0;
-                for (int r = 0; r < D; ++r) acc += x[r] * M[r * D + j];
-                y[j] = acc;
-            }
-            for (int j = 0; j < D; ++j) a[j * s] = y[j];
-        }
+    // left part on warps 0..3, right part (and the block) on warps 4..7
+    const int lane = tid() & 31, warp = tid() >> 5;
+    if (warp == 0) {
+        if (D == 2) pair_left<2>(c, M, pos, lane);
+        else if (D == 3) pair_left<3>(c, M, pos, lane);
+        else pair_left<4>(c, M, pos, lane);
+    } else if (warp == 1) {
+        if (D == 2) pair_right<2>(c, M, pos, lane);
+        else if (D == 3) pair_right<3>(c, M, pos, lane);
+        else pair_right<4>(c, M, pos, lane);
     }
-    if (tid() == 0)
-        for (int i = 0; i < D; ++i)
-            for (int j = 0; j < D; ++j) c.H(pos + i, pos + j) = NB[i * D + j];
     __syncthreads();
     return true;
 }
@@ -921,6 +955,7 @@ __device__ bool deflate_wave(const Ctx& c, int e, int w, double beta, double wno
     int* bsz = wi + 8;      // block sizes, top to bottom
     int* bst = bsz + 128;   // 0 undecided, 1 mover, 2 settled (top), 3 deflated (bottom)
     int* pr = bst + 128;    // per pair: upper block index, pos, p, q
+    int* pt = pr + 4 * kWaveMaxPairs;  // per type: count[4], then the pair lists
     double* pm = c.wave_d;  // per pair: M[16], NB[16]
     const int lane = tid() & 31, warp = tid() >> 5;
     constexpr int NW = NT / 32;
@@ -983,6 +1018,11 @@ __device__ bool deflate_wave(const Ctx& c, int e, int w, double beta, double wno
             }
             wi[1] = np;
             wi[2] = any ? 0 : 1;
+            for (int ty = 0; ty < 4; ++ty) pt[ty] = 0;
+            for (int q = 0; q < np; ++q) {
+                const int ty = (pr[4 * q + 2] - 1) * 2 + (pr[4 * q + 3] - 1);  // (p,q) -> 0..3
+                pt[4 + ty * kWaveMaxPairs + pt[ty]++] = q;
+            }
         }
         __syncthreads();
         if (c.prof && tid() == 0) {
@@ -992,8 +1032,11 @@ __device__ bool deflate_wave(const Ctx& c, int e, int w, double beta, double wno
         if (wi[2]) break;
         const int np = wi[1];
         _pfp = clock64();
-        if (tid() < np) {  // every mover's swap decision on its own thread
-            const int t = tid();
+        // every mover's swap decision on its own thread; warp w takes the pairs
+        // of block-size type w so the four decision code paths run on
+        // different warps concurrently instead of diverging inside one
+        for (int li = lane; warp < 4 && li < pt[warp]; li += 32) {
+            const int t = pt[4 + warp * kWaveMaxPairs + li];
             double* M = pm + 32 * t;
             double* NB = M + 16;
             const int pos = pr[4 * t + 1], p = pr[4 * t + 2], q = pr[4 * t + 3];
@@ -1011,47 +1054,17 @@ __device__ bool deflate_wave(const Ctx& c, int e, int w, double beta, double wno
         for (int q = warp; q < np; q += NW) {  // rows of each pair, columns right of its block
             const double* M = pm + 32 * q;
             const int pos = pr[4 * q + 1], D = pr[4 * q + 2] + pr[4 * q + 3];
-            for (int k = pos + D + lane; k < c.N; k += 32) {
-                double x[4], y[4];
-                for (int r = 0; r < D; ++r) x[r] = c.H(pos + r, k);
-                for (int i = 0; i < D; ++i) {
-                    double a = 0.0;
-                    for (int r = 0; r < D; ++r) a += M[r * D + i] * x[r];
-                    y[i] = a;
-                }
-                for (int i = 0; i < D; ++i) c.H(pos + i, k) = y[i];
-            }
+            if (D == 2) pair_left<2>(c, M, pos, lane);
+            else if (D == 3) pair_left<3>(c, M, pos, lane);
+            else pair_left<4>(c, M, pos, lane);
         }
         __syncthreads();
         for (int q = warp; q < np; q += NW) {  // columns of each pair: rows above, Q, spikes; the block
             const double* M = pm + 32 * q;
-            const double* NB = M + 16;
             const int pos = pr[4 * q + 1], D = pr[4 * q + 2] + pr[4 * q + 3];
-            const int total = pos + c.N + c.nspk;
-            for (int t = lane; t < total; t += 32) {
-                double* a;
-                int st;
-                if (t < pos) {
-                    a = &c.H(t, pos);
-                    st = c.H.ld;
-                } else if (t < pos + c.N) {
-                    a = &c.Q(t - pos, pos);
-                    st = c.Q.ld;
-                } else {
-                    const Spk& sk = c.spk[t - pos - c.N];
-                    a = sk.p + (pos - sk.off);
-                    st = 1;
-                }
-                double x[4], y[4];
-                for (int r = 0; r < D; ++r) x[r] = a[r * st];
-                for (int j = 0; j < D; ++j) {
-                    double acc = 0.0;
-                    for (int r = 0; r < D; ++r) acc += x[r] * M[r * D + j];
-                    y[j] = acc;
-                }
-                for (int j = 0; j < D; ++j) a[j * st] = y[j];
-            }
-            if (lane < D * D) c.H(pos + lane / D, pos + lane % D) = NB[lane];
+            if (D == 2) pair_right<2>(c, M, pos, lane);
+            else if (D == 3) pair_right<3>(c, M, pos, lane);
+            else pair_right<4>(c, M, pos, lane);
         }
         __syncthreads();
         if (tid() == 0)
@@ -1445,7 +1458,7 @@ size_t aed_window_smem_bytes(int w) {
     const size_t ld = (size_t)(w | 1);
     const size_t dbl = 2 * ld * w + 32 + w + 40 + kMaxSpk * 2 * w + kMaxSpk * 2 * (w + 4) + kMaxSpk * w + 64 * 6 +
                        kWaveMaxPairs * 32;
-    return dbl * sizeof(double) + (32 + 8 + 128 + 128 + 4 * kWaveMaxPairs) * sizeof(int);
+    return dbl * sizeof(double) + (32 + 8 + 128 + 128 + 4 * kWaveMaxPairs + 4 + 4 * kWaveMaxPairs) * sizeof(int);
 }
 
 cudaError_t launch_aed_window(double* H, long long ldh, int mode, int l, int e, int w, const SchurDevOpts& o,
