@@ -273,6 +273,31 @@ int teig_gen_schur_input_cols_device(int64_t n, double* dS, int64_t lds, int64_t
 int teig_set_identity_rows_device(int64_t n, double* dQ, int64_t ldq, int64_t r0, int64_t r1,
                                   void* stream);
 
+
+/* ------------------------------------------------------------------------ */
+/* Generalized Schur-pair reordering (S, T) with Q and Z (SURVEY.md 8a a16,  */
+/* config C5; no reference implementation: LAPACK DTGSEN/DTGEX2 semantics    */
+/* over the reference's reorder planner, reorder.cpp:215-404).               */
+
+/* dS upper quasi-triangular (block sizes = sizes, as from S's subdiagonal),
+ * dT upper triangular (2x2 diagonal blocks of T upper triangular), both
+ * n x n column-major on the device; dQ, dZ (or NULL) updated to Q*Qs, Z*Zs
+ * with (S, T) <- Qs^T (S, T) Zs.  opts->window_size 0 means 64 (the limit:
+ * the window kernel holds S, T, Q_w and Z_w in shared memory).  Outputs as
+ * teig_reorder_schur_device. */
+int teig_greorder_schur_device(int64_t n, double* dS, int64_t lds, double* dT, int64_t ldt, double* dQ,
+                               int64_t ldq, double* dZ, int64_t ldz, int64_t nb, const uint8_t* sizes,
+                               const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm,
+                               int64_t* rejected, teig_reorder_info* info, void* stream);
+/* Same on HOST buffers; includes H2D/D2H. */
+int teig_greorder_schur_host(int64_t n, double* S, int64_t lds, double* T, int64_t ldt, double* Q,
+                             int64_t ldq, double* Z, int64_t ldz, int64_t nb, const uint8_t* sizes,
+                             const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm,
+                             int64_t* rejected, teig_reorder_info* info, void* stream);
+/* The C5 input T: upper triangular, diagonal 1 + U[0,1),
+ * uniform [-1, 1] fill, on the synthetic S's block pattern. */
+int teig_gen_pair_t_device(int64_t n, double* dT, int64_t ldt, uint64_t seed, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

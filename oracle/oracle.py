@@ -91,6 +91,8 @@ def lib():
         L.teo_plan_free.restype = None
         L.teo_plan_flops.argtypes = [_P, _SZ, C.c_int]
         L.teo_plan_flops.restype = _D
+        L.teo_pair_t.argtypes = [_SZ, _U64, _P, _SZ]
+        L.teo_pair_t.restype = None
         L.teo_small_schur.argtypes = [_SZ, _P, _P, _P]
         L.teo_small_schur.restype = C.c_int
         L.teo_deflation_check.argtypes = [_D, _D, C.c_int, _D]
@@ -560,3 +562,52 @@ def ref_default_spectrum(n: int, seed: int) -> np.ndarray:
     out = np.zeros(2 * n)
     ref().ref_default_spectrum(n, seed, _ptr(out))
     return out[0::2] + 1j * out[1::2]
+
+
+# --------------------------------------------------------------------------
+# C5 (generalized pair): the input T and the external oracle, LAPACK DTGSEN
+# (scipy 1.18.1 / scipy-openblas 0.3.31.dev; the reference has no
+# generalized path -- SURVEY.md 8c "C5: parity unpinned by the reference")
+
+def pair_t(n: int, seed: int) -> np.ndarray:
+    t = np.zeros((n, n), order="F")
+    lib().teo_pair_t(n, seed, _ptr(t), n)
+    return t
+
+
+def lapack_tgsen(s, t, row_select):
+    """DTGSEN (ijob=0): reorders the pencil so the selected eigenvalues lead,
+    keeping the relative order inside both groups.  Returns (S, T, Q, Z,
+    eigenvalues alpha/beta in diagonal order)."""
+    from scipy.linalg import lapack
+    n = s.shape[0]
+    q = np.eye(n, order="F")
+    z = np.eye(n, order="F")
+    a, b, ar, ai, be, qs, zs, m, pl, pr, dif, info = lapack.dtgsen(
+        np.asarray(row_select, dtype=np.int32), np.asfortranarray(s), np.asfortranarray(t), q, z, ijob=0)
+    if info != 0:
+        raise RuntimeError(f"dtgsen info={info}")
+    return a, b, qs, zs, (ar + 1j * ai) / be
+
+
+def pencil_eigenvalues(s, t) -> np.ndarray:
+    """Generalized eigenvalues of the quasi-triangular pencil's diagonal
+    blocks, in diagonal order (2x2 blocks: roots of det(S_b - l T_b))."""
+    n = s.shape[0]
+    out = np.zeros(n, dtype=complex)
+    i = 0
+    while i < n:
+        if i + 1 < n and s[i + 1, i] != 0.0:
+            A = s[i:i + 2, i:i + 2]
+            B = t[i:i + 2, i:i + 2]
+            c2 = B[0, 0] * B[1, 1] - B[0, 1] * B[1, 0]
+            c1 = -(A[0, 0] * B[1, 1] + A[1, 1] * B[0, 0] - A[0, 1] * B[1, 0] - A[1, 0] * B[0, 1])
+            c0 = A[0, 0] * A[1, 1] - A[0, 1] * A[1, 0]
+            r = np.roots([c2, c1, c0])
+            r = sorted(r, key=lambda z: -z.imag)
+            out[i], out[i + 1] = r[0], r[1]
+            i += 2
+        else:
+            out[i] = s[i, i] / t[i, i]
+            i += 1
+    return out

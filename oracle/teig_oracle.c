@@ -1858,3 +1858,37 @@ int teo_schur_reduce(size_t n, double* h, size_t ldh, double* q, size_t ldq, siz
     free(pos);
     return 0;
 }
+
+/* ======================================================================= */
+/* C5 input T (generalized pair; no reference generator exists -- the      */
+/* library's gen_pair_t_kernel, restated): upper triangular on the          */
+/* synthetic S's block pattern, diagonal 1 + U[0,1) (shared inside a 2x2    */
+/* block, in-block T(p, p+1) = 0), strictly upper uniform [-1, 1]; entry    */
+/* (i, j) uses the (i*n + j)-th draw of Philox(seed).                       */
+
+static uint64_t philox_u64_at(uint64_t seed, uint64_t k) {
+    const uint64_t blk = k >> 1;
+    const uint32_t ctr[4] = {(uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u};
+    const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t out[4];
+    teo_philox_round10(ctr, key, out);
+    const int i = (int)(k & 1);
+    return ((uint64_t)out[2 * i + 1] << 32) | out[2 * i];
+}
+
+void teo_pair_t(size_t n, uint64_t seed, double* t, size_t ld) {
+    const size_t npairs = n / 4, nreal = n - 2 * npairs;
+    for (size_t j = 0; j < n; ++j)
+        for (size_t i = 0; i < n; ++i) {
+            double v = 0.0;
+            const int pair_first_i = i >= nreal && ((i - nreal) & 1) == 0;
+            if (i == j) {
+                const int second = j >= nreal && ((j - nreal) & 1) == 1;
+                const size_t r = second ? i - 1 : i;
+                v = 1.0 + (double)(philox_u64_at(seed, (uint64_t)(r * n + r)) >> 11) * (1.0 / 9007199254740992.0);
+            } else if (j > i && !(pair_first_i && j == i + 1)) {
+                v = 2.0 * ((double)(philox_u64_at(seed, (uint64_t)(i * n + j)) >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
+            }
+            A_(t, i, j, ld) = v;
+        }
+}

@@ -148,6 +148,9 @@ int teo_sweep(size_t n, double* h, size_t ldh, double* q, size_t ldq, size_t l, 
 int teo_schur_reduce(size_t n, double* h, size_t ldh, double* q, size_t ldq, size_t tile,
                      const teo_schur_opts* o, double* eig, teo_schur_info* info);
 
+/* ---- C5 (generalized pair) input T, the library generator restated ----- */
+void teo_pair_t(size_t n, uint64_t seed, double* t, size_t ld);
+
 /* ---- verification (verify.cpp) ----------------------------------------- */
 double teo_similarity_residual(size_t n, const double* a, size_t lda, const double* q,
                                size_t ldq, const double* s, size_t lds);

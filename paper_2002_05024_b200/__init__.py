@@ -8,7 +8,8 @@ the reference interface.  There is no CPU fallback.
 """
 from ._native import TaskeigError, build, lib  # noqa: F401
 from .reorder import (  # noqa: F401
-    Block, PlanWindow, ReorderOptions, ReorderResult, Selection, WindowReorderOutcome,
+    Block, GReorderResult, PlanWindow, ReorderOptions, ReorderResult, Selection, WindowReorderOutcome,
+    gen_pair_t, greorder_schur,
     apply_window_updates, colmajor_empty, gen_hessenberg, gen_schur_input, identity,
     known_spectrum_seed, plan_reorder, reorder_schur, scan_blocks, scan_blocks_device, select_by_name,
     select_eigenvalues, select_fraction, window_reorder)

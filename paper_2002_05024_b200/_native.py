@@ -93,6 +93,11 @@ SIGNATURES = {
     "teig_chase_bulges_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _I64, _P, _I64, _P, _P]),
     "teig_small_schur_device": (C.c_int, [_I64, _P, _I64, _P, _P, _P]),
     "teig_deflation_check": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.c_double]),
+    "teig_greorder_schur_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P,
+                                             _P, _P, _P]),
+    "teig_greorder_schur_host": (C.c_int, [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P,
+                                           _P, _P, _P]),
+    "teig_gen_pair_t_device": (C.c_int, [_I64, _P, _I64, C.c_uint64, _P]),
     "teig_dist_balance": (C.c_int, [_I64, _I64, _P, _P, _I64, C.c_int32, _P, _P]),
     "teig_dist_schedule": (C.c_int64, [_I64, _I64, _P, _P, _I64, C.c_int32, _P, _P, _I64]),
     "teig_dist_reorder_schur": (C.c_int, [_I64, C.c_int32, C.c_int32, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P,

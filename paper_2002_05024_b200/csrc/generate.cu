@@ -43,6 +43,42 @@ __device__ __forceinline__ double draw_uniform_sym(uint64_t seed, uint64_t k) {
     return __dsub_rn(__dmul_rn((double)u, 2.0 / 9007199254740992.0), 1.0);
 }
 
+// k-th uniform [0, 1) draw of Philox(seed)
+__device__ __forceinline__ double draw_u01(uint64_t seed, uint64_t k) {
+    const uint64_t blk = k >> 1;
+    uint32_t c[4] = {(uint32_t)blk, (uint32_t)(blk >> 32), 0u, 0u};
+    philox10(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    const int i = (int)(k & 1);
+    const uint64_t u = (((uint64_t)c[2 * i + 1] << 32) | c[2 * i]) >> 11;
+    return __dmul_rn((double)u, 1.0 / 9007199254740992.0);
+}
+
+// C5 input T ("T upper triangular with a positive diagonal,
+// uniform [-1, 1] upper fill"; no reference generator exists): on the block
+// pattern of the synthetic S (reals first, then 2x2 blocks), diagonal 1 + u
+// (both entries of a 2x2 block share the first one's draw and the in-block
+// T(p, p+1) is 0, so every 2x2 block of the pencil keeps its complex pair),
+// strictly upper fill uniform_sym.  Entry (i, j) uses draw i*n + j.
+__global__ void gen_pair_t_kernel(double* T, long long ldt, long long n, uint64_t seed) {
+    const long long j = blockIdx.y;
+    const long long npairs = n / 4, nreal = n - 2 * npairs;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double v = 0.0;
+        const bool pair_first_i = i >= nreal && ((i - nreal) & 1) == 0;
+        if (i == j) {
+            const bool second = j >= nreal && ((j - nreal) & 1) == 1;
+            const long long r = second ? i - 1 : i;
+            v = __dadd_rn(1.0, draw_u01(seed, (uint64_t)(r * n + r)));
+        } else if (j > i) {
+            if (!(pair_first_i && j == i + 1)) {
+                const uint64_t k = (uint64_t)(i * n + j);
+                v = __dsub_rn(__dmul_rn(2.0, draw_u01(seed, k)), 1.0);
+            }
+        }
+        T[i + j * ldt] = v;
+    }
+}
+
 __global__ void gen_schur_kernel(double* S, long long lds, long long n, uint64_t seed, long long c0) {
     const long long j = c0 + blockIdx.y;  // columns [c0, c0 + gridDim.y) into S[:, 0..)
     const long long npairs = n / 4, nreal = n - 2 * npairs;
@@ -115,6 +151,12 @@ dim3 grid_for(long long n) {
 cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64_t fill_seed, cudaStream_t stream) {
     if (n <= 0) return cudaSuccess;
     gen_schur_kernel<<<grid_for(n), 256, 0, stream>>>(S, lds, n, fill_seed, 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_pair_t(double* T, long long ldt, long long n, uint64_t seed, cudaStream_t stream) {
+    if (n <= 0) return cudaSuccess;
+    gen_pair_t_kernel<<<grid_for(n), 256, 0, stream>>>(T, ldt, n, seed);
     return cudaGetLastError();
 }
 

@@ -27,6 +27,13 @@ cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64
                                    cudaStream_t stream);
 cudaError_t launch_set_identity(double* Q, long long ldq, long long n, cudaStream_t stream);
 cudaError_t launch_gen_hessenberg(double* H, long long ldh, long long n, uint64_t seed, cudaStream_t stream);
+cudaError_t launch_gen_pair_t(double* T, long long ldt, long long n, uint64_t seed, cudaStream_t stream);
+// generalized (S, T) window kernel (gwindow_reorder.cu), d <= 64
+size_t gwindow_smem_bytes(int d);
+cudaError_t launch_gwindow_reorder(const WinDesc* wins, int nwin, int dmax, double* S, long long lds, double* T,
+                                   long long ldt, double* qw_pool, const uint8_t* sizes_pool,
+                                   const uint8_t* sel_pool, uint8_t* order_pool, uint8_t* stuck_pool,
+                                   int32_t* status, cudaStream_t stream);
 cudaError_t launch_gen_schur_cols(double* S, long long lds, long long n, uint64_t fill_seed, long long c0,
                                   long long c1, cudaStream_t stream);
 cudaError_t launch_identity_rows(double* Q, long long ldq, long long n, long long r0, long long r1,

@@ -382,3 +382,85 @@ def plan_reorder(n: int, sel: Selection, window_size: int = 0):
         if k <= cap:
             return win[:5 * k].reshape(k, 5), nl.value, ng.value, fl.value
         cap = k
+
+
+# ---------------------------------------------------------------------------
+# generalized Schur-pair reordering (S, T) with Q and Z
+
+@dataclass
+class GReorderResult:
+    s: object
+    t: object
+    q: object
+    z: object
+    permutation: List[int]
+    rejected_blocks: List[int]
+    clean: bool
+    info: dict
+
+
+def greorder_schur(s, t, q, z, sel: Selection, opts: Optional[ReorderOptions] = None,
+                   stream=None) -> GReorderResult:
+    """Moves the selected generalized eigenvalues of the pencil (S, T) to the
+    leading blocks: (S, T) <- Qs^T (S, T) Zs, q <- q Qs, z <- z Zs (LAPACK
+    DTGSEN semantics on the reference's reorder planner).  S upper
+    quasi-triangular with the block structure of `sel`, T upper triangular.
+    CUDA tensors are updated in place (column-major), numpy arrays through
+    the host entry point (copies returned)."""
+    opts = opts or ReorderOptions()
+    n = s.shape[0]
+    row = 0
+    for b in sel.blocks:
+        if b.start != row:
+            raise ValueError("reorder: selection does not match (S, T)")
+        row += b.size
+    if row != n or len(sel.flags) != len(sel.blocks):
+        raise ValueError("reorder: selection does not match (S, T)")
+    nb = len(sel.blocks)
+    sizes, flags = sel.sizes_array(), sel.flags_array()
+    perm = np.zeros(max(nb, 1), dtype=np.int64)
+    rej = np.zeros(max(nb, 1), dtype=np.int64)
+    info = N.ReorderInfo()
+    o = N.ReorderOpts()
+    N.lib().teig_reorder_opts_default(C.byref(o))
+    o.window_size = int(opts.window_size)
+    o.strict = int(bool(opts.strict))
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)
+    if torch is not None and isinstance(s, torch.Tensor):
+        mats = []
+        for m in (s, t, q, z):
+            if m is None:
+                mats.append((None, n, False))
+            else:
+                _need_torch_cuda(m)
+                mats.append(_as_colmajor(m))
+        ptr = lambda k: mats[k][0].data_ptr() if mats[k][0] is not None else None
+        rc = N.lib().teig_greorder_schur_device(n, ptr(0), mats[0][1], ptr(1), mats[1][1], ptr(2), mats[2][1], ptr(3),
+                                                mats[3][1], nb, vp(sizes), vp(flags), C.byref(o), vp(perm), vp(rej),
+                                                C.byref(info), _stream_ptr(stream, s))
+        if rc == -1002:
+            raise RuntimeError("reorder: swap rejected in strict mode")
+        N.check(rc)
+        for m, (w, _, cb) in zip((s, t, q, z), mats):
+            if cb:
+                m.copy_(w)
+        outs = (s, t, q, z)
+    else:
+        hs = [np.asfortranarray(np.array(m, dtype=np.float64, copy=True)) if m is not None else None for m in (s, t, q, z)]
+        p = lambda a: vp(a) if a is not None else None
+        rc = N.lib().teig_greorder_schur_host(n, p(hs[0]), n, p(hs[1]), n, p(hs[2]), n, p(hs[3]), n, nb, vp(sizes),
+                                              vp(flags), C.byref(o), vp(perm), vp(rej), C.byref(info), None)
+        if rc == -1002:
+            raise RuntimeError("reorder: swap rejected in strict mode")
+        N.check(rc)
+        outs = tuple(hs)
+    inf = {f: getattr(info, f) for f, _ in N.ReorderInfo._fields_ if f != "pad"}
+    return GReorderResult(*outs, [int(x) for x in perm[:nb]], [int(x) for x in rej[:info.n_rejected]],
+                          bool(info.clean), inf)
+
+
+def gen_pair_t(n: int, seed: int, device="cuda", stream=None):
+    """The C5 input T in HBM, column-major."""
+    tt = colmajor_empty(n, device)
+    N.check(N.lib().teig_gen_pair_t_device(n, tt.data_ptr(), n, int(seed) & (2**64 - 1), _stream_ptr(stream, tt)))
+    return tt
