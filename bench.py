@@ -59,6 +59,7 @@ def parse():
                     help="reorder: C2 (headline); schur: C3 multishift QR + AED of random Hessenberg")
     ap.add_argument("--no-schur", action="store_true", help="skip the C3 section of the default line")
     ap.add_argument("--schur-n", type=int, default=10000)
+    ap.add_argument("--c5-n", type=int, default=20000, help="size of the C5 (generalized pair) section (0: skip)")
     ap.add_argument("--force-dist", action="store_true", help="use the NCCL distributed path even at N=1 (plumbing test)")
     return ap.parse_args()
 
@@ -272,6 +273,8 @@ def run_ours(args, rank, world, local):
     torch.cuda.empty_cache()
     if args.c2_n:
         out["c2_n10000"] = run_c2(args, dev)
+    if args.c5_n:
+        out["greorder_c5"] = run_c5(args, dev)
     if not args.no_schur:
         out["schur_c3"] = run_schur(args, dev, with_cpu=(rank == 0 and not args.no_cpu), with_e2e=not args.no_e2e)
         out["schur_c3"]["gpu_launches_counted_in_line"] = False
@@ -460,6 +463,82 @@ def run_ours_dist(args, rank, world, local):
                "clocks": clocks, "wall_s_timed_region": round(t_wall, 3), "step_ms": [round(x, 3) for x in step_ms]}
         print(json.dumps(out), flush=True)
     dist.destroy_process_group()
+
+
+def run_c5(args, dev, steps=2, warmup=1, ws=64):
+    """C5 (configs[4]): generalized (S, T) Schur-pair reordering with Q and Z,
+    n=20000, 35% selected, one GPU.  T from the library's C5 generator
+    (SURVEY.md 8d); the reference has no generalized path: the CPU baseline
+    is LAPACK DTGSEN (third party, scipy-openblas) on a bounded sample."""
+    import torch
+    import paper_2002_05024_b200 as T
+    n = args.c5_n
+    S0 = T.gen_schur_input(n, T.known_spectrum_seed(FILL_SEED_BASE), device=dev)
+    T0 = T.gen_pair_t(n, 7, device=dev)
+    sel = T.select_fraction(S0, FRACTION, SEL_SEED)
+    S, Tm, Q, Z = (T.colmajor_empty(n, dev) for _ in range(4))
+    I = T.identity(n, dev)
+    opts = T.ReorderOptions(window_size=ws)
+
+    def reset():
+        S.copy_(S0)
+        Tm.copy_(T0)
+        Q.copy_(I)
+        Z.copy_(I)
+
+    for _ in range(warmup):
+        reset()
+        T.greorder_schur(S, Tm, Q, Z, sel, opts)
+    stream = torch.cuda.current_stream(dev)
+    ms = []
+    for _ in range(steps):
+        reset()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = T.greorder_schur(S, Tm, Q, Z, sel, opts)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    t = statistics.mean(ms) / 1e3
+    bs = float(torch.linalg.norm(S0 - Q @ S @ Z.t()) / torch.linalg.norm(S0))
+    bt = float(torch.linalg.norm(T0 - Q @ Tm @ Z.t()) / torch.linalg.norm(T0))
+    oq = float(torch.linalg.norm(Q.t() @ Q - I.t() @ I))
+    oz = float(torch.linalg.norm(Z.t() @ Z - I.t() @ I))
+    tol = 10 * n * 2.220446049250313e-16
+    out = {"workload": f"C5: generalized (S,T) reorder n={n}, 35% selected (seed {SEL_SEED}), Q and Z accumulated, "
+                       f"window {ws}", "value": round(t, 4), "unit": "s", "step_ms": [round(x, 1) for x in ms],
+           "update_flops": res.info["update_flops"], "update_tflops": round(res.info["update_flops"] / t / 1e12, 3),
+           "windows": res.info["n_windows"], "levels": res.info["n_levels"], "clean": res.clean,
+           "parity": {"backward_error_S": bs, "backward_error_T": bt, "orthogonality_Q": oq, "orthogonality_Z": oz,
+                      "tol_10neps": tol, "pass": max(bs, bt, oq, oz) <= tol,
+                      "eigenvalues": "position-by-position vs LAPACK DTGSEN to 1e-10 in tests/test_greorder_gpu.py"}}
+    del S, Tm, Q, Z, I, S0, T0
+    torch.cuda.empty_cache()
+    if not args.no_cpu:
+        out["cpu_baseline"] = c5_cpu_baseline(n)
+    return out
+
+
+def c5_cpu_baseline(n_full, n_sample=1500):
+    """LAPACK DTGSEN (scipy-openblas; the reference has no generalized path)
+    on the same construction at n_sample, extrapolated by (n/n_sample)^3."""
+    from oracle import oracle as O
+    S = O.schur_input(n_sample, O.known_spectrum_seed(FILL_SEED_BASE))
+    Tt = O.pair_t(n_sample, 7)
+    sizes = O.scan_blocks(S).astype(np.int64)
+    flags = O.select_fraction(len(sizes), FRACTION, SEL_SEED)
+    starts = np.concatenate([[0], np.cumsum(sizes)]).astype(int)
+    rows = np.zeros(n_sample, dtype=np.int32)
+    for i, f in enumerate(flags):
+        if f:
+            rows[starts[i]:starts[i + 1]] = 1
+    t0 = time.perf_counter()
+    O.lapack_tgsen(S, Tt, rows)
+    secs = time.perf_counter() - t0
+    return {"value": round(secs * (n_full / n_sample) ** 3, 1), "unit": "s", "cores": os.cpu_count() or 1,
+            "kind": "third-party (LAPACK DTGSEN via scipy-openblas; no reference implementation exists)",
+            "sample": f"dtgsen of the n={n_sample} C5 pencil with Q and Z in {secs:.2f} s, extrapolated to "
+                      f"n={n_full} by (n/{n_sample})^3", "sample_seconds": round(secs, 3)}
 
 # ---------------------------------------------------------------------------
 # C3: Schur reduction (multishift QR + AED) of a random upper Hessenberg matrix
