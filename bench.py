@@ -745,10 +745,10 @@ def run_reference(args, rank, world, local):
     v = statistics.mean(t)
     out = {"metric": METRIC, "impl": "reference", "value": round(v, 3), "unit": "s", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * 1e3, 1),
-           "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (SURVEY.md 8d Schur form, reference Philox generator)",
-           "config": {"workload": f"C2: reorder_schur n={n}, 35% selected (select_fraction seed {SEL_SEED}), "
-                                  f"Q accumulated, window {args.ws or 128}", "n": n,
+           "config": {"workload": f"{workload_name(n)}: reorder_schur n={n}, 35% selected (select_fraction seed "
+                                  f"{SEL_SEED}), Q accumulated, window {args.ws or 128}", "n": n,
                       "window_size": args.ws or 128, "fraction": FRACTION},
            "cpu_baseline": res,
            "e2e": {"value": round(v, 3), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

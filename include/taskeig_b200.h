@@ -260,6 +260,16 @@ int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_c
                             const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
                             int64_t* perm, int64_t* rejected, teig_reorder_info* info, void* stream);
 
+/* Generalized pencil (C5) across ranks: S and T in column slabs (same
+ * layout as dS_slabs), Q and Z in row slabs; window_size <= 64.  Same result,
+ * bit for bit, as teig_greorder_schur_device. */
+int teig_dist_greorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_comm,
+                             double* const* dS_slabs, double* const* dT_slabs, int64_t lds,
+                             double* const* dQ_slabs, double* const* dZ_slabs, const int64_t* col_bounds,
+                             const int64_t* row_bounds, int64_t nb, const uint8_t* sizes,
+                             const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm,
+                             int64_t* rejected, teig_reorder_info* info, void* stream);
+
 /* NCCL plumbing (libnccl.so.2 resolved at run time). */
 int teig_nccl_available(void);
 int teig_nccl_unique_id(uint8_t* id128);

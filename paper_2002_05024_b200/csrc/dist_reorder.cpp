@@ -126,7 +126,10 @@ struct RankBufs {
     int rank = 0;
     double* S = nullptr;  // virtual base: absolute (i, j) at S[i + j*lds]
     double* Q = nullptr;  // virtual base: absolute (i, j) at Q[i + j*ldq]
+    double* T = nullptr;  // generalized pencil (C5): T column slab, like S
+    double* Z = nullptr;  // generalized pencil: Z row slab, like Q
     int64_t ldq = 0;
+    double* mat(int m) const { return m ? T : S; }
     double* qw = nullptr;       // Q_w slots of the pass (all windows)
     WinDesc* descs = nullptr;   // per-level descriptor arrays of this rank
     uint8_t *sizes = nullptr, *sel = nullptr, *order = nullptr, *stuck = nullptr;
@@ -139,6 +142,7 @@ struct RankBufs {
 struct Xfer {
     int src, dst;
     int64_t r0, r1, c0, c1;
+    int mat = 0;  // 0: S, 1: T
 };
 
 class Comm {
@@ -169,7 +173,7 @@ class LoopbackComm : public Comm {
         for (const auto& x : xs) {
             const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
             if (rows <= 0 || cols <= 0) continue;
-            TEIG_CUDA(cudaMemcpy2DAsync(R[x.dst].S + x.r0 + x.c0 * lds, lds * 8, R[x.src].S + x.r0 + x.c0 * lds,
+            TEIG_CUDA(cudaMemcpy2DAsync(R[x.dst].mat(x.mat) + x.r0 + x.c0 * lds, lds * 8, R[x.src].mat(x.mat) + x.r0 + x.c0 * lds,
                                         lds * 8, rows * 8, cols, cudaMemcpyDeviceToDevice, s));
         }
     }
@@ -212,7 +216,7 @@ class NcclComm : public Comm {
             const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
             if (rows <= 0 || cols <= 0) continue;
             if (x.src == rank_)
-                TEIG_CUDA(cudaMemcpy2DAsync(me.stage + off, rows * 8, me.S + x.r0 + x.c0 * lds, lds * 8, rows * 8, cols,
+                TEIG_CUDA(cudaMemcpy2DAsync(me.stage + off, rows * 8, me.mat(x.mat) + x.r0 + x.c0 * lds, lds * 8, rows * 8, cols,
                                             cudaMemcpyDeviceToDevice, s));
             off += (size_t)rows * cols;
         }
@@ -229,7 +233,7 @@ class NcclComm : public Comm {
             const auto& x = xs[i];
             const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
             if (rows <= 0 || cols <= 0 || x.dst != rank_) continue;
-            TEIG_CUDA(cudaMemcpy2DAsync(me.S + x.r0 + x.c0 * lds, lds * 8, me.stage + offs[i], rows * 8, rows * 8, cols,
+            TEIG_CUDA(cudaMemcpy2DAsync(me.mat(x.mat) + x.r0 + x.c0 * lds, lds * 8, me.stage + offs[i], rows * 8, rows * 8, cols,
                                         cudaMemcpyDeviceToDevice, s));
         }
     }
@@ -248,6 +252,7 @@ struct LevelPlan {
         int64_t l_off = 0, l_cnt = 0, l_tiles = 0;     // left updates
         int64_t r_off = 0, r_cnt = 0, r_tiles = 0;     // right updates (owned)
         int64_t q_off = 0, q_cnt = 0, q_tiles = 0;     // Q updates
+        int64_t z_off = 0, z_cnt = 0;                  // Z updates (generalized; tiles as Q)
     };
     std::vector<Part> part;          // [rank]
     int64_t qw_off = 0, qw_len = 0;  // the level's Q_w slots
@@ -265,7 +270,7 @@ struct PassOut {
 };
 
 PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankBufs>& R, Comm& comm, int64_t lds,
-                      const std::vector<int64_t>& C, const std::vector<int64_t>& Rw, bool with_q,
+                      const std::vector<int64_t>& C, const std::vector<int64_t>& Rw, bool with_q, bool gen,
                       std::vector<BlockState>& blocks, std::vector<int64_t>& rejected, std::vector<int64_t>& plan_log,
                       bool strict, cudaStream_t s) {
     PassOut po;
@@ -282,7 +287,7 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
     for (int64_t k = 0; k < nw; ++k) {
         const auto& w = plan.windows[idx[k]];
         qw_off[idx[k]] = qw_total;
-        qw_total += (w.wbot - w.wtop) * (w.wbot - w.wtop);
+        qw_total += (gen ? 2 : 1) * (w.wbot - w.wtop) * (w.wbot - w.wtop);
     }
     // per-rank descriptor arrays, level by level
     std::vector<std::vector<WinDesc>> D(world);
@@ -298,7 +303,7 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
         lp.qw_len = 0;
         for (int64_t t = k0; t < k; ++t) {
             const auto& w = plan.windows[idx[t]];
-            lp.qw_len += (w.wbot - w.wtop) * (w.wbot - w.wtop);
+            lp.qw_len += (gen ? 2 : 1) * (w.wbot - w.wtop) * (w.wbot - w.wtop);
             lp.dmax = std::max<int>(lp.dmax, (int)(w.wbot - w.wtop));
         }
         lp.dmax = lp.dmax <= 64 ? 64 : 128;
@@ -339,6 +344,7 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
                 const auto& w = plan.windows[idx[t]];
                 if (owner_of(C, w.wtop) != r || w.wtop == 0) continue;
                 WinDesc d = base(t);
+                if (gen) d.qw_off += (int64_t)d.d * d.d;  // the pencil's right side uses Z_w
                 d.rr0 = 0;
                 d.rr1 = (int32_t)w.wtop;
                 d.tr_pref = (int32_t)P.r_tiles;
@@ -360,6 +366,15 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
                     Dp[r].push_back(-1);
                     ++P.q_cnt;
                 }
+            P.z_off = (int64_t)D[r].size();
+            if (gen && with_q && Rw[r + 1] > Rw[r])
+                for (int64_t t = k0; t < k; ++t) {
+                    WinDesc d = D[r][P.q_off + (t - k0)];
+                    d.qw_off += (int64_t)d.d * d.d;
+                    D[r].push_back(d);
+                    Dp[r].push_back(-1);
+                    ++P.z_cnt;
+                }
         }
         // straddling windows: halo transfers
         for (int64_t t = k0; t < k; ++t) {
@@ -369,9 +384,11 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             const int nbr = o + 1;
             if (nbr >= world || w.wbot > C[nbr + 1] || w.wbot - C[nbr] > kHalo)
                 throw std::runtime_error("distributed reorder: a window spans more than two slabs");
-            lp.halo_win.push_back(Xfer{nbr, o, w.wtop, w.wbot, C[nbr], w.wbot});
-            if (w.wtop > 0) lp.halo_panel.push_back(Xfer{nbr, o, 0, w.wtop, C[nbr], w.wbot});
-            lp.halo_back.push_back(Xfer{o, nbr, 0, w.wbot, C[nbr], w.wbot});
+            for (int m = 0; m < (gen ? 2 : 1); ++m) {
+                lp.halo_win.push_back(Xfer{nbr, o, w.wtop, w.wbot, C[nbr], w.wbot, m});
+                if (w.wtop > 0) lp.halo_panel.push_back(Xfer{nbr, o, 0, w.wtop, C[nbr], w.wbot, m});
+                lp.halo_back.push_back(Xfer{o, nbr, 0, w.wbot, C[nbr], w.wbot, m});
+            }
         }
     }
     // device buffers of the pass, per local rank
@@ -407,9 +424,14 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             if (!comm.local(r)) continue;
             const auto& P = lp.part[r];
             if (P.w_cnt) {
-                TEIG_CUDA(launch_window_reorder(R[r].descs + P.w_off, (int)P.w_cnt, lp.dmax, R[r].S, lds, R[r].qw,
-                                                R[r].sizes, R[r].sel, R[r].order, R[r].stuck, R[r].status + P.w_off,
-                                                s));
+                if (gen)
+                    TEIG_CUDA(launch_gwindow_reorder(R[r].descs + P.w_off, (int)P.w_cnt, lp.dmax, R[r].S, lds, R[r].T,
+                                                     lds, R[r].qw, R[r].sizes, R[r].sel, R[r].order, R[r].stuck,
+                                                     R[r].status + P.w_off, s));
+                else
+                    TEIG_CUDA(launch_window_reorder(R[r].descs + P.w_off, (int)P.w_cnt, lp.dmax, R[r].S, lds, R[r].qw,
+                                                    R[r].sizes, R[r].sel, R[r].order, R[r].stuck,
+                                                    R[r].status + P.w_off, s));
                 ++launches;
             }
         }
@@ -425,6 +447,9 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             if (P.l_tiles) {
                 TEIG_CUDA(launch_update_left(R[r].descs + P.l_off, (int)P.l_cnt, (int)P.l_tiles, lp.dmax, R[r].qw,
                                              R[r].S, lds, (int)n, s));
+                if (gen)
+                    TEIG_CUDA(launch_update_left(R[r].descs + P.l_off, (int)P.l_cnt, (int)P.l_tiles, lp.dmax, R[r].qw,
+                                                 R[r].T, lds, (int)n, s));
                 ++launches;
             }
         }
@@ -435,6 +460,9 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             if (P.r_tiles) {
                 TEIG_CUDA(launch_update_right(R[r].descs + P.r_off, (int)P.r_cnt, (int)P.r_tiles, lp.dmax, R[r].qw,
                                               R[r].S, lds, (int)n, false, s));
+                if (gen)
+                    TEIG_CUDA(launch_update_right(R[r].descs + P.r_off, (int)P.r_cnt, (int)P.r_tiles, lp.dmax, R[r].qw,
+                                                  R[r].T, lds, (int)n, false, s));
                 ++launches;
             }
         }
@@ -445,6 +473,9 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             if (P.q_tiles) {
                 TEIG_CUDA(launch_update_right(R[r].descs + P.q_off, (int)P.q_cnt, (int)P.q_tiles, lp.dmax, R[r].qw,
                                               R[r].Q, R[r].ldq, (int)n, true, s));
+                if (gen && P.z_cnt && R[r].Z)
+                    TEIG_CUDA(launch_update_right(R[r].descs + P.z_off, (int)P.z_cnt, (int)P.q_tiles, lp.dmax, R[r].qw,
+                                                  R[r].Z, R[r].ldq, (int)n, true, s));
                 ++launches;
             }
         }
@@ -636,11 +667,11 @@ int teig_nccl_comm_destroy(void* comm) {
     return 0;
 }
 
-int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_comm, double* const* dS_slabs,
-                            int64_t lds, double* const* dQ_slabs, const int64_t* col_bounds,
-                            const int64_t* row_bounds, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
-                            const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected_out,
-                            teig_reorder_info* info, void* stream_v) {
+static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, double* const* dS_slabs,
+                     double* const* dT_slabs, int64_t lds, double* const* dQ_slabs, double* const* dZ_slabs,
+                     const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb, const uint8_t* sizes,
+                     const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected_out,
+                     teig_reorder_info* info, void* stream_v, bool gen) {
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (world < 1) return set_error(-2, "world must be >= 1");
     const bool loop = nccl_comm == nullptr;
@@ -656,8 +687,9 @@ int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_c
     teig_reorder_opts o;
     teig_reorder_opts_default(&o);
     if (opts) o = *opts;
-    const int64_t ws = std::max<int64_t>(o.window_size ? o.window_size : default_tile_size(n), 8);
-    if (ws > 128) return set_error(TEIG_ERR_UNSUPPORTED, "window_size > 128");
+    const int64_t ws = std::max<int64_t>(o.window_size ? o.window_size : (gen ? 64 : default_tile_size(n)), 8);
+    if (ws > (gen ? 64 : 128)) return set_error(TEIG_ERR_UNSUPPORTED, gen ? "generalized window_size > 64" : "window_size > 128");
+    if (gen && !dT_slabs) return set_error(-5, "null T slabs");
     std::vector<BlockState> blocks(nb);
     int64_t rows = 0;
     for (int64_t i = 0; i < nb; ++i) {
@@ -679,6 +711,10 @@ int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_c
             R[r].S = dS_slabs[li] - C[r] * lds;
             R[r].ldq = std::max<int64_t>(Rw[r + 1] - Rw[r], 1);
             R[r].Q = (dQ_slabs && dQ_slabs[li]) ? dQ_slabs[li] - Rw[r] : nullptr;
+            if (gen) {
+                R[r].T = dT_slabs[li] - C[r] * lds;
+                R[r].Z = (dZ_slabs && dZ_slabs[li]) ? dZ_slabs[li] - Rw[r] : nullptr;
+            }
         }
         const bool with_q = dQ_slabs != nullptr;
         LoopbackComm lb(world);
@@ -689,9 +725,9 @@ int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_c
             ReorderPlan plan = plan_reorder(blocks, ws);
             if (plan.windows.empty()) break;
             if (pass == 0) inf.n_groups = plan.n_groups;
-            inf.update_flops += plan_update_flops(plan, n, with_q);
-            inf.update_bytes += plan_update_bytes(plan, n, with_q);
-            PassOut po = run_dist_pass(plan, n, world, R, comm, lds, C, Rw, with_q, blocks, rejected, plan_log,
+            inf.update_flops += (gen ? 2.0 : 1.0) * plan_update_flops(plan, n, with_q);
+            inf.update_bytes += (gen ? 2.0 : 1.0) * plan_update_bytes(plan, n, with_q);
+            PassOut po = run_dist_pass(plan, n, world, R, comm, lds, C, Rw, with_q, gen, blocks, rejected, plan_log,
                                        o.strict != 0, s);
             inf.n_windows += po.windows;
             inf.n_levels += po.levels;
@@ -720,6 +756,24 @@ int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_c
         for (size_t i = 0; i < rejected.size(); ++i) rejected_out[i] = rejected[i];
     if (info) *info = inf;
     return 0;
+}
+
+int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_comm, double* const* dS_slabs,
+                            int64_t lds, double* const* dQ_slabs, const int64_t* col_bounds,
+                            const int64_t* row_bounds, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
+                            const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected, teig_reorder_info* info,
+                            void* stream) {
+    return dist_impl(n, world, rank, nccl_comm, dS_slabs, nullptr, lds, dQ_slabs, nullptr, col_bounds, row_bounds, nb,
+                     sizes, flags, opts, perm, rejected, info, stream, false);
+}
+
+int teig_dist_greorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_comm, double* const* dS_slabs,
+                             double* const* dT_slabs, int64_t lds, double* const* dQ_slabs, double* const* dZ_slabs,
+                             const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb, const uint8_t* sizes,
+                             const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
+                             teig_reorder_info* info, void* stream) {
+    return dist_impl(n, world, rank, nccl_comm, dS_slabs, dT_slabs, lds, dQ_slabs, dZ_slabs, col_bounds, row_bounds,
+                     nb, sizes, flags, opts, perm, rejected, info, stream, true);
 }
 
 int teig_gen_schur_input_cols_device(int64_t n, double* dS, int64_t lds, int64_t c0, int64_t c1, uint64_t fill_seed,

@@ -176,3 +176,72 @@ def reorder_schur_loopback(s, q, sel: Selection, world: int, opts: Optional[Reor
         if q is not None and rb[r + 1] > rb[r]:
             q[rb[r]:rb[r + 1], :].copy_(qs[r])
     return ReorderResult(s, q, perm, rej, [], clean, inf)
+
+
+# ---------------------------------------------------------------------------
+# generalized pencil (S, T) with Q and Z (config C5) across ranks
+
+def _gcall(n, world, rank, comm, s_slabs, t_slabs, q_slabs, z_slabs, cb, rb, sel, opts, stream_t):
+    nb = len(sel.blocks)
+    sizes, flags = sel.sizes_array(), sel.flags_array()
+    perm = np.zeros(max(nb, 1), dtype=np.int64)
+    rej = np.zeros(max(nb, 1), dtype=np.int64)
+    info = N.ReorderInfo()
+    arr = lambda ts: (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts]) if ts is not None else None
+    cb = np.ascontiguousarray(cb, dtype=np.int64)
+    rb = np.ascontiguousarray(rb, dtype=np.int64)
+    o = _opts(opts)
+    rc = N.lib().teig_dist_greorder_schur(n, world, rank, comm, arr(s_slabs), arr(t_slabs), n, arr(q_slabs),
+                                          arr(z_slabs), _vp(cb), _vp(rb), nb, _vp(sizes), _vp(flags), C.byref(o),
+                                          _vp(perm), _vp(rej), C.byref(info), _stream_ptr(None, stream_t))
+    if rc == -1002:
+        raise RuntimeError("reorder: swap rejected in strict mode")
+    N.check(rc)
+    inf = {f: getattr(info, f) for f, _ in N.ReorderInfo._fields_ if f != "pad"}
+    return [int(x) for x in perm[:nb]], [int(x) for x in rej[:info.n_rejected]], bool(info.clean), inf
+
+
+def greorder_schur_dist(s_slab, t_slab, q_slab, z_slab, sel: Selection, col_bounds, row_bounds, rank: int,
+                        world: int, comm, opts: Optional[ReorderOptions] = None):
+    """One rank of the NCCL-distributed generalized reorder (slabs as for
+    reorder_schur_dist; T like S, Z like Q)."""
+    n = s_slab.shape[0]
+    one = lambda t: [t] if t is not None else None
+    return _gcall(n, world, rank, comm, [s_slab], [t_slab], one(q_slab), one(z_slab), col_bounds, row_bounds, sel,
+                  opts, s_slab)
+
+
+def greorder_schur_loopback(s, t, q, z, sel: Selection, world: int, opts: Optional[ReorderOptions] = None,
+                            col_bounds=None, row_bounds=None):
+    """All ranks of the generalized distributed reorder in this process on one
+    device; scatters, runs, gathers back in place.  Returns (perm, rejected,
+    clean, info)."""
+    n = s.shape[0]
+    opts = opts or ReorderOptions(window_size=64)
+    if col_bounds is None:
+        col_bounds, row_bounds = balance(n, sel, world, opts.window_size or 64)
+    cb, rb = list(map(int, col_bounds)), list(map(int, row_bounds))
+    ss, ts, qs, zs = [], [], [], []
+    for r in range(world):
+        for src, dst in ((s, ss), (t, ts)):
+            x = s_slab_empty(n, cb[r], cb[r + 1], s.device)
+            x[:, : cb[r + 1] - cb[r]].copy_(src[:, cb[r]:cb[r + 1]])
+            dst.append(x)
+        for src, dst in ((q, qs), (z, zs)):
+            if src is None:
+                continue
+            u = q_slab_empty(n, rb[r], rb[r + 1], s.device)
+            if rb[r + 1] > rb[r]:
+                u.copy_(src[rb[r]:rb[r + 1], :])
+            dst.append(u)
+    res = _gcall(n, world, 0, None, ss, ts, qs if q is not None else None, zs if z is not None else None, cb, rb,
+                 sel, opts, s)
+    for r in range(world):
+        s[:, cb[r]:cb[r + 1]].copy_(ss[r][:, : cb[r + 1] - cb[r]])
+        t[:, cb[r]:cb[r + 1]].copy_(ts[r][:, : cb[r + 1] - cb[r]])
+        if rb[r + 1] > rb[r]:
+            if q is not None:
+                q[rb[r]:rb[r + 1], :].copy_(qs[r])
+            if z is not None:
+                z[rb[r]:rb[r + 1], :].copy_(zs[r])
+    return res

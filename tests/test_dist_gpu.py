@@ -53,3 +53,21 @@ def test_slab_generators_match_full(T, O, cuda):
     assert torch.equal(sl[:, :400], full[:, 300:700])
     q = D.identity_rows_slab(n, 100, 350)
     assert torch.equal(q, torch.eye(n, dtype=torch.float64, device=cuda)[100:350])
+
+
+@pytest.mark.parametrize("n,world", [(800, 2), (1500, 3), (2000, 4)])
+def test_generalized_loopback_equals_single_gpu(T, O, cuda, n, world):
+    """The C5 pencil across ranks (S, T column slabs; Q, Z row slabs) equals
+    the single-GPU generalized reorder bit for bit."""
+    import torch
+    from paper_2002_05024_b200 import dist as D
+    s0 = T.gen_schur_input(n, T.known_spectrum_seed(1))
+    t0 = T.gen_pair_t(n, 7)
+    sel = T.select_fraction(s0, 0.35, 99)
+    opts = T.ReorderOptions(window_size=64)
+    s1, t1, q1, z1 = s0.clone(), t0.clone(), T.identity(n), T.identity(n)
+    r1 = T.greorder_schur(s1, t1, q1, z1, sel, opts)
+    s2, t2, q2, z2 = s0.clone(), t0.clone(), T.identity(n), T.identity(n)
+    perm, rej, clean, info = D.greorder_schur_loopback(s2, t2, q2, z2, sel, world, opts)
+    assert r1.clean and clean and perm == r1.permutation
+    assert torch.equal(s1, s2) and torch.equal(t1, t2) and torch.equal(q1, q2) and torch.equal(z1, z2)
