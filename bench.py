@@ -450,8 +450,45 @@ def run_ours_dist(args, rank, world, local):
             parity = {"bitwise_equal_to_single_gpu": bool(torch.equal(Sd, S1) and torch.equal(Qd, Q1))}
             del Sd, Qd, S1, Q1
         dist.barrier()
+    # e2e: the same distributed call on slabs held in pinned HOST memory, the
+    # H2D of the inputs and D2H of the results inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hs = torch.empty(S0.shape[::-1], dtype=torch.float64).pin_memory().t()  # column-major host slab
+        hq = torch.empty(Q0.shape[::-1], dtype=torch.float64).pin_memory().t()
+        hs.copy_(S0)
+        hq.copy_(Q0)
+        e2e_ms = []
+        for k in range(2):
+            hs.copy_(S0)
+            hq.copy_(Q0)
+            dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            S.copy_(hs, non_blocking=True)
+            Q.copy_(hq, non_blocking=True)
+            D.reorder_schur_dist(S, Q, sel, cb, rb, rank, world, comm, opts)
+            hs.copy_(S, non_blocking=True)
+            hq.copy_(Q, non_blocking=True)
+            torch.cuda.synchronize()
+            dt = torch.tensor([(time.perf_counter() - t0) * 1e3], device=dev, dtype=torch.float64)
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            e2e_ms.append(float(dt.item()))
+        hb = (S0.numel() + Q0.numel()) * 8
+        tot = torch.tensor([hb], device=dev, dtype=torch.float64)
+        dist.all_reduce(tot)
+        e2e = {"value": round(min(e2e_ms) / 1e3, 6), "unit": "s", "h2d_bytes_per_step": int(tot.item()),
+               "d2h_bytes_per_step": int(tot.item()),
+               "api": "teig_dist_reorder_schur (C ABI) on slabs copied from/to pinned host memory on every rank; "
+                      "max over ranks"}
+        del hs, hq
     D.nccl_comm_destroy(comm)
     if rank == 0:
+        agg = info["update_flops"] / (ms_step * 1e-3) / 1e12
+        roof = {"bound": "tensor", "kernel": "all DMMA update kernels of the step, all ranks (aggregate)",
+                "achieved": round(agg / world, 3), "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": round(agg / world / FP64_DMMA_PEAK_TFLOPS, 4), "traffic": None,
+                "note": "per-GPU share of the update flops / step time (max over ranks)"}
         out = {"metric": METRIC, "value": round(ms_step / 1e3, 6), "unit": "s", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms_step, 3), "higher_is_better": False,
                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -465,7 +502,7 @@ def run_ours_dist(args, rank, world, local):
                "update_tflops": round(info["update_flops"] / (ms_step * 1e-3) / 1e12, 3),
                "update_flops": info["update_flops"], "windows": info["n_windows"], "levels": info["n_levels"],
                "clean": info["clean"] == 1, "parity": parity, "gpu_launches": info["n_launches"],
-               "clocks": clocks, "wall_s_timed_region": round(t_wall, 3), "step_ms": [round(x, 3) for x in step_ms]}
+               "roofline": roof, "e2e": e2e, "clocks": clocks, "wall_s_timed_region": round(t_wall, 3), "step_ms": [round(x, 3) for x in step_ms]}
         print(json.dumps(out), flush=True)
     dist.destroy_process_group()
 

@@ -272,7 +272,7 @@ struct PassOut {
 PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankBufs>& R, Comm& comm, int64_t lds,
                       const std::vector<int64_t>& C, const std::vector<int64_t>& Rw, bool with_q, bool gen,
                       std::vector<BlockState>& blocks, std::vector<int64_t>& rejected, std::vector<int64_t>& plan_log,
-                      bool strict, cudaStream_t s) {
+                      bool strict, cudaStream_t s, cudaStream_t s2, cudaEvent_t ev) {
     PassOut po;
     const int64_t nw = (int64_t)plan.windows.size();
     schedule_levels(plan, n);
@@ -467,19 +467,33 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             }
         }
         if (!lp.halo_back.empty()) comm.transfer(R, lp.halo_back, lds, s);  // P7
+        // P8 on the second stream: the Q (and Z) updates only need the
+        // level's all-reduced Q_w; they overlap the next levels' window
+        // kernels and panel updates (the single-GPU driver's schedule)
+        const bool any_q = [&] {
+            for (int r = 0; r < world; ++r)
+                if (comm.local(r) && lp.part[r].q_tiles) return true;
+            return false;
+        }();
+        if (any_q) {
+            TEIG_CUDA(cudaEventRecord(ev, s));
+            TEIG_CUDA(cudaStreamWaitEvent(s2, ev, 0));
+        }
         for (int r = 0; r < world; ++r) {  // P8
             if (!comm.local(r)) continue;
             const auto& P = lp.part[r];
             if (P.q_tiles) {
                 TEIG_CUDA(launch_update_right(R[r].descs + P.q_off, (int)P.q_cnt, (int)P.q_tiles, lp.dmax, R[r].qw,
-                                              R[r].Q, R[r].ldq, (int)n, true, s));
+                                              R[r].Q, R[r].ldq, (int)n, true, s2));
                 if (gen && P.z_cnt && R[r].Z)
                     TEIG_CUDA(launch_update_right(R[r].descs + P.z_off, (int)P.z_cnt, (int)P.q_tiles, lp.dmax, R[r].qw,
-                                                  R[r].Z, R[r].ldq, (int)n, true, s));
+                                                  R[r].Z, R[r].ldq, (int)n, true, s2));
                 ++launches;
             }
         }
     }
+    TEIG_CUDA(cudaEventRecord(ev, s2));
+    TEIG_CUDA(cudaStreamWaitEvent(s, ev, 0));
     // share the window outcomes (each written by its owner only), fold
     comm.allreduce(ord_bufs, ne + 1, ncclUint8, s);
     comm.allreduce(stk_bufs, ne + 1, ncclUint8, s);
@@ -717,6 +731,18 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, do
             }
         }
         const bool with_q = dQ_slabs != nullptr;
+        struct Side {  // the second stream of the Q/Z updates
+            cudaStream_t s = nullptr;
+            cudaEvent_t e = nullptr;
+            ~Side() {
+                if (e) cudaEventDestroy(e);
+                if (s) cudaStreamDestroy(s);
+            }
+        } side;
+        TEIG_CUDA(cudaStreamCreateWithFlags(&side.s, cudaStreamNonBlocking));
+        TEIG_CUDA(cudaEventCreateWithFlags(&side.e, cudaEventDisableTiming));
+        cudaStream_t s2 = side.s;
+        cudaEvent_t ev = side.e;
         LoopbackComm lb(world);
         if (!loop && !nccl().ok) return set_error(TEIG_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
         NcclComm nc(static_cast<ncclComm_t>(nccl_comm), rank);
@@ -728,7 +754,7 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, do
             inf.update_flops += (gen ? 2.0 : 1.0) * plan_update_flops(plan, n, with_q);
             inf.update_bytes += (gen ? 2.0 : 1.0) * plan_update_bytes(plan, n, with_q);
             PassOut po = run_dist_pass(plan, n, world, R, comm, lds, C, Rw, with_q, gen, blocks, rejected, plan_log,
-                                       o.strict != 0, s);
+                                       o.strict != 0, s, s2, ev);
             inf.n_windows += po.windows;
             inf.n_levels += po.levels;
             inf.n_launches += po.launches;
