@@ -316,7 +316,7 @@ struct StreamPair {
 int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq, int64_t nb,
                          const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
                          int64_t* perm, int64_t* rejected_out, int64_t* plan_out, int64_t plan_cap,
-                         teig_reorder_info* info, cudaStream_t stream) {
+                         teig_reorder_info* info, cudaStream_t stream, cudaEvent_t q_ready = nullptr) {
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (!dS) return set_error(-2, "S is null");
     if (lds < n) return set_error(-3, "lds < n");
@@ -343,6 +343,8 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
     std::vector<int64_t> rejected, plan_log;
     try {
         StreamPair sp;
+        // Q may still be arriving (host entry point): only the Q updates wait
+        if (q_ready && dQ) TEIG_CUDA(cudaStreamWaitEvent(o.overlap_factor ? sp.s2 : stream, q_ready, 0));
         double plan_ms = 0.0;
         for (int pass = 0; pass < 64; ++pass) {
             const auto t0 = std::chrono::steady_clock::now();
@@ -436,22 +438,41 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
     if (lds < n) return set_error(-3, "lds < n");
     if (Q && ldq < n) return set_error(-5, "ldq < n");
     cudaStream_t stream = (cudaStream_t)stream_v;
+    cudaStream_t qs = nullptr;
+    cudaEvent_t q_ready = nullptr;
     try {
         const size_t pitch = (size_t)n * sizeof(double);
         DevBuf dS(pitch * n, stream), dQ(Q ? pitch * n : 0, stream);
+        TEIG_CUDA(cudaStreamSynchronize(stream));  // allocations visible to the side stream
         TEIG_CUDA(cudaMemcpy2DAsync(dS.p, pitch, S, lds * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
-        if (Q)
-            TEIG_CUDA(cudaMemcpy2DAsync(dQ.p, pitch, Q, ldq * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
+        if (Q) {  // Q travels on a side stream, after S, while the S-side work starts
+            TEIG_CUDA(cudaStreamCreateWithFlags(&qs, cudaStreamNonBlocking));
+            TEIG_CUDA(cudaEventCreateWithFlags(&q_ready, cudaEventDisableTiming));
+            TEIG_CUDA(cudaEventRecord(q_ready, stream));  // S is on the device
+            TEIG_CUDA(cudaStreamWaitEvent(qs, q_ready, 0));
+            TEIG_CUDA(cudaMemcpy2DAsync(dQ.p, pitch, Q, ldq * sizeof(double), pitch, n, cudaMemcpyHostToDevice, qs));
+            TEIG_CUDA(cudaEventRecord(q_ready, qs));
+        }
         const int rc = reorder_schur_device(n, dS.as<double>(), n, Q ? dQ.as<double>() : nullptr, n, nb, sizes, flags,
-                                            opts, perm, rejected, plan, plan_cap, info, stream);
-        if (rc != 0) return rc;
+                                            opts, perm, rejected, plan, plan_cap, info, stream, q_ready);
+        if (rc != 0) {
+            if (qs) cudaStreamSynchronize(qs);
+            if (q_ready) cudaEventDestroy(q_ready);
+            if (qs) cudaStreamDestroy(qs);
+            return rc;
+        }
         TEIG_CUDA(cudaMemcpy2DAsync(S, lds * sizeof(double), dS.p, pitch, pitch, n, cudaMemcpyDeviceToHost, stream));
         if (Q)
-            TEIG_CUDA(cudaMemcpy2DAsync(Q, ldq * sizeof(double), dQ.p, pitch, pitch, n, cudaMemcpyDeviceToHost, stream));
+            TEIG_CUDA(cudaMemcpy2DAsync(Q, ldq * sizeof(double), dQ.p, pitch, pitch, n, cudaMemcpyDeviceToHost, qs));
         TEIG_CUDA(cudaStreamSynchronize(stream));
+        if (qs) TEIG_CUDA(cudaStreamSynchronize(qs));
     } catch (const std::exception& e) {
+        if (q_ready) cudaEventDestroy(q_ready);
+        if (qs) cudaStreamDestroy(qs);
         return set_error(TEIG_ERR_CUDA, e.what());
     }
+    if (q_ready) cudaEventDestroy(q_ready);
+    if (qs) cudaStreamDestroy(qs);
     return 0;
 }
 
