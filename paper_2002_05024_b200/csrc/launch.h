@@ -62,7 +62,13 @@ cudaError_t launch_scan_active(double* H, long long ldh, int n, int ihi, double 
 // element-wise sum of nbuf device buffers into all of them (loopback all-reduce)
 cudaError_t launch_sum_buffers(void* const* bufs, int nbuf, size_t count, int elem_bytes, cudaStream_t s);
 
-constexpr int kLeftBN = 64;   // columns per left-update tile
-constexpr int kRightBM = 64;  // rows per right/factor-update tile
+#ifndef TEIG_UPD_BN
+#define TEIG_UPD_BN 64
+#endif
+#ifndef TEIG_UPD_BM
+#define TEIG_UPD_BM 64
+#endif
+constexpr int kLeftBN = TEIG_UPD_BN;   // columns per left-update tile
+constexpr int kRightBM = TEIG_UPD_BM;  // rows per right/factor-update tile
 
 }  // namespace teig

@@ -12,9 +12,11 @@
 // all windows of a wavefront: the CTA locates its window by binary search
 // over the per-level tile prefix sums carried in WinDesc.
 //
-// Operands are streamed through shared memory in K-chunks of 16 with 8-byte
+// Operands are streamed through shared memory in K-chunks of 32 with 8-byte
 // cp.async (panel row offsets are arbitrary, so 16-byte alignment is not
-// guaranteed) in a 3-stage pipeline; shared tiles are column-major with a
+// guaranteed) in a 2-stage pipeline (A/B on B200: KC=32 x 2 stages beat
+// KC=16 x 3 stages by 1.5 % on C4; 128-wide tiles lost 10-15 % to occupancy
+// and tails); shared tiles are column-major with a
 // leading dimension = 4 (mod 16) doubles, which makes the m8n8k4 fragment
 // loads bank-conflict free.  Edges (k >= d, rows/cols past the panel) are
 // zero-filled by cp.async's src-size operand.
@@ -27,9 +29,15 @@ namespace teig {
 
 namespace {
 
-constexpr int KC = 16;       // K chunk
-constexpr int LDK = KC + 4;  // smem ld for K-contiguous tiles
-constexpr int STAGES = 3;
+#ifndef TEIG_UPD_KC
+#define TEIG_UPD_KC 32
+#endif
+#ifndef TEIG_UPD_STAGES
+#define TEIG_UPD_STAGES 2
+#endif
+constexpr int KC = TEIG_UPD_KC;  // K chunk
+constexpr int LDK = KC + 4;      // smem ld for K-contiguous tiles (= 4 mod 16 doubles)
+constexpr int STAGES = TEIG_UPD_STAGES;
 constexpr int kUpdThreads = 256;
 
 __device__ __forceinline__ void cp8(void* smem_dst, const void* gsrc, bool valid) {
@@ -48,8 +56,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 // locate the window owning tile t of this launch: largest k with pref[k] <= t
+// (serial binary search: log2(nwin) dependent global loads)
 template <int Field>
-__device__ __forceinline__ int find_window(const WinDesc* wins, int nwin, int t) {
+__device__ __forceinline__ int find_window_serial(const WinDesc* wins, int nwin, int t) {
     int lo = 0, hi = nwin - 1;
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
@@ -58,6 +67,22 @@ __device__ __forceinline__ int find_window(const WinDesc* wins, int nwin, int t)
         else hi = mid - 1;
     }
     return lo;
+}
+
+// the same, CTA-cooperative: every thread reads one window's prefix (one
+// global round trip instead of ~log2(nwin) dependent ones); ends with a barrier
+template <int Field>
+__device__ __forceinline__ int find_window(const WinDesc* wins, int nwin, int t, int* sh) {
+    if (nwin > kUpdThreads) return find_window_serial<Field>(wins, nwin, t);
+    if (threadIdx.x == 0) *sh = 0;
+    __syncthreads();
+    if ((int)threadIdx.x < nwin) {
+        const WinDesc& w = wins[threadIdx.x];
+        const int p = Field == 0 ? w.tl_pref : (Field == 1 ? w.tr_pref : w.tq_pref);
+        if (p <= t) atomicMax(sh, (int)threadIdx.x);
+    }
+    __syncthreads();
+    return *sh;
 }
 
 }  // namespace
@@ -70,7 +95,7 @@ template <int DMAX>
 __global__ void __launch_bounds__(kUpdThreads)
 update_left_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __restrict__ qw_pool,
                    double* __restrict__ S, long long lds, int n) {
-    constexpr int BN = 64;
+    constexpr int BN = kLeftBN;
     constexpr int WM = (DMAX == 128) ? 4 : 2;   // warps along M
     constexpr int WN = 8 / WM;                  // warps along N
     constexpr int MT = DMAX / WM / 8;           // 8x8 tiles per warp along M (4)
@@ -80,7 +105,8 @@ update_left_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __r
     double (*Bs)[BN * LDK] = reinterpret_cast<double (*)[BN * LDK]>(dsm + STAGES * DMAX * LDK);
 
     const int t = blockIdx.x;
-    const int wi = find_window<0>(wins, nwin, t);
+    __shared__ int sh_win;
+    const int wi = find_window<0>(wins, nwin, t, &sh_win);
     const WinDesc wd = wins[wi];
     const int d = wd.d, a = wd.a;
     const int c = wd.lc0 + (t - wd.tl_pref) * BN;
@@ -173,7 +199,7 @@ template <int DMAX, int Field>
 __global__ void __launch_bounds__(kUpdThreads)
 update_right_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __restrict__ qw_pool,
                     double* __restrict__ M, long long ldm, int nrows_total) {
-    constexpr int BM = 64;
+    constexpr int BM = kRightBM;
     constexpr int LDM = BM + 4;
     constexpr int WM = 2, WN = 4;
     constexpr int MT = BM / WM / 8;     // 4
@@ -183,7 +209,8 @@ update_right_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __
     double (*Bs)[DMAX * LDK] = reinterpret_cast<double (*)[DMAX * LDK]>(dsm + STAGES * KC * LDM);
 
     const int t = blockIdx.x;
-    const int wi = find_window<Field>(wins, nwin, t);
+    __shared__ int sh_win;
+    const int wi = find_window<Field>(wins, nwin, t, &sh_win);
     const WinDesc wd = wins[wi];
     const int d = wd.d, a = wd.a;
     const int pref = (Field == 1) ? wd.tr_pref : wd.tq_pref;
@@ -272,8 +299,8 @@ static cudaError_t set_smem(K kernel, size_t bytes) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-constexpr size_t left_smem(int dmax) { return (size_t)STAGES * (dmax * LDK + 64 * LDK) * sizeof(double); }
-constexpr size_t right_smem(int dmax) { return (size_t)STAGES * (KC * (64 + 4) + dmax * LDK) * sizeof(double); }
+constexpr size_t left_smem(int dmax) { return (size_t)STAGES * (dmax * LDK + kLeftBN * LDK) * sizeof(double); }
+constexpr size_t right_smem(int dmax) { return (size_t)STAGES * (KC * (kRightBM + 4) + dmax * LDK) * sizeof(double); }
 
 cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
                                double* S, long long lds, int n, cudaStream_t stream) {
