@@ -173,7 +173,6 @@ class SchurRunner {
         dopts_.shift_count = o.shift_count;
         dopts_.aed_window = o.aed_window;
         dopts_.small_threshold = o.small_threshold;
-        dopts_.small_mode = (getenv("TEIG_SMALL_MODE") && atoi(getenv("TEIG_SMALL_MODE")) == 1) ? 1 : 0;
         tile_ = o.tile_size ? o.tile_size : default_tile_size(n);
         TEIG_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
         TEIG_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
@@ -859,7 +858,7 @@ int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int3
         AedDevOut hout{};
         cudaStream_t s = (cudaStream_t)stream;
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dout), sizeof(AedDevOut), s));
-        SchurDevOpts d{o.deflation, o.shift_count, o.aed_window, o.small_threshold, 0};
+        SchurDevOpts d{o.deflation, o.shift_count, o.aed_window, o.small_threshold};
         TEIG_CUDA(launch_aed_window(dH, ldh, kSchurModeSmall, 0, 0, (int)k, d, dQ, dout, nullptr, s));
         TEIG_CUDA(cudaMemcpyAsync(&hout, dout, sizeof hout, cudaMemcpyDeviceToHost, s));
         TEIG_CUDA(cudaFreeAsync(dout, s));

@@ -122,3 +122,69 @@ def test_c_abi_argument_validation_without_gpu(T):
     sel.blocks[1].start = 5
     with pytest.raises(ValueError):
         T.reorder_schur(np.diag([1.0, 2.0, 3.0]), None, sel)
+
+
+def test_schur_and_pair_c_abi_validation_without_gpu(T):
+    """Argument checks of the Schur / generalized / per-step entry points run
+    before any device work and return the LAPACK-style codes the C++ layer
+    maps onto the reference's exceptions (schur.cpp:601, 614-626)."""
+    from paper_2002_05024_b200 import _native as N
+    L = N.lib()
+    dummy = C.c_void_p(16)
+    o = N.SchurOpts()
+    L.teig_schur_opts_default(C.byref(o))
+    assert o.deflation == 1 and o.small_threshold == 64
+    assert L.teig_schur_reduce_device(0, dummy, 1, None, 1, None, None, None, None, None) == -1
+    assert L.teig_schur_reduce_device(4, None, 4, None, 4, None, None, None, None, None) == -2
+    assert L.teig_schur_reduce_device(4, dummy, 3, None, 4, None, None, None, None, None) == -3
+    o.aed_window = 200
+    assert L.teig_schur_reduce_device(200, dummy, 200, None, 200, C.byref(o), None, None, None, None) == -1001
+    o.aed_window = 0
+    o.deflation = 3
+    assert L.teig_schur_reduce_device(200, dummy, 200, None, 200, C.byref(o), None, None, None, None) == -7
+    # aed_step: window < 4 is invalid (schur.cpp:601)
+    assert L.teig_aed_step_device(50, dummy, 50, None, 50, 0, 50, 3, None, None, None, None) == -8
+    # introduce_bulges: the reference's std::invalid_argument cases (schur.cpp:614-626)
+    sh = np.array([1.0, 0.0], dtype=np.float64)
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)
+    assert L.teig_introduce_bulges_device(12, dummy, 12, None, 12, 0, 12, 1, vp(sh), None, None) == -8
+    sh3 = np.array([1.0, 0.0, 2.0, 0.0, 3.0, 0.0], dtype=np.float64)
+    assert L.teig_introduce_bulges_device(12, dummy, 12, None, 12, 0, 12, 3, vp(sh3), None, None) == -8
+    nc = np.array([1.0, 2.0, 1.0, 2.0], dtype=np.float64)  # (1+2i, 1+2i): not conjugate
+    assert L.teig_introduce_bulges_device(12, dummy, 12, None, 12, 0, 12, 2, vp(nc), None, None) == -8
+    many = np.zeros(2 * 8)
+    assert L.teig_introduce_bulges_device(12, dummy, 12, None, 12, 0, 12, 8, vp(many), None, None) == -8
+    # chase_bulges: positions must be the introduced chain (bottom first, 3 apart)
+    pos = np.array([10, 5], dtype=np.int64)
+    assert L.teig_chase_bulges_device(20, dummy, 20, None, 20, 20, 2, vp(pos), 16, None, None) == -8
+    assert L.teig_small_schur_device(200, dummy, 200, dummy, None, None) == -1001
+    # generalized pair: window <= 64, selection must match
+    sizes = np.ones(3, dtype=np.uint8)
+    flags = np.zeros(3, dtype=np.uint8)
+    ro = N.ReorderOpts()
+    L.teig_reorder_opts_default(C.byref(ro))
+    ro.window_size = 128
+    assert L.teig_greorder_schur_device(3, dummy, 3, dummy, 3, None, 3, None, 3, 3, vp(sizes), vp(flags),
+                                        C.byref(ro), None, None, None, None) == -1001
+    assert L.teig_greorder_schur_device(4, dummy, 4, dummy, 4, None, 4, None, 4, 3, vp(sizes), vp(flags),
+                                        None, None, None, None, None) == -8
+    assert L.teig_greorder_schur_device(3, dummy, 3, None, 3, None, 3, None, 3, 3, vp(sizes), vp(flags),
+                                        None, None, None, None, None) == -2
+
+
+def test_deflation_check_c_abi(T):
+    eps = 2.220446049250313e-16
+    assert T.deflation_check(0.0, 1.0, T.DeflationCondition.classic, 1.0)
+    assert not T.deflation_check(1.0, 1.0, T.DeflationCondition.norm_stable, 1.0)
+    assert T.deflation_check(0.9 * eps, 1e-3, T.DeflationCondition.norm_stable, 1.0)
+    assert not T.deflation_check(0.9 * eps, 1e-3, T.DeflationCondition.classic, 1.0)
+
+
+def test_python_mirror_errors(T):
+    import numpy as np
+    with pytest.raises(ValueError):
+        T.schur_reduce(np.zeros((3, 4)))
+    with pytest.raises(ValueError):
+        T.introduce_bulges(np.zeros((12, 12)), None, 0, 12, [1.0])
+    with pytest.raises(ValueError):
+        T.aed_step(np.zeros((12, 12)), None, 0, 12, 3)
