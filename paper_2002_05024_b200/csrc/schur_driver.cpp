@@ -196,9 +196,10 @@ class SchurRunner {
             cudaMemcpy(pf, d_prof_, sizeof pf, cudaMemcpyDeviceToHost);
             fprintf(stderr,
                     "[teig aed prof] windows(aed)=%lld chase=%lld | Mcycles: total %.1f small %.1f swap %.1f (n=%llu) "
-                    "sweep %.1f spike %.1f | sim_steps %llu small_sweeps %llu | wave steps %llu decide %.1f plan %.1f\n",
+                    "sweep %.1f spike %.1f | sim_steps %llu small_sweeps %llu | wave steps %llu decide %.1f plan %.1f | "
+                    "local %.1f\n",
                     (long long)aed_windows_, (long long)chase_windows_, pf[0] / 1e6, pf[1] / 1e6, pf[2] / 1e6, pf[3],
-                    pf[4] / 1e6, pf[5] / 1e6, pf[6], pf[7], pf[8], pf[9] / 1e6, pf[10] / 1e6);
+                    pf[4] / 1e6, pf[5] / 1e6, pf[6], pf[7], pf[8], pf[9] / 1e6, pf[10] / 1e6, pf[11] / 1e6);
             cudaFree(d_prof_);
         }
         qw_.release(s_);

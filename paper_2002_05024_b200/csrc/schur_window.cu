@@ -73,13 +73,21 @@ struct Ctx {
     int* wave_i;     // swap-wave bookkeeping (block list, pairs)
     double* wave_d;  // swap-wave pair transforms (kWaveMaxPairs x 32)
     double* snap;    // global scratch: H and Q snapshot of the top window (2 N^2)
+    double* loc;     // kLocalAedDoubles: a small nested window gathered for one warp
 };
+
+// nested AED windows up to this order run gathered (aed_local)
+#ifndef TEIG_LOCAL_AED_MAX
+#define TEIG_LOCAL_AED_MAX 16
+#endif
+constexpr int kLocalAedMax = TEIG_LOCAL_AED_MAX;
+constexpr int kLocalAedDoubles = 2 * kLocalAedMax * kLocalAedMax + kLocalAedMax + 8 + 32 + 8;
 
 constexpr int kWaveMaxPairs = 56;
 constexpr int kWaveMinWindow = 24;  // smaller AED windows use the sequential order
 
 // diagnostics (TEIG_AED_PROF=1): cycle counters kept by thread 0
-enum { kPfTotal, kPfSmall, kPfSwap, kPfSwapN, kPfSweep, kPfSpike, kPfSteps, kPfSmallSweeps, kPfWaveSteps, kPfWaveDecide, kPfWavePlan, kPfN };
+enum { kPfTotal, kPfSmall, kPfSwap, kPfSwapN, kPfSweep, kPfSpike, kPfSteps, kPfSmallSweeps, kPfWaveSteps, kPfWaveDecide, kPfWavePlan, kPfLocal, kPfN };
 #define PF_T0() const long long _pf0 = clock64()
 #define PF_ADD(i) do { if (c.prof && tid() == 0) c.prof[i] += (unsigned long long)(clock64() - _pf0); } while (0)
 #define PF_INC(i) do { if (c.prof && tid() == 0) c.prof[i] += 1ull; } while (0)
@@ -188,65 +196,67 @@ __device__ void right_apply_n(const Ctx& c, int c0, int len, int r1) {
     }
 }
 
-// make_reflector (kernels.cpp:24-58) of x = c.scr[0..len), in place: on return
-// (after a barrier) c.scr[0..len) = v, c.scr[len] = tau, c.scr[len+1] = beta.
-__device__ void make_refl_block(const Ctx& c, int len) {
-    __syncthreads();  // x written by the caller
-    if (tid() < 32) {
-        const int lane = tid();
-        double* x = c.scr;
-        double tau = 0.0, beta;
-        if (len == 1) {
-            beta = x[0];
-        } else {
-            const double alpha = x[0];
-            auto tailnorm = [&]() {
-                double mx = 0.0;
-                for (int i = 1 + lane; i < len; i += 32) mx = fmax(mx, fabs(x[i]));
+// make_reflector (kernels.cpp:24-58) of x[0..len) in place by one warp: on
+// return (after __syncwarp) x[0..len) = v, x[len] = tau, x[len+1] = beta.
+__device__ void make_refl_warp(double* x, int len, int lane) {
+    double tau = 0.0, beta;
+    if (len == 1) {
+        beta = x[0];
+    } else {
+        const double alpha = x[0];
+        auto tailnorm = [&]() {
+            double mx = 0.0;
+            for (int i = 1 + lane; i < len; i += 32) mx = fmax(mx, fabs(x[i]));
 #pragma unroll
-                for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-                if (mx == 0.0) return 0.0;
-                double acc = 0.0;
-                for (int i = 1 + lane; i < len; i += 32) {
-                    const double t = x[i] / mx;
-                    acc += t * t;
-                }
-#pragma unroll
-                for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                return mx * sqrt(acc);
-            };
-            const double tail = tailnorm();
-            if (tail == 0.0) {
-                beta = (alpha == 0.0) ? 0.0 : alpha;
-                __syncwarp();
-                for (int i = 1 + lane; i < len; i += 32) x[i] = 0.0;
-            } else {
-                beta = -sgnd(alpha) * hypot(alpha, tail);
-                double a = alpha;
-                int rescale = 0;
-                while (fabs(beta) < kSafeMinD / kEpsD && rescale < 20) {
-                    const double big = 1.0 / (kSafeMinD / kEpsD);
-                    __syncwarp();
-                    for (int i = 1 + lane; i < len; i += 32) x[i] *= big;
-                    __syncwarp();
-                    a *= big;
-                    beta = -sgnd(a) * hypot(a, tailnorm());
-                    ++rescale;
-                }
-                tau = (beta - a) / beta;
-                const double inv = 1.0 / (a - beta);
-                __syncwarp();
-                for (int i = 1 + lane; i < len; i += 32) x[i] *= inv;
-                for (int r = 0; r < rescale; ++r) beta *= kSafeMinD / kEpsD;
+            for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (mx == 0.0) return 0.0;
+            double acc = 0.0;
+            for (int i = 1 + lane; i < len; i += 32) {
+                const double t = x[i] / mx;
+                acc += t * t;
             }
-        }
-        __syncwarp();
-        if (lane == 0) {
-            x[0] = 1.0;
-            x[len] = tau;
-            x[len + 1] = beta;
+#pragma unroll
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            return mx * sqrt(acc);
+        };
+        const double tail = tailnorm();
+        if (tail == 0.0) {
+            beta = (alpha == 0.0) ? 0.0 : alpha;
+            __syncwarp();
+            for (int i = 1 + lane; i < len; i += 32) x[i] = 0.0;
+        } else {
+            beta = -sgnd(alpha) * hypot(alpha, tail);
+            double a = alpha;
+            int rescale = 0;
+            while (fabs(beta) < kSafeMinD / kEpsD && rescale < 20) {
+                const double big = 1.0 / (kSafeMinD / kEpsD);
+                __syncwarp();
+                for (int i = 1 + lane; i < len; i += 32) x[i] *= big;
+                __syncwarp();
+                a *= big;
+                beta = -sgnd(a) * hypot(a, tailnorm());
+                ++rescale;
+            }
+            tau = (beta - a) / beta;
+            const double inv = 1.0 / (a - beta);
+            __syncwarp();
+            for (int i = 1 + lane; i < len; i += 32) x[i] *= inv;
+            for (int r = 0; r < rescale; ++r) beta *= kSafeMinD / kEpsD;
         }
     }
+    __syncwarp();
+    if (lane == 0) {
+        x[0] = 1.0;
+        x[len] = tau;
+        x[len + 1] = beta;
+    }
+    __syncwarp();
+}
+
+// the same for the whole CTA (warp 0 computes): c.scr[0..len) = x on entry
+__device__ void make_refl_block(const Ctx& c, int len) {
+    __syncthreads();  // x written by the caller
+    if (tid() < 32) make_refl_warp(c.scr, len, tid());
     __syncthreads();
 }
 
@@ -779,6 +789,8 @@ struct AedCoreDev {
 
 template <int D>
 __device__ AedCoreDev aed_dev(Ctx& c, int e, int w, double beta);
+template <int D>
+__device__ AedCoreDev aed_local(Ctx& c, int e, int w, double beta);
 
 // shift_vector (schur.cpp:29-43) at the top of the window starting at b
 __device__ __forceinline__ void shift_vec_dev(const Ctx& c, int b, int rows, double ssum, double sprod,
@@ -1124,7 +1136,10 @@ __device__ bool mshift_dev(Ctx& c, int lo, int n) {
         const int e = ihi - w;
         const double beta = (e > l) ? c.H(lo + e, lo + e - 1) : 0.0;
         AedCoreDev core{0, 0, 0, 0, 0.0};
-        if constexpr (D < 8) core = aed_dev<D + 1>(c, lo + e, w, beta);
+        if constexpr (D < 8) {
+            if (D >= 1 && w <= kLocalAedMax && c.loc) core = aed_local<D + 1>(c, lo + e, w, beta);
+            else core = aed_dev<D + 1>(c, lo + e, w, beta);
+        }
         if (!core.converged) return false;
         if (e > l && tid() == 0) c.H(lo + e, lo + e - 1) = core.newbeta;
         __syncthreads();
@@ -1208,6 +1223,231 @@ __device__ bool mshift_dev(Ctx& c, int lo, int n) {
         PF_ADD(kPfSweep);
     }
     return true;
+}
+
+// aed_process_window (schur.cpp:147-248) for a small nested window, gathered:
+// warp 0 runs the whole window procedure on a private copy Hl with its own
+// accumulator Ql (no block barrier per reflector, rows of length w instead of
+// the enclosing window's), then the CTA applies the one similarity Ql to the
+// enclosing context: rows right of / columns above the window, Q and the
+// tracked spike rows.  Same decisions as the in-place aed_dev (the deflation
+// test reads Ql's first row, which is the nested spike row it tracks).
+template <int D>
+__device__ AedCoreDev aed_local(Ctx& c, int e, int w, double beta) {
+    PF_T0();
+    const int lvl = D / 2;
+    double* Hl = c.loc;
+    double* Ql = Hl + kLocalAedMax * kLocalAedMax;
+    double* xs = Ql + kLocalAedMax * kLocalAedMax;  // reflector, len + 2
+    double* MB = xs + kLocalAedMax + 8;             // swap transform + new block
+    int* res = reinterpret_cast<int*>(MB + 32);     // converged, deflated, rejected
+    double* nbeta = MB + 36;
+    __syncthreads();
+    for (int idx = tid(); idx < w * w; idx += NT) {
+        const int j = idx / w, i = idx - j * w;
+        Hl[idx] = c.H(e + i, e + j);
+        Ql[idx] = (i == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (tid() < 32) {
+        const int lane = tid();
+        Ctx L = c;
+        L.H = Mat{Hl, w};
+        L.Q = Mat{Ql, w};
+        L.N = w;
+        L.nspk = 0;
+        double mx = 0.0;
+        for (int idx = lane; idx < w * w; idx += 32) mx = fmax(mx, fabs(Hl[idx]));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        double wnorm = 0.0;
+        if (mx != 0.0) {
+            double acc = 0.0;
+            for (int idx = lane; idx < w * w; idx += 32) {
+                const double t = Hl[idx] / mx;
+                acc += t * t;
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            wnorm = mx * sqrt(acc);
+        }
+        const bool conv = small_schur_grp<32>(wctx(L), lane, 0, w, nullptr, nullptr);
+        int deflated = 0, rejected = 0;
+        double newbeta = 0.0;
+        if (conv && beta == 0.0) {
+            deflated = w;
+        } else if (conv) {
+            int ktop = 0, ns = w;
+            while (ns > ktop) {
+                const int bsize = (ns >= 2 && ns - 2 >= ktop && Hl[(ns - 1) + (ns - 2) * w] != 0.0) ? 2 : 1;
+                const int bs = ns - bsize;
+                double spike = 0.0, dsum = 0.0;
+                for (int r = bs; r < ns; ++r) {
+                    spike = fmax(spike, fabs(beta * Ql[r * w]));
+                    dsum += fabs(Hl[r + r * w]);
+                }
+                if (deflation_check_dev(spike, dsum, c.o.deflation, wnorm)) {
+                    ns = bs;
+                    continue;
+                }
+                int cur = bs;
+                bool stuck = false;
+                while (cur > ktop) {
+                    const int psize = (cur >= 2 && cur - 2 >= ktop && Hl[(cur - 1) + (cur - 2) * w] != 0.0) ? 2 : 1;
+                    const int ps = cur - psize;
+                    int st = 0;
+                    if (lane == 0) st = swap_decide(Hl, w, ps, psize, bsize, MB, MB + 16);
+                    st = __shfl_sync(0xffffffffu, st, 0);
+                    __syncwarp();
+                    if (st == 0) {
+                        stuck = true;
+                        break;
+                    }
+                    if (st == 1) {
+                        const int Dd = psize + bsize;
+                        if (Dd == 2) pair_left<2>(L, MB, ps, lane);
+                        else if (Dd == 3) pair_left<3>(L, MB, ps, lane);
+                        else pair_left<4>(L, MB, ps, lane);
+                        __syncwarp();
+                        if (Dd == 2) pair_right<2>(L, MB, ps, lane);
+                        else if (Dd == 3) pair_right<3>(L, MB, ps, lane);
+                        else pair_right<4>(L, MB, ps, lane);
+                        __syncwarp();
+                    }
+                    cur = ps;
+                }
+                if (stuck) {
+                    rejected = 1;
+                    break;
+                }
+                ktop += bsize;
+            }
+            deflated = w - ns;
+            if (lane == 0) {  // harvest (schur.cpp:206-219)
+                double* sh = c.shb + lvl * 2 * c.N;
+                int nsh = 0;
+                for (int i = 0; i < ns;) {
+                    if (i + 1 < ns && Hl[(i + 1) + i * w] != 0.0) {
+                        const double a = Hl[i + i * w], b = Hl[i + (i + 1) * w], cc = Hl[(i + 1) + i * w];
+                        const double im = sqrt(fabs(b)) * sqrt(fabs(cc));
+                        sh[2 * nsh] = a;
+                        sh[2 * nsh + 1] = im;
+                        sh[2 * nsh + 2] = a;
+                        sh[2 * nsh + 3] = -im;
+                        nsh += 2;
+                        i += 2;
+                    } else {
+                        sh[2 * nsh] = Hl[i + i * w];
+                        sh[2 * nsh + 1] = 0.0;
+                        nsh += 1;
+                        i += 1;
+                    }
+                }
+                c.nsh[lvl] = nsh;
+            }
+            // spike elimination and Hessenberg restore (schur.cpp:222-245)
+            auto left = [&](int r0, int len, int c0) {  // rows r0.., columns [c0, w)
+                const double tau = xs[len];
+                if (tau != 0.0)
+                    for (int j = c0 + lane; j < w; j += 32) {
+                        double* col = Hl + r0 + j * w;
+                        double a = 0.0;
+                        for (int i = 0; i < len; ++i) a += xs[i] * col[i];
+                        a *= tau;
+                        for (int i = 0; i < len; ++i) col[i] -= a * xs[i];
+                    }
+                __syncwarp();
+            };
+            auto right = [&](int c0, int len, int r1) {  // columns c0.., Hl rows [0, r1) and Ql
+                const double tau = xs[len];
+                if (tau != 0.0)
+                    for (int t = lane; t < r1 + w; t += 32) {
+                        double* p = (t < r1) ? Hl + t + c0 * w : Ql + (t - r1) + c0 * w;
+                        double a = 0.0;
+                        for (int j = 0; j < len; ++j) a += p[j * w] * xs[j];
+                        a *= tau;
+                        for (int j = 0; j < len; ++j) p[j * w] -= a * xs[j];
+                    }
+                __syncwarp();
+            };
+            if (ns == 1) {
+                newbeta = beta * Ql[0];
+            } else if (ns > 1) {
+                for (int i = lane; i < ns; i += 32) xs[i] = beta * Ql[i * w];
+                make_refl_warp(xs, ns, lane);
+                newbeta = xs[ns + 1];
+                left(0, ns, 0);
+                right(0, ns, ns);
+                for (int j = 0; j + 2 < ns; ++j) {
+                    const int len = ns - j - 1;
+                    for (int i = lane; i < len; i += 32) xs[i] = Hl[(j + 1 + i) + j * w];
+                    make_refl_warp(xs, len, lane);
+                    if (xs[len] == 0.0) continue;
+                    const double hb = xs[len + 1];
+                    left(j + 1, len, j + 1);
+                    for (int i = lane; i < len; i += 32) Hl[(j + 1 + i) + j * w] = (i == 0) ? hb : 0.0;
+                    __syncwarp();
+                    right(j + 1, len, ns);
+                }
+            }
+        }
+        if (lane == 0) {
+            res[0] = conv ? 1 : 0;
+            res[1] = deflated;
+            res[2] = rejected;
+            *nbeta = newbeta;
+        }
+    }
+    __syncthreads();
+    AedCoreDev core{res[1], res[0], res[2], res[0], *nbeta};
+    if (!core.converged) {
+        core.spike_eliminated = 0;
+        __syncthreads();
+        return core;
+    }
+    // the similarity on the enclosing context: H rows [e, e+w) right of the
+    // window (Ql^T x), H rows above it, Q and the spike rows (x Ql)
+    const int ncol = c.N - e - w;
+    const int total = ncol + e + c.N + c.nspk;
+    for (int t = tid(); t < total + w * w; t += NT) {
+        if (t >= total) {
+            const int idx = t - total, j = idx / w, i = idx - j * w;
+            c.H(e + i, e + j) = Hl[idx];
+            continue;
+        }
+        double* a;  // a length-w vector (stride st): x <- Ql^T x (H rows) or x^T Ql (columns)
+        int st;
+        if (t < ncol) {
+            a = &c.H(e, e + w + t);
+            st = 1;
+        } else {
+            const int u = t - ncol;
+            if (u < e) {
+                a = &c.H(u, e);
+                st = c.H.ld;
+            } else if (u < e + c.N) {
+                a = &c.Q(u - e, e);
+                st = c.Q.ld;
+            } else {
+                const Spk& sk = c.spk[u - e - c.N];
+                a = sk.p + (e - sk.off);
+                st = 1;
+            }
+        }
+        double x[kLocalAedMax];
+#pragma unroll
+        for (int r = 0; r < kLocalAedMax; ++r) x[r] = (r < w) ? a[r * st] : 0.0;
+        for (int j = 0; j < w; ++j) {
+            double acc = 0.0;
+#pragma unroll
+            for (int r = 0; r < kLocalAedMax; ++r)
+                if (r < w) acc += x[r] * Ql[r + j * w];
+            a[j * st] = acc;
+        }
+    }
+    __syncthreads();
+    PF_ADD(kPfLocal);
+    return core;
 }
 
 // aed_process_window (schur.cpp:147-248) on the window [e, e+w), in place.
@@ -1400,6 +1640,8 @@ __global__ void __launch_bounds__(NT) aed_window_kernel(double* __restrict__ Hg,
     base += 64 * 6;
     c.wave_d = base;
     base += kWaveMaxPairs * 32;
+    c.loc = base;
+    base += kLocalAedDoubles;
     c.snap = snap;
     c.iscr = reinterpret_cast<int*>(base);
     c.nsh = c.iscr + 8;
@@ -1448,7 +1690,7 @@ __global__ void __launch_bounds__(NT) aed_window_kernel(double* __restrict__ Hg,
 size_t aed_window_smem_bytes(int w) {
     const size_t ld = (size_t)(w | 1);
     const size_t dbl = 2 * ld * w + 32 + w + 40 + kMaxSpk * 2 * w + kMaxSpk * 2 * (w + 4) + kMaxSpk * w + 64 * 6 +
-                       kWaveMaxPairs * 32;
+                       kWaveMaxPairs * 32 + kLocalAedDoubles;
     return dbl * sizeof(double) + (32 + 8 + 128 + 128 + 4 * kWaveMaxPairs + 4 + 4 * kWaveMaxPairs) * sizeof(int);
 }
 
