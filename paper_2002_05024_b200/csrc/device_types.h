@@ -44,7 +44,10 @@ struct SchurDevOpts {
     int32_t shift_count;      // 0: default_shift_count
     int32_t aed_window;       // 0: 3m/2
     int32_t small_threshold;  // direct small_schur below this active size
+    int32_t flags;            // kSchurFlag* (diagnostics: disable a kernel-internal path)
 };
+
+enum { kSchurFlagNoWave = 1, kSchurFlagNoLocal = 2 };
 
 // outcome of one AED / small-solve window (AedResult, schur.hpp:32-39)
 struct AedDevOut {

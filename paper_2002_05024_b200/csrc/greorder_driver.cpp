@@ -122,22 +122,22 @@ GPass run_gpass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* d
             TEIG_CUDA(cudaEventRecord(ev, s));
             TEIG_CUDA(cudaStreamWaitEvent(s2, ev, 0));
             if (dQ) {
-                TEIG_CUDA(launch_update_right(d_q.p + o, (int)cnt, (int)tq[L], dm, d_pool.p, dQ, ldq, (int)n, true, s2));
+                TEIG_CUDA(launch_update_right(d_q.p + o, (int)cnt, (int)tq[L], dm, d_pool.p, dQ, ldq, (int)n, true, s2, n, n));
                 ++launches;
             }
             if (dZ) {
-                TEIG_CUDA(launch_update_right(d_z.p + o, (int)cnt, (int)tq[L], dm, d_pool.p, dZ, ldz, (int)n, true, s2));
+                TEIG_CUDA(launch_update_right(d_z.p + o, (int)cnt, (int)tq[L], dm, d_pool.p, dZ, ldz, (int)n, true, s2, n, n));
                 ++launches;
             }
         }
         if (tl[L]) {
-            TEIG_CUDA(launch_update_left(d_q.p + o, (int)cnt, (int)tl[L], dm, d_pool.p, dS, lds, (int)n, s));
-            TEIG_CUDA(launch_update_left(d_q.p + o, (int)cnt, (int)tl[L], dm, d_pool.p, dT, ldt, (int)n, s));
+            TEIG_CUDA(launch_update_left(d_q.p + o, (int)cnt, (int)tl[L], dm, d_pool.p, dS, lds, (int)n, s, n, n));
+            TEIG_CUDA(launch_update_left(d_q.p + o, (int)cnt, (int)tl[L], dm, d_pool.p, dT, ldt, (int)n, s, n, n));
             launches += 2;
         }
         if (tr[L]) {
-            TEIG_CUDA(launch_update_right(d_z.p + o, (int)cnt, (int)tr[L], dm, d_pool.p, dS, lds, (int)n, false, s));
-            TEIG_CUDA(launch_update_right(d_z.p + o, (int)cnt, (int)tr[L], dm, d_pool.p, dT, ldt, (int)n, false, s));
+            TEIG_CUDA(launch_update_right(d_z.p + o, (int)cnt, (int)tr[L], dm, d_pool.p, dS, lds, (int)n, false, s, n, n));
+            TEIG_CUDA(launch_update_right(d_z.p + o, (int)cnt, (int)tr[L], dm, d_pool.p, dT, ldt, (int)n, false, s, n, n));
             launches += 2;
         }
     }

@@ -16,11 +16,23 @@ cudaError_t launch_window_reorder(const WinDesc* wins, int nwin, int dmax, doubl
                                   cudaStream_t stream, unsigned long long* prof = nullptr);
 constexpr int kWindowThreads = 256;  // threads of the window kernel (8 warps)
 
+// rows/cols: the extent of the matrix `S`/`M` points at (absolute indices
+// [0, rows) x [0, cols)); when given, windows of order 65..128 take the TMA
+// kernels of update_tma.cu, otherwise (or for slab bases) the cp.async ones.
 cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
-                               double* S, long long lds, int n, cudaStream_t stream);
+                               double* S, long long lds, int n, cudaStream_t stream, long long rows = -1,
+                               long long cols = -1);
 
 cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
-                                double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream);
+                                double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream,
+                                long long rows = -1, long long cols = -1);
+
+// update_tma.cu: false = not eligible (caller falls back), *err = launch status
+bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* S,
+                            long long lds, long long rows, long long cols, cudaStream_t stream, cudaError_t* err);
+bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* M,
+                             long long ldm, long long rows, long long cols, bool factor, cudaStream_t stream,
+                             cudaError_t* err);
 
 // synthetic inputs (generate.cu)
 cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64_t fill_seed,

@@ -235,20 +235,21 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
             TEIG_CUDA(cudaStreamWaitEvent(stream2, ev, 0));
             timed(3, stream2, tq[L], [&] {
                 return launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
-                                           true, stream2);
+                                           true, stream2, n, n);
             });
         }
         timed(1, stream, tl[L], [&] {
-            return launch_update_left(dd + o, (int)cnt, (int)tl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n, stream);
+            return launch_update_left(dd + o, (int)cnt, (int)tl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n, stream,
+                                      n, n);
         });
         timed(2, stream, tr[L], [&] {
             return launch_update_right(dd + o, (int)cnt, (int)tr[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n, false,
-                                       stream);
+                                       stream, n, n);
         });
         if (dQ && !overlap)
             timed(3, stream, tq[L], [&] {
                 return launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
-                                           true, stream);
+                                           true, stream, n, n);
             });
     }
     if (dQ && overlap) {
@@ -639,9 +640,10 @@ int teig_apply_window_updates_device(int64_t n, double* dS, int64_t lds, double*
         const int tl = (int)((n - a - d + kLeftBN - 1) / kLeftBN);
         const int tr = (int)((a + kRightBM - 1) / kRightBM);
         const int tq = (int)((n + kRightBM - 1) / kRightBM);
-        TEIG_CUDA(launch_update_left(ddesc.as<WinDesc>(), 1, tl, dm, dQw, dS, lds, (int)n, stream));
-        TEIG_CUDA(launch_update_right(ddesc.as<WinDesc>(), 1, tr, dm, dQw, dS, lds, (int)n, false, stream));
-        if (dQ) TEIG_CUDA(launch_update_right(ddesc.as<WinDesc>(), 1, tq, dm, dQw, dQ, ldq, (int)n, true, stream));
+        TEIG_CUDA(launch_update_left(ddesc.as<WinDesc>(), 1, tl, dm, dQw, dS, lds, (int)n, stream, n, n));
+        TEIG_CUDA(launch_update_right(ddesc.as<WinDesc>(), 1, tr, dm, dQw, dS, lds, (int)n, false, stream, n, n));
+        if (dQ)
+            TEIG_CUDA(launch_update_right(ddesc.as<WinDesc>(), 1, tq, dm, dQw, dQ, ldq, (int)n, true, stream, n, n));
         TEIG_CUDA(cudaStreamSynchronize(stream));
     } catch (const std::exception& e) {
         return set_error(TEIG_ERR_CUDA, e.what());

@@ -173,6 +173,9 @@ class SchurRunner {
         dopts_.shift_count = o.shift_count;
         dopts_.aed_window = o.aed_window;
         dopts_.small_threshold = o.small_threshold;
+        dopts_.flags = 0;
+        if (getenv("TEIG_NO_WAVE") && atoi(getenv("TEIG_NO_WAVE"))) dopts_.flags |= kSchurFlagNoWave;
+        if (getenv("TEIG_NO_LOCAL") && atoi(getenv("TEIG_NO_LOCAL"))) dopts_.flags |= kSchurFlagNoLocal;
         tile_ = o.tile_size ? o.tile_size : default_tile_size(n);
         TEIG_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
         TEIG_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
@@ -182,24 +185,23 @@ class SchurRunner {
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_out_), sizeof(AedDevOut), s_));
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_int_), sizeof(unsigned long long) * 2, s_));
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_sh_), sizeof(double) * 2 * kAedMaxWindow, s_));
-        if (!(getenv("TEIG_NO_WAVE") && atoi(getenv("TEIG_NO_WAVE"))))
-            TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_snap_),
-                                      sizeof(double) * 2 * kAedMaxWindow * kAedMaxWindow, s_));
+        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_snap_),
+                                  sizeof(double) * 2 * kAedMaxWindow * kAedMaxWindow, s_));
         if (getenv("TEIG_AED_PROF") && atoi(getenv("TEIG_AED_PROF"))) {
-            TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_prof_), sizeof(unsigned long long) * 12, s_));
-            TEIG_CUDA(cudaMemsetAsync(d_prof_, 0, sizeof(unsigned long long) * 12, s_));
+            TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_prof_), sizeof(unsigned long long) * 16, s_));
+            TEIG_CUDA(cudaMemsetAsync(d_prof_, 0, sizeof(unsigned long long) * 16, s_));
         }
     }
     ~SchurRunner() {
         if (d_prof_) {
-            unsigned long long pf[12] = {0};
+            unsigned long long pf[16] = {0};
             cudaMemcpy(pf, d_prof_, sizeof pf, cudaMemcpyDeviceToHost);
             fprintf(stderr,
                     "[teig aed prof] windows(aed)=%lld chase=%lld | Mcycles: total %.1f small %.1f swap %.1f (n=%llu) "
                     "sweep %.1f spike %.1f | sim_steps %llu small_sweeps %llu | wave steps %llu decide %.1f plan %.1f | "
-                    "local %.1f\n",
+                    "local %.1f (n=%llu: small %.1f deflate %.1f)\n",
                     (long long)aed_windows_, (long long)chase_windows_, pf[0] / 1e6, pf[1] / 1e6, pf[2] / 1e6, pf[3],
-                    pf[4] / 1e6, pf[5] / 1e6, pf[6], pf[7], pf[8], pf[9] / 1e6, pf[10] / 1e6, pf[11] / 1e6);
+                    pf[4] / 1e6, pf[5] / 1e6, pf[6], pf[7], pf[8], pf[9] / 1e6, pf[10] / 1e6, pf[11] / 1e6, pf[14], pf[12] / 1e6, pf[13] / 1e6);
             cudaFree(d_prof_);
         }
         qw_.release(s_);
@@ -411,7 +413,7 @@ class SchurRunner {
         flops_ += dd2 * double(n_ - b) + dd2 * double(a) + (dQ_ ? dd2 * double(n_) : 0.0);
         if (tl > 0) {
             const int e0 = prof_begin(s_);
-            TEIG_CUDA(launch_update_left(dd, 1, tl, dm, qw_.p, dH_, ldh_, (int)n_, s_));
+            TEIG_CUDA(launch_update_left(dd, 1, tl, dm, qw_.p, dH_, ldh_, (int)n_, s_, n_, n_));
             prof_end(1, e0, s_);
             ++launches_;
         }
@@ -421,13 +423,13 @@ class SchurRunner {
         }
         if (tr > 0) {
             const int e0 = prof_begin(s2_);
-            TEIG_CUDA(launch_update_right(dd, 1, tr, dm, qw_.p, dH_, ldh_, (int)n_, false, s2_));
+            TEIG_CUDA(launch_update_right(dd, 1, tr, dm, qw_.p, dH_, ldh_, (int)n_, false, s2_, n_, n_));
             prof_end(1, e0, s2_);
             ++launches_;
         }
         if (tq > 0) {
             const int e0 = prof_begin(s2_);
-            TEIG_CUDA(launch_update_right(dd, 1, tq, dm, qw_.p, dQ_, ldq_, (int)n_, true, s2_));
+            TEIG_CUDA(launch_update_right(dd, 1, tq, dm, qw_.p, dQ_, ldq_, (int)n_, true, s2_, n_, n_));
             prof_end(1, e0, s2_);
             ++launches_;
         }
@@ -859,7 +861,7 @@ int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int3
         AedDevOut hout{};
         cudaStream_t s = (cudaStream_t)stream;
         TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dout), sizeof(AedDevOut), s));
-        SchurDevOpts d{o.deflation, o.shift_count, o.aed_window, o.small_threshold};
+        SchurDevOpts d{o.deflation, o.shift_count, o.aed_window, o.small_threshold, 0};
         TEIG_CUDA(launch_aed_window(dH, ldh, kSchurModeSmall, 0, 0, (int)k, d, dQ, dout, nullptr, s));
         TEIG_CUDA(cudaMemcpyAsync(&hout, dout, sizeof hout, cudaMemcpyDeviceToHost, s));
         TEIG_CUDA(cudaFreeAsync(dout, s));

@@ -87,7 +87,7 @@ constexpr int kWaveMaxPairs = 56;
 constexpr int kWaveMinWindow = 24;  // smaller AED windows use the sequential order
 
 // diagnostics (TEIG_AED_PROF=1): cycle counters kept by thread 0
-enum { kPfTotal, kPfSmall, kPfSwap, kPfSwapN, kPfSweep, kPfSpike, kPfSteps, kPfSmallSweeps, kPfWaveSteps, kPfWaveDecide, kPfWavePlan, kPfLocal, kPfN };
+enum { kPfTotal, kPfSmall, kPfSwap, kPfSwapN, kPfSweep, kPfSpike, kPfSteps, kPfSmallSweeps, kPfWaveSteps, kPfWaveDecide, kPfWavePlan, kPfLocal, kPfLocalSmall, kPfLocalDefl, kPfLocalN, kPfN };
 #define PF_T0() const long long _pf0 = clock64()
 #define PF_ADD(i) do { if (c.prof && tid() == 0) c.prof[i] += (unsigned long long)(clock64() - _pf0); } while (0)
 #define PF_INC(i) do { if (c.prof && tid() == 0) c.prof[i] += 1ull; } while (0)
@@ -1137,7 +1137,7 @@ __device__ bool mshift_dev(Ctx& c, int lo, int n) {
         const double beta = (e > l) ? c.H(lo + e, lo + e - 1) : 0.0;
         AedCoreDev core{0, 0, 0, 0, 0.0};
         if constexpr (D < 8) {
-            if (D >= 1 && w <= kLocalAedMax && c.loc) core = aed_local<D + 1>(c, lo + e, w, beta);
+            if (w <= kLocalAedMax && !(c.o.flags & kSchurFlagNoLocal)) core = aed_local<D + 1>(c, lo + e, w, beta);
             else core = aed_dev<D + 1>(c, lo + e, w, beta);
         }
         if (!core.converged) return false;
@@ -1271,7 +1271,13 @@ __device__ AedCoreDev aed_local(Ctx& c, int e, int w, double beta) {
             for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             wnorm = mx * sqrt(acc);
         }
+        const long long t_s = clock64();
         const bool conv = small_schur_grp<32>(wctx(L), lane, 0, w, nullptr, nullptr);
+        const long long t_d = clock64();
+        if (c.prof && lane == 0) {
+            c.prof[kPfLocalSmall] += (unsigned long long)(t_d - t_s);
+            c.prof[kPfLocalN] += 1ull;
+        }
         int deflated = 0, rejected = 0;
         double newbeta = 0.0;
         if (conv && beta == 0.0) {
@@ -1323,6 +1329,7 @@ __device__ AedCoreDev aed_local(Ctx& c, int e, int w, double beta) {
                 ktop += bsize;
             }
             deflated = w - ns;
+            if (c.prof && lane == 0) c.prof[kPfLocalDefl] += (unsigned long long)(clock64() - t_d);
             if (lane == 0) {  // harvest (schur.cpp:206-219)
                 double* sh = c.shb + lvl * 2 * c.N;
                 int nsh = 0;
@@ -1497,7 +1504,7 @@ __device__ AedCoreDev aed_dev(Ctx& c, int e, int w, double beta) {
     } else if (conv) {
         int ktop = 0, ns = w;
         bool waved = false;
-        if (D == 0 && w >= kWaveMinWindow && c.snap) {
+        if (D == 0 && w >= kWaveMinWindow && c.snap && !(c.o.flags & kSchurFlagNoWave)) {
             PF_T0();
             snap_copy(c, true);
             int nsw = w;

@@ -303,8 +303,12 @@ constexpr size_t left_smem(int dmax) { return (size_t)STAGES * (dmax * LDK + kLe
 constexpr size_t right_smem(int dmax) { return (size_t)STAGES * (KC * (kRightBM + 4) + dmax * LDK) * sizeof(double); }
 
 cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
-                               double* S, long long lds, int n, cudaStream_t stream) {
+                               double* S, long long lds, int n, cudaStream_t stream, long long rows, long long cols) {
     if (ntiles <= 0) return cudaSuccess;
+    if (rows > 0) {
+        cudaError_t err;
+        if (launch_update_left_tma(wins, nwin, ntiles, dmax, qw_pool, S, lds, rows, cols, stream, &err)) return err;
+    }
     static bool init = false;
     if (!init) {
         cudaError_t e = set_smem(update_left_kernel<64>, left_smem(64));
@@ -320,8 +324,14 @@ cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dm
 }
 
 cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
-                                double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream) {
+                                double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream,
+                                long long rows, long long cols) {
     if (ntiles <= 0) return cudaSuccess;
+    if (rows > 0) {
+        cudaError_t err;
+        if (launch_update_right_tma(wins, nwin, ntiles, dmax, qw_pool, M, ldm, rows, cols, factor, stream, &err))
+            return err;
+    }
     static bool init = false;
     if (!init) {
         cudaError_t e = set_smem(update_right_kernel<64, 1>, right_smem(64));

@@ -1,0 +1,493 @@
+// update_tma.cu -- the off-diagonal window updates (window_tasks.cpp:12-30,
+// 72-86) with bulk-copy (TMA engine) fed panels and register-resident Q_w
+// fragments.
+//
+// Same contract as update_dmma.cu (one launch = one wavefront, tiles located
+// through the WinDesc prefix sums, in-place output tiles) and the same
+// per-element arithmetic (k ascending in m8n8k4 groups of four, so the two
+// paths agree bit for bit), different data movement:
+//  * Q_w never goes through shared memory: each warp holds its 16-row (left:
+//    Q_w^T) or 16-column (right: Q_w) slice for the whole K = 128 extent as
+//    m8n8k4 fragments in registers (64 doubles per lane), reloaded only when
+//    the CTA's tile range crosses into the next window;
+//  * the panel streams through a 4-stage shared-memory ring.  Every panel
+//    column segment is one cp.async.bulk (SASS UBLKCP: the TMA engine's 1-D
+//    copy) completing on a per-stage mbarrier; warp 0 refills a stage as soon
+//    as all 8 warps have released it (empty mbarrier), kStages sub-tiles
+//    ahead, so the copies of the next sub-tiles overlap the DMMAs of the
+//    current one and no thread waits on its own loads;
+//  * persistent grid (one CTA per SM, grid_for): each CTA walks one
+//    contiguous range of planner tiles
+//    (one or two windows as a rule), so the fragment loads and the pipeline
+//    fill are amortised and there is no partial last wave.
+// Shared-memory column strides are 4 (left, B fragments) and 8 (right, A
+// fragments) mod 16 doubles: both fragment loads take the minimum two
+// wavefronts.  Bulk copies need 16-byte aligned sources: a column segment
+// starts one row early when its first element is odd (the fragment index
+// carries the shift; with an even leading dimension it is the same for all
+// columns of a sub-tile); a segment whose rounded end would pass the end of
+// the matrix allocation stops one pair short and the issuing lane stores its
+// last element itself before the stage's arrive.
+//
+// (2-D tensor-map TMA, cp.async.bulk.tensor, was the first choice: on this
+// pool's B200 nodes every tensor-map load -- CUTLASS's own SM90_TMA_LOAD_2D on
+// a cuTensorMapEncodeTiled descriptor included -- faults with an illegal
+// instruction while 1-D bulk copies work; tools/microbench/tma_min.cu.)
+//
+// Used for windows of order 65..128 on a matrix whose leading dimension is
+// even and whose base is 16-byte aligned; other calls take update_dmma.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+
+#include "device_types.h"
+#include "launch.h"
+
+namespace teig {
+
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kBulkThreads = kWarps * 32;  // 2 warps per SMSP: up to 255 registers each
+constexpr int kStages = 4;
+constexpr int kMinTilesPerCta = 4;  // below this the launch gets more, shorter CTAs
+constexpr int kLdB = 132;        // left: doubles per panel column in smem (<= 129 rows used, = 4 mod 16)
+constexpr int kLdA = 40;         // right: doubles per panel column in smem (<= 33 rows used, = 8 mod 16)
+constexpr int kLeftStage = 32 * kLdB * 8;    // 32 columns x 128(+1) rows
+constexpr int kRightStage = 128 * kLdA * 8;  // 128 columns x 32(+1) rows
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (16-byte aligned, multiple of 16 bytes)
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+template <int Field>
+__device__ __forceinline__ int pref_of(const WinDesc& w) {
+    return Field == 0 ? w.tl_pref : (Field == 1 ? w.tr_pref : w.tq_pref);
+}
+// largest k with pref[k] <= t (serial binary search, once per CTA)
+template <int Field>
+__device__ __forceinline__ int window_of(const WinDesc* wins, int nwin, int t) {
+    int lo = 0, hi = nwin - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (pref_of<Field>(wins[mid]) <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+// the fields of the window owning the current tile, held in registers; the
+// next window's prefix decides when to move on (one global round trip per
+// window instead of several per tile)
+struct TileWin {
+    int wi, a, d, pref, r0, r1, next_pref;
+    long long qw_off;
+};
+template <int Field>
+__device__ __forceinline__ void load_win(TileWin& tw, const WinDesc* wins, int nwin, int wi) {
+    const WinDesc& w = wins[wi];
+    tw.wi = wi;
+    tw.a = w.a;
+    tw.d = w.d;
+    tw.pref = pref_of<Field>(w);
+    tw.r0 = Field == 0 ? w.lc0 : (Field == 1 ? w.rr0 : w.qr0);
+    tw.r1 = Field == 0 ? w.lc1 : (Field == 1 ? w.rr1 : w.qr1);
+    tw.qw_off = w.qw_off;
+    tw.next_pref = (wi + 1 < nwin) ? pref_of<Field>(wins[wi + 1]) : 0x7fffffff;
+}
+template <int Field>
+__device__ __forceinline__ void seek_win(TileWin& tw, const WinDesc* wins, int nwin, int t) {
+    while (t >= tw.next_pref) load_win<Field>(tw, wins, nwin, tw.wi + 1);
+}
+
+// the copy of one column segment: `len` elements from element offset `off`
+// of `base` into dst, as a 16-byte aligned bulk copy starting at off - shift.
+// Returns the bulk doubles to copy (the edge element, if any, is stored here).
+__device__ __forceinline__ int plan_segment(double* dst, const double* base, long long off, int len,
+                                            long long alloc, long long& start) {
+    const int shift = (int)(off & 1);
+    start = off - shift;
+    int n = (len + shift + 1) & ~1;
+    if (start + n > alloc) {  // only the allocation's last column can get here
+        n -= 2;
+        const int tail = len + shift - 1;
+        if (tail >= n) dst[tail] = base[start + tail];
+    }
+    return n > 0 ? n : 0;
+}
+
+// barriers + a zeroed ring (stale stage contents are then always finite
+// matrix values, so rows/columns beyond a window's order only ever meet zero
+// fragments)
+__device__ __forceinline__ void init_ring(uint64_t* full, uint64_t* empty, double* ring, int bytes,
+                                          unsigned full_count) {
+    for (int i = threadIdx.x; i < bytes / 8; i += kBulkThreads) ring[i] = 0.0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], full_count);
+            mbar_init(&empty[s], kWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the zeroes before any bulk write
+    __syncthreads();
+}
+
+// warp 0, after its lanes' edge stores: one arrive carrying the stage's byte
+// count (release: orders the stores before the consumers' acquire)
+__device__ __forceinline__ void stage_arrive(uint64_t* bar, unsigned my_bytes) {
+    const unsigned total = __reduce_add_sync(0xffffffffu, my_bytes);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_expect_tx(bar, total);
+    __syncwarp();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// LEFT: S[a:a+d, c:c+64] <- Q_w^T S[a:a+d, c:c+64], as two 32-column
+// sub-tiles; warp w owns output rows [16w, 16w+16).
+__global__ void __launch_bounds__(kBulkThreads, 1)
+update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, const double* __restrict__ qw_pool,
+                        double* __restrict__ S, long long lds, long long alloc) {
+    extern __shared__ __align__(128) double ring[];
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    init_ring(full, empty, ring, kStages * kLeftStage, 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
+    const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
+
+    // warp 0's position in the (tile, sub-tile) sequence it loads ahead
+    int pt = t0, psub = 0;
+    TileWin pw;
+    auto produce = [&](int slot) {  // warp-uniform; lane j copies column j
+        while (pt < t1) {
+            seek_win<0>(pw, wins, nwin, pt);
+            const int c = pw.r0 + (pt - pw.pref) * kLeftBN;
+            const int ncols = min(kLeftBN, pw.r1 - c);
+            if (psub * 32 >= ncols) {
+                ++pt;
+                psub = 0;
+                continue;
+            }
+            double* dst = ring + slot * (kLeftStage / 8) + lane * kLdB;
+            long long start = 0;
+            int n = 0;
+            if (32 * psub + lane < ncols)
+                n = plan_segment(dst, S, (long long)pw.a + (long long)(c + 32 * psub + lane) * lds, pw.d, alloc,
+                                 start);
+            stage_arrive(&full[slot], (unsigned)n * 8u);
+            if (n > 0) bulk_copy(dst, S + start, (unsigned)n * 8u, &full[slot]);
+            ++psub;
+            return;
+        }
+    };
+    const int wi0 = window_of<0>(wins, nwin, t0);
+    if (warp == 0) {
+        load_win<0>(pw, wins, nwin, wi0);
+        for (int sl = 0; sl < kStages; ++sl) produce(sl);
+    }
+
+    const int gid = lane >> 2, tig = lane & 3;
+    double af[2][32];
+    TileWin wd;
+    load_win<0>(wd, wins, nwin, wi0);
+    int cur = -1, stage = 0;
+    unsigned phase = 0;
+    for (int t = t0; t < t1; ++t) {
+        seek_win<0>(wd, wins, nwin, t);
+        const int d = wd.d;
+        if (wd.wi != cur) {  // A = Q_w^T: af[mt][ks] = Q_w(k = 4ks + tig, m = 16 warp + 8 mt + gid)
+            const double* Qw = qw_pool + wd.qw_off;
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const int m = 16 * warp + 8 * mt + gid;
+#pragma unroll
+                for (int ks = 0; ks < 32; ++ks) {
+                    const int k = 4 * ks + tig;
+                    af[mt][ks] = (m < d && k < d) ? __ldg(Qw + k + (long long)m * d) : 0.0;
+                }
+            }
+            cur = wd.wi;
+        }
+        const int c = wd.r0 + (t - wd.pref) * kLeftBN;
+        const int ncols = min(kLeftBN, wd.r1 - c);
+        double* P = S + (long long)wd.a + (long long)c * lds;
+        for (int sub = 0; 32 * sub < ncols; ++sub) {
+            double acc[2][4][2];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            // column 8 nt + gid, row k = 4 ks + tig (+ the sub-tile's shift)
+            const int shift = (int)(((long long)wd.a + (long long)(c + 32 * sub) * lds) & 1);
+            const double* sb = ring + stage * (kLeftStage / 8) + gid * kLdB + tig + shift;
+            mbar_wait(&full[stage], phase);
+#pragma unroll
+            for (int ks = 0; ks < 32; ++ks) {
+                double bf[4];
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) bf[nt] = sb[nt * 8 * kLdB + 4 * ks];
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][ks], bf[nt]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (warp == 0) {
+                mbar_wait(&empty[stage], phase);
+                produce(stage);
+            }
+            if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const int r = 16 * warp + 8 * mt + gid;
+                if (r >= d) continue;
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    const int cc = 32 * sub + 8 * nt + 2 * tig;
+                    if (cc < ncols) P[r + (long long)cc * lds] = acc[mt][nt][0];
+                    if (cc + 1 < ncols) P[r + (long long)(cc + 1) * lds] = acc[mt][nt][1];
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// RIGHT: M[r0:r0+64, a:a+d] <- M[r0:r0+64, a:a+d] Q_w, as two 32-row
+// sub-tiles; warp w owns output columns [16w, 16w+16).
+template <int Field>
+__global__ void __launch_bounds__(kBulkThreads, 1)
+update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, const double* __restrict__ qw_pool,
+                         double* __restrict__ M, long long ldm, long long alloc) {
+    extern __shared__ __align__(128) double ring[];
+    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
+    init_ring(full, empty, ring, kStages * kRightStage, 128);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
+    const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
+    auto tile_rows = [&](const TileWin& w, int t, int& r0, int& nrows) {
+        r0 = w.r0 + (t - w.pref) * kRightBM;
+        nrows = min(kRightBM, w.r1 - r0);
+    };
+
+    // every thread walks the (tile, sub-tile) sequence kStages ahead of the
+    // one it computes; thread j < 128 copies panel column j of each refilled
+    // stage and arrives on its full barrier with its own byte count
+    int pt = t0, psub = 0;
+    TileWin pw;
+    const int kk = threadIdx.x;
+    auto produce = [&](int slot) {  // block-uniform
+        while (pt < t1) {
+            seek_win<Field>(pw, wins, nwin, pt);
+            int r0, nrows;
+            tile_rows(pw, pt, r0, nrows);
+            if (psub * 32 >= nrows) {
+                ++pt;
+                psub = 0;
+                continue;
+            }
+            if (kk < 128) {
+                const int rs = r0 + 32 * psub, len = min(32, nrows - 32 * psub);
+                double* dst = ring + slot * (kRightStage / 8) + kk * kLdA;
+                long long st = 0;
+                int n = 0;
+                if (kk < pw.d)
+                    n = plan_segment(dst, M, (long long)rs + (long long)(pw.a + kk) * ldm, len, alloc, st);
+                mbar_expect_tx(&full[slot], (unsigned)n * 8u);
+                if (n > 0) bulk_copy(dst, M + st, (unsigned)n * 8u, &full[slot]);
+            }
+            ++psub;
+            return;
+        }
+    };
+    const int wi0 = window_of<Field>(wins, nwin, t0);
+    load_win<Field>(pw, wins, nwin, wi0);
+    for (int sl = 0; sl < kStages; ++sl) produce(sl);
+
+    const int gid = lane >> 2, tig = lane & 3;
+    double bf[2][32];
+    TileWin wd;
+    load_win<Field>(wd, wins, nwin, wi0);
+    int cur = -1, stage = 0;
+    unsigned phase = 0;
+    for (int t = t0; t < t1; ++t) {
+        seek_win<Field>(wd, wins, nwin, t);
+        const int d = wd.d;
+        if (wd.wi != cur) {  // B = Q_w: bf[nt][ks] = Q_w(k = 4ks + tig, n = 16 warp + 8 nt + gid)
+            const double* Qw = qw_pool + wd.qw_off;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                const int nn = 16 * warp + 8 * nt + gid;
+#pragma unroll
+                for (int ks = 0; ks < 32; ++ks) {
+                    const int k = 4 * ks + tig;
+                    bf[nt][ks] = (nn < d && k < d) ? __ldg(Qw + k + (long long)nn * d) : 0.0;
+                }
+            }
+            cur = wd.wi;
+        }
+        int r0, nrows;
+        tile_rows(wd, t, r0, nrows);
+        double* P = M + (long long)r0 + (long long)wd.a * ldm;
+        for (int sub = 0; 32 * sub < nrows; ++sub) {
+            double acc[4][2][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            // row 8 mt + gid, column k = 4 ks + tig (+ the sub-tile's shift)
+            const int shift = (int)(((long long)r0 + 32 * sub + (long long)wd.a * ldm) & 1);
+            const double* sa = ring + stage * (kRightStage / 8) + tig * kLdA + gid + shift;
+            mbar_wait(&full[stage], phase);
+#pragma unroll
+            for (int ks = 0; ks < 32; ++ks) {
+                double a[4];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) a[mt] = sa[4 * ks * kLdA + 8 * mt];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt][ks]);
+            }
+            __syncthreads();  // the stage is free
+            produce(stage);
+            if (++stage == kStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+#pragma unroll
+            for (int mt = 0; mt < 4; ++mt) {
+                const int r = 32 * sub + 8 * mt + gid;
+                if (r >= nrows) continue;
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt) {
+                    const int cc = 16 * warp + 8 * nt + 2 * tig;
+                    if (cc < d) P[r + (long long)cc * ldm] = acc[mt][nt][0];
+                    if (cc + 1 < d) P[r + (long long)(cc + 1) * ldm] = acc[mt][nt][1];
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+namespace {
+
+bool bulk_disabled() {
+    static const bool off = getenv("TEIG_NO_TMA") && atoi(getenv("TEIG_NO_TMA"));
+    return off;
+}
+
+constexpr size_t kLeftSmem = (size_t)kStages * kLeftStage;
+constexpr size_t kRightSmem = (size_t)kStages * kRightStage;
+
+// one CTA per SM while every CTA gets >= kMinTilesPerCta tiles
+int grid_for(int ntiles) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return std::max(1, std::min(sms, (ntiles + kMinTilesPerCta - 1) / kMinTilesPerCta));
+}
+
+bool bulk_eligible(int dmax, const double* base, long long ld, long long rows, long long cols) {
+    return !bulk_disabled() && dmax > 64 && dmax <= 128 && rows > 0 && cols > 0 && (ld % 2) == 0 &&
+           (reinterpret_cast<uintptr_t>(base) % 16) == 0 && kLeftBN == 64 && kRightBM == 64;
+}
+
+}  // namespace
+
+bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* S,
+                            long long lds, long long rows, long long cols, cudaStream_t stream, cudaError_t* err) {
+    *err = cudaSuccess;
+    if (ntiles <= 0) return true;
+    if (!bulk_eligible(dmax, S, lds, rows, cols)) return false;
+    static bool init = false;
+    if (!init) {
+        *err = cudaFuncSetAttribute(update_left_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kLeftSmem);
+        if (*err != cudaSuccess) return true;
+        init = true;
+    }
+    const int grid = grid_for(ntiles);
+    update_left_bulk_kernel<<<grid, kBulkThreads, kLeftSmem, stream>>>(wins, nwin, ntiles, qw_pool, S, lds,
+                                                                        (cols - 1) * lds + rows);
+    *err = cudaGetLastError();
+    return true;
+}
+
+bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* M,
+                             long long ldm, long long rows, long long cols, bool factor, cudaStream_t stream,
+                             cudaError_t* err) {
+    *err = cudaSuccess;
+    if (ntiles <= 0) return true;
+    if (!bulk_eligible(dmax, M, ldm, rows, cols)) return false;
+    static bool init = false;
+    if (!init) {
+        *err = cudaFuncSetAttribute(update_right_bulk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)kRightSmem);
+        if (*err == cudaSuccess)
+            *err = cudaFuncSetAttribute(update_right_bulk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)kRightSmem);
+        if (*err != cudaSuccess) return true;
+        init = true;
+    }
+    const int grid = grid_for(ntiles);
+    const long long alloc = (cols - 1) * ldm + rows;
+    if (factor)
+        update_right_bulk_kernel<2><<<grid, kBulkThreads, kRightSmem, stream>>>(wins, nwin, ntiles, qw_pool, M, ldm,
+                                                                                 alloc);
+    else
+        update_right_bulk_kernel<1><<<grid, kBulkThreads, kRightSmem, stream>>>(wins, nwin, ntiles, qw_pool, M, ldm,
+                                                                                 alloc);
+    *err = cudaGetLastError();
+    return true;
+}
+
+}  // namespace teig

@@ -1,6 +1,7 @@
 // FP64 tensor-core shapes on sm_100a: mma.sync m8n8k4 vs m16n8k4 / m16n8k8 /
 // m16n8k16 (.f64).  Register-only issue loops, independent chains.
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 template <int CHAINS>
@@ -98,6 +99,13 @@ void run(const char* name, K kern, double flop_per_mma, int chains, int sms) {
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    if (getenv("CHAIN_SWEEP")) {
+        run("m8n8k4 c1", m8n8k4<1>, 2.0 * 8 * 8 * 4, 1, sms);
+        run("m8n8k4 c2", m8n8k4<2>, 2.0 * 8 * 8 * 4, 2, sms);
+        run("m8n8k4 c4", m8n8k4<4>, 2.0 * 8 * 8 * 4, 4, sms);
+        run("m8n8k4 c8", m8n8k4<8>, 2.0 * 8 * 8 * 4, 8, sms);
+        return 0;
+    }
     run("m8n8k4", m8n8k4<8>, 2.0 * 8 * 8 * 4, 8, sms);
     run("m16n8k4", m16n8k4<8>, 2.0 * 16 * 8 * 4, 8, sms);
     run("m16n8k8", m16n8k8<8>, 2.0 * 16 * 8 * 8, 8, sms);
