@@ -12,10 +12,12 @@
 //    the CTA's tile range crosses into the next window;
 //  * the panel streams through a 4-stage shared-memory ring.  Every panel
 //    column segment is one cp.async.bulk (SASS UBLKCP: the TMA engine's 1-D
-//    copy) completing on a per-stage mbarrier; warp 0 refills a stage as soon
-//    as all 8 warps have released it (empty mbarrier), kStages sub-tiles
-//    ahead, so the copies of the next sub-tiles overlap the DMMAs of the
-//    current one and no thread waits on its own loads;
+//    copy) completing on the stage's mbarrier; right after the block barrier
+//    that ends a sub-tile, one thread per panel column (32 left, 128 right)
+//    refills the freed stage with the sub-tile kStages ahead and arrives on
+//    its barrier with its own byte count, so the copies of the next
+//    sub-tiles overlap the DMMAs of the current one (a single producer lane
+//    or warp measured 5-40 % slower: its copies serialise);
 //  * persistent grid (one CTA per SM, grid_for): each CTA walks one
 //    contiguous range of planner tiles
 //    (one or two windows as a rule), so the fragment loads and the pipeline
@@ -53,9 +55,11 @@ constexpr int kBulkThreads = kWarps * 32;  // 2 warps per SMSP: up to 255 regist
 constexpr int kStages = 4;
 constexpr int kMinTilesPerCta = 4;  // below this the launch gets more, shorter CTAs
 constexpr int kLdB = 132;        // left: doubles per panel column in smem (<= 129 rows used, = 4 mod 16)
-constexpr int kLdA = 40;         // right: doubles per panel column in smem (<= 33 rows used, = 8 mod 16)
+constexpr int kRSub = 64;        // right: rows per sub-tile (the whole planner tile)
+constexpr int kRStages = 3;      // right: ring depth
+constexpr int kLdA = 72;         // right: doubles per panel column in smem (<= kRSub+1 rows used, = 8 mod 16)
 constexpr int kLeftStage = 32 * kLdB * 8;    // 32 columns x 128(+1) rows
-constexpr int kRightStage = 128 * kLdA * 8;  // 128 columns x 32(+1) rows
+constexpr int kRightStage = 128 * kLdA * 8;  // 128 columns x kRSub(+1) rows
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -65,9 +69,6 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
     asm volatile(
@@ -154,27 +155,14 @@ __device__ __forceinline__ int plan_segment(double* dst, const double* base, lon
 // barriers + a zeroed ring (stale stage contents are then always finite
 // matrix values, so rows/columns beyond a window's order only ever meet zero
 // fragments)
-__device__ __forceinline__ void init_ring(uint64_t* full, uint64_t* empty, double* ring, int bytes,
-                                          unsigned full_count) {
+__device__ __forceinline__ void init_ring(uint64_t* full, double* ring, int bytes, unsigned full_count) {
     for (int i = threadIdx.x; i < bytes / 8; i += kBulkThreads) ring[i] = 0.0;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], full_count);
-            mbar_init(&empty[s], kWarps);
-        }
+        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], full_count);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the zeroes before any bulk write
     __syncthreads();
-}
-
-// warp 0, after its lanes' edge stores: one arrive carrying the stage's byte
-// count (release: orders the stores before the consumers' acquire)
-__device__ __forceinline__ void stage_arrive(uint64_t* bar, unsigned my_bytes) {
-    const unsigned total = __reduce_add_sync(0xffffffffu, my_bytes);
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_expect_tx(bar, total);
-    __syncwarp();
 }
 
 }  // namespace
@@ -186,16 +174,19 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, const double* __restrict__ qw_pool,
                         double* __restrict__ S, long long lds, long long alloc) {
     extern __shared__ __align__(128) double ring[];
-    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-    init_ring(full, empty, ring, kStages * kLeftStage, 1);
+    __shared__ __align__(8) uint64_t full[kStages];
+    init_ring(full, ring, kStages * kLeftStage, 32);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
     const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
 
-    // warp 0's position in the (tile, sub-tile) sequence it loads ahead
+    // every thread walks the (tile, sub-tile) sequence kStages ahead of the
+    // one it computes; thread j < 32 copies panel column j of each refilled
+    // stage and arrives on its full barrier with its own byte count
     int pt = t0, psub = 0;
     TileWin pw;
-    auto produce = [&](int slot) {  // warp-uniform; lane j copies column j
+    const int jj = threadIdx.x;
+    auto produce = [&](int slot) {  // block-uniform
         while (pt < t1) {
             seek_win<0>(pw, wins, nwin, pt);
             const int c = pw.r0 + (pt - pw.pref) * kLeftBN;
@@ -205,23 +196,23 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
                 psub = 0;
                 continue;
             }
-            double* dst = ring + slot * (kLeftStage / 8) + lane * kLdB;
-            long long start = 0;
-            int n = 0;
-            if (32 * psub + lane < ncols)
-                n = plan_segment(dst, S, (long long)pw.a + (long long)(c + 32 * psub + lane) * lds, pw.d, alloc,
-                                 start);
-            stage_arrive(&full[slot], (unsigned)n * 8u);
-            if (n > 0) bulk_copy(dst, S + start, (unsigned)n * 8u, &full[slot]);
+            if (jj < 32) {
+                double* dst = ring + slot * (kLeftStage / 8) + jj * kLdB;
+                long long start = 0;
+                int n = 0;
+                if (32 * psub + jj < ncols)
+                    n = plan_segment(dst, S, (long long)pw.a + (long long)(c + 32 * psub + jj) * lds, pw.d, alloc,
+                                     start);
+                mbar_expect_tx(&full[slot], (unsigned)n * 8u);
+                if (n > 0) bulk_copy(dst, S + start, (unsigned)n * 8u, &full[slot]);
+            }
             ++psub;
             return;
         }
     };
     const int wi0 = window_of<0>(wins, nwin, t0);
-    if (warp == 0) {
-        load_win<0>(pw, wins, nwin, wi0);
-        for (int sl = 0; sl < kStages; ++sl) produce(sl);
-    }
+    load_win<0>(pw, wins, nwin, wi0);
+    for (int sl = 0; sl < kStages; ++sl) produce(sl);
 
     const int gid = lane >> 2, tig = lane & 3;
     double af[2][32];
@@ -268,12 +259,8 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
 #pragma unroll
                     for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][ks], bf[nt]);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
-            if (warp == 0) {
-                mbar_wait(&empty[stage], phase);
-                produce(stage);
-            }
+            __syncthreads();  // the stage is free
+            produce(stage);
             if (++stage == kStages) {
                 stage = 0;
                 phase ^= 1u;
@@ -294,15 +281,17 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
 }
 
 // ---------------------------------------------------------------------------
-// RIGHT: M[r0:r0+64, a:a+d] <- M[r0:r0+64, a:a+d] Q_w, as two 32-row
-// sub-tiles; warp w owns output columns [16w, 16w+16).
+// RIGHT: M[r0:r0+64, a:a+d] <- M[r0:r0+64, a:a+d] Q_w, in kRSub-row
+// sub-tiles; warp w owns output columns [16w, 16w+16).  (64-row sub-tiles:
+// the 128 column copies of a stage are 512 bytes each -- 32-row stages of
+// 256-byte copies left the ring starved, the TMA engine's per-copy cost.)
 template <int Field>
 __global__ void __launch_bounds__(kBulkThreads, 1)
 update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, const double* __restrict__ qw_pool,
                          double* __restrict__ M, long long ldm, long long alloc) {
     extern __shared__ __align__(128) double ring[];
-    __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
-    init_ring(full, empty, ring, kStages * kRightStage, 128);
+    __shared__ __align__(8) uint64_t full[kRStages];
+    init_ring(full, ring, kRStages * kRightStage, 128);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
     const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
@@ -322,13 +311,13 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
             seek_win<Field>(pw, wins, nwin, pt);
             int r0, nrows;
             tile_rows(pw, pt, r0, nrows);
-            if (psub * 32 >= nrows) {
+            if (psub * kRSub >= nrows) {
                 ++pt;
                 psub = 0;
                 continue;
             }
             if (kk < 128) {
-                const int rs = r0 + 32 * psub, len = min(32, nrows - 32 * psub);
+                const int rs = r0 + kRSub * psub, len = min(kRSub, nrows - kRSub * psub);
                 double* dst = ring + slot * (kRightStage / 8) + kk * kLdA;
                 long long st = 0;
                 int n = 0;
@@ -343,7 +332,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
     };
     const int wi0 = window_of<Field>(wins, nwin, t0);
     load_win<Field>(pw, wins, nwin, wi0);
-    for (int sl = 0; sl < kStages; ++sl) produce(sl);
+    for (int sl = 0; sl < kRStages; ++sl) produce(sl);
 
     const int gid = lane >> 2, tig = lane & 3;
     double bf[2][32];
@@ -370,35 +359,35 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
         int r0, nrows;
         tile_rows(wd, t, r0, nrows);
         double* P = M + (long long)r0 + (long long)wd.a * ldm;
-        for (int sub = 0; 32 * sub < nrows; ++sub) {
-            double acc[4][2][2];
+        for (int sub = 0; kRSub * sub < nrows; ++sub) {
+            double acc[kRSub / 8][2][2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < kRSub / 8; ++i)
 #pragma unroll
                 for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
             // row 8 mt + gid, column k = 4 ks + tig (+ the sub-tile's shift)
-            const int shift = (int)(((long long)r0 + 32 * sub + (long long)wd.a * ldm) & 1);
+            const int shift = (int)(((long long)r0 + kRSub * sub + (long long)wd.a * ldm) & 1);
             const double* sa = ring + stage * (kRightStage / 8) + tig * kLdA + gid + shift;
             mbar_wait(&full[stage], phase);
 #pragma unroll
             for (int ks = 0; ks < 32; ++ks) {
-                double a[4];
+                double a[kRSub / 8];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) a[mt] = sa[4 * ks * kLdA + 8 * mt];
+                for (int mt = 0; mt < kRSub / 8; ++mt) a[mt] = sa[4 * ks * kLdA + 8 * mt];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt)
+                for (int mt = 0; mt < kRSub / 8; ++mt)
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt][ks]);
             }
             __syncthreads();  // the stage is free
             produce(stage);
-            if (++stage == kStages) {
+            if (++stage == kRStages) {
                 stage = 0;
                 phase ^= 1u;
             }
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt) {
-                const int r = 32 * sub + 8 * mt + gid;
+            for (int mt = 0; mt < kRSub / 8; ++mt) {
+                const int r = kRSub * sub + 8 * mt + gid;
                 if (r >= nrows) continue;
 #pragma unroll
                 for (int nt = 0; nt < 2; ++nt) {
@@ -422,7 +411,7 @@ bool bulk_disabled() {
 }
 
 constexpr size_t kLeftSmem = (size_t)kStages * kLeftStage;
-constexpr size_t kRightSmem = (size_t)kStages * kRightStage;
+constexpr size_t kRightSmem = (size_t)kRStages * kRightStage;
 
 // one CTA per SM while every CTA gets >= kMinTilesPerCta tiles
 int grid_for(int ntiles) {
