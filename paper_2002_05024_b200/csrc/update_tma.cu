@@ -10,11 +10,11 @@
 //    Q_w^T) or 16-column (right: Q_w) slice for the whole K = 128 extent as
 //    m8n8k4 fragments in registers (64 doubles per lane), reloaded only when
 //    the CTA's tile range crosses into the next window;
-//  * the panel streams through a 4-stage shared-memory ring.  Every panel
+//  * the panel streams through a 3-stage shared-memory ring.  Every panel
 //    column segment is one cp.async.bulk (SASS UBLKCP: the TMA engine's 1-D
 //    copy) completing on the stage's mbarrier; right after the block barrier
 //    that ends a sub-tile, one thread per panel column (32 left, 128 right)
-//    refills the freed stage with the sub-tile kStages ahead and arrives on
+//    refills the freed stage with the sub-tile a ring depth ahead and arrives on
 //    its barrier with its own byte count, so the copies of the next
 //    sub-tiles overlap the DMMAs of the current one (a single producer lane
 //    or warp measured 5-40 % slower: its copies serialise);
@@ -52,13 +52,17 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kBulkThreads = kWarps * 32;  // 2 warps per SMSP: up to 255 registers each
-constexpr int kStages = 4;
 constexpr int kMinTilesPerCta = 4;  // below this the launch gets more, shorter CTAs
+#ifndef TEIG_LSUB
+#define TEIG_LSUB 64
+#endif
+constexpr int kLSub = TEIG_LSUB;                // left: columns per sub-tile
+constexpr int kLStages = kLSub == 64 ? 3 : 4;   // left: ring depth
 constexpr int kLdB = 132;        // left: doubles per panel column in smem (<= 129 rows used, = 4 mod 16)
 constexpr int kRSub = 64;        // right: rows per sub-tile (the whole planner tile)
 constexpr int kRStages = 3;      // right: ring depth
 constexpr int kLdA = 72;         // right: doubles per panel column in smem (<= kRSub+1 rows used, = 8 mod 16)
-constexpr int kLeftStage = 32 * kLdB * 8;    // 32 columns x 128(+1) rows
+constexpr int kLeftStage = kLSub * kLdB * 8;  // kLSub columns x 128(+1) rows
 constexpr int kRightStage = 128 * kLdA * 8;  // 128 columns x kRSub(+1) rows
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -155,10 +159,10 @@ __device__ __forceinline__ int plan_segment(double* dst, const double* base, lon
 // barriers + a zeroed ring (stale stage contents are then always finite
 // matrix values, so rows/columns beyond a window's order only ever meet zero
 // fragments)
-__device__ __forceinline__ void init_ring(uint64_t* full, double* ring, int bytes, unsigned full_count) {
+__device__ __forceinline__ void init_ring(uint64_t* full, int nstages, double* ring, int bytes, unsigned full_count) {
     for (int i = threadIdx.x; i < bytes / 8; i += kBulkThreads) ring[i] = 0.0;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) mbar_init(&full[s], full_count);
+        for (int s = 0; s < nstages; ++s) mbar_init(&full[s], full_count);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // the zeroes before any bulk write
@@ -168,20 +172,20 @@ __device__ __forceinline__ void init_ring(uint64_t* full, double* ring, int byte
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// LEFT: S[a:a+d, c:c+64] <- Q_w^T S[a:a+d, c:c+64], as two 32-column
+// LEFT: S[a:a+d, c:c+64] <- Q_w^T S[a:a+d, c:c+64], in kLSub-column
 // sub-tiles; warp w owns output rows [16w, 16w+16).
 __global__ void __launch_bounds__(kBulkThreads, 1)
 update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, const double* __restrict__ qw_pool,
                         double* __restrict__ S, long long lds, long long alloc) {
     extern __shared__ __align__(128) double ring[];
-    __shared__ __align__(8) uint64_t full[kStages];
-    init_ring(full, ring, kStages * kLeftStage, 32);
+    __shared__ __align__(8) uint64_t full[kLStages];
+    init_ring(full, kLStages, ring, kLStages * kLeftStage, kLSub);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
     const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
 
-    // every thread walks the (tile, sub-tile) sequence kStages ahead of the
-    // one it computes; thread j < 32 copies panel column j of each refilled
+    // every thread walks the (tile, sub-tile) sequence a ring depth ahead of the
+    // one it computes; thread j < kLSub copies panel column j of each refilled
     // stage and arrives on its full barrier with its own byte count
     int pt = t0, psub = 0;
     TileWin pw;
@@ -191,17 +195,17 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
             seek_win<0>(pw, wins, nwin, pt);
             const int c = pw.r0 + (pt - pw.pref) * kLeftBN;
             const int ncols = min(kLeftBN, pw.r1 - c);
-            if (psub * 32 >= ncols) {
+            if (psub * kLSub >= ncols) {
                 ++pt;
                 psub = 0;
                 continue;
             }
-            if (jj < 32) {
+            if (jj < kLSub) {
                 double* dst = ring + slot * (kLeftStage / 8) + jj * kLdB;
                 long long start = 0;
                 int n = 0;
-                if (32 * psub + jj < ncols)
-                    n = plan_segment(dst, S, (long long)pw.a + (long long)(c + 32 * psub + jj) * lds, pw.d, alloc,
+                if (kLSub * psub + jj < ncols)
+                    n = plan_segment(dst, S, (long long)pw.a + (long long)(c + kLSub * psub + jj) * lds, pw.d, alloc,
                                      start);
                 mbar_expect_tx(&full[slot], (unsigned)n * 8u);
                 if (n > 0) bulk_copy(dst, S + start, (unsigned)n * 8u, &full[slot]);
@@ -212,7 +216,7 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
     };
     const int wi0 = window_of<0>(wins, nwin, t0);
     load_win<0>(pw, wins, nwin, wi0);
-    for (int sl = 0; sl < kStages; ++sl) produce(sl);
+    for (int sl = 0; sl < kLStages; ++sl) produce(sl);
 
     const int gid = lane >> 2, tig = lane & 3;
     double af[2][32];
@@ -239,29 +243,29 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
         const int c = wd.r0 + (t - wd.pref) * kLeftBN;
         const int ncols = min(kLeftBN, wd.r1 - c);
         double* P = S + (long long)wd.a + (long long)c * lds;
-        for (int sub = 0; 32 * sub < ncols; ++sub) {
-            double acc[2][4][2];
+        for (int sub = 0; kLSub * sub < ncols; ++sub) {
+            double acc[2][kLSub / 8][2];
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+                for (int j = 0; j < kLSub / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
             // column 8 nt + gid, row k = 4 ks + tig (+ the sub-tile's shift)
-            const int shift = (int)(((long long)wd.a + (long long)(c + 32 * sub) * lds) & 1);
+            const int shift = (int)(((long long)wd.a + (long long)(c + kLSub * sub) * lds) & 1);
             const double* sb = ring + stage * (kLeftStage / 8) + gid * kLdB + tig + shift;
             mbar_wait(&full[stage], phase);
 #pragma unroll
             for (int ks = 0; ks < 32; ++ks) {
-                double bf[4];
+                double bf[kLSub / 8];
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) bf[nt] = sb[nt * 8 * kLdB + 4 * ks];
+                for (int nt = 0; nt < kLSub / 8; ++nt) bf[nt] = sb[nt * 8 * kLdB + 4 * ks];
 #pragma unroll
                 for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][ks], bf[nt]);
+                    for (int nt = 0; nt < kLSub / 8; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][ks], bf[nt]);
             }
             __syncthreads();  // the stage is free
             produce(stage);
-            if (++stage == kStages) {
+            if (++stage == kLStages) {
                 stage = 0;
                 phase ^= 1u;
             }
@@ -270,8 +274,8 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
                 const int r = 16 * warp + 8 * mt + gid;
                 if (r >= d) continue;
 #pragma unroll
-                for (int nt = 0; nt < 4; ++nt) {
-                    const int cc = 32 * sub + 8 * nt + 2 * tig;
+                for (int nt = 0; nt < kLSub / 8; ++nt) {
+                    const int cc = kLSub * sub + 8 * nt + 2 * tig;
                     if (cc < ncols) P[r + (long long)cc * lds] = acc[mt][nt][0];
                     if (cc + 1 < ncols) P[r + (long long)(cc + 1) * lds] = acc[mt][nt][1];
                 }
@@ -291,7 +295,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
                          double* __restrict__ M, long long ldm, long long alloc) {
     extern __shared__ __align__(128) double ring[];
     __shared__ __align__(8) uint64_t full[kRStages];
-    init_ring(full, ring, kRStages * kRightStage, 128);
+    init_ring(full, kRStages, ring, kRStages * kRightStage, 128);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
     const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
@@ -300,7 +304,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
         nrows = min(kRightBM, w.r1 - r0);
     };
 
-    // every thread walks the (tile, sub-tile) sequence kStages ahead of the
+    // every thread walks the (tile, sub-tile) sequence a ring depth ahead of the
     // one it computes; thread j < 128 copies panel column j of each refilled
     // stage and arrives on its full barrier with its own byte count
     int pt = t0, psub = 0;
@@ -410,7 +414,7 @@ bool bulk_disabled() {
     return off;
 }
 
-constexpr size_t kLeftSmem = (size_t)kStages * kLeftStage;
+constexpr size_t kLeftSmem = (size_t)kLStages * kLeftStage;
 constexpr size_t kRightSmem = (size_t)kRStages * kRightStage;
 
 // one CTA per SM while every CTA gets >= kMinTilesPerCta tiles
