@@ -230,7 +230,7 @@ def run_ours(args, rank, world, local):
             "peak_source": "FP64 DMMA.8x8x4 issue peak measured on this pool's B200 "
                            "(tools/microbench/fp64_peak.cu, profiles/r01_fp64_peak.txt); "
                            "MEASURED_PEAKS.json has no FP64 entry",
-            "traffic": None,
+            "traffic": measured_traffic(),
             "aggregate": {"achieved": round(info["update_flops"] / (ms_step * 1e-3) / 1e12, 3),
                           "frac": round(info["update_flops"] / (ms_step * 1e-3) / 1e12 / FP64_DMMA_PEAK_TFLOPS, 4),
                           "note": "update flops / step time: the Q-factor updates run on a second stream, "
@@ -292,6 +292,21 @@ def run_ours(args, rank, world, local):
 
 def workload_name(n):
     return {10000: "C2", 40000: "C4"}.get(n, "reorder")
+
+
+def measured_traffic():
+    """DRAM bytes of one captured launch of the dominant kernel (ncu --set full,
+    profiles/r02_traffic.json) -- per launch, next to that launch's algorithmic
+    bytes; None when the capture file is absent."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None
+    return {"dram_bytes_per_launch": t["dram_bytes"], "algorithmic_bytes_per_launch": t["algorithmic_bytes"],
+            "ratio": round(t["dram_bytes"] / t["algorithmic_bytes"], 3), "launch": f'{t["kernel"]}, {t["launch"]}',
+            "source": t["source"]}
 
 
 def e2e_reorder(T, S0, S_dev_result, sel, opts, n, steps):

@@ -222,8 +222,14 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         ++launches;
         if (lg.on) lg.spans[cls].push_back({e0, lg.record(st)});
     };
+    // TEIG_LAUNCH_LOG=1: per-level tile counts on stderr (to pair ncu launch
+    // indices with algorithmic bytes / flops)
+    const bool launch_log = getenv("TEIG_LAUNCH_LOG") && atoi(getenv("TEIG_LAUNCH_LOG"));
     for (int L = 0; L < nl; ++L) {
         const int64_t o = lvl_off[L], cnt = lvl_off[L + 1] - lvl_off[L];
+        if (launch_log)
+            fprintf(stderr, "[teig level] %d windows %lld left_tiles %lld right_tiles %lld factor_tiles %lld\n", L,
+                    (long long)cnt, (long long)tl[L], (long long)tr[L], (long long)tq[L]);
         timed(0, stream, cnt, [&] {
             return launch_window_reorder(dd + o, (int)cnt, dmax_k, dS, lds, d_qw.as<double>(), d_sizes.as<uint8_t>(),
                                          d_sel.as<uint8_t>(), d_order.as<uint8_t>(), d_stuck.as<uint8_t>(),
