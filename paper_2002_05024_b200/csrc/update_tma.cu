@@ -94,6 +94,35 @@ __device__ __forceinline__ void bulk_copy(void* dst, const void* src, unsigned b
         : "memory");
 }
 
+// 1-D bulk copy shared -> global (bulk-group completion)
+__device__ __forceinline__ void bulk_store(void* gdst, const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                     reinterpret_cast<uint64_t>(gdst)),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
+// one output column segment: global g[0..len) <- sm[0..len) (sm = the stage
+// column + the segment's shift).  The 16-byte aligned interior goes as one
+// bulk store; an odd first / last element is stored by the thread itself (a
+// padded bulk store would overwrite a neighbour's element).
+__device__ __forceinline__ void store_column(double* g, const double* sm, int shift, int len) {
+    int j0 = 0;
+    if (shift && len > 0) {
+        g[0] = sm[0];
+        j0 = 1;
+    }
+    const int cnt = len - j0, nb = cnt & ~1;
+    if (nb > 0) bulk_store(g + j0, sm + j0, (unsigned)nb * 8u);
+    if (cnt & 1) g[len - 1] = sm[len - 1];
+}
+
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
@@ -222,7 +251,7 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
     double af[2][32];
     TileWin wd;
     load_win<0>(wd, wins, nwin, wi0);
-    int cur = -1, stage = 0;
+    int cur = -1, stage = 0, prev = -1;
     unsigned phase = 0;
     for (int t = t0; t < t1; ++t) {
         seek_win<0>(wd, wins, nwin, t);
@@ -263,25 +292,39 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
 #pragma unroll
                     for (int nt = 0; nt < kLSub / 8; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][ks], bf[nt]);
             }
-            __syncthreads();  // the stage is free
-            produce(stage);
+            // epilogue through the consumed stage: accumulators to smem at the
+            // inputs' positions, then one bulk store per column (async: the
+            // warps go on to the next sub-tile while the TMA engine writes)
+            __syncthreads();  // every warp is done reading the stage
+            double* so = ring + stage * (kLeftStage / 8) + shift;
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const int r = 16 * warp + 8 * mt + gid;
+#pragma unroll
+                for (int nt = 0; nt < kLSub / 8; ++nt) {
+                    const int cc = 8 * nt + 2 * tig;
+                    so[cc * kLdB + r] = acc[mt][nt][0];
+                    so[(cc + 1) * kLdB + r] = acc[mt][nt][1];
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncthreads();
+            if (jj < kLSub && kLSub * sub + jj < ncols)
+                store_column(P + (long long)(kLSub * sub + jj) * lds, so + jj * kLdB, shift, d);
+            bulk_commit();
+            // refill the stage of the previous sub-tile (its stores went out
+            // one sub-tile ago) with the sub-tile a ring depth after it
+            if (prev >= 0) {
+                bulk_wait_read<1>();
+                produce(prev);
+            }
+            prev = stage;
             if (++stage == kLStages) {
                 stage = 0;
                 phase ^= 1u;
             }
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-                const int r = 16 * warp + 8 * mt + gid;
-                if (r >= d) continue;
-#pragma unroll
-                for (int nt = 0; nt < kLSub / 8; ++nt) {
-                    const int cc = kLSub * sub + 8 * nt + 2 * tig;
-                    if (cc < ncols) P[r + (long long)cc * lds] = acc[mt][nt][0];
-                    if (cc + 1 < ncols) P[r + (long long)(cc + 1) * lds] = acc[mt][nt][1];
-                }
-            }
         }
-    }
+    }    bulk_wait_all();  // the last stores land before the CTA retires
 }
 
 // ---------------------------------------------------------------------------
@@ -383,6 +426,9 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
 #pragma unroll
                     for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt][ks]);
             }
+            // direct stores: with a 3-deep ring of 64-row stages the staged
+            // (bulk-store) epilogue of the left kernel delays the refill by one
+            // sub-tile and measured 2-3 % slower here
             __syncthreads();  // the stage is free
             produce(stage);
             if (++stage == kRStages) {
