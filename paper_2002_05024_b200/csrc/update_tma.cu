@@ -14,8 +14,8 @@
 //    column segment is one cp.async.bulk (SASS UBLKCP: the TMA engine's 1-D
 //    copy) completing on the stage's mbarrier; right after the block barrier
 //    that ends a sub-tile, one thread per panel column (32 left, 128 right)
-//    refills the freed stage with the sub-tile a ring depth ahead and arrives on
-//    its barrier with its own byte count, so the copies of the next
+//    refills the freed stage with the sub-tile a ring depth ahead (one arrival
+//    per producing warp carrying its bytes), so the copies of the next
 //    sub-tiles overlap the DMMAs of the current one (a single producer lane
 //    or warp measured 5-40 % slower: its copies serialise);
 //  * persistent grid (one CTA per SM, grid_for): each CTA walks one
@@ -169,6 +169,14 @@ __device__ __forceinline__ void seek_win(TileWin& tw, const WinDesc* wins, int n
     while (t >= tw.next_pref) load_win<Field>(tw, wins, nwin, tw.wi + 1);
 }
 
+// one arrival per producing warp carrying the warp's bytes (after the lanes'
+// edge stores; 128 single-thread arrivals on one mbarrier serialise)
+__device__ __forceinline__ void warp_arrive(uint64_t* bar, unsigned my_bytes) {
+    const unsigned total = __reduce_add_sync(0xffffffffu, my_bytes);
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_expect_tx(bar, total);
+}
+
 // the copy of one column segment: `len` elements from element offset `off`
 // of `base` into dst, as a 16-byte aligned bulk copy starting at off - shift.
 // Returns the bulk doubles to copy (the edge element, if any, is stored here).
@@ -208,7 +216,7 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
                         double* __restrict__ S, long long lds, long long alloc) {
     extern __shared__ __align__(128) double ring[];
     __shared__ __align__(8) uint64_t full[kLStages];
-    init_ring(full, kLStages, ring, kLStages * kLeftStage, kLSub);
+    init_ring(full, kLStages, ring, kLStages * kLeftStage, kLSub / 32);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
     const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
@@ -236,7 +244,7 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
                 if (kLSub * psub + jj < ncols)
                     n = plan_segment(dst, S, (long long)pw.a + (long long)(c + kLSub * psub + jj) * lds, pw.d, alloc,
                                      start);
-                mbar_expect_tx(&full[slot], (unsigned)n * 8u);
+                warp_arrive(&full[slot], (unsigned)n * 8u);
                 if (n > 0) bulk_copy(dst, S + start, (unsigned)n * 8u, &full[slot]);
             }
             ++psub;
@@ -338,7 +346,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
                          double* __restrict__ M, long long ldm, long long alloc) {
     extern __shared__ __align__(128) double ring[];
     __shared__ __align__(8) uint64_t full[kRStages];
-    init_ring(full, kRStages, ring, kRStages * kRightStage, 128);
+    init_ring(full, kRStages, ring, kRStages * kRightStage, 128 / 32);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
     const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
@@ -370,7 +378,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
                 int n = 0;
                 if (kk < pw.d)
                     n = plan_segment(dst, M, (long long)rs + (long long)(pw.a + kk) * ldm, len, alloc, st);
-                mbar_expect_tx(&full[slot], (unsigned)n * 8u);
+                warp_arrive(&full[slot], (unsigned)n * 8u);
                 if (n > 0) bulk_copy(dst, M + st, (unsigned)n * 8u, &full[slot]);
             }
             ++psub;
