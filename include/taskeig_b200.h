@@ -99,6 +99,11 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
                             int64_t* plan, int64_t plan_cap, teig_reorder_info* info,
                             void* stream);
 
+/* The host entry points keep their device staging (2 n^2 doubles for the
+ * largest call so far) between calls; this returns it to the device.  Not
+ * part of the reference interface (the reference has no device memory). */
+void teig_release_host_staging(void);
+
 /* Diagonal-block scan by exact-zero subdiagonal (reorder.cpp:21-43) on a
  * device matrix.  sizes: host array of capacity n.  Returns nb (>= 0). */
 int64_t teig_scan_blocks_device(int64_t n, const double* dS, int64_t lds, uint8_t* sizes,

@@ -75,6 +75,7 @@ SIGNATURES = {
     "teig_reorder_opts_default": (None, [_P]),
     "teig_reorder_schur_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P,
                                             _I64, _P, _P]),
+    "teig_release_host_staging": (None, []),
     "teig_reorder_schur_host": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P,
                                           _I64, _P, _P]),
     "teig_scan_blocks_device": (C.c_int64, [_I64, _P, _I64, _P, _P]),

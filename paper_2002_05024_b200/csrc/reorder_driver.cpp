@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -118,6 +119,24 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
+// Device staging of the host entry points: kept between calls (the host path
+// of a 40000-order problem stages 25.6 GB; mapping it anew every call cost
+// 0.14-0.95 s and slowed the first kernels that touched it).  One cache per
+// process, grown on demand, guarded for concurrent host calls; the
+// TEIG_NO_HOST_CACHE=1 environment variable allocates per call instead.
+struct HostStaging {
+    std::mutex mu;
+    void* p = nullptr;
+    size_t bytes = 0;
+    ~HostStaging() {
+        if (p) cudaFree(p);
+    }
+};
+HostStaging& host_staging() {
+    static HostStaging hs;
+    return hs;
+}
+
 struct PassResult {
     int64_t windows = 0, levels = 0, launches = 0;
     bool deviated = false;
@@ -150,11 +169,31 @@ struct EventLog {
     }
 };
 
+// Host entry point only: device -> host copies of the parts of S and Q that
+// no later level touches, issued on a copy stream while the remaining levels
+// run.  A window [a, b) writes S rows [0, b) only (window block, left panel
+// rows, right panel rows above) and Q columns [a, b) only, so after level L
+// the S rows >= max b and the Q columns outside [min a, max b) of the levels
+// after L are final.  s_hi: S rows [s_hi, n) copied; Q columns [0, q_lo) and
+// [q_hi, n) copied.  A replanning pass invalidates the early copies (the
+// final copy then moves everything).
+struct HostDrain {
+    double* hS = nullptr;
+    int64_t lds = 0;
+    double* hQ = nullptr;
+    int64_t ldq = 0;
+    cudaStream_t ds = nullptr;
+    cudaEvent_t evS = nullptr, evQ = nullptr;
+    int64_t s_hi = 0, q_lo = 0, q_hi = 0;
+    bool valid = true;
+    int64_t min_chunk = 512;
+};
+
 // Executes one planned pass on the device and folds the outcomes into `blocks`.
 PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq,
                     std::vector<BlockState>& blocks, std::vector<int64_t>& rejected,
                     std::vector<int64_t>& plan_log, bool strict, bool overlap, bool profile,
-                    cudaStream_t stream, cudaStream_t stream2, cudaEvent_t ev) {
+                    cudaStream_t stream, cudaStream_t stream2, cudaEvent_t ev, HostDrain* drain = nullptr) {
     PassResult pr;
     EventLog lg;
     lg.on = profile;
@@ -199,6 +238,20 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     }
     for (int L = 0; L < nl; ++L) lvl_off[L + 1] += lvl_off[L];
     const int dmax_k = dmax <= 64 ? 64 : 128;
+    // early host drain: max b / min a over the levels after L
+    std::vector<int64_t> after_hi, after_lo;
+    if (drain && drain->valid) {
+        after_hi.assign(nl + 1, 0);
+        after_lo.assign(nl + 1, n);
+        for (int L = nl - 1; L >= 0; --L) {
+            after_hi[L] = after_hi[L + 1];
+            after_lo[L] = after_lo[L + 1];
+            for (int64_t k = lvl_off[L]; k < lvl_off[L + 1]; ++k) {
+                after_hi[L] = std::max<int64_t>(after_hi[L], descs[k].a + descs[k].d);
+                after_lo[L] = std::min<int64_t>(after_lo[L], descs[k].a);
+            }
+        }
+    }
 
     const size_t ne = plan.sizes.size();
     DevBuf d_desc(sizeof(WinDesc) * nw, stream), d_qw(sizeof(double) * std::max<int64_t>(qw_total, 1), stream),
@@ -257,6 +310,36 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                 return launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
                                            true, stream, n, n);
             });
+        if (drain && drain->valid && L + 1 < nl) {
+            const int64_t hi = after_hi[L + 1], lo = after_lo[L + 1];
+            if (drain->s_hi - hi >= drain->min_chunk) {  // S rows [hi, s_hi): final after this level's S work
+                TEIG_CUDA(cudaEventRecord(drain->evS, stream));
+                TEIG_CUDA(cudaStreamWaitEvent(drain->ds, drain->evS, 0));
+                TEIG_CUDA(cudaMemcpy2DAsync(drain->hS + hi, drain->lds * sizeof(double), dS + hi, lds * sizeof(double),
+                                            (size_t)(drain->s_hi - hi) * sizeof(double), (size_t)n,
+                                            cudaMemcpyDeviceToHost, drain->ds));
+                drain->s_hi = hi;
+            }
+            if (dQ && drain->hQ &&
+                (drain->q_hi - hi >= drain->min_chunk || lo - drain->q_lo >= drain->min_chunk)) {
+                TEIG_CUDA(cudaEventRecord(drain->evQ, overlap ? stream2 : stream));
+                TEIG_CUDA(cudaStreamWaitEvent(drain->ds, drain->evQ, 0));
+                auto cols = [&](int64_t c0, int64_t c1) {
+                    if (c1 > c0)
+                        TEIG_CUDA(cudaMemcpy2DAsync(drain->hQ + c0 * drain->ldq, drain->ldq * sizeof(double),
+                                                    dQ + c0 * ldq, ldq * sizeof(double), (size_t)n * sizeof(double),
+                                                    (size_t)(c1 - c0), cudaMemcpyDeviceToHost, drain->ds));
+                };
+                if (drain->q_hi - hi >= drain->min_chunk) {
+                    cols(hi, drain->q_hi);
+                    drain->q_hi = hi;
+                }
+                if (lo - drain->q_lo >= drain->min_chunk) {
+                    cols(drain->q_lo, lo);
+                    drain->q_lo = lo;
+                }
+            }
+        }
     }
     if (dQ && overlap) {
         TEIG_CUDA(cudaEventRecord(ev, stream2));
@@ -323,7 +406,8 @@ struct StreamPair {
 int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq, int64_t nb,
                          const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
                          int64_t* perm, int64_t* rejected_out, int64_t* plan_out, int64_t plan_cap,
-                         teig_reorder_info* info, cudaStream_t stream, cudaEvent_t q_ready = nullptr) {
+                         teig_reorder_info* info, cudaStream_t stream, cudaEvent_t q_ready = nullptr,
+                         HostDrain* drain = nullptr) {
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (!dS) return set_error(-2, "S is null");
     if (lds < n) return set_error(-3, "lds < n");
@@ -369,7 +453,8 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
                 if (dQ) inf.flops_factor += 2.0 * d * d * double(n);
             }
             PassResult pr = run_pass(plan, n, dS, lds, dQ, ldq, blocks, rejected, plan_log, o.strict != 0,
-                                     o.overlap_factor != 0, o.profile != 0, stream, sp.s2, sp.ev);
+                                     o.overlap_factor != 0, o.profile != 0, stream, sp.s2, sp.ev,
+                                     pass == 0 ? drain : nullptr);
             inf.n_windows += pr.windows;
             inf.n_levels += pr.levels;
             inf.n_launches += pr.launches;
@@ -379,6 +464,7 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
             inf.ms_factor += pr.ms_factor;
             inf.n_passes += 1;
             if (!pr.deviated) break;
+            if (drain) drain->valid = false;  // a replanning pass rewrites anything
         }
         inf.plan_ms = plan_ms;
     } catch (const std::domain_error& e) {
@@ -436,6 +522,14 @@ int teig_reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, in
                                 (cudaStream_t)stream);
 }
 
+void teig_release_host_staging(void) {
+    HostStaging& hs = host_staging();
+    std::lock_guard<std::mutex> g(hs.mu);
+    if (hs.p) cudaFree(hs.p);
+    hs.p = nullptr;
+    hs.bytes = 0;
+}
+
 int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_t ldq, int64_t nb,
                             const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
                             int64_t* perm, int64_t* rejected, int64_t* plan, int64_t plan_cap,
@@ -447,32 +541,119 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
     cudaStream_t stream = (cudaStream_t)stream_v;
     cudaStream_t qs = nullptr;
     cudaEvent_t q_ready = nullptr;
+    const bool hprof = getenv("TEIG_HOST_PROF") && atoi(getenv("TEIG_HOST_PROF"));
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    const auto h0 = now();
+    const bool no_cache = getenv("TEIG_NO_HOST_CACHE") && atoi(getenv("TEIG_NO_HOST_CACHE"));
+    HostStaging& hs = host_staging();
+    std::unique_lock<std::mutex> lock(hs.mu, std::defer_lock);
     try {
         const size_t pitch = (size_t)n * sizeof(double);
-        DevBuf dS(pitch * n, stream), dQ(Q ? pitch * n : 0, stream);
-        TEIG_CUDA(cudaStreamSynchronize(stream));  // allocations visible to the side stream
-        TEIG_CUDA(cudaMemcpy2DAsync(dS.p, pitch, S, lds * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
+        const size_t need = pitch * n * (Q ? 2 : 1);
+        struct Plain {  // per-call staging (cudaFree synchronizes)
+            void* p = nullptr;
+            ~Plain() {
+                if (p) cudaFree(p);
+            }
+        } tmp;
+        double* base = nullptr;
+        if (no_cache) {
+            TEIG_CUDA(cudaMalloc(&tmp.p, need));
+            base = static_cast<double*>(tmp.p);
+        } else {
+            lock.lock();
+            if (hs.bytes < need) {
+                if (hs.p) TEIG_CUDA(cudaFree(hs.p));
+                hs.p = nullptr;
+                hs.bytes = 0;
+                TEIG_CUDA(cudaMalloc(&hs.p, need));
+                hs.bytes = need;
+            }
+            base = static_cast<double*>(hs.p);
+        }
+        double* const dS = base;
+        double* const dQ = Q ? base + (size_t)n * n : nullptr;
+        TEIG_CUDA(cudaStreamSynchronize(stream));  // staging visible to the side stream
+        const auto h1 = now();
+        TEIG_CUDA(cudaMemcpy2DAsync(dS, pitch, S, lds * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
         if (Q) {  // Q travels on a side stream, after S, while the S-side work starts
             TEIG_CUDA(cudaStreamCreateWithFlags(&qs, cudaStreamNonBlocking));
             TEIG_CUDA(cudaEventCreateWithFlags(&q_ready, cudaEventDisableTiming));
             TEIG_CUDA(cudaEventRecord(q_ready, stream));  // S is on the device
             TEIG_CUDA(cudaStreamWaitEvent(qs, q_ready, 0));
-            TEIG_CUDA(cudaMemcpy2DAsync(dQ.p, pitch, Q, ldq * sizeof(double), pitch, n, cudaMemcpyHostToDevice, qs));
+            TEIG_CUDA(cudaMemcpy2DAsync(dQ, pitch, Q, ldq * sizeof(double), pitch, n, cudaMemcpyHostToDevice, qs));
             TEIG_CUDA(cudaEventRecord(q_ready, qs));
         }
-        const int rc = reorder_schur_device(n, dS.as<double>(), n, Q ? dQ.as<double>() : nullptr, n, nb, sizes, flags,
-                                            opts, perm, rejected, plan, plan_cap, info, stream, q_ready);
+        if (hprof) TEIG_CUDA(cudaStreamSynchronize(stream));
+        const auto h2 = now();
+        // the final parts of S and Q stream back while the last levels run
+        // (TEIG_NO_DRAIN=1: everything after the end)
+        HostDrain dr;
+        dr.hS = S;
+        dr.lds = lds;
+        dr.hQ = Q;
+        dr.ldq = ldq;
+        dr.s_hi = n;
+        dr.q_lo = 0;
+        dr.q_hi = n;
+        // early copies only into page-locked buffers (a copy to pageable memory
+        // would block the thread that enqueues the remaining levels)
+        auto pinned = [](const void* p) {
+            if (!p) return true;
+            cudaPointerAttributes at{};
+            if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+                cudaGetLastError();
+                return false;
+            }
+            return at.type == cudaMemoryTypeHost;
+        };
+        const bool drain_on = !(getenv("TEIG_NO_DRAIN") && atoi(getenv("TEIG_NO_DRAIN"))) && pinned(S) && pinned(Q);
+        struct DrainRes {
+            HostDrain& d;
+            ~DrainRes() {
+                if (d.ds) {
+                    cudaStreamSynchronize(d.ds);
+                    cudaStreamDestroy(d.ds);
+                }
+                if (d.evS) cudaEventDestroy(d.evS);
+                if (d.evQ) cudaEventDestroy(d.evQ);
+            }
+        } drain_res{dr};
+        TEIG_CUDA(cudaStreamCreateWithFlags(&dr.ds, cudaStreamNonBlocking));
+        TEIG_CUDA(cudaEventCreateWithFlags(&dr.evS, cudaEventDisableTiming));
+        TEIG_CUDA(cudaEventCreateWithFlags(&dr.evQ, cudaEventDisableTiming));
+        const int rc = reorder_schur_device(n, dS, n, dQ, n, nb, sizes, flags, opts, perm, rejected, plan, plan_cap,
+                                            info, stream, q_ready, drain_on ? &dr : nullptr);
+        if (hprof) {
+            TEIG_CUDA(cudaStreamSynchronize(stream));
+            if (qs) TEIG_CUDA(cudaStreamSynchronize(qs));
+        }
+        const auto h3 = now();
         if (rc != 0) {
             if (qs) cudaStreamSynchronize(qs);
             if (q_ready) cudaEventDestroy(q_ready);
             if (qs) cudaStreamDestroy(qs);
             return rc;
         }
-        TEIG_CUDA(cudaMemcpy2DAsync(S, lds * sizeof(double), dS.p, pitch, pitch, n, cudaMemcpyDeviceToHost, stream));
-        if (Q)
-            TEIG_CUDA(cudaMemcpy2DAsync(Q, ldq * sizeof(double), dQ.p, pitch, pitch, n, cudaMemcpyDeviceToHost, qs));
-        TEIG_CUDA(cudaStreamSynchronize(stream));
+        if (!dr.valid) {  // replanned: move everything
+            dr.s_hi = n;
+            dr.q_lo = 0;
+            dr.q_hi = n;
+        }
+        TEIG_CUDA(cudaEventRecord(dr.evS, stream));  // all device work (the Q stream joined `stream`)
+        TEIG_CUDA(cudaStreamWaitEvent(dr.ds, dr.evS, 0));
+        if (dr.s_hi > 0)
+            TEIG_CUDA(cudaMemcpy2DAsync(S, lds * sizeof(double), dS, pitch, (size_t)dr.s_hi * sizeof(double), n,
+                                        cudaMemcpyDeviceToHost, dr.ds));
+        if (Q && dr.q_hi > dr.q_lo)
+            TEIG_CUDA(cudaMemcpy2DAsync(Q + dr.q_lo * ldq, ldq * sizeof(double), dQ + dr.q_lo * (size_t)n, pitch,
+                                        pitch, (size_t)(dr.q_hi - dr.q_lo), cudaMemcpyDeviceToHost, dr.ds));
+        TEIG_CUDA(cudaStreamSynchronize(dr.ds));
         if (qs) TEIG_CUDA(cudaStreamSynchronize(qs));
+        if (hprof)
+            fprintf(stderr, "[teig host] alloc %.1f ms  h2d(S) %.1f ms  device %.1f ms  d2h %.1f ms\n", ms(h0, h1),
+                    ms(h1, h2), ms(h2, h3), ms(h3, now()));
     } catch (const std::exception& e) {
         if (q_ready) cudaEventDestroy(q_ready);
         if (qs) cudaStreamDestroy(qs);
