@@ -82,6 +82,16 @@ class ClockSampler:
         self.index = index
         self.samples = []
         self.proc = None
+        self.k0 = 0
+
+    def mark(self):
+        """Start of the timed region: samples before it are dropped.  The
+        sampler is started before the warm-up so that nvidia-smi's own start-up
+        (NVML init, ~1 s of driver work) is not inside the timed steps."""
+        t0 = time.time()
+        while self.proc is not None and not self.samples and time.time() - t0 < 10:
+            time.sleep(0.05)
+        self.k0 = len(self.samples)
 
     def start(self):
         try:
@@ -111,7 +121,7 @@ class ClockSampler:
         mx = None
         reasons = set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for p in self.samples:
+        for p in self.samples[self.k0:]:
             try:
                 sm.append(float(p[0]))
                 mx = float(p[1])
@@ -168,6 +178,8 @@ def run_ours(args, rank, world, local):
         Q.copy_(Q0)
 
     opts = T.ReorderOptions(window_size=args.ws)
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(max(args.warmup, 0)):
         reset()
         res = T.reorder_schur(S, Q, sel, opts)
@@ -178,11 +190,10 @@ def run_ours(args, rank, world, local):
     prof = {"ms_window": 0.0, "ms_left": 0.0, "ms_right": 0.0, "ms_factor": 0.0, "flops_left": 0.0,
             "flops_right": 0.0, "flops_factor": 0.0, "n_launches": 0}
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sampler = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
+    sampler.mark()
     t_wall0 = time.perf_counter()
     infos = []
     for k in range(args.steps):
@@ -407,16 +418,17 @@ def run_ours_dist(args, rank, world, local):
         S.copy_(S0)
         Q.copy_(Q0)
 
+    sampler = ClockSampler(local)
+    sampler.start()
     for _ in range(max(args.warmup, 0)):
         reset()
         res = D.reorder_schur_dist(S, Q, sel, cb, rb, rank, world, comm, opts)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream(dev)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sampler = ClockSampler(local)
     dist.barrier()
     torch.cuda.synchronize()
-    sampler.start()
+    sampler.mark()
     t0 = time.perf_counter()
     for k in range(args.steps):
         reset()

@@ -577,7 +577,8 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         TEIG_CUDA(cudaStreamSynchronize(stream));  // staging visible to the side stream
         const auto h1 = now();
         TEIG_CUDA(cudaMemcpy2DAsync(dS, pitch, S, lds * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
-        if (Q) {  // Q travels on a side stream, after S, while the S-side work starts
+        if (Q) {  // Q travels on a side stream, after S, while the S-side work starts (measured:
+                  // uploading Q before the work starts costs +0.5 s at n=40000)
             TEIG_CUDA(cudaStreamCreateWithFlags(&qs, cudaStreamNonBlocking));
             TEIG_CUDA(cudaEventCreateWithFlags(&q_ready, cudaEventDisableTiming));
             TEIG_CUDA(cudaEventRecord(q_ready, stream));  // S is on the device
