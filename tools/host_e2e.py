@@ -13,7 +13,7 @@ s0 = T.gen_schur_input(n, T.known_spectrum_seed(1))
 sel = T.select_fraction(s0, 0.35, 99)
 Sh = torch.empty((n, n), dtype=torch.float64).pin_memory()
 Qh = torch.empty((n, n), dtype=torch.float64).pin_memory()
-for k in range(3):
+for k in range(int(os.environ.get("CALLS", "3"))):
     Sh.copy_(s0.t())
     Qh.zero_()
     Qh.diagonal().fill_(1.0)
@@ -24,7 +24,7 @@ for k in range(3):
           flush=True)
 S, Q = T.colmajor_empty(n), T.colmajor_empty(n)
 I = T.identity(n)
-for k in range(3):
+for k in range(int(os.environ.get("CALLS", "3"))):
     S.copy_(s0)
     Q.copy_(I)
     torch.cuda.synchronize()
