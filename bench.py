@@ -228,7 +228,7 @@ def run_ours(args, rank, world, local):
     # ---------------- e2e: host buffers through the C ABI, copies inside ----------------
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_reorder(T, S0, S, sel, opts, n, min(args.steps, 3))
+        e2e = e2e_reorder(T, S0, S, sel, opts, n, 5)
 
     # ---------------- roofline of the dominant kernel class ----------------
     k_ms = prof["ms_left"] + prof["ms_right"] + prof["ms_factor"]
