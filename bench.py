@@ -185,6 +185,19 @@ def run_ours(args, rank, world, local):
         res = T.reorder_schur(S, Q, sel, opts)
     torch.cuda.synchronize()
 
+    # ---------------- e2e: host buffers through the C ABI, copies inside ----------------
+    # (before the device-timed steps and the cuBLAS parity check: the host
+    # path's device staging is then mapped while HBM is still unfragmented;
+    # staged after the parity temporaries it ran 10-40 % slower.  S holds the
+    # warm-up's result, which the timed steps reproduce bit for bit.)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        if args.warmup < 1:
+            reset()
+            T.reorder_schur(S, Q, sel, opts)
+            torch.cuda.synchronize()
+        e2e = e2e_reorder(T, S0, S, sel, opts, n, 5)
+
     # ---------------- timed region (device events per step) ----------------
     popts = T.ReorderOptions(window_size=args.ws, profile=True)
     prof = {"ms_window": 0.0, "ms_left": 0.0, "ms_right": 0.0, "ms_factor": 0.0, "flops_left": 0.0,
@@ -224,11 +237,6 @@ def run_ours(args, rank, world, local):
     resid = float(torch.linalg.norm(R) / torch.linalg.norm(S0d))
     orth = float(torch.linalg.norm(Q.t() @ Q - torch.eye(n, dtype=torch.float64, device=dev)))
     del R
-
-    # ---------------- e2e: host buffers through the C ABI, copies inside ----------------
-    e2e = None
-    if not args.no_e2e:
-        e2e = e2e_reorder(T, S0, S, sel, opts, n, 5)
 
     # ---------------- roofline of the dominant kernel class ----------------
     k_ms = prof["ms_left"] + prof["ms_right"] + prof["ms_factor"]
