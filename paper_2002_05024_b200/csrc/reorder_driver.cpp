@@ -586,7 +586,10 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
             TEIG_CUDA(cudaMemcpy2DAsync(dQ, pitch, Q, ldq * sizeof(double), pitch, n, cudaMemcpyHostToDevice, qs));
             TEIG_CUDA(cudaEventRecord(q_ready, qs));
         }
-        if (hprof) TEIG_CUDA(cudaStreamSynchronize(stream));
+        // S on the device before the levels are enqueued: measured, letting the
+        // host enqueue thousands of launches while the 12.8 GB upload runs made
+        // the device phase 0.3-4.5 s slower and erratic at n=40000
+        TEIG_CUDA(cudaStreamSynchronize(stream));
         const auto h2 = now();
         // the final parts of S and Q stream back while the last levels run
         // (TEIG_NO_DRAIN=1: everything after the end)
@@ -626,10 +629,8 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         TEIG_CUDA(cudaEventCreateWithFlags(&dr.evQ, cudaEventDisableTiming));
         const int rc = reorder_schur_device(n, dS, n, dQ, n, nb, sizes, flags, opts, perm, rejected, plan, plan_cap,
                                             info, stream, q_ready, drain_on ? &dr : nullptr);
-        if (hprof) {
-            TEIG_CUDA(cudaStreamSynchronize(stream));
-            if (qs) TEIG_CUDA(cudaStreamSynchronize(qs));
-        }
+        TEIG_CUDA(cudaStreamSynchronize(stream));
+        if (qs) TEIG_CUDA(cudaStreamSynchronize(qs));
         const auto h3 = now();
         if (rc != 0) {
             if (qs) cudaStreamSynchronize(qs);
