@@ -192,13 +192,16 @@ def run_ours(args, rank, world, local):
 
     sampler = ClockSampler(local)
     sampler.start()
-    for _ in range(max(args.warmup, 0)):
+    # the timed steps record per-launch events (profile=True); the last
+    # warm-up does too, so the first timed step does not pay the driver's
+    # first creation of ~4300 events (it ran ~15 % slower)
+    popts = T.ReorderOptions(window_size=args.ws, profile=True)
+    for k in range(max(args.warmup, 0)):
         reset()
-        res = T.reorder_schur(S, Q, sel, opts)
+        res = T.reorder_schur(S, Q, sel, popts if k == args.warmup - 1 else opts)
     torch.cuda.synchronize()
 
     # ---------------- timed region (device events per step) ----------------
-    popts = T.ReorderOptions(window_size=args.ws, profile=True)
     prof = {"ms_window": 0.0, "ms_left": 0.0, "ms_right": 0.0, "ms_factor": 0.0, "flops_left": 0.0,
             "flops_right": 0.0, "flops_factor": 0.0, "n_launches": 0}
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
