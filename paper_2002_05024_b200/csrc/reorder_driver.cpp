@@ -403,6 +403,25 @@ struct StreamPair {
 
 }  // namespace
 
+// The per-pass device buffers (window descriptors, the Q_w pool: 6.4 GB at
+// n=40000) come from the stream-ordered allocator; keep what it maps instead
+// of returning it at every synchronisation (TEIG_POOL_RELEASE=1: default
+// behaviour), so repeated calls do not remap gigabytes each time.
+void keep_pool_memory() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    if (getenv("TEIG_POOL_RELEASE") && atoi(getenv("TEIG_POOL_RELEASE"))) return;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    uint64_t keep = UINT64_MAX;
+    if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess) cudaGetLastError();
+}
+
 int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq, int64_t nb,
                          const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
                          int64_t* perm, int64_t* rejected_out, int64_t* plan_out, int64_t plan_cap,
@@ -412,6 +431,7 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
     if (!dS) return set_error(-2, "S is null");
     if (lds < n) return set_error(-3, "lds < n");
     if (dQ && ldq < n) return set_error(-5, "ldq < n");
+    keep_pool_memory();
     if (nb < 0 || (nb > 0 && (!sizes || !flags))) return set_error(-6, "malformed selection");
     teig_reorder_opts o;
     teig_reorder_opts_default(&o);
