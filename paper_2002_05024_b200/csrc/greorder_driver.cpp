@@ -241,6 +241,7 @@ int teig_greorder_schur_device(int64_t n, double* dS, int64_t lds, double* dT, i
                                double* dZ, int64_t ldz, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
                                const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
                                teig_reorder_info* info, void* stream) {
+    keep_pool_memory();
     return greorder_schur_device(n, dS, lds, dT, ldt, dQ, ldq, dZ, ldz, nb, sizes, flags, opts, perm, rejected, info,
                                  (cudaStream_t)stream);
 }
@@ -249,6 +250,7 @@ int teig_greorder_schur_host(int64_t n, double* S, int64_t lds, double* T, int64
                              double* Z, int64_t ldz, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
                              const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
                              teig_reorder_info* info, void* stream_v) {
+    keep_pool_memory();
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (!S || !T) return set_error(-2, "S or T is null");
     if (lds < n || ldt < n) return set_error(-3, "lds/ldt < n");

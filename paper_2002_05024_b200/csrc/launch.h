@@ -34,6 +34,9 @@ bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax
                              long long ldm, long long rows, long long cols, bool factor, cudaStream_t stream,
                              cudaError_t* err);
 
+// keep the stream-ordered allocator's memory between calls (reorder_driver.cpp)
+void keep_pool_memory();
+
 // synthetic inputs (generate.cu)
 cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64_t fill_seed,
                                    cudaStream_t stream);

@@ -713,11 +713,13 @@ int teig_deflation_check(double spike, double diag_sum, int32_t deflation, doubl
 
 int teig_schur_reduce_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t ldq, const teig_schur_opts* o,
                              double* eig_re, double* eig_im, teig_schur_info* info, void* stream) {
+    keep_pool_memory();
     return schur_reduce_device(n, dH, ldh, dQ, ldq, o, eig_re, eig_im, info, (cudaStream_t)stream);
 }
 
 int teig_schur_reduce_host(int64_t n, double* H, int64_t ldh, double* Q, int64_t ldq, const teig_schur_opts* o,
                            double* eig_re, double* eig_im, teig_schur_info* info, void* stream_v) {
+    keep_pool_memory();
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (!H) return set_error(-2, "H is null");
     if (ldh < n) return set_error(-3, "ldh < n");
