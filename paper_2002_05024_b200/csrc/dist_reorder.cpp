@@ -789,6 +789,7 @@ int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_c
                             const int64_t* row_bounds, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
                             const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected, teig_reorder_info* info,
                             void* stream) {
+    keep_pool_memory();
     return dist_impl(n, world, rank, nccl_comm, dS_slabs, nullptr, lds, dQ_slabs, nullptr, col_bounds, row_bounds, nb,
                      sizes, flags, opts, perm, rejected, info, stream, false);
 }
@@ -798,6 +799,7 @@ int teig_dist_greorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_
                              const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb, const uint8_t* sizes,
                              const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
                              teig_reorder_info* info, void* stream) {
+    keep_pool_memory();
     return dist_impl(n, world, rank, nccl_comm, dS_slabs, dT_slabs, lds, dQ_slabs, dZ_slabs, col_bounds, row_bounds,
                      nb, sizes, flags, opts, perm, rejected, info, stream, true);
 }
