@@ -446,10 +446,10 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             const auto& P = lp.part[r];
             if (P.l_tiles) {
                 TEIG_CUDA(launch_update_left(R[r].descs + P.l_off, (int)P.l_cnt, (int)P.l_tiles, lp.dmax, R[r].qw,
-                                             R[r].S, lds, (int)n, s));
+                                             R[r].S, lds, (int)n, s, n, C[r + 1] + kHalo));
                 if (gen)
                     TEIG_CUDA(launch_update_left(R[r].descs + P.l_off, (int)P.l_cnt, (int)P.l_tiles, lp.dmax, R[r].qw,
-                                                 R[r].T, lds, (int)n, s));
+                                                 R[r].T, lds, (int)n, s, n, C[r + 1] + kHalo));
                 ++launches;
             }
         }
@@ -459,10 +459,10 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             const auto& P = lp.part[r];
             if (P.r_tiles) {
                 TEIG_CUDA(launch_update_right(R[r].descs + P.r_off, (int)P.r_cnt, (int)P.r_tiles, lp.dmax, R[r].qw,
-                                              R[r].S, lds, (int)n, false, s));
+                                              R[r].S, lds, (int)n, false, s, n, C[r + 1] + kHalo));
                 if (gen)
                     TEIG_CUDA(launch_update_right(R[r].descs + P.r_off, (int)P.r_cnt, (int)P.r_tiles, lp.dmax, R[r].qw,
-                                                  R[r].T, lds, (int)n, false, s));
+                                                  R[r].T, lds, (int)n, false, s, n, C[r + 1] + kHalo));
                 ++launches;
             }
         }
@@ -484,10 +484,10 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             const auto& P = lp.part[r];
             if (P.q_tiles) {
                 TEIG_CUDA(launch_update_right(R[r].descs + P.q_off, (int)P.q_cnt, (int)P.q_tiles, lp.dmax, R[r].qw,
-                                              R[r].Q, R[r].ldq, (int)n, true, s2));
+                                              R[r].Q, R[r].ldq, (int)n, true, s2, Rw[r + 1], n));
                 if (gen && P.z_cnt && R[r].Z)
                     TEIG_CUDA(launch_update_right(R[r].descs + P.z_off, (int)P.z_cnt, (int)P.q_tiles, lp.dmax, R[r].qw,
-                                                  R[r].Z, R[r].ldq, (int)n, true, s2));
+                                                  R[r].Z, R[r].ldq, (int)n, true, s2, Rw[r + 1], n));
                 ++launches;
             }
         }
