@@ -525,7 +525,10 @@ bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax
         if (*err != cudaSuccess) return true;
         init = true;
     }
-    const int grid = grid_for(ntiles);
+    // Q updates (off the critical path, low-priority stream): short CTAs of 8
+    // tiles, so window-kernel CTAs can take SMs as they free up
+    static const bool persistent_q = getenv("TEIG_NO_PRIO") && atoi(getenv("TEIG_NO_PRIO"));
+    const int grid = (factor && !persistent_q) ? (ntiles + 7) / 8 : grid_for(ntiles);
     const long long alloc = (cols - 1) * ldm + rows;
     if (factor)
         update_right_bulk_kernel<2><<<grid, kBulkThreads, kRightSmem, stream>>>(wins, nwin, ntiles, qw_pool, M, ldm,
