@@ -58,7 +58,8 @@ typedef struct teig_reorder_opts {
 } teig_reorder_opts;
 
 typedef struct teig_reorder_info {
-    int64_t n_windows;     /* executed windows (all passes) */
+    int64_t n_windows;     /* windows that ran or deviated = entries of `plan` (all passes;
+                              windows skipped after a deviation are replanned, not counted) */
     int64_t n_levels;      /* wavefronts (all passes) */
     int64_t n_passes;      /* planning passes (1 for a clean run) */
     int64_t n_groups;      /* chains planned in the first pass */
@@ -99,9 +100,18 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
                             int64_t* plan, int64_t plan_cap, teig_reorder_info* info,
                             void* stream);
 
-/* The host entry points keep their device staging (2 n^2 doubles for the
- * largest call so far) between calls; this returns it to the device.  Not
- * part of the reference interface (the reference has no device memory). */
+/* Device memory policy (not part of the reference interface: the reference
+ * has no device memory).  Every per-call device buffer comes from a private
+ * stream-ordered pool per device.  Retention off (the default; TEIG_RETAIN=1
+ * in the environment turns it on at load): the pool returns its memory at
+ * every synchronisation and the host entry points allocate their device
+ * staging (2 n^2 doubles) per call.  On: both are kept between calls, so a
+ * process that calls repeatedly does not remap gigabytes every time.
+ * teig_release_memory() returns all of it (staging + pools, every device);
+ * teig_release_host_staging() only the staging. */
+void teig_set_memory_retention(int32_t on);
+int32_t teig_memory_retention(void);
+void teig_release_memory(void);
 void teig_release_host_staging(void);
 
 /* Diagonal-block scan by exact-zero subdiagonal (reorder.cpp:21-43) on a
@@ -138,6 +148,18 @@ int teig_window_reorder_device(int64_t d, double* dW, int64_t ldw, int64_t nb,
  * Q[0:n, a:b] <- Q[0:n, a:b] Qw (dQ may be NULL).  dQw: d x d, ld d. */
 int teig_apply_window_updates_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq,
                                      int64_t a, int64_t d, const double* dQw, void* stream);
+
+/* One panel of apply_window_updates on an explicit index range (the unit the
+ * distributed driver runs on a slab; window_tasks.cpp:40-86 per tile):
+ *   side 0 (L):  M[a:a+d, i0:i1] <- Qw^T M[a:a+d, i0:i1]
+ *   side 1 (R):  M[i0:i1, a:a+d] <- M[i0:i1, a:a+d] Qw
+ *   side 2 (Q):  as side 1, the factor-update kernel variant.
+ * dM is a base such that absolute (i, j) lives at dM[i + j*ldm] for
+ * i < rows, j < cols (a slab's base may point before its allocation).
+ * Synchronous on `stream`. */
+int teig_update_panel_device(int32_t side, int64_t d, const double* dQw, int64_t a, double* dM,
+                             int64_t ldm, int64_t rows, int64_t cols, int64_t i0, int64_t i1,
+                             void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Schur reduction: multishift QR with aggressive early deflation           */

@@ -154,6 +154,11 @@ def ref():
         R.ref_reorder_schur.argtypes = [_SZ, _SZ, _P, _P, _SZ, _P, _SZ, _SZ, C.c_int, _P, _P,
                                         _P, _P, _SZ, _P, _P, _P]
         R.ref_reorder_schur.restype = C.c_int
+        R.ref_problem_create.argtypes = [_SZ, _SZ, _P]
+        R.ref_problem_create.restype = C.c_void_p
+        R.ref_problem_destroy.argtypes = [C.c_void_p]
+        R.ref_problem_reorder.argtypes = [C.c_void_p, _SZ, _P, _SZ, _SZ, C.c_int, _P, _P, _P]
+        R.ref_problem_reorder.restype = C.c_int
         R.ref_hessenberg_reduce.argtypes = [_SZ, _P, _P, _P, _SZ]
         R.ref_hessenberg_reduce.restype = C.c_int
         R.ref_schur_reduce.argtypes = [_SZ, _SZ, _P, _P, _SZ, C.c_int, _SZ, _SZ, _SZ, _SZ, _P,
@@ -437,6 +442,38 @@ def ref_reorder_schur(s_rm, q_rm, flags, window_size=0, workers=0, tile=0, stric
     return dict(permutation=perm[:nb].astype(np.int64), rejected=rej[:nrej.value].astype(np.int64),
                 plan=plan[:3 * k].reshape(k, 3).astype(np.int64), clean=bool(clean.value),
                 seconds=secs.value)
+
+
+class RefProblem:
+    """A reorder problem resident in the reference's TiledMatrix form (built
+    once from a column-major S); run() times reorder_schur alone."""
+
+    def __init__(self, s_cm: np.ndarray, tile: int = 0):
+        assert s_cm.flags.f_contiguous
+        self.n = s_cm.shape[0]
+        self.h = ref().ref_problem_create(self.n, tile, _ptr(s_cm))
+        if not self.h:
+            raise RuntimeError("reference: " + ref().ref_last_error().decode())
+
+    def run(self, flags, window_size=0, workers=0, with_q=True):
+        flags = np.asarray(flags, dtype=np.uint8)
+        secs = C.c_double(0)
+        nplan = _SZ(0)
+        clean = C.c_int(0)
+        _chk_ref(ref().ref_problem_reorder(self.h, len(flags), _ptr(flags), window_size, workers,
+                                           int(with_q), C.byref(secs), C.byref(nplan), C.byref(clean)))
+        return dict(seconds=secs.value, n_plan=nplan.value, clean=bool(clean.value))
+
+    def close(self):
+        if self.h:
+            ref().ref_problem_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def ref_hessenberg_reduce(a_rm, workers=0):

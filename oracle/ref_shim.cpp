@@ -210,6 +210,61 @@ int ref_reorder_schur(std::size_t n, std::size_t tile, double* s_rm, double* q_r
     }
 }
 
+// A resident reorder problem for timing (bench.py's reference arm and
+// cpu_baseline): the pristine S is converted to a TiledMatrix ONCE, straight
+// from a column-major buffer tile by tile (tiles are column-major,
+// tiled_matrix.hpp:27-35); every ref_problem_reorder copies it, builds Q = I
+// (TiledMatrix::identity) and times reorder_schur alone -- no per-step
+// row-major conversions of the n x n inputs and outputs.
+struct RefProblem {
+    TiledMatrix s0;
+    std::size_t n;
+};
+
+void* ref_problem_create(std::size_t n, std::size_t tile, const double* s_cm) {
+    try {
+        if (!tile) tile = default_tile_size(n);
+        auto* p = new RefProblem{TiledMatrix(n, n, tile), n};
+        for (std::size_t tj = 0; tj < p->s0.grid_cols(); ++tj)
+            for (std::size_t ti = 0; ti < p->s0.grid_rows(); ++ti) {
+                Tile& t = p->s0.tile(ti, tj);
+                const std::size_t r0 = ti * tile, c0 = tj * tile;
+                for (std::size_t j = 0; j < t.cols; ++j)
+                    std::memcpy(&t.data[j * t.rows], s_cm + r0 + (c0 + j) * n, sizeof(double) * t.rows);
+            }
+        return p;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+void ref_problem_destroy(void* h) { delete static_cast<RefProblem*>(h); }
+
+int ref_problem_reorder(void* h, std::size_t nb, const std::uint8_t* flags, std::size_t window_size,
+                        std::size_t workers, int with_q, double* seconds, std::size_t* n_plan, int* clean) {
+    try {
+        auto* p = static_cast<RefProblem*>(h);
+        TiledMatrix s = p->s0;
+        std::optional<TiledMatrix> q;
+        if (with_q) q = TiledMatrix::identity(p->n, p->s0.tile_size());
+        auto sel = make_sel(s, flags, nb);
+        ReorderOptions o;
+        o.window_size = window_size;
+        o.workers = workers;
+        const auto t0 = std::chrono::steady_clock::now();
+        auto res = reorder_schur(std::move(s), std::move(q), sel, o);
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+        if (n_plan) *n_plan = res.plan.size();
+        if (clean) *clean = res.clean ? 1 : 0;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
 // hessenberg_reduce (hessenberg.cpp:185-280): a_rm in -> h_rm, q_rm out.
 int ref_hessenberg_reduce(std::size_t n, const double* a_rm, double* h_rm, double* q_rm,
                           std::size_t workers) {

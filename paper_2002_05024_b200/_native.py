@@ -76,6 +76,9 @@ SIGNATURES = {
     "teig_reorder_schur_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P,
                                             _I64, _P, _P]),
     "teig_release_host_staging": (None, []),
+    "teig_set_memory_retention": (None, [C.c_int32]),
+    "teig_memory_retention": (C.c_int32, []),
+    "teig_release_memory": (None, []),
     "teig_reorder_schur_host": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P,
                                           _I64, _P, _P]),
     "teig_scan_blocks_device": (C.c_int64, [_I64, _P, _I64, _P, _P]),
@@ -83,6 +86,7 @@ SIGNATURES = {
     "teig_plan_reorder": (C.c_int64, [_I64, _I64, _P, _P, _I64, _P, _I64, _P, _P, _P]),
     "teig_window_reorder_device": (C.c_int, [_I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P]),
     "teig_apply_window_updates_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _I64, _P, _P]),
+    "teig_update_panel_device": (C.c_int, [C.c_int32, _I64, _P, _I64, _P, _I64, _I64, _I64, _I64, _I64, _P]),
     "teig_gen_schur_input_device": (C.c_int, [_I64, _P, _I64, C.c_uint64, _P]),
     "teig_gen_hessenberg_device": (C.c_int, [_I64, _P, _I64, C.c_uint64, _P]),
     "teig_set_identity_device": (C.c_int, [_I64, _P, _I64, _P]),
@@ -137,3 +141,18 @@ def check(rc: int) -> int:
     if rc < 0:
         raise TaskeigError(rc, lib().teig_last_error().decode(errors="replace"))
     return rc
+
+
+def set_memory_retention(on: bool) -> None:
+    """Keep the library's device pool and host-path staging between calls
+    (teig_set_memory_retention; off by default)."""
+    lib().teig_set_memory_retention(1 if on else 0)
+
+
+def memory_retention() -> bool:
+    return bool(lib().teig_memory_retention())
+
+
+def release_memory() -> None:
+    """Return the library's cached device memory (staging + pools, every device)."""
+    lib().teig_release_memory()

@@ -14,7 +14,7 @@ struct WinDesc {
     int32_t a;         // first row/column of the window
     int32_t d;         // window order (b = a + d)
     int32_t nb;        // number of diagonal blocks inside the window
-    int32_t flags;     // reserved
+    int32_t level;     // wavefront level (deviation flag of the window kernels)
     int64_t qw_off;    // offset (doubles) of this window's Q_w (d x d, ld d)
     int64_t blk_off;   // offset into the per-block pools (sizes/sel/order/stuck)
     int32_t tl_pref;   // exclusive prefix of left-update tiles within the level
@@ -34,6 +34,7 @@ struct WinDesc {
 enum : int32_t {
     kWinExecuted = 1,     // layout matched and the bubble ran
     kWinStuck = 2,        // at least one swap was rejected
+    kWinSkipped = 4,      // not run: an earlier level deviated (the plan is stale)
 };
 
 // ---- Schur reduction (schur_window.cu) --------------------------------------

@@ -27,7 +27,21 @@ __global__ void sum_buffers_kernel(BufSet b, int nbuf, size_t count) {
     }
 }
 
+// Deviation flag of the distributed pass (see window_reorder.cu): publish
+// (mode 0) writes this rank's "deviated at a level <= L" into the level's
+// flag slot, which travels inside the level's Q_w all-reduce; absorb (mode 1)
+// lowers the rank's deviation level to L when any rank published.
+__global__ void dist_flag_kernel(int32_t* dev_level, double* slot, int level, int mode) {
+    if (mode == 0) *slot = (*dev_level <= level) ? 1.0 : 0.0;
+    else if (*slot > 0.5 && *dev_level > level) *dev_level = level;
+}
+
 }  // namespace
+
+cudaError_t launch_dist_flag(int32_t* dev_level, double* slot, int level, int mode, cudaStream_t s) {
+    dist_flag_kernel<<<1, 1, 0, s>>>(dev_level, slot, level, mode);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_sum_buffers(void* const* bufs, int nbuf, size_t count, int elem_bytes, cudaStream_t s) {
     if (count == 0 || nbuf <= 1) return cudaSuccess;

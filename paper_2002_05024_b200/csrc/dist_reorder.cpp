@@ -134,6 +134,7 @@ struct RankBufs {
     WinDesc* descs = nullptr;   // per-level descriptor arrays of this rank
     uint8_t *sizes = nullptr, *sel = nullptr, *order = nullptr, *stuck = nullptr;
     int32_t* status = nullptr;
+    int32_t* dev_level = nullptr;  // deviation level of the pass (window_reorder.cu)
     double* stage = nullptr;    // contiguous staging for NCCL transfers
     size_t stage_cap = 0;
 };
@@ -205,7 +206,7 @@ class NcclComm : public Comm {
         if (need > me.stage_cap) {
             if (me.stage) TEIG_CUDA(cudaFreeAsync(me.stage, s));
             me.stage_cap = std::max(need, me.stage_cap * 2);
-            TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&me.stage), me.stage_cap * 8, s));
+            TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&me.stage), me.stage_cap * 8, s));
         }
         size_t off = 0;
         std::vector<size_t> offs(xs.size());
@@ -281,13 +282,15 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
     for (int64_t i = 0; i < nw; ++i) idx[i] = i;
     std::stable_sort(idx.begin(), idx.end(),
                      [&](int64_t x, int64_t y) { return plan.windows[x].level < plan.windows[y].level; });
-    // Q_w slots in level order; window kernel status in plan order
+    // Q_w slots in level order, each level followed by one deviation-flag
+    // slot (it rides the level's all-reduce); window kernel status in plan order
     std::vector<int64_t> qw_off(nw);
     int64_t qw_total = 0;
     for (int64_t k = 0; k < nw; ++k) {
         const auto& w = plan.windows[idx[k]];
         qw_off[idx[k]] = qw_total;
         qw_total += (gen ? 2 : 1) * (w.wbot - w.wtop) * (w.wbot - w.wtop);
+        if (k + 1 == nw || plan.windows[idx[k + 1]].level != w.level) qw_total += 1;
     }
     // per-rank descriptor arrays, level by level
     std::vector<std::vector<WinDesc>> D(world);
@@ -306,6 +309,7 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             lp.qw_len += (gen ? 2 : 1) * (w.wbot - w.wtop) * (w.wbot - w.wtop);
             lp.dmax = std::max<int>(lp.dmax, (int)(w.wbot - w.wtop));
         }
+        lp.qw_len += 1;  // the level's deviation flag
         lp.dmax = lp.dmax <= 64 ? 64 : 128;
         for (int r = 0; r < world; ++r) {
             auto& P = lp.part[r];
@@ -315,6 +319,7 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
                 d.a = (int32_t)w.wtop;
                 d.d = (int32_t)(w.wbot - w.wtop);
                 d.nb = (int32_t)w.count;
+                d.level = lv;
                 d.qw_off = qw_off[idx[t]];
                 d.blk_off = w.blk_off;
                 return d;
@@ -397,19 +402,21 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
     for (int r = 0; r < world; ++r) {
         if (!comm.local(r)) continue;
         RankBufs& B = R[r];
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.qw), sizeof(double) * std::max<int64_t>(qw_total, 1), s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.qw), sizeof(double) * std::max<int64_t>(qw_total, 1), s));
         TEIG_CUDA(cudaMemsetAsync(B.qw, 0, sizeof(double) * std::max<int64_t>(qw_total, 1), s));
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.descs), sizeof(WinDesc) * std::max<size_t>(D[r].size(), 1), s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.descs), sizeof(WinDesc) * std::max<size_t>(D[r].size(), 1), s));
         if (!D[r].empty())
             TEIG_CUDA(cudaMemcpyAsync(B.descs, D[r].data(), sizeof(WinDesc) * D[r].size(), cudaMemcpyHostToDevice, s));
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.sizes), ne + 1, s));
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.sel), ne + 1, s));
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.order), ne + 1, s));
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.stuck), ne + 1, s));
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&B.status), sizeof(int32_t) * std::max<size_t>(D[r].size(), 1), s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.sizes), ne + 1, s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.sel), ne + 1, s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.order), ne + 1, s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.stuck), ne + 1, s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.status), sizeof(int32_t) * std::max<size_t>(D[r].size(), 1), s));
         TEIG_CUDA(cudaMemsetAsync(B.order, 0, ne + 1, s));
         TEIG_CUDA(cudaMemsetAsync(B.stuck, 0, ne + 1, s));
         TEIG_CUDA(cudaMemsetAsync(B.status, 0, sizeof(int32_t) * std::max<size_t>(D[r].size(), 1), s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.dev_level), sizeof(int32_t), s));
+        TEIG_CUDA(cudaMemsetAsync(B.dev_level, 0x7f, sizeof(int32_t), s));
         TEIG_CUDA(cudaMemcpyAsync(B.sizes, plan.sizes.data(), ne, cudaMemcpyHostToDevice, s));
         TEIG_CUDA(cudaMemcpyAsync(B.sel, plan.sel.data(), ne, cudaMemcpyHostToDevice, s));
         qw_bufs[r] = B.qw;
@@ -427,19 +434,25 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
                 if (gen)
                     TEIG_CUDA(launch_gwindow_reorder(R[r].descs + P.w_off, (int)P.w_cnt, lp.dmax, R[r].S, lds, R[r].T,
                                                      lds, R[r].qw, R[r].sizes, R[r].sel, R[r].order, R[r].stuck,
-                                                     R[r].status + P.w_off, s));
+                                                     R[r].status + P.w_off, s, R[r].dev_level));
                 else
                     TEIG_CUDA(launch_window_reorder(R[r].descs + P.w_off, (int)P.w_cnt, lp.dmax, R[r].S, lds, R[r].qw,
                                                     R[r].sizes, R[r].sel, R[r].order, R[r].stuck,
-                                                    R[r].status + P.w_off, s));
+                                                    R[r].status + P.w_off, s, nullptr, R[r].dev_level));
                 ++launches;
             }
         }
-        {  // P3
+        {  // P3 (with the deviation flag: published before, absorbed after)
+            const int64_t flag = lp.qw_off + lp.qw_len - 1;
             std::vector<void*> b(world, nullptr);
             for (int r = 0; r < world; ++r)
-                if (comm.local(r)) b[r] = R[r].qw + lp.qw_off;
+                if (comm.local(r)) {
+                    b[r] = R[r].qw + lp.qw_off;
+                    TEIG_CUDA(launch_dist_flag(R[r].dev_level, R[r].qw + flag, lv, 0, s));
+                }
             comm.allreduce(b, (size_t)lp.qw_len, ncclFloat64, s);
+            for (int r = 0; r < world; ++r)
+                if (comm.local(r)) TEIG_CUDA(launch_dist_flag(R[r].dev_level, R[r].qw + flag, lv, 1, s));
         }
         for (int r = 0; r < world; ++r) {  // P4
             if (!comm.local(r)) continue;
@@ -513,7 +526,7 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
     }
     if (!comm.local((me + 1) % world) && world > 1) {  // NCCL: combine the ranks' statuses
         int32_t* dst = nullptr;
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dst), sizeof(int32_t) * status.size(), s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&dst), sizeof(int32_t) * status.size(), s));
         TEIG_CUDA(cudaMemcpyAsync(dst, status.data(), sizeof(int32_t) * status.size(), cudaMemcpyHostToDevice, s));
         std::vector<void*> b(world, nullptr);
         b[me] = dst;
@@ -532,11 +545,13 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
         cudaFreeAsync(B.order, s);
         cudaFreeAsync(B.stuck, s);
         cudaFreeAsync(B.status, s);
+        cudaFreeAsync(B.dev_level, s);
         B.qw = nullptr;
     }
     status.resize(nw);
     po.deviated = fold_outcomes(plan, blocks, status, order, stuck, rejected, plan_log, strict);
-    po.windows = nw;
+    po.windows = 0;
+    for (int64_t k = 0; k < nw; ++k) po.windows += (status[k] & kWinSkipped) ? 0 : 1;
     po.levels = nl;
     po.launches = launches;
     return po;
@@ -789,7 +804,6 @@ int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_c
                             const int64_t* row_bounds, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
                             const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected, teig_reorder_info* info,
                             void* stream) {
-    keep_pool_memory();
     return dist_impl(n, world, rank, nccl_comm, dS_slabs, nullptr, lds, dQ_slabs, nullptr, col_bounds, row_bounds, nb,
                      sizes, flags, opts, perm, rejected, info, stream, false);
 }
@@ -799,19 +813,20 @@ int teig_dist_greorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_
                              const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb, const uint8_t* sizes,
                              const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
                              teig_reorder_info* info, void* stream) {
-    keep_pool_memory();
     return dist_impl(n, world, rank, nccl_comm, dS_slabs, dT_slabs, lds, dQ_slabs, dZ_slabs, col_bounds, row_bounds,
                      nb, sizes, flags, opts, perm, rejected, info, stream, true);
 }
 
 int teig_gen_schur_input_cols_device(int64_t n, double* dS, int64_t lds, int64_t c0, int64_t c1, uint64_t fill_seed,
                                      void* stream) {
+    DeviceGuard device_guard(dS);
     if (n < 1 || lds < n || c0 < 0 || c1 > n || c1 < c0) return set_error(-1, "bad shape");
     cudaError_t e = launch_gen_schur_cols(dS, lds, n, fill_seed, c0, c1, (cudaStream_t)stream);
     return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));
 }
 
 int teig_set_identity_rows_device(int64_t n, double* dQ, int64_t ldq, int64_t r0, int64_t r1, void* stream) {
+    DeviceGuard device_guard(dQ);
     if (n < 1 || r0 < 0 || r1 > n || r1 < r0 || ldq < r1 - r0) return set_error(-1, "bad shape");
     cudaError_t e = launch_identity_rows(dQ, ldq, n, r0, r1, (cudaStream_t)stream);
     return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));

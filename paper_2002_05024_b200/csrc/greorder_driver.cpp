@@ -24,6 +24,7 @@
 #include "device_types.h"
 #include "launch.h"
 #include "plan.h"
+#include "qw_ring.h"
 
 namespace teig {
 
@@ -45,7 +46,7 @@ struct DBuf {
     T* p = nullptr;
     cudaStream_t s;
     DBuf(size_t n, cudaStream_t st) : s(st) {
-        if (n) TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), n * sizeof(T), st));
+        if (n) TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&p), n * sizeof(T), st));
     }
     ~DBuf() {
         if (p) cudaFreeAsync(p, s);
@@ -80,6 +81,7 @@ GPass run_gpass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* d
         d.a = (int32_t)w.wtop;
         d.d = (int32_t)(w.wbot - w.wtop);
         d.nb = (int32_t)w.count;
+        d.level = L;
         d.qw_off = pool;
         pool += 2 * (int64_t)d.d * d.d;
         d.blk_off = w.blk_off;
@@ -102,11 +104,17 @@ GPass run_gpass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* d
     }
     for (int L = 0; L < nl; ++L) lvl_off[L + 1] += lvl_off[L];
     const int dm = dmax <= 64 ? 64 : 128;
+    // accumulators in a per-level ring (qw_ring.h): Q_w at qw_off, Z_w behind it
+    const QwRing ring = make_qw_ring(dq, lvl_off, nl, 2);
+    pool = ring.total;
+    for (int64_t k = 0; k < nw; ++k) dz[k].qw_off = dq[k].qw_off + (int64_t)dq[k].d * dq[k].d;
+    RingEvents ring_ev(ring.k > 0 && (dQ || dZ) ? ring.k : 0);
     const size_t ne = plan.sizes.size();
     DBuf<WinDesc> d_q(nw, s), d_z(nw, s);
     DBuf<double> d_pool(std::max<int64_t>(pool, 1), s);
     DBuf<uint8_t> d_sizes(ne + 1, s), d_sel(ne + 1, s), d_order(ne + 1, s), d_stuck(ne + 1, s);
-    DBuf<int32_t> d_status(std::max<int64_t>(nw, 1), s);
+    DBuf<int32_t> d_status(std::max<int64_t>(nw, 1), s), d_devlvl(1, s);
+    TEIG_CUDA(cudaMemsetAsync(d_devlvl.p, 0x7f, sizeof(int32_t), s));
     TEIG_CUDA(cudaMemcpyAsync(d_q.p, dq.data(), sizeof(WinDesc) * nw, cudaMemcpyHostToDevice, s));
     TEIG_CUDA(cudaMemcpyAsync(d_z.p, dz.data(), sizeof(WinDesc) * nw, cudaMemcpyHostToDevice, s));
     TEIG_CUDA(cudaMemcpyAsync(d_sizes.p, plan.sizes.data(), ne, cudaMemcpyHostToDevice, s));
@@ -115,8 +123,9 @@ GPass run_gpass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* d
     for (int L = 0; L < nl; ++L) {
         const int64_t o = lvl_off[L], cnt = lvl_off[L + 1] - lvl_off[L];
         if (!cnt) continue;
+        if (ring_ev.n && L >= ring.k) TEIG_CUDA(cudaStreamWaitEvent(s, ring_ev.ev[L % ring.k], 0));
         TEIG_CUDA(launch_gwindow_reorder(d_q.p + o, (int)cnt, dmax, dS, lds, dT, ldt, d_pool.p, d_sizes.p, d_sel.p,
-                                         d_order.p, d_stuck.p, d_status.p + o, s));
+                                         d_order.p, d_stuck.p, d_status.p + o, s, d_devlvl.p));
         ++launches;
         if (dQ || dZ) {  // factor updates on the second stream
             TEIG_CUDA(cudaEventRecord(ev, s));
@@ -129,6 +138,7 @@ GPass run_gpass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* d
                 TEIG_CUDA(launch_update_right(d_z.p + o, (int)cnt, (int)tq[L], dm, d_pool.p, dZ, ldz, (int)n, true, s2, n, n));
                 ++launches;
             }
+            if (ring_ev.n) TEIG_CUDA(cudaEventRecord(ring_ev.ev[L % ring.k], s2));
         }
         if (tl[L]) {
             TEIG_CUDA(launch_update_left(d_q.p + o, (int)cnt, (int)tl[L], dm, d_pool.p, dS, lds, (int)n, s, n, n));
@@ -154,7 +164,8 @@ GPass run_gpass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* d
     std::vector<int32_t> st_by_plan(nw);
     for (int64_t k = 0; k < nw; ++k) st_by_plan[idx[k]] = status[k];
     gp.deviated = fold_outcomes(plan, blocks, st_by_plan, order, stuck, rejected, plan_log, strict);
-    gp.windows = nw;
+    gp.windows = 0;
+    for (int64_t k = 0; k < nw; ++k) gp.windows += (status[k] & kWinSkipped) ? 0 : 1;
     gp.levels = nl;
     gp.launches = launches;
     return gp;
@@ -241,7 +252,7 @@ int teig_greorder_schur_device(int64_t n, double* dS, int64_t lds, double* dT, i
                                double* dZ, int64_t ldz, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
                                const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
                                teig_reorder_info* info, void* stream) {
-    keep_pool_memory();
+    DeviceGuard device_guard(dS);
     return greorder_schur_device(n, dS, lds, dT, ldt, dQ, ldq, dZ, ldz, nb, sizes, flags, opts, perm, rejected, info,
                                  (cudaStream_t)stream);
 }
@@ -250,7 +261,6 @@ int teig_greorder_schur_host(int64_t n, double* S, int64_t lds, double* T, int64
                              double* Z, int64_t ldz, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
                              const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
                              teig_reorder_info* info, void* stream_v) {
-    keep_pool_memory();
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (!S || !T) return set_error(-2, "S or T is null");
     if (lds < n || ldt < n) return set_error(-3, "lds/ldt < n");
@@ -264,7 +274,7 @@ int teig_greorder_schur_host(int64_t n, double* S, int64_t lds, double* T, int64
     try {
         for (int k = 0; k < 4; ++k)
             if (h[k]) {
-                TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d[k]), pitch * n, s));
+                TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&d[k]), pitch * n, s));
                 TEIG_CUDA(cudaMemcpy2DAsync(d[k], pitch, h[k], ld[k] * sizeof(double), pitch, n, cudaMemcpyHostToDevice, s));
             }
         rc = greorder_schur_device(n, d[0], n, d[1], n, d[2], n, d[3], n, nb, sizes, flags, opts, perm, rejected,
@@ -284,6 +294,7 @@ int teig_greorder_schur_host(int64_t n, double* S, int64_t lds, double* T, int64
 }
 
 int teig_gen_pair_t_device(int64_t n, double* dT, int64_t ldt, uint64_t seed, void* stream) {
+    DeviceGuard device_guard(dT);
     if (n < 1 || ldt < n) return set_error(-1, "bad shape");
     cudaError_t e = launch_gen_pair_t(dT, ldt, n, seed, (cudaStream_t)stream);
     return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));

@@ -50,6 +50,7 @@ struct GShared {
     int tcnt[4];
     int npairs;
     int executed;
+    int skipped;
     double Qm[kGMaxPairs][16], Zm[kGMaxPairs][16], An[kGMaxPairs][16], Bn[kGMaxPairs][16];
 };
 
@@ -153,7 +154,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
 gwindow_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S, long long lds, double* __restrict__ T,
                        long long ldt, double* __restrict__ qw_pool, const uint8_t* __restrict__ sizes_pool,
                        const uint8_t* __restrict__ sel_pool, uint8_t* __restrict__ order_pool,
-                       uint8_t* __restrict__ stuck_pool, int32_t* __restrict__ status) {
+                       uint8_t* __restrict__ stuck_pool, int32_t* __restrict__ status,
+                       int32_t* __restrict__ dev_level) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     GShared& sh = *reinterpret_cast<GShared*>(smem_raw);
     const WinDesc wd = wins[blockIdx.x];
@@ -180,7 +182,10 @@ gwindow_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S,
     }
     __syncthreads();
     if (tid == 0) {  // expected layout vs S's subdiagonal (reorder.cpp:132-154)
-        int row = 0, ok = 1;
+        // an earlier level deviated: this window's planned layout is stale
+        const bool skip = dev_level && __ldcg(dev_level) < wd.level;
+        int row = 0, ok = skip ? 0 : 1;
+        sh.skipped = skip;
         for (int b = 0; b < nb && ok; ++b) {
             const int sz = sh.bsz[b];
             if (row + sz > d) ok = 0;
@@ -188,7 +193,7 @@ gwindow_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S,
             else if (row + sz < d && Sw[(row + sz) + (row + sz - 1) * ld] != 0.0) ok = 0;
             row += sz;
         }
-        if (row != d) ok = 0;
+        if (ok && row != d) ok = 0;
         sh.executed = ok;
     }
     __syncthreads();
@@ -281,11 +286,12 @@ gwindow_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S,
         stuck_pool[wd.blk_off + tid] = sh.executed ? sh.bstuck[tid] : 0;
     }
     if (tid == 0) {
-        int32_t st = sh.executed ? kWinExecuted : 0;
+        int32_t st = sh.executed ? kWinExecuted : (sh.skipped ? kWinSkipped : 0);
         if (sh.executed)
             for (int b = 0; b < nb; ++b)
                 if (sh.bstuck[b]) st |= kWinStuck;
         status[blockIdx.x] = st;
+        if (dev_level && ((st & kWinStuck) || !(st & (kWinExecuted | kWinSkipped)))) atomicMin(dev_level, wd.level);
     }
 }
 
@@ -297,18 +303,15 @@ size_t gwindow_smem_bytes(int d) {
 cudaError_t launch_gwindow_reorder(const WinDesc* wins, int nwin, int dmax, double* S, long long lds, double* T,
                                    long long ldt, double* qw_pool, const uint8_t* sizes_pool,
                                    const uint8_t* sel_pool, uint8_t* order_pool, uint8_t* stuck_pool,
-                                   int32_t* status, cudaStream_t stream) {
+                                   int32_t* status, cudaStream_t stream, int32_t* dev_level) {
     if (nwin <= 0) return cudaSuccess;
     if (dmax > kGMaxD) return cudaErrorInvalidValue;
-    static bool init = false;
-    if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(gwindow_reorder_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)gwindow_smem_bytes(kGMaxD));
+    {
+        cudaError_t e = ensure_dyn_smem((const void*)gwindow_reorder_kernel, gwindow_smem_bytes(kGMaxD));
         if (e != cudaSuccess) return e;
-        init = true;
     }
     gwindow_reorder_kernel<<<nwin, kGThreads, gwindow_smem_bytes(dmax), stream>>>(
-        wins, S, lds, T, ldt, qw_pool, sizes_pool, sel_pool, order_pool, stuck_pool, status);
+        wins, S, lds, T, ldt, qw_pool, sizes_pool, sel_pool, order_pool, stuck_pool, status, dev_level);
     return cudaGetLastError();
 }
 

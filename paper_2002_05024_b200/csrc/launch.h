@@ -8,12 +8,35 @@
 
 namespace teig {
 
+// devctx.cpp: per-device (thread-safe) kernel attribute cache and SM count
+cudaError_t ensure_dyn_smem(const void* func, size_t bytes);
+int device_sm_count();
+// private per-device stream-ordered pool of the library (devctx.cpp) and its
+// retention policy (teig_set_memory_retention)
+cudaError_t lib_malloc_async(void** p, size_t bytes, cudaStream_t s);
+bool memory_retention();
+void set_memory_retention(bool on);
+void trim_memory_pools();
+struct DeviceGuard {  // current device := the device owning p (restored on exit)
+    explicit DeviceGuard(const void* p);
+    ~DeviceGuard();
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+    int prev_ = 0;
+    bool switched_ = false;
+};
+
 size_t window_reorder_smem_bytes(int dmax);
 
+// dev_level (nullable): the pass's deviation level.  A window of level L
+// (WinDesc::level) is skipped (status kWinSkipped, Q_w = I) when an earlier
+// level deviated (*dev_level < L); a window that deviates (a rejected swap or
+// a layout mismatch) lowers *dev_level to its level.  Initialise to INT_MAX.
 cudaError_t launch_window_reorder(const WinDesc* wins, int nwin, int dmax, double* S, long long lds,
                                   double* qw_pool, const uint8_t* sizes_pool, const uint8_t* sel_pool,
                                   uint8_t* order_pool, uint8_t* stuck_pool, int32_t* status,
-                                  cudaStream_t stream, unsigned long long* prof = nullptr);
+                                  cudaStream_t stream, unsigned long long* prof = nullptr,
+                                  int32_t* dev_level = nullptr);
 constexpr int kWindowThreads = 256;  // threads of the window kernel (8 warps)
 
 // rows/cols: the extent of the matrix `S`/`M` points at (absolute indices
@@ -23,19 +46,21 @@ cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dm
                                double* S, long long lds, int n, cudaStream_t stream, long long rows = -1,
                                long long cols = -1);
 
+// short_ctas: launch the bulk factor kernel as short CTAs (8 tiles each)
+// instead of a persistent grid -- for a caller that runs the factor updates on
+// a LOW-priority stream beside a critical path, so critical-path CTAs take SMs
+// as they free up.
 cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
                                 double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream,
-                                long long rows = -1, long long cols = -1);
+                                long long rows = -1, long long cols = -1, bool short_ctas = false);
 
 // update_tma.cu: false = not eligible (caller falls back), *err = launch status
 bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* S,
                             long long lds, long long rows, long long cols, cudaStream_t stream, cudaError_t* err);
 bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* M,
                              long long ldm, long long rows, long long cols, bool factor, cudaStream_t stream,
-                             cudaError_t* err);
+                             cudaError_t* err, bool short_ctas = false);
 
-// keep the stream-ordered allocator's memory between calls (reorder_driver.cpp)
-void keep_pool_memory();
 
 // synthetic inputs (generate.cu)
 cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64_t fill_seed,
@@ -48,7 +73,7 @@ size_t gwindow_smem_bytes(int d);
 cudaError_t launch_gwindow_reorder(const WinDesc* wins, int nwin, int dmax, double* S, long long lds, double* T,
                                    long long ldt, double* qw_pool, const uint8_t* sizes_pool,
                                    const uint8_t* sel_pool, uint8_t* order_pool, uint8_t* stuck_pool,
-                                   int32_t* status, cudaStream_t stream);
+                                   int32_t* status, cudaStream_t stream, int32_t* dev_level = nullptr);
 cudaError_t launch_gen_schur_cols(double* S, long long lds, long long n, uint64_t fill_seed, long long c0,
                                   long long c1, cudaStream_t stream);
 cudaError_t launch_identity_rows(double* Q, long long ldq, long long n, long long r0, long long r1,
@@ -74,6 +99,8 @@ cudaError_t launch_hess_norm(const double* H, long long ldh, int n, unsigned lon
 cudaError_t launch_scan_active(double* H, long long ldh, int n, int ihi, double hnorm, int* out,
                                cudaStream_t stream);
 
+// distributed deviation flag: mode 0 publish into the level's slot, 1 absorb
+cudaError_t launch_dist_flag(int32_t* dev_level, double* slot, int level, int mode, cudaStream_t s);
 // element-wise sum of nbuf device buffers into all of them (loopback all-reduce)
 cudaError_t launch_sum_buffers(void* const* bufs, int nbuf, size_t count, int elem_bytes, cudaStream_t s);
 

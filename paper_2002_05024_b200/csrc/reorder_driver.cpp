@@ -20,6 +20,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <cstdlib>
 #include <stdexcept>
@@ -30,6 +31,7 @@
 #include "device_types.h"
 #include "launch.h"
 #include "plan.h"
+#include "qw_ring.h"
 
 namespace teig {
 
@@ -60,6 +62,24 @@ int64_t default_tile_size(int64_t n) {
 // window in plan order; order/stuck: per-block pools (WinDesc::blk_off).
 // Returns true when a window deviated from the plan (rejection or layout
 // mismatch), i.e. a replanning pass is needed.
+//
+// Deviation semantics.  The reference plans one group at a time and stops
+// folding at the first deviating window (reorder.cpp:372-395); here all
+// groups' chains are planned up front and pipelined, so windows of later
+// groups may already have run when a window deviates.  The window kernels
+// carry a device-side deviation level (window_reorder.cu): once a window of
+// level L deviates, every window of a level > L is skipped (status
+// kWinSkipped, Q_w = I).  Every window that did run therefore ran on exactly
+// its planned layout (no deviation before its level means the plan's
+// simulated state is the true state), and folding the executed windows in
+// plan order reproduces the device's block arrangement; the skipped windows
+// are replanned from that state in the next pass.  Windows that ran at
+// levels <= L but belong to groups after the deviating one are folded too
+// (the reference would not have run them yet): the final permutation and the
+// rejected blocks agree with the reference whenever its swap decisions do,
+// and a stale plan can never move an unselected block (the reference's own
+// caveat).  `plan` logs every window that ran or deviated, not the
+// skipped ones.
 bool fold_outcomes(const ReorderPlan& plan, std::vector<BlockState>& blocks, const std::vector<int32_t>& st_by_plan,
                    const std::vector<uint8_t>& order, const std::vector<uint8_t>& stuck,
                    std::vector<int64_t>& rejected, std::vector<int64_t>& plan_log, bool strict) {
@@ -70,10 +90,14 @@ bool fold_outcomes(const ReorderPlan& plan, std::vector<BlockState>& blocks, con
     std::vector<BlockState> slice;
     for (int64_t wi = 0; wi < nw; ++wi) {
         const PlannedWindow& w = plan.windows[wi];
+        const int32_t st = st_by_plan[wi];
+        if (st & kWinSkipped) {
+            deviated = true;
+            continue;
+        }
         plan_log.push_back(w.wtop);
         plan_log.push_back(w.wbot - w.wtop);
         plan_log.push_back(w.count);
-        const int32_t st = st_by_plan[wi];
         if (!(st & kWinExecuted)) {
             deviated = true;
             continue;
@@ -108,7 +132,7 @@ struct DevBuf {
     cudaStream_t s = nullptr;
     DevBuf() = default;
     DevBuf(size_t bytes, cudaStream_t st) : s(st) {
-        if (bytes) TEIG_CUDA(cudaMallocAsync(&p, bytes, st));
+        if (bytes) TEIG_CUDA(lib_malloc_async(&p, bytes, st));
     }
     ~DevBuf() {
         if (p) cudaFreeAsync(p, s);
@@ -119,22 +143,41 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
-// Device staging of the host entry points: kept between calls (the host path
-// of a 40000-order problem stages 25.6 GB; mapping it anew every call cost
-// 0.14-0.95 s and slowed the first kernels that touched it).  One cache per
-// process, grown on demand, guarded for concurrent host calls; the
-// TEIG_NO_HOST_CACHE=1 environment variable allocates per call instead.
+// Device staging of the host entry points.  With memory retention on
+// (teig_set_memory_retention) it is kept between calls (the host path of a
+// 40000-order problem stages 25.6 GB; mapping it anew every call cost
+// 0.14-0.95 s and slowed the first kernels that touched it): one cache per
+// DEVICE, grown on demand, guarded for concurrent host calls.  Off (the
+// default): allocated per call.
 struct HostStaging {
     std::mutex mu;
     void* p = nullptr;
     size_t bytes = 0;
-    ~HostStaging() {
-        if (p) cudaFree(p);
+    int dev = 0;
+    void release() {
+        if (p) {
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(dev);
+            cudaFree(p);
+            cudaSetDevice(cur);
+        }
+        p = nullptr;
+        bytes = 0;
     }
 };
+std::mutex g_staging_mu;
+std::map<int, HostStaging*> g_staging;
 HostStaging& host_staging() {
-    static HostStaging hs;
-    return hs;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_staging_mu);
+    HostStaging*& hs = g_staging[dev];
+    if (!hs) {
+        hs = new HostStaging;  // lives for the process (released by teig_release_memory)
+        hs->dev = dev;
+    }
+    return *hs;
 }
 
 struct PassResult {
@@ -193,7 +236,8 @@ struct HostDrain {
 PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq,
                     std::vector<BlockState>& blocks, std::vector<int64_t>& rejected,
                     std::vector<int64_t>& plan_log, bool strict, bool overlap, bool profile,
-                    cudaStream_t stream, cudaStream_t stream2, cudaEvent_t ev, HostDrain* drain = nullptr) {
+                    cudaStream_t stream, cudaStream_t stream2, cudaEvent_t ev, bool short_q,
+                    HostDrain* drain = nullptr) {
     PassResult pr;
     EventLog lg;
     lg.on = profile;
@@ -216,7 +260,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         dsc.a = (int32_t)w.wtop;
         dsc.d = (int32_t)(w.wbot - w.wtop);
         dsc.nb = (int32_t)w.count;
-        dsc.flags = 0;
+        dsc.level = L;
         dsc.qw_off = qw_total;
         qw_total += (int64_t)dsc.d * dsc.d;
         dsc.blk_off = w.blk_off;
@@ -238,6 +282,11 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     }
     for (int L = 0; L < nl; ++L) lvl_off[L + 1] += lvl_off[L];
     const int dmax_k = dmax <= 64 ? 64 : 128;
+    // Q_w ring: level L's accumulators live in region L % K; region reuse by
+    // level L + K waits for level L's factor update (the only reader not
+    // already ordered before it on the critical-path stream)
+    const QwRing ring = make_qw_ring(descs, lvl_off, nl, 1);
+    qw_total = ring.total;
     // early host drain: max b / min a over the levels after L
     std::vector<int64_t> after_hi, after_lo;
     if (drain && drain->valid) {
@@ -256,12 +305,14 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     const size_t ne = plan.sizes.size();
     DevBuf d_desc(sizeof(WinDesc) * nw, stream), d_qw(sizeof(double) * std::max<int64_t>(qw_total, 1), stream),
         d_sizes(ne + 1, stream), d_sel(ne + 1, stream), d_order(ne + 1, stream), d_stuck(ne + 1, stream),
-        d_status(sizeof(int32_t) * nw, stream);
+        d_status(sizeof(int32_t) * nw, stream), d_devlvl(sizeof(int32_t), stream);
+    TEIG_CUDA(cudaMemsetAsync(d_devlvl.p, 0x7f, sizeof(int32_t), stream));
     TEIG_CUDA(cudaMemcpyAsync(d_desc.p, descs.data(), sizeof(WinDesc) * nw, cudaMemcpyHostToDevice, stream));
     TEIG_CUDA(cudaMemcpyAsync(d_sizes.p, plan.sizes.data(), ne, cudaMemcpyHostToDevice, stream));
     TEIG_CUDA(cudaMemcpyAsync(d_sel.p, plan.sel.data(), ne, cudaMemcpyHostToDevice, stream));
 
     const WinDesc* dd = d_desc.as<WinDesc>();
+    RingEvents ring_ev(ring.k > 0 && dQ && overlap ? ring.k : 0);
     int64_t launches = 0;
     // TEIG_WINDOW_PROF=1: per-warp phase timing of every window CTA (diagnostics)
     static const bool wprof = getenv("TEIG_WINDOW_PROF") && atoi(getenv("TEIG_WINDOW_PROF")) != 0;
@@ -283,19 +334,22 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         if (launch_log)
             fprintf(stderr, "[teig level] %d windows %lld left_tiles %lld right_tiles %lld factor_tiles %lld\n", L,
                     (long long)cnt, (long long)tl[L], (long long)tr[L], (long long)tq[L]);
+        if (ring_ev.n && L >= ring.k) TEIG_CUDA(cudaStreamWaitEvent(stream, ring_ev.ev[L % ring.k], 0));
         timed(0, stream, cnt, [&] {
             return launch_window_reorder(dd + o, (int)cnt, dmax_k, dS, lds, d_qw.as<double>(), d_sizes.as<uint8_t>(),
                                          d_sel.as<uint8_t>(), d_order.as<uint8_t>(), d_stuck.as<uint8_t>(),
                                          d_status.as<int32_t>() + o, stream,
-                                         wprof ? d_prof.as<unsigned long long>() + o * (kWindowThreads / 32) * 4 : nullptr);
+                                         wprof ? d_prof.as<unsigned long long>() + o * (kWindowThreads / 32) * 4 : nullptr,
+                                         d_devlvl.as<int32_t>());
         });
         if (dQ && overlap) {
             TEIG_CUDA(cudaEventRecord(ev, stream));
             TEIG_CUDA(cudaStreamWaitEvent(stream2, ev, 0));
             timed(3, stream2, tq[L], [&] {
                 return launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
-                                           true, stream2, n, n);
+                                           true, stream2, n, n, short_q);
             });
+            if (ring_ev.n) TEIG_CUDA(cudaEventRecord(ring_ev.ev[L % ring.k], stream2));
         }
         timed(1, stream, tl[L], [&] {
             return launch_update_left(dd + o, (int)cnt, (int)tl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n, stream,
@@ -376,7 +430,8 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     std::vector<int32_t> st_by_plan(nw);
     for (int64_t k = 0; k < nw; ++k) st_by_plan[idx[k]] = status[k];
     pr.deviated = fold_outcomes(plan, blocks, st_by_plan, order, stuck, rejected, plan_log, strict);
-    pr.windows = nw;
+    pr.windows = 0;
+    for (int32_t st : status) pr.windows += (st & kWinSkipped) ? 0 : 1;  // = entries logged in `plan`
     pr.levels = nl;
     pr.launches = launches;
     if (lg.on) {
@@ -394,56 +449,60 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
 // CTAs take SMs ahead of pending Q-update CTAs as they free up: C2 (n=10000,
 // window kernels ~50 % of the step) 0.161 -> 0.149 s, C4 unchanged.
 // TEIG_NO_PRIO=1: both on default priority, Q updates persistent.
+// Whatever happens inside the call (a CUDA error thrown mid-pass included),
+// the destructor joins both internal streams into the caller's stream before
+// releasing them, so no enqueued work outlives the call unordered.
 struct StreamPair {
     cudaStream_t s1 = nullptr, s2 = nullptr, caller = nullptr;
     cudaEvent_t ev = nullptr, join = nullptr;
+    bool prio = true;
     explicit StreamPair(cudaStream_t user) : s1(user), caller(user) {
-        const bool prio = !(getenv("TEIG_NO_PRIO") && atoi(getenv("TEIG_NO_PRIO")));
-        int least = 0, greatest = 0;
-        TEIG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        TEIG_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, prio ? least : 0));
-        TEIG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        TEIG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-        if (prio) {
-            TEIG_CUDA(cudaStreamCreateWithPriority(&s1, cudaStreamNonBlocking, greatest));
-            TEIG_CUDA(cudaEventRecord(join, user));
-            TEIG_CUDA(cudaStreamWaitEvent(s1, join, 0));
+        prio = !(getenv("TEIG_NO_PRIO") && atoi(getenv("TEIG_NO_PRIO")));
+        try {
+            int least = 0, greatest = 0;
+            TEIG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            TEIG_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, prio ? least : 0));
+            TEIG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            TEIG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+            if (prio) {
+                cudaStream_t hi = nullptr;
+                TEIG_CUDA(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, greatest));
+                s1 = hi;
+                TEIG_CUDA(cudaEventRecord(join, user));
+                TEIG_CUDA(cudaStreamWaitEvent(s1, join, 0));
+            }
+        } catch (...) {
+            release();
+            throw;
         }
     }
+    // the factor updates run in short CTAs on the low-priority stream
+    bool short_factor_ctas(bool overlap) const { return prio && overlap; }
     void finish() {
         if (s1 != caller) {
             TEIG_CUDA(cudaEventRecord(join, s1));
             TEIG_CUDA(cudaStreamWaitEvent(caller, join, 0));
         }
     }
-    ~StreamPair() {
+    void release() {
+        // join (errors ignored: this also runs on the error path)
+        if (join) {
+            if (s2 && cudaEventRecord(join, s2) == cudaSuccess) cudaStreamWaitEvent(caller, join, 0);
+            if (s1 && s1 != caller && cudaEventRecord(join, s1) == cudaSuccess) cudaStreamWaitEvent(caller, join, 0);
+        }
         if (ev) cudaEventDestroy(ev);
         if (join) cudaEventDestroy(join);
         if (s2) cudaStreamDestroy(s2);
         if (s1 && s1 != caller) cudaStreamDestroy(s1);
+        ev = join = nullptr;
+        s2 = nullptr;
+        s1 = caller;
+        cudaGetLastError();
     }
+    ~StreamPair() { release(); }
 };
 
 }  // namespace
-
-// The per-pass device buffers (window descriptors, the Q_w pool: 6.4 GB at
-// n=40000) come from the stream-ordered allocator; keep what it maps instead
-// of returning it at every synchronisation (TEIG_POOL_RELEASE=1: default
-// behaviour), so repeated calls do not remap gigabytes each time.
-void keep_pool_memory() {
-    static bool done = false;
-    if (done) return;
-    done = true;
-    if (getenv("TEIG_POOL_RELEASE") && atoi(getenv("TEIG_POOL_RELEASE"))) return;
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) {
-        cudaGetLastError();
-        return;
-    }
-    uint64_t keep = UINT64_MAX;
-    if (cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep) != cudaSuccess) cudaGetLastError();
-}
 
 int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq, int64_t nb,
                          const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
@@ -454,7 +513,6 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
     if (!dS) return set_error(-2, "S is null");
     if (lds < n) return set_error(-3, "lds < n");
     if (dQ && ldq < n) return set_error(-5, "ldq < n");
-    keep_pool_memory();
     if (nb < 0 || (nb > 0 && (!sizes || !flags))) return set_error(-6, "malformed selection");
     teig_reorder_opts o;
     teig_reorder_opts_default(&o);
@@ -497,6 +555,7 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
             }
             PassResult pr = run_pass(plan, n, dS, lds, dQ, ldq, blocks, rejected, plan_log, o.strict != 0,
                                      o.overlap_factor != 0, o.profile != 0, sp.s1, sp.s2, sp.ev,
+                                     sp.short_factor_ctas(o.overlap_factor != 0),
                                      pass == 0 ? drain : nullptr);
             inf.n_windows += pr.windows;
             inf.n_levels += pr.levels;
@@ -562,16 +621,29 @@ int teig_reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, in
                               const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
                               int64_t* perm, int64_t* rejected, int64_t* plan, int64_t plan_cap,
                               teig_reorder_info* info, void* stream) {
+    DeviceGuard device_guard(dS);
     return reorder_schur_device(n, dS, lds, dQ, ldq, nb, sizes, flags, opts, perm, rejected, plan, plan_cap, info,
                                 (cudaStream_t)stream);
 }
 
 void teig_release_host_staging(void) {
-    HostStaging& hs = host_staging();
-    std::lock_guard<std::mutex> g(hs.mu);
-    if (hs.p) cudaFree(hs.p);
-    hs.p = nullptr;
-    hs.bytes = 0;
+    std::lock_guard<std::mutex> lk(g_staging_mu);
+    for (auto& kv : g_staging) {
+        std::lock_guard<std::mutex> g(kv.second->mu);
+        kv.second->release();
+    }
+}
+
+void teig_set_memory_retention(int32_t on) {
+    set_memory_retention(on != 0);
+    if (!on) teig_release_host_staging();
+}
+
+int32_t teig_memory_retention(void) { return memory_retention() ? 1 : 0; }
+
+void teig_release_memory(void) {
+    teig_release_host_staging();
+    trim_memory_pools();
 }
 
 int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_t ldq, int64_t nb,
@@ -589,7 +661,7 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
     auto now = [] { return std::chrono::steady_clock::now(); };
     auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
     const auto h0 = now();
-    const bool no_cache = getenv("TEIG_NO_HOST_CACHE") && atoi(getenv("TEIG_NO_HOST_CACHE"));
+    const bool no_cache = !memory_retention();
     HostStaging& hs = host_staging();
     std::unique_lock<std::mutex> lock(hs.mu, std::defer_lock);
     try {
@@ -711,6 +783,7 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
 }
 
 int64_t teig_scan_blocks_device(int64_t n, const double* dS, int64_t lds, uint8_t* sizes, void* stream_v) {
+    DeviceGuard device_guard(dS);
     if (n < 1) return set_error(-1, "n must be >= 1");
     cudaStream_t stream = (cudaStream_t)stream_v;
     std::vector<double> sub(n > 1 ? n - 1 : 1, 0.0);
@@ -811,6 +884,7 @@ int teig_select_fraction(int64_t nb, double fraction, uint64_t seed, uint8_t* fl
 int teig_window_reorder_device(int64_t d, double* dW, int64_t ldw, int64_t nb, const uint8_t* sizes,
                                const uint8_t* sel, double* dAcc, uint32_t* order, uint8_t* stuck,
                                int32_t* executed, void* stream_v) {
+    DeviceGuard device_guard(dW);
     if (d < 1 || d > 128) return set_error(d < 1 ? -1 : TEIG_ERR_UNSUPPORTED, "window order must be in [1, 128]");
     if (ldw < d) return set_error(-3, "ldw < d");
     if (nb < 1 || nb > d) return set_error(-4, "bad block count");
@@ -849,6 +923,7 @@ int teig_window_reorder_device(int64_t d, double* dW, int64_t ldw, int64_t nb, c
 
 int teig_apply_window_updates_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq, int64_t a,
                                      int64_t d, const double* dQw, void* stream_v) {
+    DeviceGuard device_guard(dS);
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (lds < n) return set_error(-3, "lds < n");
     if (dQ && ldq < n) return set_error(-5, "ldq < n");
@@ -884,19 +959,59 @@ int teig_apply_window_updates_device(int64_t n, double* dS, int64_t lds, double*
     return 0;
 }
 
+int teig_update_panel_device(int32_t side, int64_t d, const double* dQw, int64_t a, double* dM, int64_t ldm,
+                             int64_t rows, int64_t cols, int64_t i0, int64_t i1, void* stream_v) {
+    DeviceGuard device_guard(dM);
+    if (side < 0 || side > 2) return set_error(-1, "side must be 0 (left), 1 (right) or 2 (factor)");
+    if (d < 1 || d > 128) return set_error(d < 1 ? -2 : TEIG_ERR_UNSUPPORTED, "window order must be in [1, 128]");
+    if (!dQw || !dM) return set_error(-3, "null pointer");
+    if (ldm < rows || rows < 1 || cols < 1) return set_error(-6, "bad extent");
+    if (a < 0 || i0 < 0 || i1 < i0) return set_error(-5, "bad range");
+    if (side == 0 ? (a + d > rows || i1 > cols) : (a + d > cols || i1 > rows)) return set_error(-5, "range outside M");
+    if (i1 == i0) return 0;
+    cudaStream_t stream = (cudaStream_t)stream_v;
+    try {
+        WinDesc wd{};
+        wd.a = (int32_t)a;
+        wd.d = (int32_t)d;
+        wd.lc0 = (int32_t)i0;
+        wd.lc1 = (int32_t)i1;
+        wd.rr0 = wd.qr0 = (int32_t)i0;
+        wd.rr1 = wd.qr1 = (int32_t)i1;
+        DevBuf ddesc(sizeof(WinDesc), stream);
+        TEIG_CUDA(cudaMemcpyAsync(ddesc.p, &wd, sizeof wd, cudaMemcpyHostToDevice, stream));
+        const int dm = d <= 64 ? 64 : 128;
+        if (side == 0) {
+            const int tiles = (int)((i1 - i0 + kLeftBN - 1) / kLeftBN);
+            TEIG_CUDA(launch_update_left(ddesc.as<WinDesc>(), 1, tiles, dm, dQw, dM, ldm, (int)rows, stream, rows, cols));
+        } else {
+            const int tiles = (int)((i1 - i0 + kRightBM - 1) / kRightBM);
+            TEIG_CUDA(launch_update_right(ddesc.as<WinDesc>(), 1, tiles, dm, dQw, dM, ldm, (int)rows, side == 2, stream,
+                                          rows, cols));
+        }
+        TEIG_CUDA(cudaStreamSynchronize(stream));
+    } catch (const std::exception& e) {
+        return set_error(TEIG_ERR_CUDA, e.what());
+    }
+    return 0;
+}
+
 int teig_gen_schur_input_device(int64_t n, double* dS, int64_t lds, uint64_t fill_seed, void* stream) {
+    DeviceGuard device_guard(dS);
     if (n < 1 || lds < n) return set_error(-1, "bad shape");
     cudaError_t e = launch_gen_schur_input(dS, lds, n, fill_seed, (cudaStream_t)stream);
     return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));
 }
 
 int teig_gen_hessenberg_device(int64_t n, double* dH, int64_t ldh, uint64_t seed, void* stream) {
+    DeviceGuard device_guard(dH);
     if (n < 1 || ldh < n) return set_error(-1, "bad shape");
     cudaError_t e = launch_gen_hessenberg(dH, ldh, n, seed, (cudaStream_t)stream);
     return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));
 }
 
 int teig_set_identity_device(int64_t n, double* dQ, int64_t ldq, void* stream) {
+    DeviceGuard device_guard(dQ);
     if (n < 1 || ldq < n) return set_error(-1, "bad shape");
     cudaError_t e = launch_set_identity(dQ, ldq, n, (cudaStream_t)stream);
     return e == cudaSuccess ? 0 : set_error(TEIG_ERR_CUDA, cudaGetErrorString(e));

@@ -254,12 +254,9 @@ int chase_window_packed_len(int d) {
 
 cudaError_t launch_chase_window(double* H, long long ldh, const ChaseWin* wins_dev, int idx, int d,
                                 const double* shift_pairs, double* qw_pool, cudaStream_t stream) {
-    static bool init = false;
-    if (!init) {
-        cudaError_t err = cudaFuncSetAttribute(chase_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)chase_window_smem_bytes(kChaseMaxWindow));
+    {
+        cudaError_t err = ensure_dyn_smem((const void*)chase_window_kernel, chase_window_smem_bytes(kChaseMaxWindow));
         if (err != cudaSuccess) return err;
-        init = true;
     }
     chase_window_kernel<<<1, NTC, chase_window_smem_bytes(d), stream>>>(H, ldh, wins_dev + idx, shift_pairs, qw_pool);
     return cudaGetLastError();

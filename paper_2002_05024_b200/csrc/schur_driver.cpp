@@ -156,7 +156,7 @@ struct Grow {  // device buffer that only grows
         if (cnt <= cap) return;
         if (p) TEIG_CUDA(cudaFreeAsync(p, s));
         cap = std::max(cnt, cap * 2);
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), cap * sizeof(T), s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&p), cap * sizeof(T), s));
     }
     void release(cudaStream_t s) {
         if (p) cudaFreeAsync(p, s);
@@ -182,13 +182,13 @@ class SchurRunner {
         TEIG_CUDA(cudaMallocHost(&h_out_, sizeof(AedDevOut) + sizeof(int) * 4 + sizeof(double) * 2 * kAedMaxWindow + 64));
         h_int_ = reinterpret_cast<int*>(h_out_ + 1);
         h_sh_ = reinterpret_cast<double*>(h_int_ + 4);
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_out_), sizeof(AedDevOut), s_));
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_int_), sizeof(unsigned long long) * 2, s_));
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_sh_), sizeof(double) * 2 * kAedMaxWindow, s_));
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_snap_),
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&d_out_), sizeof(AedDevOut), s_));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&d_int_), sizeof(unsigned long long) * 2, s_));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&d_sh_), sizeof(double) * 2 * kAedMaxWindow, s_));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&d_snap_),
                                   sizeof(double) * 2 * kAedMaxWindow * kAedMaxWindow, s_));
         if (getenv("TEIG_AED_PROF") && atoi(getenv("TEIG_AED_PROF"))) {
-            TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d_prof_), sizeof(unsigned long long) * 16, s_));
+            TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&d_prof_), sizeof(unsigned long long) * 16, s_));
             TEIG_CUDA(cudaMemsetAsync(d_prof_, 0, sizeof(unsigned long long) * 16, s_));
         }
     }
@@ -713,13 +713,12 @@ int teig_deflation_check(double spike, double diag_sum, int32_t deflation, doubl
 
 int teig_schur_reduce_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t ldq, const teig_schur_opts* o,
                              double* eig_re, double* eig_im, teig_schur_info* info, void* stream) {
-    keep_pool_memory();
+    DeviceGuard device_guard(dH);
     return schur_reduce_device(n, dH, ldh, dQ, ldq, o, eig_re, eig_im, info, (cudaStream_t)stream);
 }
 
 int teig_schur_reduce_host(int64_t n, double* H, int64_t ldh, double* Q, int64_t ldq, const teig_schur_opts* o,
                            double* eig_re, double* eig_im, teig_schur_info* info, void* stream_v) {
-    keep_pool_memory();
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (!H) return set_error(-2, "H is null");
     if (ldh < n) return set_error(-3, "ldh < n");
@@ -729,8 +728,8 @@ int teig_schur_reduce_host(int64_t n, double* H, int64_t ldh, double* Q, int64_t
     int rc = 0;
     try {
         const size_t pitch = (size_t)n * sizeof(double);
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dH), pitch * n, stream));
-        if (Q) TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dQ), pitch * n, stream));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&dH), pitch * n, stream));
+        if (Q) TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&dQ), pitch * n, stream));
         TEIG_CUDA(cudaMemcpy2DAsync(dH, pitch, H, ldh * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
         if (Q) TEIG_CUDA(cudaMemcpy2DAsync(dQ, pitch, Q, ldq * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
         rc = schur_reduce_device(n, dH, n, dQ, n, o, eig_re, eig_im, info, stream);
@@ -749,6 +748,7 @@ int teig_schur_reduce_host(int64_t n, double* H, int64_t ldh, double* Q, int64_t
 
 int teig_aed_step_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t ldq, int64_t l, int64_t ihi,
                          int64_t window, const teig_schur_opts* opts, teig_aed_result* r, double* shifts, void* stream) {
+    DeviceGuard device_guard(dH);
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (!dH || ldh < n) return set_error(-3, "bad H");
     if (dQ && ldq < n) return set_error(-5, "ldq < n");
@@ -786,6 +786,7 @@ int teig_aed_step_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t
 
 int teig_introduce_bulges_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t ldq, int64_t l, int64_t ihi,
                                  int64_t nshifts, const double* shifts, int64_t* positions, void* stream) {
+    DeviceGuard device_guard(dH);
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (!dH || ldh < n) return set_error(-3, "bad H");
     if (dQ && ldq < n) return set_error(-5, "ldq < n");
@@ -821,6 +822,7 @@ int teig_introduce_bulges_device(int64_t n, double* dH, int64_t ldh, double* dQ,
 int teig_chase_bulges_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t ldq, int64_t chain_end,
                              int64_t nb, const int64_t* positions, int64_t window_size, int64_t* n_windows,
                              void* stream) {
+    DeviceGuard device_guard(dH);
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (!dH || ldh < n) return set_error(-3, "bad H");
     if (dQ && ldq < n) return set_error(-5, "ldq < n");
@@ -852,6 +854,7 @@ int teig_chase_bulges_device(int64_t n, double* dH, int64_t ldh, double* dQ, int
 }
 
 int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int32_t* converged, void* stream) {
+    DeviceGuard device_guard(dH);
     if (k < 1) return set_error(-1, "k must be >= 1");
     if (!dH || ldh < k) return set_error(-3, "bad H");
     if (!dQ) return set_error(-4, "Q is null");
@@ -862,7 +865,7 @@ int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int3
         AedDevOut* dout = nullptr;
         AedDevOut hout{};
         cudaStream_t s = (cudaStream_t)stream;
-        TEIG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dout), sizeof(AedDevOut), s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&dout), sizeof(AedDevOut), s));
         SchurDevOpts d{o.deflation, o.shift_count, o.aed_window, o.small_threshold, 0};
         TEIG_CUDA(launch_aed_window(dH, ldh, kSchurModeSmall, 0, 0, (int)k, d, dQ, dout, nullptr, s));
         TEIG_CUDA(cudaMemcpyAsync(&hout, dout, sizeof hout, cudaMemcpyDeviceToHost, s));

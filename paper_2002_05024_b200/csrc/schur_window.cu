@@ -1705,12 +1705,9 @@ cudaError_t launch_aed_window(double* H, long long ldh, int mode, int l, int e, 
                               double* qw_out, AedDevOut* out, double* shifts_out, cudaStream_t stream,
                               unsigned long long* prof, double* snap) {
     const size_t smem = aed_window_smem_bytes(w);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t err = cudaFuncSetAttribute(aed_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               (int)aed_window_smem_bytes(kAedMaxWindow));
+    {
+        cudaError_t err = ensure_dyn_smem((const void*)aed_window_kernel, aed_window_smem_bytes(kAedMaxWindow));
         if (err != cudaSuccess) return err;
-        configured = aed_window_smem_bytes(kAedMaxWindow);
     }
     aed_window_kernel<<<1, NT, smem, stream>>>(H, ldh, mode, l, e, w, o, qw_out, out, shifts_out, prof, snap);
     return cudaGetLastError();

@@ -296,7 +296,7 @@ update_right_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __
 
 template <typename K>
 static cudaError_t set_smem(K kernel, size_t bytes) {
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    return ensure_dyn_smem((const void*)kernel, bytes);
 }
 
 constexpr size_t left_smem(int dmax) { return (size_t)STAGES * (dmax * LDK + kLeftBN * LDK) * sizeof(double); }
@@ -309,12 +309,10 @@ cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dm
         cudaError_t err;
         if (launch_update_left_tma(wins, nwin, ntiles, dmax, qw_pool, S, lds, rows, cols, stream, &err)) return err;
     }
-    static bool init = false;
-    if (!init) {
+    {
         cudaError_t e = set_smem(update_left_kernel<64>, left_smem(64));
         if (e == cudaSuccess) e = set_smem(update_left_kernel<128>, left_smem(128));
         if (e != cudaSuccess) return e;
-        init = true;
     }
     if (dmax <= 64)
         update_left_kernel<64><<<ntiles, kUpdThreads, left_smem(64), stream>>>(wins, nwin, qw_pool, S, lds, n);
@@ -325,21 +323,20 @@ cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dm
 
 cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
                                 double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream,
-                                long long rows, long long cols) {
+                                long long rows, long long cols, bool short_ctas) {
     if (ntiles <= 0) return cudaSuccess;
     if (rows > 0) {
         cudaError_t err;
-        if (launch_update_right_tma(wins, nwin, ntiles, dmax, qw_pool, M, ldm, rows, cols, factor, stream, &err))
+        if (launch_update_right_tma(wins, nwin, ntiles, dmax, qw_pool, M, ldm, rows, cols, factor, stream, &err,
+                                    short_ctas))
             return err;
     }
-    static bool init = false;
-    if (!init) {
+    {
         cudaError_t e = set_smem(update_right_kernel<64, 1>, right_smem(64));
         if (e == cudaSuccess) e = set_smem(update_right_kernel<64, 2>, right_smem(64));
         if (e == cudaSuccess) e = set_smem(update_right_kernel<128, 1>, right_smem(128));
         if (e == cudaSuccess) e = set_smem(update_right_kernel<128, 2>, right_smem(128));
         if (e != cudaSuccess) return e;
-        init = true;
     }
     const size_t sm = right_smem(dmax <= 64 ? 64 : 128);
     if (dmax <= 64) {

@@ -473,13 +473,7 @@ constexpr size_t kRightSmem = (size_t)kRStages * kRightStage;
 
 // one CTA per SM while every CTA gets >= kMinTilesPerCta tiles
 int grid_for(int ntiles) {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    const int sms = device_sm_count();
     return std::max(1, std::min(sms, (ntiles + kMinTilesPerCta - 1) / kMinTilesPerCta));
 }
 
@@ -495,13 +489,8 @@ bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax,
     *err = cudaSuccess;
     if (ntiles <= 0) return true;
     if (!bulk_eligible(dmax, S, lds, rows, cols)) return false;
-    static bool init = false;
-    if (!init) {
-        *err = cudaFuncSetAttribute(update_left_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kLeftSmem);
-        if (*err != cudaSuccess) return true;
-        init = true;
-    }
+    *err = ensure_dyn_smem((const void*)update_left_bulk_kernel, kLeftSmem);
+    if (*err != cudaSuccess) return true;
     const int grid = grid_for(ntiles);
     update_left_bulk_kernel<<<grid, kBulkThreads, kLeftSmem, stream>>>(wins, nwin, ntiles, qw_pool, S, lds,
                                                                         (cols - 1) * lds + rows);
@@ -511,24 +500,17 @@ bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax,
 
 bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* M,
                              long long ldm, long long rows, long long cols, bool factor, cudaStream_t stream,
-                             cudaError_t* err) {
+                             cudaError_t* err, bool short_ctas) {
     *err = cudaSuccess;
     if (ntiles <= 0) return true;
     if (!bulk_eligible(dmax, M, ldm, rows, cols)) return false;
-    static bool init = false;
-    if (!init) {
-        *err = cudaFuncSetAttribute(update_right_bulk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)kRightSmem);
-        if (*err == cudaSuccess)
-            *err = cudaFuncSetAttribute(update_right_bulk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        (int)kRightSmem);
-        if (*err != cudaSuccess) return true;
-        init = true;
-    }
-    // Q updates (off the critical path, low-priority stream): short CTAs of 8
-    // tiles, so window-kernel CTAs can take SMs as they free up
-    static const bool persistent_q = getenv("TEIG_NO_PRIO") && atoi(getenv("TEIG_NO_PRIO"));
-    const int grid = (factor && !persistent_q) ? (ntiles + 7) / 8 : grid_for(ntiles);
+    *err = ensure_dyn_smem((const void*)update_right_bulk_kernel<1>, kRightSmem);
+    if (*err == cudaSuccess) *err = ensure_dyn_smem((const void*)update_right_bulk_kernel<2>, kRightSmem);
+    if (*err != cudaSuccess) return true;
+    // short_ctas: the caller runs these updates on a low-priority stream beside
+    // the critical path -- CTAs of 8 tiles, so critical-path CTAs can take SMs
+    // as they free up; otherwise a persistent grid
+    const int grid = short_ctas ? (ntiles + 7) / 8 : grid_for(ntiles);
     const long long alloc = (cols - 1) * ldm + rows;
     if (factor)
         update_right_bulk_kernel<2><<<grid, kBulkThreads, kRightSmem, stream>>>(wins, nwin, ntiles, qw_pool, M, ldm,

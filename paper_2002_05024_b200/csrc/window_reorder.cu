@@ -315,7 +315,7 @@ window_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S, 
                       double* __restrict__ qw_pool, const uint8_t* __restrict__ sizes_pool,
                       const uint8_t* __restrict__ sel_pool, uint8_t* __restrict__ order_pool,
                       uint8_t* __restrict__ stuck_pool, int32_t* __restrict__ status,
-                      unsigned long long* __restrict__ prof) {
+                      unsigned long long* __restrict__ prof, int32_t* __restrict__ dev_level) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     // optional per-warp phase timing (prof != nullptr): [warp][0] phase-1
     // busy cycles, [1] phase-2 busy cycles, [2] steps, [3] kernel cycles
@@ -355,6 +355,9 @@ window_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S, 
         // layout check against the exact-zero subdiagonal (reorder.cpp:132-154)
         bool ok = true;
         if (lane == 0) {
+            // an earlier level deviated: this window's planned layout is stale
+            const bool skip = dev_level && __ldcg(dev_level) < wd.level;
+            ok = !skip;
             int row = 0;
             for (int k = 0; k < nb && ok; ++k) {
                 const int sz = sh.bsz[k];
@@ -364,7 +367,7 @@ window_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S, 
                 row += sz;
             }
             if (ok && row != d) ok = false;
-            sh.status = ok ? kWinExecuted : 0;
+            sh.status = ok ? kWinExecuted : (skip ? kWinSkipped : 0);
         }
         ok = __shfl_sync(0xffffffffu, ok, 0);
         if (ok) find_pairs(sh, nb, d, 0, lane);
@@ -469,7 +472,11 @@ window_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S, 
     }
     double* qw = qw_pool + wd.qw_off;
     for (int idx = tid; idx < d * d; idx += kWinThreads) qw[idx] = acc[idx];
-    if (tid == 0) status[blockIdx.x] = st;
+    if (tid == 0) {
+        status[blockIdx.x] = st;
+        // a rejected swap or a layout mismatch: later levels' plans are stale
+        if (dev_level && ((st & kWinStuck) || !(st & (kWinExecuted | kWinSkipped)))) atomicMin(dev_level, wd.level);
+    }
     if (prof && lane == 0) {
         unsigned long long* pw = prof + (blockIdx.x * (size_t)NW + warp) * 4;
         pw[0] = t_p1;
@@ -487,18 +494,15 @@ size_t window_reorder_smem_bytes(int dmax) {
 cudaError_t launch_window_reorder(const WinDesc* wins, int nwin, int dmax, double* S, long long lds,
                                   double* qw_pool, const uint8_t* sizes_pool, const uint8_t* sel_pool,
                                   uint8_t* order_pool, uint8_t* stuck_pool, int32_t* status,
-                                  cudaStream_t stream, unsigned long long* prof) {
+                                  cudaStream_t stream, unsigned long long* prof, int32_t* dev_level) {
     if (nwin <= 0) return cudaSuccess;
     const size_t smem = window_reorder_smem_bytes(dmax);
-    static size_t configured = 0;
-    if (smem > configured) {
-        cudaError_t e = cudaFuncSetAttribute(window_reorder_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    {
+        cudaError_t e = ensure_dyn_smem((const void*)window_reorder_kernel, window_reorder_smem_bytes(128));
         if (e != cudaSuccess) return e;
-        configured = smem;
     }
     window_reorder_kernel<<<nwin, kWinThreads, smem, stream>>>(wins, S, lds, qw_pool, sizes_pool, sel_pool,
-                                                               order_pool, stuck_pool, status, prof);
+                                                               order_pool, stuck_pool, status, prof, dev_level);
     return cudaGetLastError();
 }
 

@@ -6,6 +6,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 EPS = 2.220446049250313e-16
 
@@ -39,3 +40,8 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.fail("GPU test collected on a machine without CUDA (run with -m 'not gpu' here)")
     return torch.device("cuda", 0)
+
+
+@pytest.fixture(scope="session")
+def golden_rej():
+    return np.load(os.path.join(ROOT, "tests", "golden", "rejection_golden.npz"))
