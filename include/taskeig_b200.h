@@ -232,6 +232,12 @@ int teig_chase_bulges_device(int64_t n, double* dH, int64_t ldh, double* dQ, int
                              int64_t chain_end, int64_t nb, const int64_t* positions,
                              int64_t window_size, int64_t* n_windows, void* stream);
 
+/* plan_chase (schur.cpp:484-505), host only: the windows chase_bulges runs
+ * for the chain (positions bottom first), as (a, d, mode) triples (mode 0 hop,
+ * 1 final) in win (3*cap int64 or NULL).  Returns the window count or < 0. */
+int64_t teig_plan_chase(int64_t nb, const int64_t* positions, int64_t chain_end, int64_t window_size,
+                        int64_t* win, int64_t cap);
+
 /* kernels::small_schur (kernels.hpp:93): dH k x k (ld ldh) in place, dQ
  * (k x k, ld k) receives the similarity.  k <= 104. */
 int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int32_t* converged,

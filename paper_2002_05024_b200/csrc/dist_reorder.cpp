@@ -789,6 +789,10 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, do
         if (!b.selected) seen_unsel = true;
         else if (seen_unsel) leading = false;
     }
+    // ascending original index: the reference's order of discovery (it runs
+    // the groups top-down and a window's stuck blocks in slice order, so its
+    // rejected_blocks come out sorted; pipelined groups here fold out of it)
+    std::sort(rejected.begin(), rejected.end());
     inf.n_rejected = (int64_t)rejected.size();
     inf.clean = (rejected.empty() && leading) ? 1 : 0;
     if (perm)

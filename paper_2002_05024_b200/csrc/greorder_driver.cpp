@@ -232,6 +232,10 @@ int greorder_schur_device(int64_t n, double* dS, int64_t lds, double* dT, int64_
         if (!b.selected) seen = true;
         else if (seen) leading = false;
     }
+    // ascending original index: the reference's order of discovery (it runs
+    // the groups top-down and a window's stuck blocks in slice order, so its
+    // rejected_blocks come out sorted; pipelined groups here fold out of it)
+    std::sort(rejected.begin(), rejected.end());
     inf.n_rejected = (int64_t)rejected.size();
     inf.clean = (rejected.empty() && leading) ? 1 : 0;
     if (perm)

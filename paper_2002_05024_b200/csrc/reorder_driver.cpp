@@ -584,6 +584,10 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
             else if (seen_unsel) leading = false;
         }
     }
+    // ascending original index: the reference's order of discovery (it runs
+    // the groups top-down and a window's stuck blocks in slice order, so its
+    // rejected_blocks come out sorted; pipelined groups here fold out of it)
+    std::sort(rejected.begin(), rejected.end());
     inf.n_rejected = (int64_t)rejected.size();
     inf.clean = (rejected.empty() && leading) ? 1 : 0;
     if (perm)

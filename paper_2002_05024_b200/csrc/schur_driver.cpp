@@ -36,6 +36,35 @@
 
 namespace teig {
 
+// plan_chase (schur.cpp:484-505): the chase windows of a chain of nb bulges
+// whose bottom bulge enters at p_bot, window order cw, active range end ihi.
+std::vector<ChaseWin> plan_chase_windows(int64_t p_bot, int64_t nb, int64_t ihi, int64_t cw) {
+    std::vector<ChaseWin> out;
+    for (;;) {
+        const int64_t p_top = p_bot - 3 * (nb - 1);
+        const int64_t a = p_top - 1;
+        const int64_t b = std::min(a + cw, ihi);
+        ChaseWin c{};
+        c.a = (int32_t)a;
+        c.d = (int32_t)(b - a);
+        c.ihi = (int32_t)ihi;
+        c.nb = (int32_t)nb;
+        c.p_bot = (int32_t)p_bot;
+        c.packed_len = chase_window_packed_len(c.d);
+        if (b == ihi) {
+            c.mode = kChaseFinal;
+            out.push_back(c);
+            return out;
+        }
+        const int64_t hop = (b >= p_bot + 4) ? (b - 4 - p_bot) : 0;
+        if (hop == 0) throw std::logic_error("chase window too small for the chain");
+        c.mode = kChaseHop;
+        c.hop = (int32_t)hop;
+        out.push_back(c);
+        p_bot += hop;
+    }
+}
+
 int set_error(int code, const std::string& msg);
 int64_t default_tile_size(int64_t n);
 
@@ -362,29 +391,7 @@ class SchurRunner {
 
     // plan_chase (schur.cpp:484-505) for a chain whose bottom bulge enters at p_bot
     void plan_chain(int64_t p_bot, int64_t nb, int64_t ihi, int64_t cw) {
-        for (;;) {
-            const int64_t p_top = p_bot - 3 * (nb - 1);
-            const int64_t a = p_top - 1;
-            const int64_t b = std::min(a + cw, ihi);
-            ChaseWin c{};
-            c.a = (int32_t)a;
-            c.d = (int32_t)(b - a);
-            c.ihi = (int32_t)ihi;
-            c.nb = (int32_t)nb;
-            c.p_bot = (int32_t)p_bot;
-            c.packed_len = chase_window_packed_len(c.d);
-            if (b == ihi) {
-                c.mode = kChaseFinal;
-                add_chase(c);
-                return;
-            }
-            const int64_t hop = (b >= p_bot + 4) ? (b - 4 - p_bot) : 0;
-            if (hop == 0) throw std::logic_error("chase window too small for the chain");
-            c.mode = kChaseHop;
-            c.hop = (int32_t)hop;
-            add_chase(c);
-            p_bot += hop;
-        }
+        for (const ChaseWin& c : plan_chase_windows(p_bot, nb, ihi, cw)) add_chase(c);
     }
 
     int64_t round_windows() const { return (int64_t)wins_.size(); }
@@ -851,6 +858,24 @@ int teig_chase_bulges_device(int64_t n, double* dH, int64_t ldh, double* dQ, int
         return set_error(TEIG_ERR_CUDA, e.what());
     }
     return 0;
+}
+
+int64_t teig_plan_chase(int64_t nb, const int64_t* positions, int64_t chain_end, int64_t window_size,
+                        int64_t* win, int64_t cap) {
+    if (nb <= 0) return 0;
+    if (!positions) return set_error(-2, "positions is null");
+    const int64_t cw = std::max<int64_t>(window_size, 3 * nb + 6);
+    try {
+        const auto w = plan_chase_windows(positions[0], nb, chain_end, cw);
+        for (int64_t i = 0; win && i < (int64_t)w.size() && i < cap; ++i) {
+            win[3 * i] = w[i].a;
+            win[3 * i + 1] = w[i].d;
+            win[3 * i + 2] = w[i].mode;
+        }
+        return (int64_t)w.size();
+    } catch (const std::logic_error& e) {
+        return set_error(-9, e.what());
+    }
 }
 
 int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int32_t* converged, void* stream) {
