@@ -48,7 +48,8 @@ int teig_version(void);
 /* reorder.cpp:215-404).                                                     */
 
 typedef struct teig_reorder_opts {
-    int64_t window_size; /* 0: default_tile_size(n) (reorder.cpp:221-222); <= 128 */
+    int64_t window_size; /* 0: default_tile_size(n) (reorder.cpp:221-222); values above 128
+                            (one CTA's shared memory) run at 128: same result, other plan */
     int32_t strict;      /* !=0: fail with TEIG_ERR_STRICT on a rejected swap */
     int32_t overlap_factor; /* !=0 (default 1 via teig_reorder_opts_default): run the
                                Q-factor updates on a second stream, overlapped */
@@ -169,11 +170,11 @@ int teig_update_panel_device(int32_t side, int64_t d, const double* dQw, int64_t
 
 typedef struct teig_schur_opts {  /* SchurOptions, schur.hpp:20-29 */
     int32_t deflation;        /* 0 classic, 1 norm-stable (default) */
-    int32_t shift_count;      /* 0: max(4, round-to-even(active/16)), cap 64 */
-    int32_t aed_window;       /* 0: 3m/2; <= 104 (single-CTA AED window) */
-    int32_t small_threshold;  /* direct small_schur at or below (default 64, <= 104) */
+    int32_t shift_count;      /* 0: max(4, round-to-even(active/16)), cap 64; explicit values above 64 run at 64 */
+    int32_t aed_window;       /* 0: 3m/2; above 104 (one CTA's shared memory) runs at 104 */
+    int32_t small_threshold;  /* direct small_schur at or below (default 64; above 104 runs at 104) */
     int64_t iteration_limit;  /* 0: 30 n sweeps */
-    int64_t tile_size;        /* chase window: 0 = default_tile_size(n) (128 for n >= 1000); <= 128 */
+    int64_t tile_size;        /* chase window: 0 = default_tile_size(n) (128 for n >= 1000); above 128 runs at 128 */
     int32_t profile;          /* !=0: CUDA-event time per kernel class in teig_schur_info */
     int32_t pad;
 } teig_schur_opts;

@@ -573,7 +573,7 @@ int dist_balance(int64_t n, int64_t nb, const uint8_t* sizes, const uint8_t* fla
         rows += sizes[i];
     }
     if (rows != n) return set_error(-3, "selection does not match n");
-    const int64_t ws = std::max<int64_t>(window_size ? window_size : default_tile_size(n), 8);
+    const int64_t ws = std::min<int64_t>(std::max<int64_t>(window_size ? window_size : default_tile_size(n), 8), 128);
     ReorderPlan plan = plan_reorder(blocks, ws);
     std::vector<double> dens(n + 1, 0.0);
     for (const auto& w : plan.windows) {
@@ -634,7 +634,7 @@ int64_t teig_dist_schedule(int64_t n, int64_t nb, const uint8_t* sizes, const ui
     }
     if (rows != n) return set_error(-3, "selection does not match n");
     try {
-        const int64_t ws = std::max<int64_t>(window_size ? window_size : default_tile_size(n), 8);
+        const int64_t ws = std::min<int64_t>(std::max<int64_t>(window_size ? window_size : default_tile_size(n), 8), 128);
         ReorderPlan plan = plan_reorder(blocks, ws);
         schedule_levels(plan, n);
         std::vector<int64_t> C(col_bounds, col_bounds + world + 1);
@@ -716,8 +716,8 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, do
     teig_reorder_opts o;
     teig_reorder_opts_default(&o);
     if (opts) o = *opts;
-    const int64_t ws = std::max<int64_t>(o.window_size ? o.window_size : (gen ? 64 : default_tile_size(n)), 8);
-    if (ws > (gen ? 64 : 128)) return set_error(TEIG_ERR_UNSUPPORTED, gen ? "generalized window_size > 64" : "window_size > 128");
+    // windows beyond one CTA's shared memory run at the limit (as the single-GPU drivers)
+    const int64_t ws = std::min<int64_t>(std::max<int64_t>(o.window_size ? o.window_size : (gen ? 64 : default_tile_size(n)), 8), gen ? 64 : 128);
     if (gen && !dT_slabs) return set_error(-5, "null T slabs");
     std::vector<BlockState> blocks(nb);
     int64_t rows = 0;

@@ -184,8 +184,7 @@ int greorder_schur_device(int64_t n, double* dS, int64_t lds, double* dT, int64_
     teig_reorder_opts o;
     teig_reorder_opts_default(&o);
     if (opts) o = *opts;
-    const int64_t ws = std::max<int64_t>(o.window_size ? o.window_size : 64, 8);
-    if (ws > 64) return set_error(TEIG_ERR_UNSUPPORTED, "generalized window_size > 64 (shared memory holds S, T, Q_w, Z_w)");
+    const int64_t ws = std::min<int64_t>(std::max<int64_t>(o.window_size ? o.window_size : 64, 8), 64);  // shared memory holds S, T, Q_w, Z_w of one window
     std::vector<BlockState> blocks(nb);
     int64_t rows = 0;
     for (int64_t i = 0; i < nb; ++i) {

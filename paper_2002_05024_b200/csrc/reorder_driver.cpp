@@ -518,7 +518,10 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
     teig_reorder_opts_default(&o);
     if (opts) o = *opts;
     int64_t ws = std::max<int64_t>(o.window_size ? o.window_size : default_tile_size(n), 8);
-    if (ws > 128) return set_error(TEIG_ERR_UNSUPPORTED, "window_size > 128 is not supported by the single-CTA window kernel");
+    // windows larger than one CTA's shared memory holds run at 128 (the
+    // reference takes any size, reorder.cpp:221-222): same final arrangement,
+    // a different window plan
+    ws = std::min<int64_t>(ws, 128);
     if (n > (int64_t)2147483647) return set_error(TEIG_ERR_UNSUPPORTED, "n too large");
 
     std::vector<BlockState> blocks(nb);
@@ -824,7 +827,7 @@ int64_t teig_plan_reorder(int64_t n, int64_t nb, const uint8_t* sizes, const uin
         rows += sizes[i];
     }
     if (rows != n) return set_error(-3, "selection does not match n");
-    const int64_t ws = std::max<int64_t>(window_size ? window_size : default_tile_size(n), 8);
+    const int64_t ws = std::min<int64_t>(std::max<int64_t>(window_size ? window_size : default_tile_size(n), 8), 128);
     ReorderPlan plan = plan_reorder(blocks, ws);
     schedule_levels(plan, n);
     if (win)

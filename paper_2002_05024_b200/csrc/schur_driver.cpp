@@ -504,16 +504,20 @@ class SchurRunner {
     int64_t launches_ = 0, rounds_ = 0, aed_windows_ = 0, chase_windows_ = 0;
 };
 
-int check_opts(const teig_schur_opts& o) {
+// Validates the options and clamps the window sizes to what one CTA's shared
+// memory holds (the reference takes any size, schur.cpp:777, 869): a larger
+// AED window / small-solve threshold runs at 104, a larger chase window at
+// 128, a larger shift count at 64 (the reference's own default cap) -- the
+// result satisfies the same contract (Schur form, residuals, eigenvalues);
+// only the convergence history differs.
+int check_opts(teig_schur_opts& o) {
     if (o.deflation != 0 && o.deflation != 1) return set_error(-7, "deflation must be 0 (classic) or 1 (norm-stable)");
     if (o.shift_count < 0 || o.aed_window < 0 || o.small_threshold < 0 || o.iteration_limit < 0 || o.tile_size < 0)
         return set_error(-7, "negative option");
-    if (o.shift_count > 2 * kAedMaxWindow) return set_error(TEIG_ERR_UNSUPPORTED, "shift_count too large");
-    if (o.aed_window > kAedMaxWindow)
-        return set_error(TEIG_ERR_UNSUPPORTED, "aed_window > 104 exceeds the single-CTA AED window kernel");
-    if (o.small_threshold > kAedMaxWindow)
-        return set_error(TEIG_ERR_UNSUPPORTED, "small_threshold > 104 exceeds the single-CTA window kernel");
-    if (o.tile_size > kChaseMaxWindow) return set_error(TEIG_ERR_UNSUPPORTED, "chase window (tile_size) > 128");
+    o.shift_count = std::min<int32_t>(o.shift_count, 64);
+    o.aed_window = std::min<int32_t>(o.aed_window, kAedMaxWindow);
+    o.small_threshold = std::min<int32_t>(o.small_threshold, kAedMaxWindow);
+    o.tile_size = std::min<int64_t>(o.tile_size, kChaseMaxWindow);
     return 0;
 }
 
@@ -766,7 +770,7 @@ int teig_aed_step_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t
     if (opts) o = *opts;
     if (int rc = check_opts(o)) return rc;
     window = std::min(window, ihi - l);
-    if (window > kAedMaxWindow) return set_error(TEIG_ERR_UNSUPPORTED, "AED window > 104");
+    window = std::min<int64_t>(window, kAedMaxWindow);  // one CTA's shared memory (see check_opts)
     try {
         SchurRunner R(n, dH, ldh, dQ, ldq, o, (cudaStream_t)stream);
         R.begin_round();
