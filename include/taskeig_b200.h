@@ -39,6 +39,7 @@ extern "C" {
 #define TEIG_ERR_UNSUPPORTED (-1001)
 #define TEIG_ERR_STRICT (-1002)    /* rejected swap in strict mode (reorder.cpp:383-385) */
 #define TEIG_ERR_INTERNAL (-1003)
+#define TEIG_ERR_NONFINITE (-1004)  /* a non-finite result (the reference's assert_finite) */
 
 const char* teig_last_error(void);
 int teig_version(void);
@@ -246,6 +247,18 @@ int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int3
 
 /* deflation_check (schur.hpp:63-64); host only. */
 int teig_deflation_check(double spike, double diag_sum, int32_t deflation, double wnorm);
+
+/* ------------------------------------------------------------------------ */
+/* Eigenvector back-transformation (replaces taskeig::backtransform,          */
+/* eigvec.hpp:88-89 / eigvec.cpp:448-516): X = Q Y on the FP64 tensor pipe   */
+/* with the device-resident Q of a reorder / Schur call, then every real      */
+/* column and every complex pair renormalised to unit max-norm with a         */
+/* positive lead entry.  dQ n x n, dY / dX n x k (column-major, device; X    */
+/* must not alias Y).  col_kind (host, k; NULL: no renormalisation): 0 real,  */
+/* 1 real part of a pair (next column = imaginary part), 2 imaginary part.    */
+/* Returns 0, < 0 on bad arguments, TEIG_ERR_NONFINITE on Inf/NaN in X.       */
+int teig_backtransform_device(int64_t n, int64_t k, const double* dQ, int64_t ldq, const double* dY,
+                              int64_t ldy, double* dX, int64_t ldx, const int8_t* col_kind, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Synthetic inputs directly in HBM (bit-identical to the      */

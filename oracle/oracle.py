@@ -159,6 +159,8 @@ def ref():
         R.ref_problem_destroy.argtypes = [C.c_void_p]
         R.ref_problem_reorder.argtypes = [C.c_void_p, _SZ, _P, _SZ, _SZ, C.c_int, _P, _P, _P]
         R.ref_problem_reorder.restype = C.c_int
+        R.ref_backtransform.argtypes = [_SZ, _SZ, _P, _P, _P, _P, _SZ]
+        R.ref_backtransform.restype = C.c_int
         R.ref_hessenberg_reduce.argtypes = [_SZ, _P, _P, _P, _SZ]
         R.ref_hessenberg_reduce.restype = C.c_int
         R.ref_schur_reduce.argtypes = [_SZ, _SZ, _P, _P, _SZ, C.c_int, _SZ, _SZ, _SZ, _SZ, _P,
@@ -474,6 +476,17 @@ class RefProblem:
             self.close()
         except Exception:
             pass
+
+
+def ref_backtransform(y_cm: np.ndarray, q_rm: np.ndarray, col_kind, workers=0) -> np.ndarray:
+    """The reference's backtransform: X = Q Y, renormalised per column / pair."""
+    n, k = y_cm.shape
+    y_cm = np.asfortranarray(y_cm, dtype=np.float64)
+    q_rm = np.ascontiguousarray(q_rm, dtype=np.float64)
+    kind = np.ascontiguousarray(col_kind, dtype=np.int32)
+    x = np.zeros((n, k), order="F")
+    _chk_ref(ref().ref_backtransform(n, k, _ptr(y_cm), _ptr(q_rm), _ptr(kind), _ptr(x), workers))
+    return x
 
 
 def ref_hessenberg_reduce(a_rm, workers=0):

@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "taskeig/dense.hpp"
+#include "taskeig/eigvec.hpp"
 #include "taskeig/generate.hpp"
 #include "taskeig/hessenberg.hpp"
 #include "taskeig/kernels.hpp"
@@ -258,6 +259,31 @@ int ref_problem_reorder(void* h, std::size_t nb, const std::uint8_t* flags, std:
         *seconds = std::chrono::duration<double>(t1 - t0).count();
         if (n_plan) *n_plan = res.plan.size();
         if (clean) *clean = res.clean ? 1 : 0;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+}
+
+// backtransform (eigvec.cpp:448-516): y_cm n x k column-major (the
+// EigenvectorSet's DenseMatrix convention), q_rm row-major, col_kind per
+// column; x_cm receives the renormalised X = Q Y.
+int ref_backtransform(std::size_t n, std::size_t k, const double* y_cm, const double* q_rm, const int* col_kind,
+                      double* x_cm, std::size_t workers) {
+    try {
+        EigenvectorSet y;
+        y.n = n;
+        y.lambdas.assign(k, {0.0, 0.0});
+        y.col_kind.assign(col_kind, col_kind + k);
+        y.positions.assign(k, 0);
+        y.flagged.assign(k, false);
+        y.columns = dense_from(y_cm, n, k);
+        auto q = TiledMatrix::from_dense(vec(q_rm, n * n), n, n, default_tile_size(n));
+        EigvecOptions o;
+        o.workers = workers;
+        auto x = backtransform(y, q, o);
+        std::memcpy(x_cm, x.columns.data(), sizeof(double) * n * k);
         return 0;
     } catch (const std::exception& e) {
         g_err = e.what();

@@ -98,6 +98,7 @@ SIGNATURES = {
     "teig_chase_bulges_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _I64, _P, _I64, _P, _P]),
     "teig_small_schur_device": (C.c_int, [_I64, _P, _I64, _P, _P, _P]),
     "teig_plan_chase": (C.c_int64, [_I64, _P, _I64, _I64, _P, _I64]),
+    "teig_backtransform_device": (C.c_int, [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _P]),
     "teig_deflation_check": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.c_double]),
     "teig_greorder_schur_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P,
                                              _P, _P, _P]),

@@ -99,6 +99,14 @@ cudaError_t launch_hess_norm(const double* H, long long ldh, int n, unsigned lon
 cudaError_t launch_scan_active(double* H, long long ldh, int n, int ihi, double hnorm, int* out,
                                cudaStream_t stream);
 
+// backtransform.cu: C = A B (DMMA, column-major, any ld) and the reference's
+// eigenvector column renormalisation (kind: 0 real, 1 pair start, 2 pair
+// second half, other / NULL: finiteness check only; *nonfinite |= 1 on
+// Inf / NaN)
+cudaError_t launch_gemm_nn(int m, int n, int kdim, const double* A, long long lda, const double* B, long long ldb,
+                           double* C, long long ldc, cudaStream_t s);
+cudaError_t launch_renorm_columns(int n, double* X, long long ldx, const int8_t* kind_dev, int k, int* nonfinite,
+                                  cudaStream_t s);
 // distributed deviation flag: mode 0 publish into the level's slot, 1 absorb
 cudaError_t launch_dist_flag(int32_t* dev_level, double* slot, int level, int mode, cudaStream_t s);
 // element-wise sum of nbuf device buffers into all of them (loopback all-reduce)

@@ -45,3 +45,8 @@ def cuda():
 @pytest.fixture(scope="session")
 def golden_rej():
     return np.load(os.path.join(ROOT, "tests", "golden", "rejection_golden.npz"))
+
+
+@pytest.fixture(scope="session")
+def golden_r2():
+    return np.load(os.path.join(ROOT, "tests", "golden", "r2_golden.npz"))
