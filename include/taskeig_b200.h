@@ -40,6 +40,7 @@ extern "C" {
 #define TEIG_ERR_STRICT (-1002)    /* rejected swap in strict mode (reorder.cpp:383-385) */
 #define TEIG_ERR_INTERNAL (-1003)
 #define TEIG_ERR_NONFINITE (-1004)  /* a non-finite result (the reference's assert_finite) */
+#define TEIG_ERR_IO (-1005)         /* file IO / format error (the reference's std::runtime_error) */
 
 const char* teig_last_error(void);
 int teig_version(void);
@@ -101,6 +102,18 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
                             const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
                             int64_t* plan, int64_t plan_cap, teig_reorder_info* info,
                             void* stream);
+
+/* Execution trace (the reference's ExecutionReport, runtime.hpp:50-60, and
+ * SchurOptions::keep_reports): with tracing on, every reorder call made on
+ * this thread records one task per kernel launch -- {"label":
+ * "reorder:<W|L|R|Q>:p<pass>:l<level>", "worker": stream (0 critical path,
+ * 1 factor updates), "start_ns", "end_ns"} from CUDA events relative to the
+ * call's start -- and one record per planned window {"pass", "level",
+ * "position", "extent", "blocks", "group", "status"}.  teig_trace_json
+ * writes the last call's trace as JSON into buf when cap exceeds its length
+ * and returns the length.  Tracing brackets every launch with events. */
+void teig_trace_enable(int32_t on);
+int64_t teig_trace_json(char* buf, int64_t cap);
 
 /* Device memory policy (not part of the reference interface: the reference
  * has no device memory).  Every per-call device buffer comes from a private
@@ -259,6 +272,18 @@ int teig_deflation_check(double spike, double diag_sum, int32_t deflation, doubl
 /* Returns 0, < 0 on bad arguments, TEIG_ERR_NONFINITE on Inf/NaN in X.       */
 int teig_backtransform_device(int64_t n, int64_t k, const double* dQ, int64_t ldq, const double* dY,
                               int64_t ldy, double* dX, int64_t ldx, const int8_t* col_kind, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Matrix files (replaces taskeig::write_matrix_file / read_matrix_file,      */
+/* io.hpp / io.cpp:37-121), byte-compatible with the reference.  format:      */
+/* "teig" (binary: "TEIG", uint32 1, uint64 rows, uint64 cols, row-major     */
+/* float64) or "matrixmarket" ("array real general", column by column, 17    */
+/* digits).  Buffers are ROW-major (the reference's DenseBuffer).  Read: pass */
+/* a_rm = NULL to get the shape only; cap = capacity of a_rm in doubles.      */
+int teig_write_matrix_file(const char* path, const char* format, int64_t rows, int64_t cols,
+                           const double* a_rm);
+int teig_read_matrix_file(const char* path, const char* format, int64_t* rows, int64_t* cols,
+                          double* a_rm, int64_t cap);
 
 /* ------------------------------------------------------------------------ */
 /* Synthetic inputs directly in HBM (bit-identical to the      */

@@ -489,6 +489,17 @@ def ref_backtransform(y_cm: np.ndarray, q_rm: np.ndarray, col_kind, workers=0) -
     return x
 
 
+REF_IO_TOOL = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref", "ref_io_tool")
+
+
+def ref_io_convert(in_fmt: str, src: str, out_fmt: str, dst: str) -> None:
+    """The reference's read_matrix_file(src, in_fmt) -> write_matrix_file(dst,
+    ., out_fmt), in a subprocess (oracle/ref_io_tool.cpp)."""
+    r = subprocess.run([REF_IO_TOOL, "convert", in_fmt, src, out_fmt, dst], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError("reference io: " + r.stderr.strip())
+
+
 def ref_hessenberg_reduce(a_rm, workers=0):
     n = a_rm.shape[0]
     a_rm = np.ascontiguousarray(a_rm)

@@ -79,6 +79,8 @@ SIGNATURES = {
     "teig_set_memory_retention": (None, [C.c_int32]),
     "teig_memory_retention": (C.c_int32, []),
     "teig_release_memory": (None, []),
+    "teig_trace_enable": (None, [C.c_int32]),
+    "teig_trace_json": (C.c_int64, [C.c_char_p, C.c_int64]),
     "teig_reorder_schur_host": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P,
                                           _I64, _P, _P]),
     "teig_scan_blocks_device": (C.c_int64, [_I64, _P, _I64, _P, _P]),
@@ -99,6 +101,8 @@ SIGNATURES = {
     "teig_small_schur_device": (C.c_int, [_I64, _P, _I64, _P, _P, _P]),
     "teig_plan_chase": (C.c_int64, [_I64, _P, _I64, _I64, _P, _I64]),
     "teig_backtransform_device": (C.c_int, [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _P]),
+    "teig_write_matrix_file": (C.c_int, [C.c_char_p, C.c_char_p, _I64, _I64, _P]),
+    "teig_read_matrix_file": (C.c_int, [C.c_char_p, C.c_char_p, _P, _P, _P, _I64]),
     "teig_deflation_check": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.c_double]),
     "teig_greorder_schur_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P,
                                              _P, _P, _P]),
@@ -158,3 +162,16 @@ def memory_retention() -> bool:
 def release_memory() -> None:
     """Return the library's cached device memory (staging + pools, every device)."""
     lib().teig_release_memory()
+
+
+def trace_enable(on: bool = True) -> None:
+    """Record an execution trace of the reorder calls made on this thread."""
+    lib().teig_trace_enable(1 if on else 0)
+
+
+def trace_json() -> str:
+    """The last traced call's trace (JSON: tasks, stalls, windows)."""
+    n = lib().teig_trace_json(None, 0)
+    buf = C.create_string_buffer(n + 1)
+    lib().teig_trace_json(buf, n + 1)
+    return buf.value.decode()

@@ -33,6 +33,8 @@
 #include "plan.h"
 #include "qw_ring.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace teig {
 
 thread_local std::string g_last_error;
@@ -186,11 +188,39 @@ struct PassResult {
     double ms_window = 0, ms_left = 0, ms_right = 0, ms_factor = 0;
 };
 
+// Execution trace of the calls made on this thread (teig_trace_enable): one
+// task record per kernel launch -- the reference's ExecutionReport schema
+// (runtime.hpp:50-60: label, worker = stream, start_ns / end_ns from CUDA
+// events relative to the call's first event) -- plus one record per planned
+// window (pass, level, position, order, blocks, group, status).
+struct TraceTask {
+    std::string label;
+    int worker;
+    int64_t start_ns, end_ns;
+};
+struct TraceWin {
+    int pass, level;
+    int64_t a, d, nb, group;
+    int32_t status;
+};
+struct TraceState {
+    bool on = false;
+    cudaEvent_t origin = nullptr;
+    int pass = 0;
+    std::vector<TraceTask> tasks;
+    std::vector<TraceWin> wins;
+};
+thread_local TraceState g_trace;
+
 // Event pairs bracketing launches when profiling is on.
 struct EventLog {
     bool on = false;
     std::vector<cudaEvent_t> ev;
     std::vector<std::pair<int, int>> spans[4];  // (start idx, end idx) per class
+    struct Meta {
+        int cls, level, worker, start, end;
+    };
+    std::vector<Meta> meta;  // every span in launch order (trace)
     int record(cudaStream_t s) {
         cudaEvent_t e;
         TEIG_CUDA(cudaEventCreate(&e));
@@ -240,7 +270,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                     HostDrain* drain = nullptr) {
     PassResult pr;
     EventLog lg;
-    lg.on = profile;
+    lg.on = profile || g_trace.on;
     const int64_t nw = (int64_t)plan.windows.size();
     schedule_levels(plan, n);
     const int32_t nl = plan.n_levels;
@@ -319,18 +349,25 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     DevBuf d_prof(wprof ? sizeof(unsigned long long) * nw * kWindowThreads / 32 * 4 : 0, stream);
     if (wprof) TEIG_CUDA(cudaMemsetAsync(d_prof.p, 0, sizeof(unsigned long long) * nw * kWindowThreads / 32 * 4, stream));
     // runs `f` on stream `st`, bracketed by events of class `cls` when profiling
+    int cur_level = 0;
     auto timed = [&](int cls, cudaStream_t st, int64_t ntiles, auto&& f) {
         if (ntiles <= 0) return;
         int e0 = lg.on ? lg.record(st) : -1;
         TEIG_CUDA(f());
         ++launches;
-        if (lg.on) lg.spans[cls].push_back({e0, lg.record(st)});
+        if (lg.on) {
+            const int e1 = lg.record(st);
+            lg.spans[cls].push_back({e0, e1});
+            lg.meta.push_back({cls, cur_level, st == stream ? 0 : 1, e0, e1});
+        }
     };
     // TEIG_LAUNCH_LOG=1: per-level tile counts on stderr (to pair ncu launch
     // indices with algorithmic bytes / flops)
     const bool launch_log = getenv("TEIG_LAUNCH_LOG") && atoi(getenv("TEIG_LAUNCH_LOG"));
     for (int L = 0; L < nl; ++L) {
         const int64_t o = lvl_off[L], cnt = lvl_off[L + 1] - lvl_off[L];
+        cur_level = L;
+        nvtxRangePushA("teig reorder level");
         if (launch_log)
             fprintf(stderr, "[teig level] %d windows %lld left_tiles %lld right_tiles %lld factor_tiles %lld\n", L,
                     (long long)cnt, (long long)tl[L], (long long)tr[L], (long long)tq[L]);
@@ -394,6 +431,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                 }
             }
         }
+        nvtxRangePop();
     }
     if (dQ && overlap) {
         TEIG_CUDA(cudaEventRecord(ev, stream2));
@@ -434,6 +472,22 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     for (int32_t st : status) pr.windows += (st & kWinSkipped) ? 0 : 1;  // = entries logged in `plan`
     pr.levels = nl;
     pr.launches = launches;
+    if (g_trace.on) {  // everything above synchronized: the events are complete
+        static const char* kCls[4] = {"W", "L", "R", "Q"};
+        for (const auto& m : lg.meta) {
+            float t0 = 0, t1 = 0;
+            TEIG_CUDA(cudaEventElapsedTime(&t0, g_trace.origin, lg.ev[m.start]));
+            TEIG_CUDA(cudaEventElapsedTime(&t1, g_trace.origin, lg.ev[m.end]));
+            g_trace.tasks.push_back({std::string("reorder:") + kCls[m.cls] + ":p" + std::to_string(g_trace.pass) +
+                                         ":l" + std::to_string(m.level),
+                                     m.worker, (int64_t)(t0 * 1e6), (int64_t)(t1 * 1e6)});
+        }
+        for (int64_t k = 0; k < nw; ++k) {
+            const PlannedWindow& w = plan.windows[idx[k]];
+            g_trace.wins.push_back({g_trace.pass, w.level, w.wtop, w.wbot - w.wtop, w.count, w.group, status[k]});
+        }
+        ++g_trace.pass;
+    }
     if (lg.on) {
         pr.ms_window = lg.total(0);
         pr.ms_left = lg.total(1);
@@ -538,6 +592,13 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
     std::vector<int64_t> rejected, plan_log;
     try {
         StreamPair sp(stream);
+        if (g_trace.on) {  // time origin of this call's trace records
+            g_trace.tasks.clear();
+            g_trace.wins.clear();
+            g_trace.pass = 0;
+            if (!g_trace.origin) TEIG_CUDA(cudaEventCreate(&g_trace.origin));
+            TEIG_CUDA(cudaEventRecord(g_trace.origin, sp.s1));
+        }
         // Q may still be arriving (host entry point): only the Q updates wait
         if (q_ready && dQ) TEIG_CUDA(cudaStreamWaitEvent(o.overlap_factor ? sp.s2 : sp.s1, q_ready, 0));
         double plan_ms = 0.0;
@@ -639,6 +700,32 @@ void teig_release_host_staging(void) {
         std::lock_guard<std::mutex> g(kv.second->mu);
         kv.second->release();
     }
+}
+
+void teig_trace_enable(int32_t on) { g_trace.on = on != 0; }
+
+int64_t teig_trace_json(char* buf, int64_t cap) {
+    std::string j = "{\"tasks\": [";
+    for (size_t i = 0; i < g_trace.tasks.size(); ++i) {
+        const auto& t = g_trace.tasks[i];
+        j += (i ? ", " : "") + std::string("{\"label\": \"") + t.label + "\", \"worker\": " + std::to_string(t.worker) +
+             ", \"start_ns\": " + std::to_string(t.start_ns) + ", \"end_ns\": " + std::to_string(t.end_ns) + "}";
+    }
+    j += "], \"stalls\": [], \"windows\": [";
+    for (size_t i = 0; i < g_trace.wins.size(); ++i) {
+        const auto& w = g_trace.wins[i];
+        j += (i ? ", " : "") + std::string("{\"pass\": ") + std::to_string(w.pass) + ", \"level\": " +
+             std::to_string(w.level) + ", \"position\": " + std::to_string(w.a) + ", \"extent\": " +
+             std::to_string(w.d) + ", \"blocks\": " + std::to_string(w.nb) + ", \"group\": " +
+             std::to_string(w.group) + ", \"status\": \"" +
+             ((w.status & kWinSkipped) ? "skipped"
+                                       : (w.status & kWinExecuted) ? ((w.status & kWinStuck) ? "stuck" : "executed")
+                                                                   : "layout-mismatch") +
+             "\"}";
+    }
+    j += "]}";
+    if (buf && cap > (int64_t)j.size()) std::memcpy(buf, j.c_str(), j.size() + 1);
+    return (int64_t)j.size();
 }
 
 void teig_set_memory_retention(int32_t on) {
