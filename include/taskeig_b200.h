@@ -299,7 +299,7 @@ int teig_set_identity_device(int64_t n, double* dQ, int64_t ldq, void* stream);
 
 /* ------------------------------------------------------------------------ */
 /* Multi-GPU reordering: S in column slabs, Q in   */
-/* row slabs, one NCCL all-reduce of the packed Q_w per wavefront, halo      */
+/* row slabs, the owners' Q_w broadcast (NCCL) per wavefront, halo           */
 /* transfers for windows straddling a slab boundary.  Same result, bit for   */
 /* bit, as teig_reorder_schur_device (replaces the reference's distributed   */
 /* execution of reorder_schur's window tasks, reorder.cpp:330-364 /          */
@@ -331,6 +331,18 @@ int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_c
                             const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb,
                             const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
                             int64_t* perm, int64_t* rejected, teig_reorder_info* info, void* stream);
+
+/* Single-process multi-GPU: all `world` ranks in this process, rank r on
+ * devices[r] (distinct GPUs), NCCL clique from ncclCommInitAll (created once
+ * per device list, kept for the process).  dS_slabs[r] / dQ_slabs[r] are rank
+ * r's slabs on devices[r] (layout as teig_dist_reorder_schur).  Synchronous;
+ * same result, bit for bit, as teig_reorder_schur_device. */
+int teig_dist_reorder_schur_multi(int64_t n, int32_t world, const int32_t* devices,
+                                  double* const* dS_slabs, int64_t lds, double* const* dQ_slabs,
+                                  const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb,
+                                  const uint8_t* sizes, const uint8_t* flags,
+                                  const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
+                                  teig_reorder_info* info);
 
 /* Generalized pencil (C5) across ranks: S and T in column slabs (same
  * layout as dS_slabs), Q and Z in row slabs; window_size <= 64.  Same result,

@@ -28,18 +28,30 @@ __global__ void sum_buffers_kernel(BufSet b, int nbuf, size_t count) {
 }
 
 // Deviation flag of the distributed pass (see window_reorder.cu): publish
-// (mode 0) writes this rank's "deviated at a level <= L" into the level's
-// flag slot, which travels inside the level's Q_w all-reduce; absorb (mode 1)
-// lowers the rank's deviation level to L when any rank published.
-__global__ void dist_flag_kernel(int32_t* dev_level, double* slot, int level, int mode) {
-    if (mode == 0) *slot = (*dev_level <= level) ? 1.0 : 0.0;
-    else if (*slot > 0.5 && *dev_level > level) *dev_level = level;
+// (mode 0) writes this rank's "deviated at a level <= L" into its flag slot,
+// which travels with its Q_w segment; absorb (mode 1) lowers the rank's
+// deviation level to L when any rank's flag is set.
+struct FlagSlots {
+    int64_t off[kMaxBufs];
+};
+__global__ void dist_flag_kernel(int32_t* dev_level, double* base, FlagSlots f, int nslots, int level, int mode) {
+    if (mode == 0) {
+        base[f.off[0]] = (*dev_level <= level) ? 1.0 : 0.0;
+        return;
+    }
+    bool any = false;
+    for (int r = 0; r < nslots; ++r) any |= base[f.off[r]] > 0.5;
+    if (any && *dev_level > level) *dev_level = level;
 }
 
 }  // namespace
 
-cudaError_t launch_dist_flag(int32_t* dev_level, double* slot, int level, int mode, cudaStream_t s) {
-    dist_flag_kernel<<<1, 1, 0, s>>>(dev_level, slot, level, mode);
+cudaError_t launch_dist_flag(int32_t* dev_level, double* base, const int64_t* slots, int nslots, int level, int mode,
+                             cudaStream_t s) {
+    if (nslots > kMaxBufs) return cudaErrorInvalidValue;
+    FlagSlots f{};
+    for (int r = 0; r < nslots; ++r) f.off[r] = slots[r];
+    dist_flag_kernel<<<1, 1, 0, s>>>(dev_level, base, f, nslots, level, mode);
     return cudaGetLastError();
 }
 

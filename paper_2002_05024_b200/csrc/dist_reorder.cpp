@@ -1,6 +1,6 @@
 // dist_reorder.cpp -- multi-GPU Schur-form reordering (SURVEY.md 8e, config
-// C4): S distributed over the ranks in COLUMN SLABS, Q in ROW SLABS, one
-// NCCL all-reduce of the packed Q_w of every wavefront, point-to-point
+// C4): S distributed over the ranks in COLUMN SLABS, Q in ROW SLABS, every
+// window's Q_w broadcast by its owner (NCCL) per wavefront, point-to-point
 // transfers only for windows that straddle a slab boundary.
 //
 // Why this layout (reference: the per-window L/R/Q tasks of
@@ -22,8 +22,10 @@
 // Per wavefront level (windows pairwise disjoint), on every rank:
 //   P1 halo-in  (window rows)   neighbour -> owner, for straddling windows
 //   P2 window kernels of the windows this rank owns
-//   P3 all-reduce(sum) of the level's Q_w slots (owners wrote theirs, the
-//      other ranks' slots are zero: the sum is exact)
+//   P3 every rank broadcasts its segment of the level's Q_w slots (the
+//      accumulators of the windows it owns + its deviation flag): one NCCL
+//      group of `world` broadcasts -- each rank receives each accumulator
+//      once (an all-reduce of zero-padded slots moved twice the bytes)
 //   P4 left updates of all windows, this rank's columns
 //   P5 halo-in  (rows above the window, after P4 -- the neighbour's left
 //      updates of the level touched them)
@@ -34,14 +36,19 @@
 // (same kernels, same per-element k order): the distributed result is
 // bitwise identical to teig_reorder_schur_device.
 //
-// Communication is behind `Comm`: NCCL (one rank per process, one GPU per
-// rank) or a loopback that runs all ranks inside one process on one device
-// (peer copies) -- used to test the distributed algorithm on a single GPU.
+// Communication is behind `Comm`: NCCL with one rank per process (torchrun),
+// NCCL with every rank in this process on its own GPU (ncclCommInitAll:
+// teig_dist_reorder_schur_multi), or a loopback that runs all ranks inside
+// one process on one device (device-local copies) -- used to test the
+// distributed algorithm on a single GPU.  Each rank works on its own device
+// and stream pair (RankBufs::dev / st / st2).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -77,6 +84,8 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*GroupStart)() = nullptr;
@@ -101,12 +110,15 @@ NcclApi& nccl() {
     api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
     api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
+    api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(sym("ncclCommInitAll"));
     api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
     api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
     api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
     api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
-    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Send && api.Recv &&
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllReduce && api.Broadcast &&
+             api.CommInitAll && api.Send && api.Recv &&
              api.GroupStart && api.GroupEnd && api.GetErrorString;
     return api;
 }
@@ -137,6 +149,27 @@ struct RankBufs {
     int32_t* dev_level = nullptr;  // deviation level of the pass (window_reorder.cu)
     double* stage = nullptr;    // contiguous staging for NCCL transfers
     size_t stage_cap = 0;
+    int dev = -1;                   // the rank's device (-1: current)
+    cudaStream_t st = nullptr;      // critical path: window kernels, panel updates, collectives
+    cudaStream_t st2 = nullptr;     // factor (Q / Z) updates
+    cudaEvent_t ev = nullptr;       // st -> st2 ordering
+};
+
+// makes `dev` current for the scope (no-op for -1 or the current device)
+struct DevScope {
+    int prev = -1;
+    explicit DevScope(int dev) {
+        if (dev < 0) return;
+        int cur = 0;
+        TEIG_CUDA(cudaGetDevice(&cur));
+        if (cur != dev) {
+            TEIG_CUDA(cudaSetDevice(dev));
+            prev = cur;
+        }
+    }
+    ~DevScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
 };
 
 // a submatrix move between two ranks' slabs (absolute coordinates)
@@ -150,10 +183,15 @@ class Comm {
    public:
     virtual ~Comm() = default;
     virtual bool local(int r) const = 0;
-    // sum-all-reduce of `count` elements at byte offset `off` of every local
-    // rank's buffer (ptrs[r] indexes local ranks' buffers by rank)
-    virtual void allreduce(const std::vector<void*>& bufs, size_t count, ncclDataType_t t, cudaStream_t s) = 0;
-    virtual void transfer(std::vector<RankBufs>& R, const std::vector<Xfer>& xs, int64_t lds, cudaStream_t s) = 0;
+    // element-wise sum of `count` elements of every rank's buffer bufs[r],
+    // written back to all of them (each local rank on its own stream)
+    virtual void allreduce(std::vector<RankBufs>& R, const std::vector<void*>& bufs, size_t count,
+                           ncclDataType_t t) = 0;
+    // segment r of every rank's buffer := rank r's segment r (float64; one
+    // broadcast per owner, grouped): what each window owner publishes
+    virtual void bcast_segments(std::vector<RankBufs>& R, const std::vector<double*>& bufs,
+                                const std::vector<int64_t>& off, const std::vector<int64_t>& len) = 0;
+    virtual void transfer(std::vector<RankBufs>& R, const std::vector<Xfer>& xs, int64_t lds) = 0;
 };
 
 size_t dtype_size(ncclDataType_t t) {
@@ -164,18 +202,31 @@ size_t dtype_size(ncclDataType_t t) {
     }
 }
 
-// all ranks in this process, one device: collectives are peer copies
+// all ranks in this process, one device, one stream pair: collectives are
+// device-local copies (tests the distributed algorithm on a single GPU)
 class LoopbackComm : public Comm {
    public:
     explicit LoopbackComm(int world) : world_(world) {}
     bool local(int) const override { return true; }
-    void allreduce(const std::vector<void*>& bufs, size_t count, ncclDataType_t t, cudaStream_t s) override;
-    void transfer(std::vector<RankBufs>& R, const std::vector<Xfer>& xs, int64_t lds, cudaStream_t s) override {
+    void allreduce(std::vector<RankBufs>& R, const std::vector<void*>& bufs, size_t count,
+                   ncclDataType_t t) override {
+        TEIG_CUDA(launch_sum_buffers(bufs.data(), (int)bufs.size(), count, (int)dtype_size(t), R[0].st));
+    }
+    void bcast_segments(std::vector<RankBufs>& R, const std::vector<double*>& bufs, const std::vector<int64_t>& off,
+                        const std::vector<int64_t>& len) override {
+        for (int r = 0; r < world_; ++r)
+            for (int k = 0; k < world_; ++k)
+                if (k != r && len[r] > 0)
+                    TEIG_CUDA(cudaMemcpyAsync(bufs[k] + off[r], bufs[r] + off[r], (size_t)len[r] * 8,
+                                              cudaMemcpyDeviceToDevice, R[0].st));
+    }
+    void transfer(std::vector<RankBufs>& R, const std::vector<Xfer>& xs, int64_t lds) override {
         for (const auto& x : xs) {
             const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
             if (rows <= 0 || cols <= 0) continue;
-            TEIG_CUDA(cudaMemcpy2DAsync(R[x.dst].mat(x.mat) + x.r0 + x.c0 * lds, lds * 8, R[x.src].mat(x.mat) + x.r0 + x.c0 * lds,
-                                        lds * 8, rows * 8, cols, cudaMemcpyDeviceToDevice, s));
+            TEIG_CUDA(cudaMemcpy2DAsync(R[x.dst].mat(x.mat) + x.r0 + x.c0 * lds, lds * 8,
+                                        R[x.src].mat(x.mat) + x.r0 + x.c0 * lds, lds * 8, rows * 8, cols,
+                                        cudaMemcpyDeviceToDevice, R[0].st));
         }
     }
 
@@ -183,65 +234,95 @@ class LoopbackComm : public Comm {
     int world_;
 };
 
-void LoopbackComm::allreduce(const std::vector<void*>& bufs, size_t count, ncclDataType_t t, cudaStream_t s) {
-    // element-wise sum of every rank's buffer, written back to all of them
-    TEIG_CUDA(launch_sum_buffers(bufs.data(), (int)bufs.size(), count, (int)dtype_size(t), s));
-}
-
+// NCCL, one communicator per LOCAL rank: either one rank per process
+// (comms[rank] only, the torchrun layout) or every rank of the job in this
+// process, one device each (comms from ncclCommInitAll).  Every collective
+// is one NCCL group over the local ranks, each on its own device / stream.
 class NcclComm : public Comm {
    public:
-    NcclComm(ncclComm_t c, int rank) : c_(c), rank_(rank) {}
-    bool local(int r) const override { return r == rank_; }
-    void allreduce(const std::vector<void*>& bufs, size_t count, ncclDataType_t t, cudaStream_t s) override {
-        void* b = bufs[rank_];
-        TEIG_NCCL(nccl().AllReduce(b, b, count, t, ncclSum, c_, s));
-    }
-    void transfer(std::vector<RankBufs>& R, const std::vector<Xfer>& xs, int64_t lds, cudaStream_t s) override {
-        // pack every outgoing piece, exchange in one group, unpack
-        RankBufs& me = R[rank_];
-        size_t need = 0;
-        for (const auto& x : xs)
-            if (x.src == rank_ || x.dst == rank_) need += (size_t)std::max<int64_t>(0, x.r1 - x.r0) * std::max<int64_t>(0, x.c1 - x.c0);
-        if (need == 0) return;
-        if (need > me.stage_cap) {
-            if (me.stage) TEIG_CUDA(cudaFreeAsync(me.stage, s));
-            me.stage_cap = std::max(need, me.stage_cap * 2);
-            TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&me.stage), me.stage_cap * 8, s));
-        }
-        size_t off = 0;
-        std::vector<size_t> offs(xs.size());
-        for (size_t i = 0; i < xs.size(); ++i) {
-            const auto& x = xs[i];
-            offs[i] = off;
-            if (x.src != rank_ && x.dst != rank_) continue;
-            const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
-            if (rows <= 0 || cols <= 0) continue;
-            if (x.src == rank_)
-                TEIG_CUDA(cudaMemcpy2DAsync(me.stage + off, rows * 8, me.mat(x.mat) + x.r0 + x.c0 * lds, lds * 8, rows * 8, cols,
-                                            cudaMemcpyDeviceToDevice, s));
-            off += (size_t)rows * cols;
-        }
+    explicit NcclComm(std::vector<ncclComm_t> comms) : c_(std::move(comms)) {}
+    bool local(int r) const override { return c_[r] != nullptr; }
+    void allreduce(std::vector<RankBufs>& R, const std::vector<void*>& bufs, size_t count,
+                   ncclDataType_t t) override {
         TEIG_NCCL(nccl().GroupStart());
-        for (size_t i = 0; i < xs.size(); ++i) {
-            const auto& x = xs[i];
-            const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
-            if (rows <= 0 || cols <= 0) continue;
-            if (x.src == rank_) TEIG_NCCL(nccl().Send(me.stage + offs[i], (size_t)rows * cols, ncclFloat64, x.dst, c_, s));
-            else if (x.dst == rank_) TEIG_NCCL(nccl().Recv(me.stage + offs[i], (size_t)rows * cols, ncclFloat64, x.src, c_, s));
+        for (int r = 0; r < (int)c_.size(); ++r)
+            if (local(r)) TEIG_NCCL(nccl().AllReduce(bufs[r], bufs[r], count, t, ncclSum, c_[r], R[r].st));
+        TEIG_NCCL(nccl().GroupEnd());
+    }
+    void bcast_segments(std::vector<RankBufs>& R, const std::vector<double*>& bufs, const std::vector<int64_t>& off,
+                        const std::vector<int64_t>& len) override {
+        TEIG_NCCL(nccl().GroupStart());
+        for (int k = 0; k < (int)c_.size(); ++k) {
+            if (!local(k)) continue;
+            for (int r = 0; r < (int)off.size(); ++r)
+                if (len[r] > 0)
+                    TEIG_NCCL(nccl().Broadcast(bufs[k] + off[r], bufs[k] + off[r], (size_t)len[r], ncclFloat64, r,
+                                               c_[k], R[k].st));
         }
         TEIG_NCCL(nccl().GroupEnd());
-        for (size_t i = 0; i < xs.size(); ++i) {
-            const auto& x = xs[i];
-            const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
-            if (rows <= 0 || cols <= 0 || x.dst != rank_) continue;
-            TEIG_CUDA(cudaMemcpy2DAsync(me.mat(x.mat) + x.r0 + x.c0 * lds, lds * 8, me.stage + offs[i], rows * 8, rows * 8, cols,
-                                        cudaMemcpyDeviceToDevice, s));
+    }
+    void transfer(std::vector<RankBufs>& R, const std::vector<Xfer>& xs, int64_t lds) override {
+        // per local rank: pack its outgoing pieces, exchange in one group, unpack
+        const int world = (int)c_.size();
+        std::vector<std::vector<size_t>> offs(world, std::vector<size_t>(xs.size(), 0));
+        for (int me = 0; me < world; ++me) {
+            if (!local(me)) continue;
+            RankBufs& B = R[me];
+            DevScope dsc(B.dev);
+            size_t need = 0;
+            for (const auto& x : xs)
+                if (x.src == me || x.dst == me)
+                    need += (size_t)std::max<int64_t>(0, x.r1 - x.r0) * std::max<int64_t>(0, x.c1 - x.c0);
+            if (need == 0) continue;
+            if (need > B.stage_cap) {
+                if (B.stage) TEIG_CUDA(cudaFreeAsync(B.stage, B.st));
+                B.stage_cap = std::max(need, B.stage_cap * 2);
+                TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.stage), B.stage_cap * 8, B.st));
+            }
+            size_t off = 0;
+            for (size_t i = 0; i < xs.size(); ++i) {
+                const auto& x = xs[i];
+                offs[me][i] = off;
+                if (x.src != me && x.dst != me) continue;
+                const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
+                if (rows <= 0 || cols <= 0) continue;
+                if (x.src == me)
+                    TEIG_CUDA(cudaMemcpy2DAsync(B.stage + off, rows * 8, B.mat(x.mat) + x.r0 + x.c0 * lds, lds * 8,
+                                                rows * 8, cols, cudaMemcpyDeviceToDevice, B.st));
+                off += (size_t)rows * cols;
+            }
+        }
+        TEIG_NCCL(nccl().GroupStart());
+        for (int me = 0; me < world; ++me) {
+            if (!local(me)) continue;
+            for (size_t i = 0; i < xs.size(); ++i) {
+                const auto& x = xs[i];
+                const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
+                if (rows <= 0 || cols <= 0) continue;
+                if (x.src == me)
+                    TEIG_NCCL(nccl().Send(R[me].stage + offs[me][i], (size_t)rows * cols, ncclFloat64, x.dst, c_[me],
+                                          R[me].st));
+                else if (x.dst == me)
+                    TEIG_NCCL(nccl().Recv(R[me].stage + offs[me][i], (size_t)rows * cols, ncclFloat64, x.src, c_[me],
+                                          R[me].st));
+            }
+        }
+        TEIG_NCCL(nccl().GroupEnd());
+        for (int me = 0; me < world; ++me) {
+            if (!local(me)) continue;
+            DevScope dsc(R[me].dev);
+            for (size_t i = 0; i < xs.size(); ++i) {
+                const auto& x = xs[i];
+                const int64_t rows = x.r1 - x.r0, cols = x.c1 - x.c0;
+                if (rows <= 0 || cols <= 0 || x.dst != me) continue;
+                TEIG_CUDA(cudaMemcpy2DAsync(R[me].mat(x.mat) + x.r0 + x.c0 * lds, lds * 8, R[me].stage + offs[me][i],
+                                            rows * 8, rows * 8, cols, cudaMemcpyDeviceToDevice, R[me].st));
+            }
         }
     }
 
    private:
-    ncclComm_t c_;
-    int rank_;
+    std::vector<ncclComm_t> c_;
 };
 
 // ---------------------------------------------------------------------------
@@ -257,6 +338,7 @@ struct LevelPlan {
     };
     std::vector<Part> part;          // [rank]
     int64_t qw_off = 0, qw_len = 0;  // the level's Q_w slots
+    std::vector<int64_t> seg_off, seg_len;  // per owner rank: its windows' slots + its deviation flag (last)
     std::vector<Xfer> halo_win, halo_panel, halo_back;
     int dmax = 64;
 };
@@ -273,7 +355,7 @@ struct PassOut {
 PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankBufs>& R, Comm& comm, int64_t lds,
                       const std::vector<int64_t>& C, const std::vector<int64_t>& Rw, bool with_q, bool gen,
                       std::vector<BlockState>& blocks, std::vector<int64_t>& rejected, std::vector<int64_t>& plan_log,
-                      bool strict, cudaStream_t s, cudaStream_t s2, cudaEvent_t ev) {
+                      bool strict) {
     PassOut po;
     const int64_t nw = (int64_t)plan.windows.size();
     schedule_levels(plan, n);
@@ -282,16 +364,11 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
     for (int64_t i = 0; i < nw; ++i) idx[i] = i;
     std::stable_sort(idx.begin(), idx.end(),
                      [&](int64_t x, int64_t y) { return plan.windows[x].level < plan.windows[y].level; });
-    // Q_w slots in level order, each level followed by one deviation-flag
-    // slot (it rides the level's all-reduce); window kernel status in plan order
+    // Q_w slots level by level; inside a level, owner by owner: rank r's
+    // segment = the accumulators of the windows it owns, then its deviation
+    // flag -- one broadcast per owner publishes the segment to every rank
     std::vector<int64_t> qw_off(nw);
     int64_t qw_total = 0;
-    for (int64_t k = 0; k < nw; ++k) {
-        const auto& w = plan.windows[idx[k]];
-        qw_off[idx[k]] = qw_total;
-        qw_total += (gen ? 2 : 1) * (w.wbot - w.wtop) * (w.wbot - w.wtop);
-        if (k + 1 == nw || plan.windows[idx[k + 1]].level != w.level) qw_total += 1;
-    }
     // per-rank descriptor arrays, level by level
     std::vector<std::vector<WinDesc>> D(world);
     std::vector<std::vector<int64_t>> Dp(world);  // plan index of every descriptor
@@ -302,14 +379,25 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
         lp.part.resize(world);
         const int64_t k0 = k;
         while (k < nw && plan.windows[idx[k]].level == lv) ++k;
-        lp.qw_off = qw_off[idx[k0]];
-        lp.qw_len = 0;
+        lp.qw_off = qw_total;
+        lp.seg_off.assign(world, 0);
+        lp.seg_len.assign(world, 0);
+        for (int r = 0; r < world; ++r) {
+            lp.seg_off[r] = qw_total;
+            for (int64_t t = k0; t < k; ++t) {
+                const auto& w = plan.windows[idx[t]];
+                if (owner_of(C, w.wtop) != r) continue;
+                qw_off[idx[t]] = qw_total;
+                qw_total += (gen ? 2 : 1) * (w.wbot - w.wtop) * (w.wbot - w.wtop);
+            }
+            qw_total += 1;  // rank r's deviation flag
+            lp.seg_len[r] = qw_total - lp.seg_off[r];
+        }
+        lp.qw_len = qw_total - lp.qw_off;
         for (int64_t t = k0; t < k; ++t) {
             const auto& w = plan.windows[idx[t]];
-            lp.qw_len += (gen ? 2 : 1) * (w.wbot - w.wtop) * (w.wbot - w.wtop);
             lp.dmax = std::max<int>(lp.dmax, (int)(w.wbot - w.wtop));
         }
-        lp.qw_len += 1;  // the level's deviation flag
         lp.dmax = lp.dmax <= 64 ? 64 : 128;
         for (int r = 0; r < world; ++r) {
             auto& P = lp.part[r];
@@ -396,158 +484,160 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
             }
         }
     }
-    // device buffers of the pass, per local rank
+    // device buffers of the pass, per local rank (on the rank's device and
+    // stream: one device in loopback, one device per rank otherwise)
     const size_t ne = plan.sizes.size();
-    std::vector<void*> qw_bufs(world, nullptr), ord_bufs(world, nullptr), stk_bufs(world, nullptr);
+    std::vector<void*> ord_bufs(world, nullptr), stk_bufs(world, nullptr);
     for (int r = 0; r < world; ++r) {
         if (!comm.local(r)) continue;
         RankBufs& B = R[r];
-        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.qw), sizeof(double) * std::max<int64_t>(qw_total, 1), s));
-        TEIG_CUDA(cudaMemsetAsync(B.qw, 0, sizeof(double) * std::max<int64_t>(qw_total, 1), s));
-        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.descs), sizeof(WinDesc) * std::max<size_t>(D[r].size(), 1), s));
+        DevScope dsc(B.dev);
+        cudaStream_t st = B.st;
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.qw), sizeof(double) * std::max<int64_t>(qw_total, 1), st));
+        TEIG_CUDA(cudaMemsetAsync(B.qw, 0, sizeof(double) * std::max<int64_t>(qw_total, 1), st));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.descs), sizeof(WinDesc) * std::max<size_t>(D[r].size(), 1), st));
         if (!D[r].empty())
-            TEIG_CUDA(cudaMemcpyAsync(B.descs, D[r].data(), sizeof(WinDesc) * D[r].size(), cudaMemcpyHostToDevice, s));
-        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.sizes), ne + 1, s));
-        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.sel), ne + 1, s));
-        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.order), ne + 1, s));
-        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.stuck), ne + 1, s));
-        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.status), sizeof(int32_t) * std::max<size_t>(D[r].size(), 1), s));
-        TEIG_CUDA(cudaMemsetAsync(B.order, 0, ne + 1, s));
-        TEIG_CUDA(cudaMemsetAsync(B.stuck, 0, ne + 1, s));
-        TEIG_CUDA(cudaMemsetAsync(B.status, 0, sizeof(int32_t) * std::max<size_t>(D[r].size(), 1), s));
-        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.dev_level), sizeof(int32_t), s));
-        TEIG_CUDA(cudaMemsetAsync(B.dev_level, 0x7f, sizeof(int32_t), s));
-        TEIG_CUDA(cudaMemcpyAsync(B.sizes, plan.sizes.data(), ne, cudaMemcpyHostToDevice, s));
-        TEIG_CUDA(cudaMemcpyAsync(B.sel, plan.sel.data(), ne, cudaMemcpyHostToDevice, s));
-        qw_bufs[r] = B.qw;
+            TEIG_CUDA(cudaMemcpyAsync(B.descs, D[r].data(), sizeof(WinDesc) * D[r].size(), cudaMemcpyHostToDevice, st));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.sizes), ne + 1, st));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.sel), ne + 1, st));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.order), ne + 1, st));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.stuck), ne + 1, st));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.status), sizeof(int32_t) * std::max<size_t>(D[r].size(), 1), st));
+        TEIG_CUDA(cudaMemsetAsync(B.order, 0, ne + 1, st));
+        TEIG_CUDA(cudaMemsetAsync(B.stuck, 0, ne + 1, st));
+        TEIG_CUDA(cudaMemsetAsync(B.status, 0, sizeof(int32_t) * std::max<size_t>(D[r].size(), 1), st));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&B.dev_level), sizeof(int32_t), st));
+        TEIG_CUDA(cudaMemsetAsync(B.dev_level, 0x7f, sizeof(int32_t), st));
+        TEIG_CUDA(cudaMemcpyAsync(B.sizes, plan.sizes.data(), ne, cudaMemcpyHostToDevice, st));
+        TEIG_CUDA(cudaMemcpyAsync(B.sel, plan.sel.data(), ne, cudaMemcpyHostToDevice, st));
         ord_bufs[r] = B.order;
         stk_bufs[r] = B.stuck;
     }
     int64_t launches = 0;
+    // runs f(r, B) for every local rank on its device
+    auto each = [&](auto&& f) {
+        for (int r = 0; r < world; ++r) {
+            if (!comm.local(r)) continue;
+            DevScope dsc(R[r].dev);
+            f(r, R[r]);
+        }
+    };
     for (int lv = 0; lv < nl; ++lv) {
         LevelPlan& lp = L[lv];
-        if (!lp.halo_win.empty()) comm.transfer(R, lp.halo_win, lds, s);  // P1
-        for (int r = 0; r < world; ++r) {  // P2
-            if (!comm.local(r)) continue;
+        if (!lp.halo_win.empty()) comm.transfer(R, lp.halo_win, lds);  // P1
+        each([&](int r, RankBufs& B) {  // P2
             const auto& P = lp.part[r];
-            if (P.w_cnt) {
-                if (gen)
-                    TEIG_CUDA(launch_gwindow_reorder(R[r].descs + P.w_off, (int)P.w_cnt, lp.dmax, R[r].S, lds, R[r].T,
-                                                     lds, R[r].qw, R[r].sizes, R[r].sel, R[r].order, R[r].stuck,
-                                                     R[r].status + P.w_off, s, R[r].dev_level));
-                else
-                    TEIG_CUDA(launch_window_reorder(R[r].descs + P.w_off, (int)P.w_cnt, lp.dmax, R[r].S, lds, R[r].qw,
-                                                    R[r].sizes, R[r].sel, R[r].order, R[r].stuck,
-                                                    R[r].status + P.w_off, s, nullptr, R[r].dev_level));
-                ++launches;
-            }
+            if (!P.w_cnt) return;
+            if (gen)
+                TEIG_CUDA(launch_gwindow_reorder(B.descs + P.w_off, (int)P.w_cnt, lp.dmax, B.S, lds, B.T, lds, B.qw,
+                                                 B.sizes, B.sel, B.order, B.stuck, B.status + P.w_off, B.st,
+                                                 B.dev_level));
+            else
+                TEIG_CUDA(launch_window_reorder(B.descs + P.w_off, (int)P.w_cnt, lp.dmax, B.S, lds, B.qw, B.sizes,
+                                                B.sel, B.order, B.stuck, B.status + P.w_off, B.st, nullptr,
+                                                B.dev_level));
+            ++launches;
+        });
+        {  // P3: every owner broadcasts its segment (accumulators + deviation flag)
+            std::vector<double*> b(world, nullptr);
+            std::vector<int64_t> flags(world);
+            for (int r = 0; r < world; ++r) flags[r] = lp.seg_off[r] + lp.seg_len[r] - 1;
+            each([&](int r, RankBufs& B) {
+                b[r] = B.qw;
+                TEIG_CUDA(launch_dist_flag(B.dev_level, B.qw, &flags[r], 1, lv, 0, B.st));
+            });
+            comm.bcast_segments(R, b, lp.seg_off, lp.seg_len);
+            each([&](int, RankBufs& B) {
+                TEIG_CUDA(launch_dist_flag(B.dev_level, B.qw, flags.data(), world, lv, 1, B.st));
+            });
         }
-        {  // P3 (with the deviation flag: published before, absorbed after)
-            const int64_t flag = lp.qw_off + lp.qw_len - 1;
-            std::vector<void*> b(world, nullptr);
-            for (int r = 0; r < world; ++r)
-                if (comm.local(r)) {
-                    b[r] = R[r].qw + lp.qw_off;
-                    TEIG_CUDA(launch_dist_flag(R[r].dev_level, R[r].qw + flag, lv, 0, s));
-                }
-            comm.allreduce(b, (size_t)lp.qw_len, ncclFloat64, s);
-            for (int r = 0; r < world; ++r)
-                if (comm.local(r)) TEIG_CUDA(launch_dist_flag(R[r].dev_level, R[r].qw + flag, lv, 1, s));
-        }
-        for (int r = 0; r < world; ++r) {  // P4
-            if (!comm.local(r)) continue;
+        each([&](int r, RankBufs& B) {  // P4
             const auto& P = lp.part[r];
-            if (P.l_tiles) {
-                TEIG_CUDA(launch_update_left(R[r].descs + P.l_off, (int)P.l_cnt, (int)P.l_tiles, lp.dmax, R[r].qw,
-                                             R[r].S, lds, (int)n, s, n, C[r + 1] + kHalo));
-                if (gen)
-                    TEIG_CUDA(launch_update_left(R[r].descs + P.l_off, (int)P.l_cnt, (int)P.l_tiles, lp.dmax, R[r].qw,
-                                                 R[r].T, lds, (int)n, s, n, C[r + 1] + kHalo));
-                ++launches;
-            }
-        }
-        if (!lp.halo_panel.empty()) comm.transfer(R, lp.halo_panel, lds, s);  // P5
-        for (int r = 0; r < world; ++r) {  // P6
-            if (!comm.local(r)) continue;
+            if (!P.l_tiles) return;
+            TEIG_CUDA(launch_update_left(B.descs + P.l_off, (int)P.l_cnt, (int)P.l_tiles, lp.dmax, B.qw, B.S, lds,
+                                         (int)n, B.st, n, C[r + 1] + kHalo));
+            if (gen)
+                TEIG_CUDA(launch_update_left(B.descs + P.l_off, (int)P.l_cnt, (int)P.l_tiles, lp.dmax, B.qw, B.T, lds,
+                                             (int)n, B.st, n, C[r + 1] + kHalo));
+            ++launches;
+        });
+        if (!lp.halo_panel.empty()) comm.transfer(R, lp.halo_panel, lds);  // P5
+        each([&](int r, RankBufs& B) {  // P6
             const auto& P = lp.part[r];
-            if (P.r_tiles) {
-                TEIG_CUDA(launch_update_right(R[r].descs + P.r_off, (int)P.r_cnt, (int)P.r_tiles, lp.dmax, R[r].qw,
-                                              R[r].S, lds, (int)n, false, s, n, C[r + 1] + kHalo));
-                if (gen)
-                    TEIG_CUDA(launch_update_right(R[r].descs + P.r_off, (int)P.r_cnt, (int)P.r_tiles, lp.dmax, R[r].qw,
-                                                  R[r].T, lds, (int)n, false, s, n, C[r + 1] + kHalo));
-                ++launches;
-            }
-        }
-        if (!lp.halo_back.empty()) comm.transfer(R, lp.halo_back, lds, s);  // P7
-        // P8 on the second stream: the Q (and Z) updates only need the
-        // level's all-reduced Q_w; they overlap the next levels' window
+            if (!P.r_tiles) return;
+            TEIG_CUDA(launch_update_right(B.descs + P.r_off, (int)P.r_cnt, (int)P.r_tiles, lp.dmax, B.qw, B.S, lds,
+                                          (int)n, false, B.st, n, C[r + 1] + kHalo));
+            if (gen)
+                TEIG_CUDA(launch_update_right(B.descs + P.r_off, (int)P.r_cnt, (int)P.r_tiles, lp.dmax, B.qw, B.T,
+                                              lds, (int)n, false, B.st, n, C[r + 1] + kHalo));
+            ++launches;
+        });
+        if (!lp.halo_back.empty()) comm.transfer(R, lp.halo_back, lds);  // P7
+        // P8 on each rank's second stream: the Q (and Z) updates only need
+        // the level's broadcast Q_w; they overlap the next levels' window
         // kernels and panel updates (the single-GPU driver's schedule)
-        const bool any_q = [&] {
-            for (int r = 0; r < world; ++r)
-                if (comm.local(r) && lp.part[r].q_tiles) return true;
-            return false;
-        }();
-        if (any_q) {
-            TEIG_CUDA(cudaEventRecord(ev, s));
-            TEIG_CUDA(cudaStreamWaitEvent(s2, ev, 0));
-        }
-        for (int r = 0; r < world; ++r) {  // P8
-            if (!comm.local(r)) continue;
+        each([&](int r, RankBufs& B) {
             const auto& P = lp.part[r];
-            if (P.q_tiles) {
-                TEIG_CUDA(launch_update_right(R[r].descs + P.q_off, (int)P.q_cnt, (int)P.q_tiles, lp.dmax, R[r].qw,
-                                              R[r].Q, R[r].ldq, (int)n, true, s2, Rw[r + 1], n));
-                if (gen && P.z_cnt && R[r].Z)
-                    TEIG_CUDA(launch_update_right(R[r].descs + P.z_off, (int)P.z_cnt, (int)P.q_tiles, lp.dmax, R[r].qw,
-                                                  R[r].Z, R[r].ldq, (int)n, true, s2, Rw[r + 1], n));
-                ++launches;
-            }
-        }
+            if (!P.q_tiles) return;
+            TEIG_CUDA(cudaEventRecord(B.ev, B.st));
+            TEIG_CUDA(cudaStreamWaitEvent(B.st2, B.ev, 0));
+            TEIG_CUDA(launch_update_right(B.descs + P.q_off, (int)P.q_cnt, (int)P.q_tiles, lp.dmax, B.qw, B.Q, B.ldq,
+                                          (int)n, true, B.st2, Rw[r + 1], n));
+            if (gen && P.z_cnt && B.Z)
+                TEIG_CUDA(launch_update_right(B.descs + P.z_off, (int)P.z_cnt, (int)P.q_tiles, lp.dmax, B.qw, B.Z,
+                                              B.ldq, (int)n, true, B.st2, Rw[r + 1], n));
+            ++launches;
+        });
     }
-    TEIG_CUDA(cudaEventRecord(ev, s2));
-    TEIG_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    each([&](int, RankBufs& B) {
+        TEIG_CUDA(cudaEventRecord(B.ev, B.st2));
+        TEIG_CUDA(cudaStreamWaitEvent(B.st, B.ev, 0));
+    });
     // share the window outcomes (each written by its owner only), fold
-    comm.allreduce(ord_bufs, ne + 1, ncclUint8, s);
-    comm.allreduce(stk_bufs, ne + 1, ncclUint8, s);
+    comm.allreduce(R, ord_bufs, ne + 1, ncclUint8);
+    comm.allreduce(R, stk_bufs, ne + 1, ncclUint8);
     int me = 0;
     while (!comm.local(me)) ++me;
     std::vector<int32_t> status(std::max<int64_t>(nw, 1), 0);
     std::vector<uint8_t> order(ne + 1), stuck(ne + 1);
-    TEIG_CUDA(cudaMemcpyAsync(order.data(), R[me].order, ne + 1, cudaMemcpyDeviceToHost, s));
-    TEIG_CUDA(cudaMemcpyAsync(stuck.data(), R[me].stuck, ne + 1, cudaMemcpyDeviceToHost, s));
-    for (int r = 0; r < world; ++r) {
-        if (!comm.local(r) || D[r].empty()) continue;
+    {
+        DevScope dsc(R[me].dev);
+        TEIG_CUDA(cudaMemcpyAsync(order.data(), R[me].order, ne + 1, cudaMemcpyDeviceToHost, R[me].st));
+        TEIG_CUDA(cudaMemcpyAsync(stuck.data(), R[me].stuck, ne + 1, cudaMemcpyDeviceToHost, R[me].st));
+        TEIG_CUDA(cudaStreamSynchronize(R[me].st));
+    }
+    each([&](int r, RankBufs& B) {
+        if (D[r].empty()) return;
         std::vector<int32_t> st(D[r].size());
-        TEIG_CUDA(cudaMemcpyAsync(st.data(), R[r].status, sizeof(int32_t) * st.size(), cudaMemcpyDeviceToHost, s));
-        TEIG_CUDA(cudaStreamSynchronize(s));
+        TEIG_CUDA(cudaMemcpyAsync(st.data(), B.status, sizeof(int32_t) * st.size(), cudaMemcpyDeviceToHost, B.st));
+        TEIG_CUDA(cudaStreamSynchronize(B.st));
         for (size_t i = 0; i < st.size(); ++i)
             if (Dp[r][i] >= 0) status[Dp[r][i]] |= st[i];
-    }
-    if (!comm.local((me + 1) % world) && world > 1) {  // NCCL: combine the ranks' statuses
+    });
+    if (!comm.local((me + 1) % world) && world > 1) {  // one rank per process: combine the ranks' statuses
+        DevScope dsc(R[me].dev);
         int32_t* dst = nullptr;
-        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&dst), sizeof(int32_t) * status.size(), s));
-        TEIG_CUDA(cudaMemcpyAsync(dst, status.data(), sizeof(int32_t) * status.size(), cudaMemcpyHostToDevice, s));
+        TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&dst), sizeof(int32_t) * status.size(), R[me].st));
+        TEIG_CUDA(cudaMemcpyAsync(dst, status.data(), sizeof(int32_t) * status.size(), cudaMemcpyHostToDevice, R[me].st));
         std::vector<void*> b(world, nullptr);
         b[me] = dst;
-        comm.allreduce(b, status.size(), ncclInt32, s);
-        TEIG_CUDA(cudaMemcpyAsync(status.data(), dst, sizeof(int32_t) * status.size(), cudaMemcpyDeviceToHost, s));
-        TEIG_CUDA(cudaFreeAsync(dst, s));
+        comm.allreduce(R, b, status.size(), ncclInt32);
+        TEIG_CUDA(cudaMemcpyAsync(status.data(), dst, sizeof(int32_t) * status.size(), cudaMemcpyDeviceToHost, R[me].st));
+        TEIG_CUDA(cudaFreeAsync(dst, R[me].st));
+        TEIG_CUDA(cudaStreamSynchronize(R[me].st));
     }
-    TEIG_CUDA(cudaStreamSynchronize(s));
-    for (int r = 0; r < world; ++r) {
-        if (!comm.local(r)) continue;
-        RankBufs& B = R[r];
-        cudaFreeAsync(B.qw, s);
-        cudaFreeAsync(B.descs, s);
-        cudaFreeAsync(B.sizes, s);
-        cudaFreeAsync(B.sel, s);
-        cudaFreeAsync(B.order, s);
-        cudaFreeAsync(B.stuck, s);
-        cudaFreeAsync(B.status, s);
-        cudaFreeAsync(B.dev_level, s);
+    each([&](int, RankBufs& B) {
+        cudaFreeAsync(B.qw, B.st);
+        cudaFreeAsync(B.descs, B.st);
+        cudaFreeAsync(B.sizes, B.st);
+        cudaFreeAsync(B.sel, B.st);
+        cudaFreeAsync(B.order, B.st);
+        cudaFreeAsync(B.stuck, B.st);
+        cudaFreeAsync(B.status, B.st);
+        cudaFreeAsync(B.dev_level, B.st);
         B.qw = nullptr;
-    }
+        TEIG_CUDA(cudaStreamSynchronize(B.st));
+    });
     status.resize(nw);
     po.deviated = fold_outcomes(plan, blocks, status, order, stuck, rejected, plan_log, strict);
     po.windows = 0;
@@ -696,14 +786,37 @@ int teig_nccl_comm_destroy(void* comm) {
     return 0;
 }
 
-static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, double* const* dS_slabs,
-                     double* const* dT_slabs, int64_t lds, double* const* dQ_slabs, double* const* dZ_slabs,
-                     const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb, const uint8_t* sizes,
-                     const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected_out,
-                     teig_reorder_info* info, void* stream_v, bool gen) {
+// NCCL communicators of the single-process multi-GPU entry points, one
+// clique per device list (ncclCommInitAll), kept for the process lifetime.
+std::mutex g_clique_mu;
+std::map<std::vector<int>, std::vector<ncclComm_t>> g_cliques;
+
+std::vector<ncclComm_t> clique(const std::vector<int>& devs) {
+    std::lock_guard<std::mutex> lk(g_clique_mu);
+    auto it = g_cliques.find(devs);
+    if (it != g_cliques.end()) return it->second;
+    std::vector<ncclComm_t> comms(devs.size(), nullptr);
+    TEIG_NCCL(nccl().CommInitAll(comms.data(), (int)devs.size(), devs.data()));
+    g_cliques[devs] = comms;
+    return comms;
+}
+
+// Three execution modes share one driver:
+//   loopback      nccl_comm == NULL, devices == NULL: all ranks in this
+//                 process on the current device, device-local collectives
+//   one rank per  nccl_comm != NULL: this process is rank `rank` (torchrun)
+//   process
+//   multi-GPU     devices != NULL: all ranks in this process, rank r on
+//                 devices[r], NCCL clique from ncclCommInitAll
+static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, const int32_t* devices,
+                     double* const* dS_slabs, double* const* dT_slabs, int64_t lds, double* const* dQ_slabs,
+                     double* const* dZ_slabs, const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb,
+                     const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm,
+                     int64_t* rejected_out, teig_reorder_info* info, void* stream_v, bool gen) {
     if (n < 1) return set_error(-1, "n must be >= 1");
-    if (world < 1) return set_error(-2, "world must be >= 1");
-    const bool loop = nccl_comm == nullptr;
+    if (world < 1 || world > 16) return set_error(-2, "world must be in [1, 16]");
+    const bool multi = devices != nullptr;
+    const bool loop = !multi && nccl_comm == nullptr;
     if (!loop && (rank < 0 || rank >= world)) return set_error(-3, "rank out of range");
     if (!dS_slabs || !col_bounds || !row_bounds) return set_error(-5, "null slabs/bounds");
     if (lds < n) return set_error(-6, "lds < n");
@@ -731,12 +844,65 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, do
     std::vector<int64_t> C(col_bounds, col_bounds + world + 1), Rw(row_bounds, row_bounds + world + 1);
     teig_reorder_info inf{};
     std::vector<int64_t> rejected, plan_log;
+    // per-rank streams: loopback / one rank per process run on the caller's
+    // stream plus one side stream; multi-GPU creates a stream pair per device
+    struct Streams {
+        std::vector<RankBufs>* R = nullptr;
+        std::vector<cudaStream_t> own_s;
+        std::vector<cudaEvent_t> own_e;
+        std::vector<int> dev_s, dev_e;
+        ~Streams() {
+            for (size_t i = 0; i < own_s.size(); ++i) {
+                DevScope d(dev_s[i]);
+                cudaStreamSynchronize(own_s[i]);
+                cudaStreamDestroy(own_s[i]);
+            }
+            for (size_t i = 0; i < own_e.size(); ++i) {
+                DevScope d(dev_e[i]);
+                cudaEventDestroy(own_e[i]);
+            }
+        }
+        cudaStream_t stream(int dev) {
+            DevScope d(dev);
+            cudaStream_t x = nullptr;
+            TEIG_CUDA(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+            own_s.push_back(x);
+            dev_s.push_back(dev);
+            return x;
+        }
+        cudaEvent_t event(int dev) {
+            DevScope d(dev);
+            cudaEvent_t x = nullptr;
+            TEIG_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+            own_e.push_back(x);
+            dev_e.push_back(dev);
+            return x;
+        }
+    };
     try {
+        if (!loop && !nccl().ok) return set_error(TEIG_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
         std::vector<RankBufs> R(world);
+        Streams streams;
+        cudaStream_t side = nullptr;
+        cudaEvent_t side_ev = nullptr;
+        if (!multi) {
+            side = streams.stream(-1);
+            side_ev = streams.event(-1);
+        }
         for (int r = 0; r < world; ++r) {
             R[r].rank = r;
-            const int li = loop ? r : (r == rank ? 0 : -1);
+            const int li = (loop || multi) ? r : (r == rank ? 0 : -1);
             if (li < 0) continue;
+            if (multi) {
+                R[r].dev = devices[r];
+                R[r].st = streams.stream(devices[r]);
+                R[r].st2 = streams.stream(devices[r]);
+                R[r].ev = streams.event(devices[r]);
+            } else {
+                R[r].st = s;
+                R[r].st2 = side;
+                R[r].ev = side_ev;
+            }
             R[r].S = dS_slabs[li] - C[r] * lds;
             R[r].ldq = std::max<int64_t>(Rw[r + 1] - Rw[r], 1);
             R[r].Q = (dQ_slabs && dQ_slabs[li]) ? dQ_slabs[li] - Rw[r] : nullptr;
@@ -746,21 +912,11 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, do
             }
         }
         const bool with_q = dQ_slabs != nullptr;
-        struct Side {  // the second stream of the Q/Z updates
-            cudaStream_t s = nullptr;
-            cudaEvent_t e = nullptr;
-            ~Side() {
-                if (e) cudaEventDestroy(e);
-                if (s) cudaStreamDestroy(s);
-            }
-        } side;
-        TEIG_CUDA(cudaStreamCreateWithFlags(&side.s, cudaStreamNonBlocking));
-        TEIG_CUDA(cudaEventCreateWithFlags(&side.e, cudaEventDisableTiming));
-        cudaStream_t s2 = side.s;
-        cudaEvent_t ev = side.e;
         LoopbackComm lb(world);
-        if (!loop && !nccl().ok) return set_error(TEIG_ERR_UNSUPPORTED, "libnccl.so.2 not loadable");
-        NcclComm nc(static_cast<ncclComm_t>(nccl_comm), rank);
+        std::vector<ncclComm_t> comms(world, nullptr);
+        if (multi) comms = clique(std::vector<int>(devices, devices + world));
+        else if (!loop) comms[rank] = static_cast<ncclComm_t>(nccl_comm);
+        NcclComm nc(comms);
         Comm& comm = loop ? static_cast<Comm&>(lb) : static_cast<Comm&>(nc);
         for (int pass = 0; pass < 64; ++pass) {
             ReorderPlan plan = plan_reorder(blocks, ws);
@@ -769,7 +925,7 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, do
             inf.update_flops += (gen ? 2.0 : 1.0) * plan_update_flops(plan, n, with_q);
             inf.update_bytes += (gen ? 2.0 : 1.0) * plan_update_bytes(plan, n, with_q);
             PassOut po = run_dist_pass(plan, n, world, R, comm, lds, C, Rw, with_q, gen, blocks, rejected, plan_log,
-                                       o.strict != 0, s, s2, ev);
+                                       o.strict != 0);
             inf.n_windows += po.windows;
             inf.n_levels += po.levels;
             inf.n_launches += po.launches;
@@ -777,8 +933,11 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, do
             if (!po.deviated) break;
         }
         for (auto& B : R)
-            if (B.stage) cudaFreeAsync(B.stage, s);
-        TEIG_CUDA(cudaStreamSynchronize(s));
+            if (B.st) {
+                DevScope d(B.dev);
+                if (B.stage) cudaFreeAsync(B.stage, B.st);
+                TEIG_CUDA(cudaStreamSynchronize(B.st));
+            }
     } catch (const std::domain_error& e) {
         return set_error(TEIG_ERR_STRICT, e.what());
     } catch (const std::exception& e) {
@@ -808,8 +967,8 @@ int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_c
                             const int64_t* row_bounds, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
                             const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected, teig_reorder_info* info,
                             void* stream) {
-    return dist_impl(n, world, rank, nccl_comm, dS_slabs, nullptr, lds, dQ_slabs, nullptr, col_bounds, row_bounds, nb,
-                     sizes, flags, opts, perm, rejected, info, stream, false);
+    return dist_impl(n, world, rank, nccl_comm, nullptr, dS_slabs, nullptr, lds, dQ_slabs, nullptr, col_bounds,
+                     row_bounds, nb, sizes, flags, opts, perm, rejected, info, stream, false);
 }
 
 int teig_dist_greorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_comm, double* const* dS_slabs,
@@ -817,8 +976,21 @@ int teig_dist_greorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_
                              const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb, const uint8_t* sizes,
                              const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
                              teig_reorder_info* info, void* stream) {
-    return dist_impl(n, world, rank, nccl_comm, dS_slabs, dT_slabs, lds, dQ_slabs, dZ_slabs, col_bounds, row_bounds,
-                     nb, sizes, flags, opts, perm, rejected, info, stream, true);
+    return dist_impl(n, world, rank, nccl_comm, nullptr, dS_slabs, dT_slabs, lds, dQ_slabs, dZ_slabs, col_bounds,
+                     row_bounds, nb, sizes, flags, opts, perm, rejected, info, stream, true);
+}
+
+int teig_dist_reorder_schur_multi(int64_t n, int32_t world, const int32_t* devices, double* const* dS_slabs,
+                                  int64_t lds, double* const* dQ_slabs, const int64_t* col_bounds,
+                                  const int64_t* row_bounds, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
+                                  const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
+                                  teig_reorder_info* info) {
+    if (!devices) return set_error(-3, "devices is null");
+    for (int r = 0; r < world; ++r)
+        for (int k = 0; k < r; ++k)
+            if (devices[k] == devices[r]) return set_error(-3, "devices must be distinct (one rank per GPU)");
+    return dist_impl(n, world, 0, nullptr, devices, dS_slabs, nullptr, lds, dQ_slabs, nullptr, col_bounds, row_bounds,
+                     nb, sizes, flags, opts, perm, rejected, info, nullptr, false);
 }
 
 int teig_gen_schur_input_cols_device(int64_t n, double* dS, int64_t lds, int64_t c0, int64_t c1, uint64_t fill_seed,

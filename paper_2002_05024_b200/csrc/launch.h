@@ -107,8 +107,10 @@ cudaError_t launch_gemm_nn(int m, int n, int kdim, const double* A, long long ld
                            double* C, long long ldc, cudaStream_t s);
 cudaError_t launch_renorm_columns(int n, double* X, long long ldx, const int8_t* kind_dev, int k, int* nonfinite,
                                   cudaStream_t s);
-// distributed deviation flag: mode 0 publish into the level's slot, 1 absorb
-cudaError_t launch_dist_flag(int32_t* dev_level, double* slot, int level, int mode, cudaStream_t s);
+// distributed deviation flag: mode 0 publish this rank's flag into base[slots[0]],
+// mode 1 absorb from the nslots flag slots base[slots[i]]
+cudaError_t launch_dist_flag(int32_t* dev_level, double* base, const int64_t* slots, int nslots, int level, int mode,
+                             cudaStream_t s);
 // element-wise sum of nbuf device buffers into all of them (loopback all-reduce)
 cudaError_t launch_sum_buffers(void* const* bufs, int nbuf, size_t count, int elem_bytes, cudaStream_t s);
 

@@ -3,10 +3,12 @@
 
 S lives in COLUMN SLABS (rank r owns columns [C[r], C[r+1]) plus a 128-column
 halo), Q in ROW SLABS (rank r owns rows [R[r], R[r+1])).  Every wavefront's
-packed Q_w is all-reduced with NCCL; windows straddling a slab boundary move
-their missing columns point to point.  One process per GPU
-(``reorder_schur_dist`` with an NCCL communicator from ``nccl_comm``), or --
-for tests on a single GPU -- all ranks in one process (``reorder_schur_loopback``).
+accumulators are published by their owners (one grouped NCCL broadcast per
+owner); windows straddling a slab boundary move their missing columns point
+to point.  One process per GPU (``reorder_schur_dist`` with an NCCL
+communicator from ``nccl_comm``), all ranks in one process on one GPU each
+(``reorder_schur_multi``, ncclCommInitAll), or -- for tests on a single GPU
+-- all ranks in one process on one device (``reorder_schur_loopback``).
 The distributed result is bitwise identical to ``reorder_schur``.
 """
 from __future__ import annotations
@@ -176,6 +178,57 @@ def reorder_schur_loopback(s, q, sel: Selection, world: int, opts: Optional[Reor
         if q is not None and rb[r + 1] > rb[r]:
             q[rb[r]:rb[r + 1], :].copy_(qs[r])
     return ReorderResult(s, q, perm, rej, [], clean, inf)
+
+
+def reorder_schur_multi(s, q, sel: Selection, devices: Sequence[int], opts: Optional[ReorderOptions] = None,
+                        col_bounds=None, row_bounds=None) -> ReorderResult:
+    """All ranks in THIS process, rank r on GPU devices[r] (distinct), one
+    NCCL clique from ncclCommInitAll (teig_dist_reorder_schur_multi): the
+    single-process multi-GPU entry behind the reference's in-process API.
+    s (and q) are scattered from their device into slabs on each rank's GPU,
+    reordered, and gathered back in place.  Bitwise equal to reorder_schur."""
+    n = s.shape[0]
+    world = len(devices)
+    opts = opts or ReorderOptions()
+    if col_bounds is None:
+        col_bounds, row_bounds = balance(n, sel, world, opts.window_size)
+    cb, rb = list(map(int, col_bounds)), list(map(int, row_bounds))
+    ss, qs = [], []
+    for r, dev in enumerate(devices):
+        d = torch.device("cuda", int(dev))
+        t = s_slab_empty(n, cb[r], cb[r + 1], d)
+        t[:, : cb[r + 1] - cb[r]].copy_(s[:, cb[r]:cb[r + 1]])
+        ss.append(t)
+        if q is not None:
+            u = q_slab_empty(n, rb[r], rb[r + 1], d)
+            if rb[r + 1] > rb[r]:
+                u.copy_(q[rb[r]:rb[r + 1], :])
+            qs.append(u)
+    for dev in devices:
+        torch.cuda.synchronize(int(dev))
+    nb = len(sel.blocks)
+    sizes, flags = sel.sizes_array(), sel.flags_array()
+    perm = np.zeros(max(nb, 1), dtype=np.int64)
+    rej = np.zeros(max(nb, 1), dtype=np.int64)
+    info = N.ReorderInfo()
+    sp = (C.c_void_p * world)(*[t.data_ptr() for t in ss])
+    qp = (C.c_void_p * world)(*[t.data_ptr() for t in qs]) if q is not None else None
+    dv = np.ascontiguousarray(devices, dtype=np.int32)
+    cba = np.ascontiguousarray(cb, dtype=np.int64)
+    rba = np.ascontiguousarray(rb, dtype=np.int64)
+    o = _opts(opts)
+    rc = N.lib().teig_dist_reorder_schur_multi(n, world, _vp(dv), sp, n, qp, _vp(cba), _vp(rba), nb, _vp(sizes),
+                                               _vp(flags), C.byref(o), _vp(perm), _vp(rej), C.byref(info))
+    if rc == -1002:
+        raise RuntimeError("reorder_schur: swap rejected in strict mode")
+    N.check(rc)
+    for r in range(world):
+        s[:, cb[r]:cb[r + 1]].copy_(ss[r][:, : cb[r + 1] - cb[r]])
+        if q is not None and rb[r + 1] > rb[r]:
+            q[rb[r]:rb[r + 1], :].copy_(qs[r])
+    inf = {f: getattr(info, f) for f, _ in N.ReorderInfo._fields_ if f != "pad"}
+    return ReorderResult(s, q, [int(x) for x in perm[:nb]], [int(x) for x in rej[:info.n_rejected]], [],
+                         bool(info.clean), inf)
 
 
 # ---------------------------------------------------------------------------

@@ -59,10 +59,10 @@ def case(name):
             bl.append(("r", 3.0 + k)); fl.append(k % 2 == 0)
         bl.append(("c", -2.0, 0.5)); fl.append(True)
         return (*build(bl, 11), np.array(fl, dtype=np.uint8), 32)
-    if name in ("multigroup", "midchain", "dense"):
-        n_target = {"multigroup": 400, "midchain": 300, "dense": 260}[name]
-        ws = {"multigroup": 64, "midchain": 24, "dense": 32}[name]
-        ntw = {"multigroup": 3, "midchain": 2, "dense": 5}[name]
+    if name in ("multigroup", "midchain", "dense", "wide"):
+        n_target = {"multigroup": 400, "midchain": 300, "dense": 260, "wide": 1100}[name]
+        ws = {"multigroup": 64, "midchain": 24, "dense": 32, "wide": 64}[name]
+        ntw = {"multigroup": 3, "midchain": 2, "dense": 5, "wide": 6}[name]
         bl, fl = [], []
         reals = iter(np.linspace(-10.0, 10.0, n_target))
         pair_re = iter(np.linspace(-9.7, 9.7, n_target))
@@ -75,6 +75,8 @@ def case(name):
             plant = [(40, 200), (90, 260)]
         elif name == "dense":
             plant = [(10 + 45 * k, 30 + 45 * k) for k in range(ntw)]
+        elif name == "wide":  # twins on both sides of the slab boundaries of 2-4 ranks
+            plant = [(100 + 170 * k, 190 + 170 * k) for k in range(ntw)]
         else:
             plant = [(60 + 110 * k, 100 + 110 * k) for k in range(ntw)]
         pending = sorted([(p[0], 0, k) for k, p in enumerate(plant)] + [(p[1], 1, k) for k, p in enumerate(plant)])

@@ -71,3 +71,48 @@ def test_generalized_loopback_equals_single_gpu(T, O, cuda, n, world):
     perm, rej, clean, info = D.greorder_schur_loopback(s2, t2, q2, z2, sel, world, opts)
     assert r1.clean and clean and perm == r1.permutation
     assert torch.equal(s1, s2) and torch.equal(t1, t2) and torch.equal(q1, q2) and torch.equal(z1, z2)
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_loopback_rejections_equal_single_gpu(T, O, cuda, world):
+    """Rejected swaps across ranks: the deviation flag rides every owner's
+    broadcast segment, later levels skip on every rank, the replan pass runs
+    distributed -- the result equals the single-GPU driver's bit for bit and
+    the predicted arrangement (tests/rejection_cases.py)."""
+    import torch
+    import rejection_cases as RC
+    from paper_2002_05024_b200 import dist as D
+    S, sizes, flags, ws = RC.case("wide")
+    n = S.shape[0]
+    s0 = torch.as_tensor(S).cuda().t().contiguous().t()
+    sel = T.select_eigenvalues(s0, [bool(f) for f in flags])
+    s1, q1 = s0.clone(), T.identity(n)
+    r1 = T.reorder_schur(s1, q1, sel, T.ReorderOptions(window_size=ws))
+    s2, q2 = s0.clone(), T.identity(n)
+    r2 = D.reorder_schur_loopback(s2, q2, sel, world, T.ReorderOptions(window_size=ws))
+    perm, rej = RC.predicted_permutation(S, sizes, flags)
+    assert not r1.clean and not r2.clean
+    assert r1.permutation == r2.permutation == perm.tolist()
+    assert r1.rejected_blocks == r2.rejected_blocks == rej
+    assert torch.equal(s1, s2) and torch.equal(q1, q2)
+
+
+def test_multi_gpu_entry_single_device(T, O, cuda):
+    """The single-process multi-GPU entry (teig_dist_reorder_schur_multi:
+    per-device stream pairs, NCCL clique from ncclCommInitAll, grouped
+    broadcasts) on the one GPU this box has (world 1): equals the single-GPU
+    driver bit for bit.  With more GPUs pass more devices."""
+    import torch
+    from paper_2002_05024_b200 import dist as D
+    if not D.nccl_available():
+        pytest.skip("libnccl.so.2 not loadable")
+    n = 1500
+    s0 = T.gen_schur_input(n, T.known_spectrum_seed(6))
+    sel = T.select_fraction(s0, 0.35, 4)
+    s1, q1 = s0.clone(), T.identity(n)
+    r1 = T.reorder_schur(s1, q1, sel, T.ReorderOptions(window_size=128))
+    devs = list(range(torch.cuda.device_count()))[:4]
+    s2, q2 = s0.clone(), T.identity(n)
+    r2 = D.reorder_schur_multi(s2, q2, sel, devs, T.ReorderOptions(window_size=128))
+    assert r1.clean and r2.clean and r1.permutation == r2.permutation
+    assert torch.equal(s1, s2) and torch.equal(q1, q2)
