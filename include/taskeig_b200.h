@@ -262,6 +262,22 @@ int teig_small_schur_device(int64_t k, double* dH, int64_t ldh, double* dQ, int3
 int teig_deflation_check(double spike, double diag_sum, int32_t deflation, double wnorm);
 
 /* ------------------------------------------------------------------------ */
+/* Hessenberg reduction (replaces taskeig::hessenberg_reduce,                 */
+/* hessenberg.hpp / hessenberg.cpp:185-280): dA (n x n, column-major, device) */
+/* is reduced in place to upper Hessenberg H = Q1^T A Q1 by the reference's   */
+/* blocked compact-WY algorithm (panels of panel_width columns; 0: min(tile,  */
+/* 64) as the reference, larger values run at 64); dQ (device, or NULL)       */
+/* receives Q1.  Entries below the subdiagonal are exact zeros.  Synchronous. */
+typedef struct teig_hessenberg_info {
+    int64_t panels;
+    int64_t launches;
+    double flops;
+    int64_t panel_width;
+} teig_hessenberg_info;
+int teig_hessenberg_reduce_device(int64_t n, double* dA, int64_t lda, double* dQ, int64_t ldq,
+                                  int64_t panel_width, teig_hessenberg_info* info, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Eigenvector back-transformation (replaces taskeig::backtransform,          */
 /* eigvec.hpp:88-89 / eigvec.cpp:448-516): X = Q Y on the FP64 tensor pipe   */
 /* with the device-resident Q of a reorder / Schur call, then every real      */

@@ -15,6 +15,7 @@ from .reorder import (  # noqa: F401
     known_spectrum_seed, plan_reorder, reorder_schur, scan_blocks, scan_blocks_device, select_by_name,
     select_eigenvalues, select_fraction, window_reorder)
 from .eigvec import backtransform  # noqa: F401
+from .hessenberg import HessenbergOptions, HessenbergResult, hessenberg_reduce  # noqa: F401
 from .schur import (  # noqa: F401
     AedResult, BulgeChain, DeflationCondition, SchurDecomposition, SchurOptions, aed_step, chase_bulges,
     deflation_check, introduce_bulges, schur_reduce, small_schur)

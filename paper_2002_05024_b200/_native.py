@@ -101,6 +101,7 @@ SIGNATURES = {
     "teig_small_schur_device": (C.c_int, [_I64, _P, _I64, _P, _P, _P]),
     "teig_plan_chase": (C.c_int64, [_I64, _P, _I64, _I64, _P, _I64]),
     "teig_backtransform_device": (C.c_int, [_I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _P]),
+    "teig_hessenberg_reduce_device": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _P, _P]),
     "teig_write_matrix_file": (C.c_int, [C.c_char_p, C.c_char_p, _I64, _I64, _P]),
     "teig_read_matrix_file": (C.c_int, [C.c_char_p, C.c_char_p, _P, _P, _P, _I64]),
     "teig_deflation_check": (C.c_int, [C.c_double, C.c_double, C.c_int32, C.c_double]),

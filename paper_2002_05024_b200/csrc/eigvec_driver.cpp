@@ -38,7 +38,7 @@ int teig_backtransform_device(int64_t n, int64_t k, const double* dQ, int64_t ld
     if (e == cudaSuccess && col_kind) e = lib_malloc_async(reinterpret_cast<void**>(&d_kind), (size_t)k, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(d_flag, 0, sizeof(int), s);
     if (e == cudaSuccess && col_kind) e = cudaMemcpyAsync(d_kind, col_kind, (size_t)k, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) e = launch_gemm_nn((int)n, (int)k, (int)n, dQ, ldq, dY, ldy, dX, ldx, s);
+    if (e == cudaSuccess) e = launch_dgemm(false, false, (int)n, (int)k, (int)n, 1.0, dQ, ldq, dY, ldy, 0.0, dX, ldx, s);
     if (e == cudaSuccess) e = launch_renorm_columns((int)n, dX, ldx, d_kind, (int)k, d_flag, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, s);
     if (d_kind) cudaFreeAsync(d_kind, s);

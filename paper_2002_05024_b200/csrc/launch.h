@@ -99,12 +99,12 @@ cudaError_t launch_hess_norm(const double* H, long long ldh, int n, unsigned lon
 cudaError_t launch_scan_active(double* H, long long ldh, int n, int ihi, double hnorm, int* out,
                                cudaStream_t stream);
 
-// backtransform.cu: C = A B (DMMA, column-major, any ld) and the reference's
+// backtransform.cu: C = beta C + alpha op(A) op(B) (DMMA, dgemm.cuh) and the reference's
 // eigenvector column renormalisation (kind: 0 real, 1 pair start, 2 pair
 // second half, other / NULL: finiteness check only; *nonfinite |= 1 on
 // Inf / NaN)
-cudaError_t launch_gemm_nn(int m, int n, int kdim, const double* A, long long lda, const double* B, long long ldb,
-                           double* C, long long ldc, cudaStream_t s);
+cudaError_t launch_dgemm(bool ta, bool tb, int m, int n, int kdim, double alpha, const double* A, long long lda,
+                         const double* B, long long ldb, double beta, double* C, long long ldc, cudaStream_t s);
 cudaError_t launch_renorm_columns(int n, double* X, long long ldx, const int8_t* kind_dev, int k, int* nonfinite,
                                   cudaStream_t s);
 // distributed deviation flag: mode 0 publish this rank's flag into base[slots[0]],
