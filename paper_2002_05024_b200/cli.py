@@ -5,16 +5,19 @@ reports with residuals, eigenvalues, timings and optional execution traces.
 
   python -m paper_2002_05024_b200.cli <command> [flags]
 
-  generate   --kind {schur,hessenberg,pair-t} --n N --seed S --out PATH
+  generate   --kind {schur,hessenberg,dense,pair-t} --n N --seed S --out PATH
              (schur: the synthetic standardized Schur form of SURVEY 8d, with
              a sidecar PATH.json listing its spectrum; hessenberg: the
-             reference's generate(hessenberg_random); pair-t: the C5 T factor)
+             reference's generate(hessenberg_random); dense: uniform [-1, 1)
+             entries; pair-t: the C5 T factor)
   reorder    --s S [--q Q] --select SPEC [--window-size W] [--strict]
              --out-s S2 [--out-q Q2] [--report R.json] [--trace T.json]
+  hessenberg --a A --out-h H [--out-q Q] [--panel-width B] [--report R.json]
   schur      --h H [--q Q] [--deflation {classic,norm-stable}] [--shift-count M]
              [--aed-window W] --out-s S [--out-q Q] [--report R.json]
-  pipeline   --h H [--select SPEC] --out-s S --out-q Q [--report R.json]
-             (schur_reduce, then reorder_schur if --select, then verify)
+  pipeline   (--a A | --h H) [--select SPEC] --out-s S --out-q Q [--report R.json]
+             (hessenberg_reduce for --a, schur_reduce, reorder_schur if
+             --select, then verify against the input)
   verify     --a A --q Q --s S [--tol-backward T] [--tol-orth T] [--report R.json]
   trace-dump --trace T.json   (per-kind launch counts and device time)
 
@@ -53,7 +56,7 @@ def _parser():
     p = _Parser(prog="taskeig_b200", description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     sub = p.add_subparsers(dest="command")
     g = sub.add_parser("generate")
-    g.add_argument("--kind", required=True, choices=["schur", "hessenberg", "pair-t"])
+    g.add_argument("--kind", required=True, choices=["schur", "hessenberg", "dense", "pair-t"])
     g.add_argument("--n", type=int, required=True)
     g.add_argument("--seed", type=int, default=1)
     g.add_argument("--out", required=True)
@@ -66,6 +69,11 @@ def _parser():
     r.add_argument("--out-s", required=True)
     r.add_argument("--out-q")
     r.add_argument("--trace")
+    hs = sub.add_parser("hessenberg")
+    hs.add_argument("--a", required=True)
+    hs.add_argument("--out-h", required=True)
+    hs.add_argument("--out-q")
+    hs.add_argument("--panel-width", type=int, default=0)
     s = sub.add_parser("schur")
     s.add_argument("--h", required=True)
     s.add_argument("--q")
@@ -75,7 +83,9 @@ def _parser():
     s.add_argument("--out-s", required=True)
     s.add_argument("--out-q")
     pl = sub.add_parser("pipeline")
-    pl.add_argument("--h", required=True)
+    src = pl.add_mutually_exclusive_group(required=True)
+    src.add_argument("--a")
+    src.add_argument("--h")
     pl.add_argument("--select")
     pl.add_argument("--deflation", choices=["classic", "norm-stable"], default="norm-stable")
     pl.add_argument("--window-size", type=int, default=0)
@@ -91,9 +101,9 @@ def _parser():
     v.add_argument("--tol-orth", type=float, default=None)
     t = sub.add_parser("trace-dump")
     t.add_argument("--trace", required=True)
-    for sp in (g, r, s, pl, v):
+    for sp in (g, r, hs, s, pl, v):
         sp.add_argument("--format", choices=["teig", "matrixmarket"], default="teig")
-    for sp in (r, s, pl, v):
+    for sp in (r, hs, s, pl, v):
         sp.add_argument("--report")
     return p
 
@@ -205,6 +215,9 @@ def cmd_generate(a, T):
         m = T.gen_schur_input(a.n, T.known_spectrum_seed(a.seed), device=dev)
     elif a.kind == "hessenberg":
         m = T.gen_hessenberg(a.n, a.seed, device=dev)
+    elif a.kind == "dense":
+        g = torch.Generator(device=dev).manual_seed(a.seed)
+        m = (torch.rand(a.n, a.n, dtype=torch.float64, device=dev, generator=g) * 2 - 1).t().contiguous().t()
     else:
         m = T.gen_pair_t(a.n, a.seed, device=dev)
     torch.cuda.synchronize()
@@ -250,6 +263,23 @@ def cmd_reorder(a, T):
     return code
 
 
+def cmd_hessenberg(a, T):
+    A = _load(a.a, a.format)
+    n = A.shape[0]
+    A0 = A.clone()
+    t0 = time.perf_counter()
+    r = T.hessenberg_reduce(A, True, T.HessenbergOptions(panel_width=a.panel_width))
+    wall = time.perf_counter() - t0
+    _save(a.out_h, r.h, a.format)
+    if a.out_q:
+        _save(a.out_q, r.q, a.format)
+    back, orth = _residuals(A0, r.q, r.h)
+    rep = {"config": vars(a), "n": n, "phase_seconds": {"hessenberg": wall}, "panels": r.info["panels"]}
+    code = _verdict(rep, back, orth, n, None, None)
+    _write_report(a.report, rep)
+    return code
+
+
 def _schur(T, h, q, deflation, shift_count=0, aed_window=0):
     d = T.DeflationCondition.classic if deflation == "classic" else T.DeflationCondition.norm_stable
     opts = T.SchurOptions(deflation=d, shift_count=shift_count, aed_window=aed_window)
@@ -280,12 +310,21 @@ def cmd_schur(a, T):
 
 
 def cmd_pipeline(a, T):
-    h = _load(a.h, a.format)
+    phases = {}
+    if a.a:  # general matrix: Hessenberg reduction first, on the device
+        h = _load(a.a, a.format)
+        h0 = h.clone()
+        t0 = time.perf_counter()
+        hr = T.hessenberg_reduce(h, True)
+        phases["hessenberg"] = time.perf_counter() - t0
+        q = hr.q
+    else:
+        h = _load(a.h, a.format)
+        h0 = h.clone()
+        q = T.identity(h.shape[0])
     n = h.shape[0]
-    h0 = h.clone()
-    q = T.identity(n)
-    sd, t_schur = _schur(T, h, q, a.deflation)
-    rep = {"config": vars(a), "n": n, "phase_seconds": {"schur": t_schur}, "converged": sd.converged,
+    sd, phases["schur"] = _schur(T, h, q, a.deflation)
+    rep = {"config": vars(a), "n": n, "phase_seconds": phases, "converged": sd.converged,
            "sweeps": sd.sweeps}
     if not sd.converged:
         rep["converged_trailing"] = sd.converged_trailing
@@ -348,10 +387,11 @@ def main(argv=None) -> int:
     try:
         a = _parser().parse_args(argv)
         if not a.command:
-            raise UsageError("a command is required (generate, reorder, schur, pipeline, verify, trace-dump)")
+            raise UsageError("a command is required (generate, reorder, hessenberg, schur, pipeline, verify, "
+                             "trace-dump)")
         import paper_2002_05024_b200 as T
-        fn = {"generate": cmd_generate, "reorder": cmd_reorder, "schur": cmd_schur, "pipeline": cmd_pipeline,
-              "verify": cmd_verify, "trace-dump": cmd_trace_dump}[a.command]
+        fn = {"generate": cmd_generate, "reorder": cmd_reorder, "hessenberg": cmd_hessenberg, "schur": cmd_schur,
+              "pipeline": cmd_pipeline, "verify": cmd_verify, "trace-dump": cmd_trace_dump}[a.command]
         return fn(a, T)
     except UsageError as e:
         sys.stderr.write(f"usage error: {e}\n")

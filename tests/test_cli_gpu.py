@@ -76,3 +76,21 @@ def test_one_by_one(cuda, tmp_path):
                      "--report", rep]) == 0
     r = json.load(open(rep))
     assert r["eigenvalues"] == [[5.0, 0.0]] and r["backward_error"] == 0.0 and r["orthogonality"] == 0.0
+
+
+def test_full_pipeline_from_a_general_matrix(cuda, tmp_path):
+    """SPEC cmd_pipeline: hessenberg -> schur -> reorder on a general matrix,
+    report passes, verify of the written files passes (A = Q S Q^T)."""
+    a = str(tmp_path / "a.teig")
+    assert cli.main(["generate", "--kind", "dense", "--n", "500", "--seed", "2", "--out", a]) == 0
+    s, q, rep = str(tmp_path / "s"), str(tmp_path / "q"), str(tmp_path / "r.json")
+    assert cli.main(["pipeline", "--a", a, "--select", "frac=0.35,seed=99", "--out-s", s, "--out-q", q,
+                     "--report", rep]) == 0
+    r = json.load(open(rep))
+    assert r["pass"] and r["converged"] and set(r["phase_seconds"]) == {"hessenberg", "schur", "reorder"}
+    assert cli.main(["verify", "--a", a, "--q", q, "--s", s, "--report", str(tmp_path / "v.json")]) == 0
+    h, hq = str(tmp_path / "h"), str(tmp_path / "hq")
+    assert cli.main(["hessenberg", "--a", a, "--out-h", h, "--out-q", hq, "--report", str(tmp_path / "h.json")]) == 0
+    from paper_2002_05024_b200 import io
+    H = io.read_matrix_file(h, "teig")
+    assert np.all(np.tril(H, -2) == 0.0)
