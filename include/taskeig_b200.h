@@ -104,16 +104,20 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
                             void* stream);
 
 /* Execution trace (the reference's ExecutionReport, runtime.hpp:50-60, and
- * SchurOptions::keep_reports): with tracing on, every reorder call made on
- * this thread records one task per kernel launch -- {"label":
- * "reorder:<W|L|R|Q>:p<pass>:l<level>", "worker": stream (0 critical path,
- * 1 factor updates), "start_ns", "end_ns"} from CUDA events relative to the
- * call's start -- and one record per planned window {"pass", "level",
- * "position", "extent", "blocks", "group", "status"}.  teig_trace_json
- * writes the last call's trace as JSON into buf when cap exceeds its length
- * and returns the length.  Tracing brackets every launch with events. */
+ * SchurOptions::keep_reports): with tracing on, every reorder / Schur call
+ * made on this thread records one task per kernel launch -- {"label":
+ * "reorder:<W|L|R|Q>:p<pass>:l<level>" or "schur:<A|C|L|R|Q>:r<round>",
+ * "worker": stream (0 critical path, 1 second stream), "start_ns",
+ * "end_ns"} from CUDA events relative to the call's start -- and, for
+ * reorder, one record per planned window {"pass", "level", "position",
+ * "extent", "blocks", "group", "status"}.  teig_trace_json writes the last
+ * call's trace as JSON into buf when cap exceeds its length and returns the
+ * length; teig_trace_task reads task i.  Tracing brackets every launch with
+ * events. */
 void teig_trace_enable(int32_t on);
 int64_t teig_trace_json(char* buf, int64_t cap);
+int64_t teig_trace_task_count(void);
+int teig_trace_task(int64_t i, char* label, int64_t cap, int32_t* worker, int64_t* start_ns, int64_t* end_ns);
 
 /* Device memory policy (not part of the reference interface: the reference
  * has no device memory).  Every per-call device buffer comes from a private

@@ -16,6 +16,7 @@ from .reorder import (  # noqa: F401
     select_eigenvalues, select_fraction, window_reorder)
 from .eigvec import backtransform  # noqa: F401
 from .hessenberg import HessenbergOptions, HessenbergResult, hessenberg_reduce  # noqa: F401
+from . import io  # noqa: F401  (matrix files: T.io.read_matrix_file / write_matrix_file)
 from .schur import (  # noqa: F401
     AedResult, BulgeChain, DeflationCondition, SchurDecomposition, SchurOptions, aed_step, chase_bulges,
     deflation_check, introduce_bulges, schur_reduce, small_schur)

@@ -81,6 +81,8 @@ SIGNATURES = {
     "teig_release_memory": (None, []),
     "teig_trace_enable": (None, [C.c_int32]),
     "teig_trace_json": (C.c_int64, [C.c_char_p, C.c_int64]),
+    "teig_trace_task_count": (C.c_int64, []),
+    "teig_trace_task": (C.c_int, [_I64, C.c_char_p, _I64, _P, _P, _P]),
     "teig_reorder_schur_host": (C.c_int, [_I64, _P, _I64, _P, _I64, _I64, _P, _P, _P, _P, _P, _P,
                                           _I64, _P, _P]),
     "teig_scan_blocks_device": (C.c_int64, [_I64, _P, _I64, _P, _P]),

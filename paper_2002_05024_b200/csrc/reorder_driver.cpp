@@ -32,6 +32,7 @@
 #include "launch.h"
 #include "plan.h"
 #include "qw_ring.h"
+#include "trace.h"
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -188,29 +189,25 @@ struct PassResult {
     double ms_window = 0, ms_left = 0, ms_right = 0, ms_factor = 0;
 };
 
+}  // namespace
+
 // Execution trace of the calls made on this thread (teig_trace_enable): one
 // task record per kernel launch -- the reference's ExecutionReport schema
 // (runtime.hpp:50-60: label, worker = stream, start_ns / end_ns from CUDA
-// events relative to the call's first event) -- plus one record per planned
-// window (pass, level, position, order, blocks, group, status).
-struct TraceTask {
-    std::string label;
-    int worker;
-    int64_t start_ns, end_ns;
-};
-struct TraceWin {
-    int pass, level;
-    int64_t a, d, nb, group;
-    int32_t status;
-};
-struct TraceState {
-    bool on = false;
-    cudaEvent_t origin = nullptr;
-    int pass = 0;
-    std::vector<TraceTask> tasks;
-    std::vector<TraceWin> wins;
-};
+// events relative to the call's first event) -- plus, for reorder calls, one
+// record per planned window (pass, level, position, order, blocks, group,
+// status).
 thread_local TraceState g_trace;
+
+void TraceState::begin(cudaStream_t s) {
+    tasks.clear();
+    wins.clear();
+    pass = 0;
+    if (!origin) TEIG_CUDA(cudaEventCreate(&origin));
+    TEIG_CUDA(cudaEventRecord(origin, s));
+}
+
+namespace {
 
 // Event pairs bracketing launches when profiling is on.
 struct EventLog {
@@ -592,13 +589,7 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
     std::vector<int64_t> rejected, plan_log;
     try {
         StreamPair sp(stream);
-        if (g_trace.on) {  // time origin of this call's trace records
-            g_trace.tasks.clear();
-            g_trace.wins.clear();
-            g_trace.pass = 0;
-            if (!g_trace.origin) TEIG_CUDA(cudaEventCreate(&g_trace.origin));
-            TEIG_CUDA(cudaEventRecord(g_trace.origin, sp.s1));
-        }
+        if (g_trace.on) g_trace.begin(sp.s1);  // time origin of this call's trace records
         // Q may still be arriving (host entry point): only the Q updates wait
         if (q_ready && dQ) TEIG_CUDA(cudaStreamWaitEvent(o.overlap_factor ? sp.s2 : sp.s1, q_ready, 0));
         double plan_ms = 0.0;
@@ -703,6 +694,22 @@ void teig_release_host_staging(void) {
 }
 
 void teig_trace_enable(int32_t on) { g_trace.on = on != 0; }
+
+int64_t teig_trace_task_count(void) { return (int64_t)g_trace.tasks.size(); }
+
+int teig_trace_task(int64_t i, char* label, int64_t cap, int32_t* worker, int64_t* start_ns, int64_t* end_ns) {
+    if (i < 0 || i >= (int64_t)g_trace.tasks.size()) return set_error(-1, "trace task index out of range");
+    const TraceTask& t = g_trace.tasks[i];
+    if (label && cap > 0) {
+        const size_t k = std::min<size_t>(t.label.size(), (size_t)cap - 1);
+        std::memcpy(label, t.label.data(), k);
+        label[k] = 0;
+    }
+    if (worker) *worker = t.worker;
+    if (start_ns) *start_ns = t.start_ns;
+    if (end_ns) *end_ns = t.end_ns;
+    return 0;
+}
 
 int64_t teig_trace_json(char* buf, int64_t cap) {
     std::string j = "{\"tasks\": [";

@@ -33,6 +33,7 @@
 #include "../../include/taskeig_b200.h"
 #include "device_types.h"
 #include "launch.h"
+#include "trace.h"
 
 namespace teig {
 
@@ -331,7 +332,7 @@ class SchurRunner {
                 TEIG_CUDA(launch_chase_window(dH_, ldh_, cwins_.p, w.cw_idx, (int)w.d, pairs_.p, qw_.p, s_));
                 ++chase_windows_;
             }
-            prof_end(0, ew0, s_);
+            prof_end(0, ew0, s_, w.kind == 0 ? 'A' : 'C');
             ++launches_;
             updates(k, w.a, w.d);
         }
@@ -421,7 +422,7 @@ class SchurRunner {
         if (tl > 0) {
             const int e0 = prof_begin(s_);
             TEIG_CUDA(launch_update_left(dd, 1, tl, dm, qw_.p, dH_, ldh_, (int)n_, s_, n_, n_));
-            prof_end(1, e0, s_);
+            prof_end(1, e0, s_, 'L');
             ++launches_;
         }
         if (tr > 0 || tq > 0) {
@@ -431,13 +432,13 @@ class SchurRunner {
         if (tr > 0) {
             const int e0 = prof_begin(s2_);
             TEIG_CUDA(launch_update_right(dd, 1, tr, dm, qw_.p, dH_, ldh_, (int)n_, false, s2_, n_, n_));
-            prof_end(1, e0, s2_);
+            prof_end(1, e0, s2_, 'R');
             ++launches_;
         }
         if (tq > 0) {
             const int e0 = prof_begin(s2_);
             TEIG_CUDA(launch_update_right(dd, 1, tq, dm, qw_.p, dQ_, ldq_, (int)n_, true, s2_, n_, n_));
-            prof_end(1, e0, s2_);
+            prof_end(1, e0, s2_, 'Q');
             ++launches_;
         }
     }
@@ -452,16 +453,25 @@ class SchurRunner {
         TEIG_CUDA(cudaEventRecord(evpool_[nev_], s));
         return (int)nev_++;
     }
-    void prof_end(int cls, int e0, cudaStream_t s) {
+    // kind (trace label): 'A' AED / small-solve window, 'C' chase window,
+    // 'L' / 'R' / 'Q' updates
+    void prof_end(int cls, int e0, cudaStream_t s, char kind = '?') {
         if (e0 < 0) return;
         const int e1 = prof_begin(s);
-        spans_.push_back({cls, e0, e1});
+        spans_.push_back({cls, e0, e1, kind, s == s_ ? 0 : 1});
     }
     void prof_collect() {
         for (auto& sp : spans_) {
             float ms = 0.f;
             TEIG_CUDA(cudaEventElapsedTime(&ms, evpool_[sp.e0], evpool_[sp.e1]));
             ms_[sp.cls] += ms;
+            if (g_trace.on) {  // SchurOptions::keep_reports: one record per launch
+                float t0 = 0.f, t1 = 0.f;
+                TEIG_CUDA(cudaEventElapsedTime(&t0, g_trace.origin, evpool_[sp.e0]));
+                TEIG_CUDA(cudaEventElapsedTime(&t1, g_trace.origin, evpool_[sp.e1]));
+                g_trace.tasks.push_back({std::string("schur:") + sp.kind + ":r" + std::to_string(rounds_), sp.worker,
+                                         (int64_t)(t0 * 1e6), (int64_t)(t1 * 1e6)});
+            }
         }
         spans_.clear();
         nev_ = 0;
@@ -469,6 +479,8 @@ class SchurRunner {
 
     struct Span {
         int cls, e0, e1;
+        char kind;
+        int worker;
     };
 
     int64_t n_;
@@ -538,6 +550,10 @@ int schur_reduce_device(int64_t n, double* dH, int64_t ldh, double* dQ, int64_t 
     teig_schur_info inf{};
     const auto t0 = std::chrono::steady_clock::now();
     try {
+        if (g_trace.on) {  // the trace needs the per-launch events
+            o.profile = 1;
+            g_trace.begin(stream);
+        }
         SchurRunner R(n, dH, ldh, dQ, ldq, o, stream);
         const int64_t limit = o.iteration_limit ? o.iteration_limit : 30 * n;
         const double hnorm = R.hnorm();

@@ -465,16 +465,36 @@ SchurDecomposition schur_reduce(TiledMatrix h_in, std::optional<TiledMatrix> q_i
     DeviceProblem dp(h, q);
     std::vector<double> re(n), im(n);
     teig_schur_info info{};
-    teig_check(teig_schur_reduce_device((int64_t)n, dp.h.p, (int64_t)n, q ? dp.q.p : nullptr, (int64_t)n, &o, re.data(),
-                                        im.data(), &info, dp.st.s),
-               "schur_reduce");
+    if (opts.keep_reports) teig_trace_enable(1);
+    const int rc = teig_schur_reduce_device((int64_t)n, dp.h.p, (int64_t)n, q ? dp.q.p : nullptr, (int64_t)n, &o,
+                                            re.data(), im.data(), &info, dp.st.s);
+    if (opts.keep_reports) teig_trace_enable(0);
+    teig_check(rc, "schur_reduce");
     dp.back(h, q);
+    if (opts.keep_reports) {
+        // one ExecutionReport per round (the reference keeps one per round's
+        // TaskGraph, schur.hpp:57): the round's kernel launches, worker =
+        // stream, device-event times
+        const int64_t cnt = teig_trace_task_count();
+        char label[128];
+        std::string cur;
+        for (int64_t i = 0; i < cnt; ++i) {
+            int32_t worker = 0;
+            int64_t t0 = 0, t1 = 0;
+            teig_trace_task(i, label, sizeof label, &worker, &t0, &t1);
+            std::string lb(label);
+            const std::string round = lb.substr(lb.rfind(':') + 1);
+            if (out.round_reports.empty() || round != cur) {
+                out.round_reports.emplace_back();
+                cur = round;
+            }
+            out.round_reports.back().tasks.push_back(TaskRecord{lb, (int)worker, t0, t1});
+        }
+    }
     for (size_t i = 0; i < n; ++i) out.eigenvalues.emplace_back(re[i], im[i]);
     out.sweeps = (size_t)info.sweeps;
     out.converged = info.converged != 0;
     out.converged_trailing = (size_t)info.converged_trailing;
-    // round_reports (SchurOptions::keep_reports): the reference's per-round
-    // TaskGraph reports have no counterpart in the device stream program
     return out;
 }
 

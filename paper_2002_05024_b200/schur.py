@@ -42,7 +42,7 @@ class SchurOptions:  # schur.hpp:20-29
     small_threshold: int = 64
     workers: int = 0           # accepted for API parity; the GPU path ignores it
     seed: int = 0              # accepted for API parity
-    keep_reports: bool = False  # accepted for API parity (no task-graph reports)
+    keep_reports: bool = False  # the call's execution trace in SchurDecomposition.info['round_reports'] (JSON)
     tile_size: int = 0         # chase window; 0 = default_tile_size(n) (the TiledMatrix tile)
     profile: bool = False      # CUDA-event time per kernel class in SchurDecomposition.info
 
@@ -132,6 +132,23 @@ def schur_reduce(h, q=None, opts: Optional[SchurOptions] = None, stream=None) ->
     info = N.SchurInfo()
     re = np.zeros(n)
     im = np.zeros(n)
+    keep = bool(opts is not None and opts.keep_reports)
+    if keep:  # SchurOptions::keep_reports: the call's execution trace
+        N.trace_enable(True)
+    try:
+        s_out, q_out = _schur_call(h, q, n, o, re, im, info, stream)
+    finally:
+        if keep:
+            N.trace_enable(False)
+    conv = bool(info.converged)
+    eig = [complex(a, b) for a, b in zip(re, im)] if conv else []
+    inf = {f: getattr(info, f) for f, _ in N.SchurInfo._fields_ if f != "pad"}
+    if keep:
+        inf["round_reports"] = N.trace_json()
+    return SchurDecomposition(s_out, q_out, eig, int(info.sweeps), conv, int(info.converged_trailing), inf)
+
+
+def _schur_call(h, q, n, o, re, im, info, stream):
     if torch is not None and isinstance(h, torch.Tensor):
         hw, ldh, cb_h, qw, ldq, cb_q = _dev_mats(h, q)
         N.check(N.lib().teig_schur_reduce_device(n, hw.data_ptr(), ldh, qw.data_ptr() if qw is not None else None,
@@ -145,10 +162,7 @@ def schur_reduce(h, q=None, opts: Optional[SchurOptions] = None, stream=None) ->
         N.check(N.lib().teig_schur_reduce_host(n, _vp(hf), n, _vp(qf) if qf is not None else None, n, C.byref(o),
                                                _vp(re), _vp(im), C.byref(info), None))
         s_out, q_out = hf, qf
-    conv = bool(info.converged)
-    eig = [complex(a, b) for a, b in zip(re, im)] if conv else []
-    inf = {f: getattr(info, f) for f, _ in N.SchurInfo._fields_ if f != "pad"}
-    return SchurDecomposition(s_out, q_out, eig, int(info.sweeps), conv, int(info.converged_trailing), inf)
+    return s_out, q_out
 
 
 def aed_step(h, q, l: int, ihi: int, window: int, opts: Optional[SchurOptions] = None,
