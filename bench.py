@@ -416,9 +416,9 @@ def workload_name(n):
 
 def measured_traffic():
     """DRAM bytes of one captured launch of the dominant kernel (ncu --set full,
-    profiles/r02_traffic.json) -- per launch, next to that launch's algorithmic
+    profiles/r03_traffic.json) -- per launch, next to that launch's algorithmic
     bytes; None when the capture file is absent."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r02_traffic.json")
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r03_traffic.json")
     try:
         with open(path) as f:
             t = json.load(f)
