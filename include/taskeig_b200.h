@@ -77,7 +77,11 @@ typedef struct teig_reorder_info {
     double ms_left;        /*   ... of the left (row-panel) update kernels */
     double ms_right;       /*   ... of the right (column-panel) update kernels */
     double ms_factor;      /*   ... of the Q-factor update kernels */
-    double flops_left, flops_right, flops_factor; /* update flops per kernel class */
+    double flops_left, flops_right, flops_factor; /* update flops per kernel class (the
+                                     reference's count: factor updates over all n rows) */
+    double flops_factor_exec;  /* factor-update flops actually executed: rows outside the
+                                  tracked support of Q's columns are exact zeros and skipped
+                                  (Q_in = I: about half; TEIG_NO_Q_SUPPORT=1 disables) */
 } teig_reorder_info;
 
 void teig_reorder_opts_default(teig_reorder_opts* o);

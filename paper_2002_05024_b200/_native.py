@@ -42,7 +42,8 @@ class ReorderInfo(C.Structure):
                 ("pad", C.c_int32), ("update_flops", C.c_double), ("update_bytes", C.c_double),
                 ("plan_ms", C.c_double), ("n_launches", C.c_int64), ("ms_window", C.c_double),
                 ("ms_left", C.c_double), ("ms_right", C.c_double), ("ms_factor", C.c_double),
-                ("flops_left", C.c_double), ("flops_right", C.c_double), ("flops_factor", C.c_double)]
+                ("flops_left", C.c_double), ("flops_right", C.c_double), ("flops_factor", C.c_double),
+                ("flops_factor_exec", C.c_double)]
 
 
 class SchurOpts(C.Structure):

@@ -334,7 +334,7 @@ struct LevelPlan {
         int64_t l_off = 0, l_cnt = 0, l_tiles = 0;     // left updates
         int64_t r_off = 0, r_cnt = 0, r_tiles = 0;     // right updates (owned)
         int64_t q_off = 0, q_cnt = 0, q_tiles = 0;     // Q updates
-        int64_t z_off = 0, z_cnt = 0;                  // Z updates (generalized; tiles as Q)
+        int64_t z_off = 0, z_cnt = 0, z_tiles = 0;     // Z updates (generalized)
     };
     std::vector<Part> part;          // [rank]
     int64_t qw_off = 0, qw_len = 0;  // the level's Q_w slots
@@ -355,7 +355,7 @@ struct PassOut {
 PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankBufs>& R, Comm& comm, int64_t lds,
                       const std::vector<int64_t>& C, const std::vector<int64_t>& Rw, bool with_q, bool gen,
                       std::vector<BlockState>& blocks, std::vector<int64_t>& rejected, std::vector<int64_t>& plan_log,
-                      bool strict) {
+                      bool strict, std::vector<FactorSupport>* qsupp, std::vector<FactorSupport>* zsupp) {
     PassOut po;
     const int64_t nw = (int64_t)plan.windows.size();
     schedule_levels(plan, n);
@@ -446,15 +446,25 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
                 Dp[r].push_back(-1);
                 ++P.r_cnt;
             }
-            // Q updates: this rank's Q rows
+            // Q updates: this rank's Q rows -- within them, only the tracked
+            // support of the window's columns (plan.h FactorSupport; per rank:
+            // a row of the result depends only on the same row of the input)
+            auto factor_rows = [&](FactorSupport* fs, int64_t t, int64_t* q0, int64_t* q1) {
+                const auto& w = plan.windows[idx[t]];
+                *q0 = Rw[r];
+                *q1 = Rw[r + 1];
+                if (fs && fs->on) fs->window(w.wtop, w.wbot, q0, q1);
+            };
             P.q_off = (int64_t)D[r].size();
             if (with_q && Rw[r + 1] > Rw[r])
                 for (int64_t t = k0; t < k; ++t) {
                     WinDesc d = base(t);
-                    d.qr0 = (int32_t)Rw[r];
-                    d.qr1 = (int32_t)Rw[r + 1];
+                    int64_t q0, q1;
+                    factor_rows(qsupp ? &(*qsupp)[r] : nullptr, t, &q0, &q1);
+                    d.qr0 = (int32_t)q0;
+                    d.qr1 = (int32_t)q1;
                     d.tq_pref = (int32_t)P.q_tiles;
-                    P.q_tiles += (Rw[r + 1] - Rw[r] + kRightBM - 1) / kRightBM;
+                    P.q_tiles += (q1 - q0 + kRightBM - 1) / kRightBM;
                     D[r].push_back(d);
                     Dp[r].push_back(-1);
                     ++P.q_cnt;
@@ -464,6 +474,12 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
                 for (int64_t t = k0; t < k; ++t) {
                     WinDesc d = D[r][P.q_off + (t - k0)];
                     d.qw_off += (int64_t)d.d * d.d;
+                    int64_t z0, z1;
+                    factor_rows(zsupp ? &(*zsupp)[r] : nullptr, t, &z0, &z1);
+                    d.qr0 = (int32_t)z0;
+                    d.qr1 = (int32_t)z1;
+                    d.tq_pref = (int32_t)P.z_tiles;
+                    P.z_tiles += (z1 - z0 + kRightBM - 1) / kRightBM;
                     D[r].push_back(d);
                     Dp[r].push_back(-1);
                     ++P.z_cnt;
@@ -578,13 +594,13 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
         // kernels and panel updates (the single-GPU driver's schedule)
         each([&](int r, RankBufs& B) {
             const auto& P = lp.part[r];
-            if (!P.q_tiles) return;
+            if (!P.q_tiles && !P.z_tiles) return;
             TEIG_CUDA(cudaEventRecord(B.ev, B.st));
             TEIG_CUDA(cudaStreamWaitEvent(B.st2, B.ev, 0));
             TEIG_CUDA(launch_update_right(B.descs + P.q_off, (int)P.q_cnt, (int)P.q_tiles, lp.dmax, B.qw, B.Q, B.ldq,
                                           (int)n, true, B.st2, Rw[r + 1], n));
             if (gen && P.z_cnt && B.Z)
-                TEIG_CUDA(launch_update_right(B.descs + P.z_off, (int)P.z_cnt, (int)P.q_tiles, lp.dmax, B.qw, B.Z,
+                TEIG_CUDA(launch_update_right(B.descs + P.z_off, (int)P.z_cnt, (int)P.z_tiles, lp.dmax, B.qw, B.Z,
                                               B.ldq, (int)n, true, B.st2, Rw[r + 1], n));
             ++launches;
         });
@@ -918,6 +934,41 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, co
         else if (!loop) comms[rank] = static_cast<ncclComm_t>(nccl_comm);
         NcclComm nc(comms);
         Comm& comm = loop ? static_cast<Comm&>(lb) : static_cast<Comm&>(nc);
+        // per-rank row supports of the local Q (Z) slabs: one device scan each
+        std::vector<FactorSupport> qsupp(world), zsupp(world);
+        static const bool no_supp = getenv("TEIG_NO_Q_SUPPORT") && atoi(getenv("TEIG_NO_Q_SUPPORT"));
+        auto scan = [&](int r, double* M, FactorSupport& fs) {
+            const int64_t rows = Rw[r + 1] - Rw[r];
+            fs.lo.assign(n, (int32_t)Rw[r]);
+            fs.hi.assign(n, (int32_t)Rw[r] - 1);
+            fs.on = true;
+            if (rows <= 0) return;
+            DevScope dsc(R[r].dev);
+            int32_t *dlo = nullptr, *dhi = nullptr;
+            TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&dlo), sizeof(int32_t) * n, R[r].st));
+            TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&dhi), sizeof(int32_t) * n, R[r].st));
+            // M is the virtual base (absolute row i at M[i]): the slab starts at row Rw[r]
+            TEIG_CUDA(launch_column_support(M + Rw[r], R[r].ldq, rows, n, dlo, dhi, R[r].st));
+            TEIG_CUDA(cudaMemcpyAsync(fs.lo.data(), dlo, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, R[r].st));
+            TEIG_CUDA(cudaMemcpyAsync(fs.hi.data(), dhi, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, R[r].st));
+            TEIG_CUDA(cudaFreeAsync(dlo, R[r].st));
+            TEIG_CUDA(cudaFreeAsync(dhi, R[r].st));
+            TEIG_CUDA(cudaStreamSynchronize(R[r].st));
+            for (int64_t c = 0; c < n; ++c) {  // slab-relative -> absolute rows
+                if (fs.lo[c] <= fs.hi[c]) {
+                    fs.lo[c] += (int32_t)Rw[r];
+                    fs.hi[c] += (int32_t)Rw[r];
+                } else {
+                    fs.lo[c] = (int32_t)Rw[r];
+                    fs.hi[c] = (int32_t)Rw[r] - 1;
+                }
+            }
+        };
+        for (int r = 0; r < world && with_q && !no_supp; ++r) {
+            if (!comm.local(r)) continue;
+            scan(r, R[r].Q, qsupp[r]);
+            if (gen && R[r].Z) scan(r, R[r].Z, zsupp[r]);
+        }
         for (int pass = 0; pass < 64; ++pass) {
             ReorderPlan plan = plan_reorder(blocks, ws);
             if (plan.windows.empty()) break;
@@ -925,7 +976,7 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, co
             inf.update_flops += (gen ? 2.0 : 1.0) * plan_update_flops(plan, n, with_q);
             inf.update_bytes += (gen ? 2.0 : 1.0) * plan_update_bytes(plan, n, with_q);
             PassOut po = run_dist_pass(plan, n, world, R, comm, lds, C, Rw, with_q, gen, blocks, rejected, plan_log,
-                                       o.strict != 0);
+                                       o.strict != 0, with_q ? &qsupp : nullptr, (gen && with_q) ? &zsupp : nullptr);
             inf.n_windows += po.windows;
             inf.n_levels += po.levels;
             inf.n_launches += po.launches;

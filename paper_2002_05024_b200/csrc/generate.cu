@@ -190,4 +190,44 @@ cudaError_t launch_gen_hessenberg(double* H, long long ldh, long long n, uint64_
     return cudaGetLastError();
 }
 
+// Row support of every column: the first and last row holding a nonzero
+// (bit pattern != 0: +0.0 is the only zero) -- the factor-support tracking of
+// the reorder drivers (plan.h FactorSupport).  One CTA per column.
+__global__ void column_support_kernel(const double* __restrict__ Q, long long ldq, int rows, int32_t* __restrict__ lo,
+                                      int32_t* __restrict__ hi) {
+    const long long c = blockIdx.x;
+    const unsigned long long* col = reinterpret_cast<const unsigned long long*>(Q + c * ldq);
+    int l = rows, h = -1;
+    for (int r = threadIdx.x; r < rows; r += blockDim.x)
+        if (col[r] != 0ull) {
+            l = min(l, r);
+            h = max(h, r);
+        }
+    for (int o = 16; o > 0; o >>= 1) {
+        l = min(l, __shfl_xor_sync(0xffffffffu, l, o));
+        h = max(h, __shfl_xor_sync(0xffffffffu, h, o));
+    }
+    __shared__ int sl[32], sh[32];
+    if ((threadIdx.x & 31) == 0) {
+        sl[threadIdx.x >> 5] = l;
+        sh[threadIdx.x >> 5] = h;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            l = min(l, sl[w]);
+            h = max(h, sh[w]);
+        }
+        lo[c] = l;
+        hi[c] = h;
+    }
+}
+
+cudaError_t launch_column_support(const double* Q, long long ldq, long long rows, long long cols, int32_t* lo,
+                                  int32_t* hi, cudaStream_t stream) {
+    if (cols <= 0) return cudaSuccess;
+    column_support_kernel<<<(unsigned)cols, 256, 0, stream>>>(Q, ldq, (int)rows, lo, hi);
+    return cudaGetLastError();
+}
+
 }  // namespace teig

@@ -60,7 +60,8 @@ struct GPass {
 
 GPass run_gpass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* dT, int64_t ldt, double* dQ,
                 int64_t ldq, double* dZ, int64_t ldz, std::vector<BlockState>& blocks, std::vector<int64_t>& rejected,
-                std::vector<int64_t>& plan_log, bool strict, cudaStream_t s, cudaStream_t s2, cudaEvent_t ev) {
+                std::vector<int64_t>& plan_log, bool strict, cudaStream_t s, cudaStream_t s2, cudaEvent_t ev,
+                FactorSupport& qsupp, FactorSupport& zsupp, double* flops_exec) {
     GPass gp;
     const int64_t nw = (int64_t)plan.windows.size();
     schedule_levels(plan, n);
@@ -70,7 +71,7 @@ GPass run_gpass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* d
     std::stable_sort(idx.begin(), idx.end(),
                      [&](int64_t x, int64_t y) { return plan.windows[x].level < plan.windows[y].level; });
     std::vector<WinDesc> dq(nw), dz(nw);
-    std::vector<int64_t> lvl_off(nl + 1, 0), tl(nl, 0), tr(nl, 0), tq(nl, 0);
+    std::vector<int64_t> lvl_off(nl + 1, 0), tl(nl, 0), tr(nl, 0), tq(nl, 0), tz(nl, 0);
     int dmax = 0;
     int64_t pool = 0;
     for (int64_t k = 0; k < nw; ++k) {
@@ -92,15 +93,25 @@ GPass run_gpass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* d
         d.lc1 = (int32_t)n;
         d.rr0 = 0;
         d.rr1 = (int32_t)w.wtop;
-        d.qr0 = 0;
-        d.qr1 = (int32_t)n;
+        // factor rows: the tracked supports of Q's and Z's columns (plan.h)
+        int64_t q0 = 0, q1 = n, z0 = 0, z1 = n;
+        if (dQ && qsupp.on) qsupp.window(w.wtop, w.wbot, &q0, &q1);
+        if (dZ && zsupp.on) zsupp.window(w.wtop, w.wbot, &z0, &z1);
+        const double dd2 = 2.0 * double(d.d) * double(d.d);
+        *flops_exec += (dQ ? dd2 * double(q1 - q0) : 0.0) + (dZ ? dd2 * double(z1 - z0) : 0.0);
+        d.qr0 = (int32_t)q0;
+        d.qr1 = (int32_t)q1;
         tl[L] += (n - w.wbot + kLeftBN - 1) / kLeftBN;
         tr[L] += (w.wtop + kRightBM - 1) / kRightBM;
-        tq[L] += (n + kRightBM - 1) / kRightBM;
+        tq[L] += (q1 - q0 + kRightBM - 1) / kRightBM;
         lvl_off[L + 1]++;
         dmax = std::max(dmax, d.d);
         dz[k] = d;
         dz[k].qw_off = d.qw_off + (int64_t)d.d * d.d;  // Z_w behind Q_w
+        dz[k].qr0 = (int32_t)z0;
+        dz[k].qr1 = (int32_t)z1;
+        dz[k].tq_pref = (int32_t)tz[L];
+        tz[L] += (z1 - z0 + kRightBM - 1) / kRightBM;
     }
     for (int L = 0; L < nl; ++L) lvl_off[L + 1] += lvl_off[L];
     const int dm = dmax <= 64 ? 64 : 128;
@@ -135,7 +146,7 @@ GPass run_gpass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, double* d
                 ++launches;
             }
             if (dZ) {
-                TEIG_CUDA(launch_update_right(d_z.p + o, (int)cnt, (int)tq[L], dm, d_pool.p, dZ, ldz, (int)n, true, s2, n, n));
+                TEIG_CUDA(launch_update_right(d_z.p + o, (int)cnt, (int)tz[L], dm, d_pool.p, dZ, ldz, (int)n, true, s2, n, n));
                 ++launches;
             }
             if (ring_ev.n) TEIG_CUDA(cudaEventRecord(ring_ev.ev[L % ring.k], s2));
@@ -200,6 +211,23 @@ int greorder_schur_device(int64_t n, double* dS, int64_t lds, double* dT, int64_
     try {
         TEIG_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
         TEIG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        // row supports of Q's and Z's columns (one device scan each)
+        FactorSupport qsupp, zsupp;
+        static const bool no_supp = getenv("TEIG_NO_Q_SUPPORT") && atoi(getenv("TEIG_NO_Q_SUPPORT"));
+        auto scan = [&](const double* M, int64_t ld, FactorSupport& fs) {
+            if (!M || no_supp) return;
+            DBuf<int32_t> dlo(n, stream), dhi(n, stream);
+            fs.lo.resize(n);
+            fs.hi.resize(n);
+            TEIG_CUDA(launch_column_support(M, ld, n, n, dlo.p, dhi.p, stream));
+            TEIG_CUDA(cudaMemcpyAsync(fs.lo.data(), dlo.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, stream));
+            TEIG_CUDA(cudaMemcpyAsync(fs.hi.data(), dhi.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, stream));
+            TEIG_CUDA(cudaStreamSynchronize(stream));
+            fs.on = true;
+        };
+        scan(dQ, ldq, qsupp);
+        scan(dZ, ldz, zsupp);
+        double exec = 0.0;
         for (int pass = 0; pass < 64; ++pass) {
             ReorderPlan plan = plan_reorder(blocks, ws);
             if (plan.windows.empty()) break;
@@ -207,14 +235,21 @@ int greorder_schur_device(int64_t n, double* dS, int64_t lds, double* dT, int64_
             // two panels per side and two factors: twice the standard flops
             inf.update_flops += 2.0 * plan_update_flops(plan, n, dQ != nullptr || dZ != nullptr);
             inf.update_bytes += 2.0 * plan_update_bytes(plan, n, dQ != nullptr || dZ != nullptr);
+            for (const auto& w : plan.windows) {  // per class: (S, T) panels, (Q, Z) factors
+                const double d2 = 2.0 * double(w.wbot - w.wtop) * double(w.wbot - w.wtop);
+                inf.flops_left += 2.0 * d2 * double(n - w.wbot);
+                inf.flops_right += 2.0 * d2 * double(w.wtop);
+                inf.flops_factor += ((dQ ? 1.0 : 0.0) + (dZ ? 1.0 : 0.0)) * d2 * double(n);
+            }
             GPass gp = run_gpass(plan, n, dS, lds, dT, ldt, dQ, ldq, dZ, ldz, blocks, rejected, plan_log,
-                                 o.strict != 0, stream, s2, ev);
+                                 o.strict != 0, stream, s2, ev, qsupp, zsupp, &exec);
             inf.n_windows += gp.windows;
             inf.n_levels += gp.levels;
             inf.n_launches += gp.launches;
             inf.n_passes += 1;
             if (!gp.deviated) break;
         }
+        inf.flops_factor_exec = exec;
     } catch (const std::domain_error& e) {
         if (ev) cudaEventDestroy(ev);
         if (s2) cudaStreamDestroy(s2);

@@ -66,6 +66,10 @@ bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax
 cudaError_t launch_gen_schur_input(double* S, long long lds, long long n, uint64_t fill_seed,
                                    cudaStream_t stream);
 cudaError_t launch_set_identity(double* Q, long long ldq, long long n, cudaStream_t stream);
+// per column c < cols: lo[c] / hi[c] = first / last row < rows with a nonzero
+// bit pattern (rows / -1 for a zero column)
+cudaError_t launch_column_support(const double* Q, long long ldq, long long rows, long long cols, int32_t* lo,
+                                  int32_t* hi, cudaStream_t stream);
 cudaError_t launch_gen_hessenberg(double* H, long long ldh, long long n, uint64_t seed, cudaStream_t stream);
 cudaError_t launch_gen_pair_t(double* T, long long ldt, long long n, uint64_t seed, cudaStream_t stream);
 // generalized (S, T) window kernel (gwindow_reorder.cu), d <= 64

@@ -22,6 +22,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
@@ -187,6 +188,7 @@ struct PassResult {
     int64_t windows = 0, levels = 0, launches = 0;
     bool deviated = false;
     double ms_window = 0, ms_left = 0, ms_right = 0, ms_factor = 0;
+    double flops_factor_exec = 0;
 };
 
 }  // namespace
@@ -264,7 +266,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                     std::vector<BlockState>& blocks, std::vector<int64_t>& rejected,
                     std::vector<int64_t>& plan_log, bool strict, bool overlap, bool profile,
                     cudaStream_t stream, cudaStream_t stream2, cudaEvent_t ev, bool short_q,
-                    HostDrain* drain = nullptr) {
+                    HostDrain* drain = nullptr, FactorSupport* qsupp = nullptr) {
     PassResult pr;
     EventLog lg;
     lg.on = profile || g_trace.on;
@@ -299,11 +301,14 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         dsc.lc1 = (int32_t)n;
         dsc.rr0 = 0;
         dsc.rr1 = (int32_t)w.wtop;
-        dsc.qr0 = 0;
-        dsc.qr1 = (int32_t)n;
+        int64_t q0 = 0, q1 = n;  // factor rows: all, or the tracked support (plan.h)
+        if (dQ && qsupp && qsupp->on) qsupp->window(w.wtop, w.wbot, &q0, &q1);
+        pr.flops_factor_exec += 2.0 * double(dsc.d) * double(dsc.d) * double(q1 - q0);
+        dsc.qr0 = (int32_t)q0;
+        dsc.qr1 = (int32_t)q1;
         tl[L] += (n - w.wbot + kLeftBN - 1) / kLeftBN;
         tr[L] += (w.wtop + kRightBM - 1) / kRightBM;
-        if (dQ) tq[L] += (n + kRightBM - 1) / kRightBM;
+        if (dQ) tq[L] += (q1 - q0 + kRightBM - 1) / kRightBM;
         lvl_off[L + 1]++;
         dmax = std::max(dmax, dsc.d);
     }
@@ -559,7 +564,7 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
                          const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
                          int64_t* perm, int64_t* rejected_out, int64_t* plan_out, int64_t plan_cap,
                          teig_reorder_info* info, cudaStream_t stream, cudaEvent_t q_ready = nullptr,
-                         HostDrain* drain = nullptr) {
+                         HostDrain* drain = nullptr, FactorSupport* qsupp_in = nullptr) {
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (!dS) return set_error(-2, "S is null");
     if (lds < n) return set_error(-3, "lds < n");
@@ -590,6 +595,24 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
     try {
         StreamPair sp(stream);
         if (g_trace.on) g_trace.begin(sp.s1);  // time origin of this call's trace records
+        // the factor's row support (plan.h FactorSupport): from the host path's
+        // scan, else one device scan of Q (n^2 reads, ~3 ms at n=40000)
+        FactorSupport qsupp;
+        static const bool no_supp = getenv("TEIG_NO_Q_SUPPORT") && atoi(getenv("TEIG_NO_Q_SUPPORT"));
+        if (dQ && !no_supp) {
+            if (qsupp_in && qsupp_in->on) {
+                qsupp = *qsupp_in;
+            } else if (!q_ready) {  // (Q still arriving and no host scan: full updates)
+                DevBuf dlo(sizeof(int32_t) * n, sp.s1), dhi(sizeof(int32_t) * n, sp.s1);
+                qsupp.lo.resize(n);
+                qsupp.hi.resize(n);
+                TEIG_CUDA(launch_column_support(dQ, ldq, n, n, dlo.as<int32_t>(), dhi.as<int32_t>(), sp.s1));
+                TEIG_CUDA(cudaMemcpyAsync(qsupp.lo.data(), dlo.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, sp.s1));
+                TEIG_CUDA(cudaMemcpyAsync(qsupp.hi.data(), dhi.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, sp.s1));
+                TEIG_CUDA(cudaStreamSynchronize(sp.s1));
+                qsupp.on = true;
+            }
+        }
         // Q may still be arriving (host entry point): only the Q updates wait
         if (q_ready && dQ) TEIG_CUDA(cudaStreamWaitEvent(o.overlap_factor ? sp.s2 : sp.s1, q_ready, 0));
         double plan_ms = 0.0;
@@ -611,7 +634,8 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
             PassResult pr = run_pass(plan, n, dS, lds, dQ, ldq, blocks, rejected, plan_log, o.strict != 0,
                                      o.overlap_factor != 0, o.profile != 0, sp.s1, sp.s2, sp.ev,
                                      sp.short_factor_ctas(o.overlap_factor != 0),
-                                     pass == 0 ? drain : nullptr);
+                                     pass == 0 ? drain : nullptr, &qsupp);
+            inf.flops_factor_exec += pr.flops_factor_exec;
             inf.n_windows += pr.windows;
             inf.n_levels += pr.levels;
             inf.n_launches += pr.launches;
@@ -793,6 +817,34 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         double* const dQ = Q ? base + (size_t)n * n : nullptr;
         TEIG_CUDA(cudaStreamSynchronize(stream));  // staging visible to the side stream
         const auto h1 = now();
+        // the factor's row support (plan.h FactorSupport), scanned on the host
+        // cores while S travels to the device (hidden behind the upload)
+        FactorSupport qsupp;
+        std::vector<std::thread> scan;
+        const bool no_supp = getenv("TEIG_NO_Q_SUPPORT") && atoi(getenv("TEIG_NO_Q_SUPPORT"));
+        if (Q && !no_supp) {
+            qsupp.lo.resize(n);
+            qsupp.hi.resize(n);
+            const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+            for (int t = 0; t < nt; ++t)
+                scan.emplace_back([&, t] {
+                    for (int64_t c = n * t / nt; c < n * (t + 1) / nt; ++c) {
+                        const uint64_t* col = reinterpret_cast<const uint64_t*>(Q + c * ldq);
+                        int64_t l = 0, h = n - 1;
+                        while (l < n && col[l] == 0) ++l;
+                        while (h > l && col[h] == 0) --h;
+                        qsupp.lo[c] = (int32_t)l;
+                        qsupp.hi[c] = l < n ? (int32_t)h : -1;
+                    }
+                });
+        }
+        struct Join {
+            std::vector<std::thread>& v;
+            ~Join() {
+                for (auto& t : v)
+                    if (t.joinable()) t.join();
+            }
+        } join_scan{scan};
         TEIG_CUDA(cudaMemcpy2DAsync(dS, pitch, S, lds * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
         if (Q) {  // Q travels on a side stream, after S, while the S-side work starts (measured:
                   // uploading Q before the work starts costs +0.5 s at n=40000)
@@ -844,8 +896,10 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         TEIG_CUDA(cudaStreamCreateWithFlags(&dr.ds, cudaStreamNonBlocking));
         TEIG_CUDA(cudaEventCreateWithFlags(&dr.evS, cudaEventDisableTiming));
         TEIG_CUDA(cudaEventCreateWithFlags(&dr.evQ, cudaEventDisableTiming));
+        for (auto& t : scan) t.join();
+        qsupp.on = Q && !no_supp;
         const int rc = reorder_schur_device(n, dS, n, dQ, n, nb, sizes, flags, opts, perm, rejected, plan, plan_cap,
-                                            info, stream, q_ready, drain_on ? &dr : nullptr);
+                                            info, stream, q_ready, drain_on ? &dr : nullptr, &qsupp);
         TEIG_CUDA(cudaStreamSynchronize(stream));
         if (qs) TEIG_CUDA(cudaStreamSynchronize(qs));
         const auto h3 = now();
