@@ -57,7 +57,8 @@ typedef struct teig_reorder_opts {
                                Q-factor updates on a second stream, overlapped */
     int32_t profile;     /* !=0: bracket every launch with CUDA events and report
                             per-kernel-class device time in teig_reorder_info */
-    int32_t pad;
+    int32_t full_factor; /* !=0: update the factor(s) over all rows (no skipping of the
+                            exactly-zero rows; same bits, the reference's flop count) */
 } teig_reorder_opts;
 
 typedef struct teig_reorder_info {

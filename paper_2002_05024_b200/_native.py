@@ -33,7 +33,7 @@ def build(verbose: bool = False) -> str:
 
 class ReorderOpts(C.Structure):
     _fields_ = [("window_size", C.c_int64), ("strict", C.c_int32), ("overlap_factor", C.c_int32),
-                ("profile", C.c_int32), ("pad", C.c_int32)]
+                ("profile", C.c_int32), ("full_factor", C.c_int32)]
 
 
 class ReorderInfo(C.Structure):

@@ -17,6 +17,7 @@
 // reduction, then the scale pass.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "dgemm.cuh"
@@ -101,14 +102,36 @@ __global__ void __launch_bounds__(RT) renorm_kernel(int n, double* __restrict__ 
 }  // namespace
 
 cudaError_t launch_dgemm(bool ta, bool tb, int m, int n, int kdim, double alpha, const double* A, long long lda,
-                         const double* B, long long ldb, double beta, double* C, long long ldc, cudaStream_t s) {
+                         const double* B, long long ldb, double beta, double* C, long long ldc, cudaStream_t s,
+                         double* work, size_t work_doubles) {
     if (m <= 0 || n <= 0) return cudaSuccess;
-    const dim3 grid((m + dg::BM - 1) / dg::BM, (n + dg::BN - 1) / dg::BN);
+    dim3 grid((m + dg::BM - 1) / dg::BM, (n + dg::BN - 1) / dg::BN);
+    // split K when the output has too few tiles to fill the GPU and K is long
+    // (the Hessenberg panel products V^T G, A V: 64 columns, thousands of K)
+    int kz = kdim;
+    double* Cout = C;
+    long long ldo = ldc, cz = 0;
+    const long long tiles = (long long)grid.x * grid.y;
+    if (work && tiles < 2 * 148 && kdim >= 1024) {
+        int splits = (int)std::min<long long>(16, (2 * 148 + tiles - 1) / tiles);
+        splits = std::min(splits, kdim / 256);
+        kz = (((kdim + splits - 1) / splits) + dg::KC - 1) / dg::KC * dg::KC;
+        splits = (kdim + kz - 1) / kz;
+        if (splits > 1 && (size_t)splits * m * n <= work_doubles) {
+            grid.z = splits;
+            Cout = work;
+            ldo = m;
+            cz = (long long)m * n;
+        } else {
+            kz = kdim;
+        }
+    }
+    const double a1 = grid.z > 1 ? 1.0 : alpha, b1 = grid.z > 1 ? 0.0 : beta;
     cudaError_t e = cudaSuccess;
 #define TEIG_DG(TA, TB)                                                                                       \
     e = ensure_dyn_smem((const void*)dg::gemm_kernel<TA, TB>, dg::kSmem);                                      \
     if (e != cudaSuccess) return e;                                                                            \
-    dg::gemm_kernel<TA, TB><<<grid, dg::NT, dg::kSmem, s>>>(m, n, kdim, alpha, A, lda, B, ldb, beta, C, ldc);
+    dg::gemm_kernel<TA, TB><<<grid, dg::NT, dg::kSmem, s>>>(m, n, kdim, a1, A, lda, B, ldb, b1, Cout, ldo, kz, cz);
     if (!ta && !tb) {
         TEIG_DG(false, false)
     } else if (!ta && tb) {
@@ -119,6 +142,13 @@ cudaError_t launch_dgemm(bool ta, bool tb, int m, int n, int kdim, double alpha,
         TEIG_DG(true, true)
     }
 #undef TEIG_DG
+    if (grid.z > 1) {
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        const long long tot = (long long)m * n;
+        dg::dgemm_reduce<<<(unsigned)std::min<long long>((tot + 255) / 256, 4096), 256, 0, s>>>(
+            m, n, (int)grid.z, alpha, work, m, cz, beta, C, ldc);
+    }
     return cudaGetLastError();
 }
 

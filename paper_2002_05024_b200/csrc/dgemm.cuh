@@ -34,10 +34,21 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// gridDim.z > 1 (split K): slice z multiplies the K range [z*kz, (z+1)*kz)
+// and writes its partial product to C + z*cz (beta must be 0; a fixed-order
+// reduction of the slices follows, dgemm_reduce)
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(NT) gemm_kernel(int m, int n, int kdim, double alpha, const double* __restrict__ A,
                                                   long long lda, const double* __restrict__ B, long long ldb,
-                                                  double beta, double* __restrict__ C, long long ldc) {
+                                                  double beta, double* __restrict__ C, long long ldc, int kz,
+                                                  long long cz) {
+    if (gridDim.z > 1) {
+        const int z = blockIdx.z, k0 = z * kz;
+        A += TA ? (long long)k0 : (long long)k0 * lda;
+        B += TB ? (long long)k0 * ldb : (long long)k0;
+        C += (long long)z * cz;
+        kdim = min(kz, kdim - k0);
+    }
     extern __shared__ __align__(16) double sm[];
     double* As = sm;                  // ST x KC x LDA   (As[kk * LDA + mm] = op(A)(m0+mm, k0+kk))
     double* Bs = sm + ST * KC * LDA;  // ST x BN x LDB   (Bs[nn * LDB + kk] = op(B)(k0+kk, n0+nn))
@@ -117,6 +128,19 @@ __global__ void __launch_bounds__(NT) gemm_kernel(int m, int n, int kdim, double
                 *dst = (beta != 0.0 ? *dst : 0.0) + alpha * acc[i][j][h];
             }
         }
+    }
+}
+
+// C = beta C + alpha sum_z P[z] (z ascending: deterministic)
+__global__ void dgemm_reduce(int m, int n, int nz, double alpha, const double* __restrict__ P, long long ldp,
+                             long long pz, double beta, double* __restrict__ C, long long ldc) {
+    const long long tot = (long long)m * n;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot; t += (long long)gridDim.x * blockDim.x) {
+        const int i = (int)(t % m), j = (int)(t / m);
+        double s = 0.0;
+        for (int z = 0; z < nz; ++z) s += P[(long long)z * pz + i + (long long)j * ldp];
+        double* dst = C + i + (long long)j * ldc;
+        *dst = (beta != 0.0 ? *dst : 0.0) + alpha * s;
     }
 }
 

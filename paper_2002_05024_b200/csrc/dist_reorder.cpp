@@ -964,7 +964,7 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, co
                 }
             }
         };
-        for (int r = 0; r < world && with_q && !no_supp; ++r) {
+        for (int r = 0; r < world && with_q && !no_supp && !o.full_factor; ++r) {
             if (!comm.local(r)) continue;
             scan(r, R[r].Q, qsupp[r]);
             if (gen && R[r].Z) scan(r, R[r].Z, zsupp[r]);

@@ -215,7 +215,7 @@ int greorder_schur_device(int64_t n, double* dS, int64_t lds, double* dT, int64_
         FactorSupport qsupp, zsupp;
         static const bool no_supp = getenv("TEIG_NO_Q_SUPPORT") && atoi(getenv("TEIG_NO_Q_SUPPORT"));
         auto scan = [&](const double* M, int64_t ld, FactorSupport& fs) {
-            if (!M || no_supp) return;
+            if (!M || no_supp || o.full_factor) return;
             DBuf<int32_t> dlo(n, stream), dhi(n, stream);
             fs.lo.resize(n);
             fs.hi.resize(n);

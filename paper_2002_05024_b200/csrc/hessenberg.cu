@@ -45,7 +45,9 @@ namespace {
 
 constexpr int HT = 256;        // threads per CTA of the column kernels
 constexpr int HB = 64;         // max panel width
-constexpr int MV_COLS = 128;   // columns per GEMV chunk
+constexpr int MV_COLS = 128;   // max columns per GEMV chunk
+constexpr int MV_MIN = 16;     // min columns per GEMV chunk
+constexpr int MV_CTAS = 4 * 148;  // GEMV CTAs aimed for (four per SM)
 constexpr double kSafe = DBL_MIN / 2.220446049250313e-16;  // safmin / eps (kernels.cpp:45)
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -285,10 +287,10 @@ __global__ void col_tcol(Col c, int i) {
 }
 
 // ww[chunk][r] = sum over the chunk's columns c >= i of A(k+1+r, k+1+c) v_c
-__global__ void __launch_bounds__(HT) col_matvec(Col c, int i) {
+__global__ void __launch_bounds__(HT) col_matvec(Col c, int i, int chunk) {
     __shared__ double vs[MV_COLS];
-    const int c0 = i + blockIdx.y * MV_COLS;
-    const int cn = min(MV_COLS, c.m - c0);
+    const int c0 = i + blockIdx.y * chunk;
+    const int cn = min(chunk, c.m - c0);
     for (int t = threadIdx.x; t < cn; t += HT) vs[t] = c.V[(c0 + t) + (long long)i * c.ldv];
     __syncthreads();
     const int r = blockIdx.x * HT + threadIdx.x;
@@ -356,10 +358,10 @@ int hessenberg_reduce_device(int64_t n, double* dA, int64_t lda, double* dQ, int
         if (n >= 3) {
             const int64_t mmax = n - 1;
             const int nb_cta = (int)((mmax + HT - 1) / HT);
-            const int nchunk_max = (int)((mmax + MV_COLS - 1) / MV_COLS);
+            const int nchunk_max = (int)((mmax + MV_MIN - 1) / MV_MIN);
             Buf V(mmax * HB, s), Y(mmax * HB, s), T(HB * HB, s), X(mmax, s), part((size_t)nb_cta * HB, s),
                 pscal(nb_cta, s), psum(nb_cta, s), scal(8, s), s2(HB, s), ww((size_t)nchunk_max * mmax, s), W(HB * n, s),
-                W2(HB * n, s), P(n * HB, s), P2(n * HB, s);
+                W2(HB * n, s), P(n * HB, s), P2(n * HB, s), K(16 * HB * n, s);
             for (int64_t k = 0; k + 2 < n; k += bdef) {
                 const int b = (int)std::min<int64_t>(bdef, n - 2 - k);
                 const int m = (int)(n - k - 1);
@@ -374,8 +376,11 @@ int hessenberg_reduce_device(int64_t n, double* dA, int64_t lda, double* dQ, int
                     col_sumsq<<<c.nb_cta, HT, 0, s>>>(c, i);
                     col_reflect<<<c.nb_cta, HT, 0, s>>>(c, i);
                     col_tcol<<<1, 64, 0, s>>>(c, i);
-                    const int nchunk = (m - i + MV_COLS - 1) / MV_COLS;
-                    col_matvec<<<dim3(c.nb_cta, nchunk), HT, 0, s>>>(c, i);
+                    // column chunks: enough CTAs to fill the GPU at every panel size
+                    const int want = std::max(1, MV_CTAS / c.nb_cta);
+                    const int chunk = std::min(MV_COLS, std::max(MV_MIN, (m - i + want - 1) / want));
+                    const int nchunk = (m - i + chunk - 1) / chunk;
+                    col_matvec<<<dim3(c.nb_cta, nchunk), HT, 0, s>>>(c, i, chunk);
                     col_y<<<c.nb_cta, HT, 0, s>>>(c, i, nchunk);
                     inf.launches += 7;
                 }
@@ -385,19 +390,19 @@ int hessenberg_reduce_device(int64_t n, double* dA, int64_t lda, double* dQ, int
                 const int cw = (int)(n - k - b);
                 double* G = dA + (k + 1) + (k + b) * lda;
                 HCUDA(launch_dgemm(false, true, m, cw, b, -1.0, Y.p, m, V.p + (b - 1), m, 1.0, G, lda, s));
-                HCUDA(launch_dgemm(true, false, b, cw, m, 1.0, V.p, m, G, lda, 0.0, W.p, HB, s));
+                HCUDA(launch_dgemm(true, false, b, cw, m, 1.0, V.p, m, G, lda, 0.0, W.p, HB, s, K.p, 16 * HB * n));
                 HCUDA(launch_dgemm(true, false, b, cw, b, 1.0, T.p, HB, W.p, HB, 0.0, W2.p, HB, s));
                 HCUDA(launch_dgemm(false, false, m, cw, b, -1.0, V.p, m, W2.p, HB, 1.0, G, lda, s));
                 // rows above (hessenberg.cpp:140-160): A[:k+1, k+1:] -= ((A V) T) V^T
                 const int rt = (int)(k + 1);
                 double* Gt = dA + (k + 1) * lda;
-                HCUDA(launch_dgemm(false, false, rt, b, m, 1.0, Gt, lda, V.p, m, 0.0, P.p, n, s));
+                HCUDA(launch_dgemm(false, false, rt, b, m, 1.0, Gt, lda, V.p, m, 0.0, P.p, n, s, K.p, 16 * HB * n));
                 HCUDA(launch_dgemm(false, false, rt, b, b, 1.0, P.p, n, T.p, HB, 0.0, P2.p, n, s));
                 HCUDA(launch_dgemm(false, true, rt, m, b, -1.0, P2.p, n, V.p, m, 1.0, Gt, lda, s));
                 inf.launches += 7;
                 if (dQ) {  // Q[:, k+1:] <- Q (I - V T V^T) (hessenberg.cpp:165-181)
                     double* Gq = dQ + (k + 1) * ldq;
-                    HCUDA(launch_dgemm(false, false, (int)n, b, m, 1.0, Gq, ldq, V.p, m, 0.0, P.p, n, s));
+                    HCUDA(launch_dgemm(false, false, (int)n, b, m, 1.0, Gq, ldq, V.p, m, 0.0, P.p, n, s, K.p, 16 * HB * n));
                     HCUDA(launch_dgemm(false, false, (int)n, b, b, 1.0, P.p, n, T.p, HB, 0.0, P2.p, n, s));
                     HCUDA(launch_dgemm(false, true, (int)n, m, b, -1.0, P2.p, n, V.p, m, 1.0, Gq, ldq, s));
                     inf.launches += 3;

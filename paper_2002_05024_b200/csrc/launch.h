@@ -107,8 +107,11 @@ cudaError_t launch_scan_active(double* H, long long ldh, int n, int ihi, double 
 // eigenvector column renormalisation (kind: 0 real, 1 pair start, 2 pair
 // second half, other / NULL: finiteness check only; *nonfinite |= 1 on
 // Inf / NaN)
+// work (optional, work_doubles long): split-K partials for products with few
+// output tiles and a long K (reduced in a fixed order: deterministic)
 cudaError_t launch_dgemm(bool ta, bool tb, int m, int n, int kdim, double alpha, const double* A, long long lda,
-                         const double* B, long long ldb, double beta, double* C, long long ldc, cudaStream_t s);
+                         const double* B, long long ldb, double beta, double* C, long long ldc, cudaStream_t s,
+                         double* work = nullptr, size_t work_doubles = 0);
 cudaError_t launch_renorm_columns(int n, double* X, long long ldx, const int8_t* kind_dev, int k, int* nonfinite,
                                   cudaStream_t s);
 // distributed deviation flag: mode 0 publish this rank's flag into base[slots[0]],

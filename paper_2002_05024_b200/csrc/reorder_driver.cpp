@@ -599,7 +599,7 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
         // scan, else one device scan of Q (n^2 reads, ~3 ms at n=40000)
         FactorSupport qsupp;
         static const bool no_supp = getenv("TEIG_NO_Q_SUPPORT") && atoi(getenv("TEIG_NO_Q_SUPPORT"));
-        if (dQ && !no_supp) {
+        if (dQ && !no_supp && !o.full_factor) {
             if (qsupp_in && qsupp_in->on) {
                 qsupp = *qsupp_in;
             } else if (!q_ready) {  // (Q still arriving and no host scan: full updates)
@@ -697,7 +697,7 @@ void teig_reorder_opts_default(teig_reorder_opts* o) {
     o->strict = 0;
     o->overlap_factor = 1;
     o->profile = 0;
-    o->pad = 0;
+    o->full_factor = 0;
 }
 
 int teig_reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t ldq, int64_t nb,
@@ -822,7 +822,7 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         FactorSupport qsupp;
         std::vector<std::thread> scan;
         const bool no_supp = getenv("TEIG_NO_Q_SUPPORT") && atoi(getenv("TEIG_NO_Q_SUPPORT"));
-        if (Q && !no_supp) {
+        if (Q && !no_supp && !(opts && opts->full_factor)) {
             qsupp.lo.resize(n);
             qsupp.hi.resize(n);
             const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
@@ -897,7 +897,7 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         TEIG_CUDA(cudaEventCreateWithFlags(&dr.evS, cudaEventDisableTiming));
         TEIG_CUDA(cudaEventCreateWithFlags(&dr.evQ, cudaEventDisableTiming));
         for (auto& t : scan) t.join();
-        qsupp.on = Q && !no_supp;
+        qsupp.on = !scan.empty();
         const int rc = reorder_schur_device(n, dS, n, dQ, n, nb, sizes, flags, opts, perm, rejected, plan, plan_cap,
                                             info, stream, q_ready, drain_on ? &dr : nullptr, &qsupp);
         TEIG_CUDA(cudaStreamSynchronize(stream));

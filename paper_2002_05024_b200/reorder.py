@@ -171,6 +171,7 @@ class ReorderOptions:
     strict: bool = False      # raise on rejected swaps instead of recording
     overlap_factor: bool = True
     profile: bool = False     # per-kernel-class CUDA-event timing in ReorderResult.info
+    full_factor: bool = False  # update Q over all rows (no skipping of its exactly-zero rows)
 
 
 @dataclass
@@ -249,6 +250,7 @@ def reorder_schur(s, q, sel: Selection, opts: Optional[ReorderOptions] = None,
     o.strict = int(bool(opts.strict))
     o.overlap_factor = int(bool(opts.overlap_factor))
     o.profile = int(bool(opts.profile))
+    o.full_factor = int(bool(opts.full_factor))
     vp = lambda a: a.ctypes.data_as(C.c_void_p)
     if torch is not None and isinstance(s, torch.Tensor):
         _need_torch_cuda(s)
