@@ -827,7 +827,7 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
             qsupp.hi.resize(n);
             const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
             for (int t = 0; t < nt; ++t)
-                scan.emplace_back([&, t] {
+                scan.emplace_back([&qsupp, Q, ldq, n, nt, t] {  // nt by value: it leaves scope before the join
                     for (int64_t c = n * t / nt; c < n * (t + 1) / nt; ++c) {
                         const uint64_t* col = reinterpret_cast<const uint64_t*>(Q + c * ldq);
                         int64_t l = 0, h = n - 1;
