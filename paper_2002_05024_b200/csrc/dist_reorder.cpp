@@ -350,6 +350,7 @@ int owner_of(const std::vector<int64_t>& C, int64_t col) {
 struct PassOut {
     int64_t windows = 0, levels = 0, launches = 0;
     bool deviated = false;
+    double fl = 0, fr = 0, fq = 0;  // executed update flops of the LOCAL ranks (left, right, factors)
 };
 
 PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankBufs>& R, Comm& comm, int64_t lds,
@@ -424,6 +425,7 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
                 if (c1 <= c0) continue;
                 WinDesc d = base(t);
                 d.lc0 = (int32_t)c0;
+                if (comm.local(r)) po.fl += (gen ? 2.0 : 1.0) * 2.0 * double(d.d) * d.d * double(c1 - c0);
                 d.lc1 = (int32_t)c1;
                 d.tl_pref = (int32_t)P.l_tiles;
                 P.l_tiles += (c1 - c0 + kLeftBN - 1) / kLeftBN;
@@ -440,6 +442,7 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
                 if (gen) d.qw_off += (int64_t)d.d * d.d;  // the pencil's right side uses Z_w
                 d.rr0 = 0;
                 d.rr1 = (int32_t)w.wtop;
+                if (comm.local(r)) po.fr += (gen ? 2.0 : 1.0) * 2.0 * double(d.d) * d.d * double(w.wtop);
                 d.tr_pref = (int32_t)P.r_tiles;
                 P.r_tiles += (w.wtop + kRightBM - 1) / kRightBM;
                 D[r].push_back(d);
@@ -463,6 +466,7 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
                     factor_rows(qsupp ? &(*qsupp)[r] : nullptr, t, &q0, &q1);
                     d.qr0 = (int32_t)q0;
                     d.qr1 = (int32_t)q1;
+                    if (comm.local(r)) po.fq += 2.0 * double(d.d) * d.d * double(q1 - q0);
                     d.tq_pref = (int32_t)P.q_tiles;
                     P.q_tiles += (q1 - q0 + kRightBM - 1) / kRightBM;
                     D[r].push_back(d);
@@ -478,6 +482,7 @@ PassOut run_dist_pass(ReorderPlan& plan, int64_t n, int world, std::vector<RankB
                     factor_rows(zsupp ? &(*zsupp)[r] : nullptr, t, &z0, &z1);
                     d.qr0 = (int32_t)z0;
                     d.qr1 = (int32_t)z1;
+                    if (comm.local(r)) po.fq += 2.0 * double(d.d) * d.d * double(z1 - z0);
                     d.tq_pref = (int32_t)P.z_tiles;
                     P.z_tiles += (z1 - z0 + kRightBM - 1) / kRightBM;
                     D[r].push_back(d);
@@ -981,6 +986,10 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, co
             inf.n_levels += po.levels;
             inf.n_launches += po.launches;
             inf.n_passes += 1;
+            // per-class flops: executed by this process's ranks (the slabs it owns)
+            inf.flops_left += po.fl;
+            inf.flops_right += po.fr;
+            inf.flops_factor_exec += po.fq;
             if (!po.deviated) break;
         }
         for (auto& B : R)
