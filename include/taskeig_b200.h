@@ -360,14 +360,16 @@ int teig_dist_reorder_schur(int64_t n, int32_t world, int32_t rank, void* nccl_c
 /* Single-process multi-GPU: all `world` ranks in this process, rank r on
  * devices[r] (distinct GPUs), NCCL clique from ncclCommInitAll (created once
  * per device list, kept for the process).  dS_slabs[r] / dQ_slabs[r] are rank
- * r's slabs on devices[r] (layout as teig_dist_reorder_schur).  Synchronous;
- * same result, bit for bit, as teig_reorder_schur_device. */
+ * r's slabs on devices[r] (layout as teig_dist_reorder_schur); plan as
+ * teig_reorder_schur_device.  Synchronous; same result, bit for bit, as
+ * teig_reorder_schur_device.  The C++ drop-in takes this path when the
+ * TASKEIG_GPUS environment variable asks for GPUs (taskeig_adapter.cpp). */
 int teig_dist_reorder_schur_multi(int64_t n, int32_t world, const int32_t* devices,
                                   double* const* dS_slabs, int64_t lds, double* const* dQ_slabs,
                                   const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb,
                                   const uint8_t* sizes, const uint8_t* flags,
                                   const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
-                                  teig_reorder_info* info);
+                                  int64_t* plan, int64_t plan_cap, teig_reorder_info* info);
 
 /* Generalized pencil (C5) across ranks: S and T in column slabs (same
  * layout as dS_slabs), Q and Z in row slabs; window_size <= 64.  Same result,

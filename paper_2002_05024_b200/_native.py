@@ -120,7 +120,7 @@ SIGNATURES = {
     "teig_dist_greorder_schur": (C.c_int, [_I64, C.c_int32, C.c_int32, _P, _P, _P, _I64, _P, _P, _P, _P, _I64, _P,
                                            _P, _P, _P, _P, _P, _P]),
     "teig_dist_reorder_schur_multi": (C.c_int, [_I64, C.c_int32, _P, _P, _I64, _P, _P, _P, _I64, _P, _P, _P, _P, _P,
-                                                _P]),
+                                                _P, _I64, _P]),
     "teig_nccl_available": (C.c_int, []),
     "teig_nccl_unique_id": (C.c_int, [_P]),
     "teig_nccl_comm_init": (C.c_int, [C.c_int32, C.c_int32, _P, _P]),

@@ -833,7 +833,8 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, co
                      double* const* dS_slabs, double* const* dT_slabs, int64_t lds, double* const* dQ_slabs,
                      double* const* dZ_slabs, const int64_t* col_bounds, const int64_t* row_bounds, int64_t nb,
                      const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts, int64_t* perm,
-                     int64_t* rejected_out, teig_reorder_info* info, void* stream_v, bool gen) {
+                     int64_t* rejected_out, teig_reorder_info* info, void* stream_v, bool gen,
+                     int64_t* plan_out = nullptr, int64_t plan_cap = 0) {
     if (n < 1) return set_error(-1, "n must be >= 1");
     if (world < 1 || world > 16) return set_error(-2, "world must be in [1, 16]");
     const bool multi = devices != nullptr;
@@ -1018,6 +1019,9 @@ static int dist_impl(int64_t n, int32_t world, int32_t rank, void* nccl_comm, co
         for (int64_t i = 0; i < nb; ++i) perm[blocks[i].orig] = i;
     if (rejected_out)
         for (size_t i = 0; i < rejected.size(); ++i) rejected_out[i] = rejected[i];
+    if (plan_out)
+        for (int64_t i = 0; i < (int64_t)plan_log.size() / 3 && i < plan_cap; ++i)
+            for (int k = 0; k < 3; ++k) plan_out[3 * i + k] = plan_log[3 * i + k];
     if (info) *info = inf;
     return 0;
 }
@@ -1044,13 +1048,13 @@ int teig_dist_reorder_schur_multi(int64_t n, int32_t world, const int32_t* devic
                                   int64_t lds, double* const* dQ_slabs, const int64_t* col_bounds,
                                   const int64_t* row_bounds, int64_t nb, const uint8_t* sizes, const uint8_t* flags,
                                   const teig_reorder_opts* opts, int64_t* perm, int64_t* rejected,
-                                  teig_reorder_info* info) {
+                                  int64_t* plan, int64_t plan_cap, teig_reorder_info* info) {
     if (!devices) return set_error(-3, "devices is null");
     for (int r = 0; r < world; ++r)
         for (int k = 0; k < r; ++k)
             if (devices[k] == devices[r]) return set_error(-3, "devices must be distinct (one rank per GPU)");
     return dist_impl(n, world, 0, nullptr, devices, dS_slabs, nullptr, lds, dQ_slabs, nullptr, col_bounds, row_bounds,
-                     nb, sizes, flags, opts, perm, rejected, info, nullptr, false);
+                     nb, sizes, flags, opts, perm, rejected, info, nullptr, false, plan, plan_cap);
 }
 
 int teig_gen_schur_input_cols_device(int64_t n, double* dS, int64_t lds, int64_t c0, int64_t c1, uint64_t fill_seed,

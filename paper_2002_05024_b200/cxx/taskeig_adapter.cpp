@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <complex>
 #include <cstring>
 #include <stdexcept>
@@ -169,6 +170,73 @@ struct DeviceProblem {
         if (f) download(q.p, *f, st.s);
     }
 };
+
+// Multi-GPU from the reference's in-process API: TASKEIG_GPUS=k (the GPU
+// counterpart of the reference's TASKEIG_WORKERS, runtime.cpp:251-258) runs
+// reorder_schur over min(k, visible GPUs) devices in this process
+// (teig_dist_reorder_schur_multi: S column slabs, Q row slabs, NCCL clique);
+// the result is bitwise the single-GPU one.  Unset: one GPU.  Problems too
+// small for the slab layout (< 256 columns per rank) use fewer ranks.
+int gpu_world(size_t n) {
+    const char* e = getenv("TASKEIG_GPUS");
+    if (!e || atoi(e) <= 0) return 0;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int world = std::min(std::min(atoi(e), ndev), 16);
+    while (world > 1 && n < (size_t)256 * world) --world;
+    return n >= 256 ? world : 0;
+}
+
+void reorder_multi(DeviceProblem& dp, int world, const teig_reorder_opts& o, size_t nb, const uint8_t* sizes,
+                   const uint8_t* flags, int64_t* perm, int64_t* rej, int64_t* plan, int64_t cap,
+                   teig_reorder_info* info) {
+    const int64_t n = (int64_t)dp.n;
+    std::vector<int64_t> cb(world + 1), rb(world + 1);
+    teig_check(teig_dist_balance(n, (int64_t)nb, sizes, flags, o.window_size, world, cb.data(), rb.data()),
+               "reorder_schur (slabs)");
+    int cur = 0;
+    cuda_check(cudaGetDevice(&cur), "device");
+    std::vector<int32_t> devs(world);
+    for (int r = 0; r < world; ++r) devs[r] = r;
+    std::vector<double*> ss(world, nullptr), qs(world, nullptr);
+    struct Free {
+        std::vector<double*>& a;
+        std::vector<double*>& b;
+        ~Free() {
+            for (double* p : a)
+                if (p) cudaFree(p);
+            for (double* p : b)
+                if (p) cudaFree(p);
+        }
+    } release{ss, qs};
+    const bool with_q = dp.q.p != nullptr;
+    for (int r = 0; r < world; ++r) {  // scatter: S column slabs (+ halo), Q row slabs
+        cuda_check(cudaSetDevice(devs[r]), "device");
+        const int64_t w = cb[r + 1] - cb[r], h = rb[r + 1] - rb[r];
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&ss[r]), sizeof(double) * n * (w + 128)), "cudaMalloc");
+        cuda_check(cudaMemcpy(ss[r], dp.h.p + cb[r] * n, sizeof(double) * n * w, cudaMemcpyDefault), "scatter S");
+        if (with_q) {
+            cuda_check(cudaMalloc(reinterpret_cast<void**>(&qs[r]), sizeof(double) * std::max<int64_t>(h, 1) * n),
+                       "cudaMalloc");
+            if (h > 0)
+                cuda_check(cudaMemcpy2D(qs[r], h * 8, dp.q.p + rb[r], n * 8, h * 8, n, cudaMemcpyDefault), "scatter Q");
+        }
+    }
+    cuda_check(cudaSetDevice(cur), "device");
+    teig_check(teig_dist_reorder_schur_multi(n, world, devs.data(), ss.data(), n, with_q ? qs.data() : nullptr,
+                                             cb.data(), rb.data(), (int64_t)nb, sizes, flags, &o, perm, rej, plan, cap,
+                                             info),
+               "reorder_schur");
+    for (int r = 0; r < world; ++r) {  // gather
+        const int64_t w = cb[r + 1] - cb[r], h = rb[r + 1] - rb[r];
+        cuda_check(cudaMemcpy(dp.h.p + cb[r] * n, ss[r], sizeof(double) * n * w, cudaMemcpyDefault), "gather S");
+        if (with_q && h > 0)
+            cuda_check(cudaMemcpy2D(dp.q.p + rb[r], n * 8, qs[r], h * 8, h * 8, n, cudaMemcpyDefault), "gather Q");
+    }
+}
 
 // scan_blocks: diagonal blocks by exact-zero subdiagonal (reorder.cpp:21-43)
 std::vector<Selection::Block> scan(const TiledMatrix& s) {
@@ -339,10 +407,14 @@ ReorderResult reorder_schur(TiledMatrix s_in, std::optional<TiledMatrix> q_in, c
     const int64_t cap = (int64_t)std::max<size_t>(8 * nb, 1024);
     std::vector<int64_t> plan(3 * cap);
     teig_reorder_info info{};
-    teig_check(teig_reorder_schur_device((int64_t)n, dp.h.p, (int64_t)n, q ? dp.q.p : nullptr, (int64_t)n,
-                                         (int64_t)nb, sizes.data(), flags.data(), &o, perm.data(), rej.data(),
-                                         plan.data(), cap, &info, dp.st.s),
-               "reorder_schur");
+    const int world = gpu_world(n);
+    if (world > 0)
+        reorder_multi(dp, world, o, nb, sizes.data(), flags.data(), perm.data(), rej.data(), plan.data(), cap, &info);
+    else
+        teig_check(teig_reorder_schur_device((int64_t)n, dp.h.p, (int64_t)n, q ? dp.q.p : nullptr, (int64_t)n,
+                                             (int64_t)nb, sizes.data(), flags.data(), &o, perm.data(), rej.data(),
+                                             plan.data(), cap, &info, dp.st.s),
+                   "reorder_schur");
     dp.back(s, q);
     out.permutation.assign(nb, 0);
     for (size_t i = 0; i < nb; ++i) out.permutation[i] = (size_t)perm[i];

@@ -218,7 +218,7 @@ def reorder_schur_multi(s, q, sel: Selection, devices: Sequence[int], opts: Opti
     rba = np.ascontiguousarray(rb, dtype=np.int64)
     o = _opts(opts)
     rc = N.lib().teig_dist_reorder_schur_multi(n, world, _vp(dv), sp, n, qp, _vp(cba), _vp(rba), nb, _vp(sizes),
-                                               _vp(flags), C.byref(o), _vp(perm), _vp(rej), C.byref(info))
+                                               _vp(flags), C.byref(o), _vp(perm), _vp(rej), None, 0, C.byref(info))
     if rc == -1002:
         raise RuntimeError("reorder_schur: swap rejected in strict mode")
     N.check(rc)

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BUILD = os.path.join(ROOT, "tests", "refcpp", "_build")
 
 
-@pytest.mark.parametrize("name", ["reorder", "schur"])
+@pytest.mark.parametrize("name", ["reorder", "schur", "multi_gpu"])
 def test_reference_suite_through_the_dropin(cuda, name):
     exe = os.path.join(BUILD, f"test_{name}_b200")
     if not os.path.exists(exe):
