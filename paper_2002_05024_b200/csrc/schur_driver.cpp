@@ -33,6 +33,7 @@
 #include "../../include/taskeig_b200.h"
 #include "device_types.h"
 #include "launch.h"
+#include "plan.h"
 #include "trace.h"
 
 namespace teig {
@@ -221,6 +222,22 @@ class SchurRunner {
             TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&d_prof_), sizeof(unsigned long long) * 16, s_));
             TEIG_CUDA(cudaMemsetAsync(d_prof_, 0, sizeof(unsigned long long) * 16, s_));
         }
+        // the factor's row support (plan.h FactorSupport): its updates skip the
+        // rows of Q[:, a:b] that are exact zeros (Q_in = I)
+        if (dQ_ && !(getenv("TEIG_NO_Q_SUPPORT") && atoi(getenv("TEIG_NO_Q_SUPPORT")))) {
+            int32_t *dlo = nullptr, *dhi = nullptr;
+            TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&dlo), sizeof(int32_t) * n, s_));
+            TEIG_CUDA(lib_malloc_async(reinterpret_cast<void**>(&dhi), sizeof(int32_t) * n, s_));
+            qsupp_.lo.resize(n);
+            qsupp_.hi.resize(n);
+            TEIG_CUDA(launch_column_support(dQ_, ldq_, n, n, dlo, dhi, s_));
+            TEIG_CUDA(cudaMemcpyAsync(qsupp_.lo.data(), dlo, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s_));
+            TEIG_CUDA(cudaMemcpyAsync(qsupp_.hi.data(), dhi, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s_));
+            TEIG_CUDA(cudaFreeAsync(dlo, s_));
+            TEIG_CUDA(cudaFreeAsync(dhi, s_));
+            TEIG_CUDA(cudaStreamSynchronize(s_));
+            qsupp_.on = true;
+        }
     }
     ~SchurRunner() {
         if (d_prof_) {
@@ -290,6 +307,7 @@ class SchurRunner {
         const int64_t nw = (int64_t)wins_.size();
         qw_.need((size_t)nw * kSlot, s_);
         std::vector<WinDesc> descs(nw);
+        hdesc_rows_.assign(nw, 0);
         for (int64_t k = 0; k < nw; ++k) {
             WinDesc& w = descs[k];
             std::memset(&w, 0, sizeof w);
@@ -298,10 +316,13 @@ class SchurRunner {
             w.qw_off = k * kSlot;
             w.lc0 = (int32_t)(wins_[k].a + wins_[k].d);
             w.lc1 = (int32_t)n_;
+            int64_t q0 = 0, q1 = n_;  // factor rows (windows in execution order)
+            if (dQ_ && qsupp_.on) qsupp_.window(wins_[k].a, wins_[k].a + wins_[k].d, &q0, &q1);
             w.rr0 = 0;
             w.rr1 = (int32_t)wins_[k].a;
-            w.qr0 = 0;
-            w.qr1 = (int32_t)n_;
+            w.qr0 = (int32_t)q0;
+            w.qr1 = (int32_t)q1;
+            hdesc_rows_[k] = q1 - q0;
             if (wins_[k].kind == 1) hchase_[wins_[k].cw_idx].qw_off = k * kSlot;
         }
         descs_.need(nw, s_);
@@ -416,7 +437,8 @@ class SchurRunner {
         const WinDesc* dd = descs_.p + k;
         const int tl = (int)((n_ - b + kLeftBN - 1) / kLeftBN);
         const int tr = (int)((a + kRightBM - 1) / kRightBM);
-        const int tq = dQ_ ? (int)((n_ + kRightBM - 1) / kRightBM) : 0;
+        const int64_t qrows = dQ_ ? (int64_t)hdesc_rows_[k] : 0;
+        const int tq = dQ_ ? (int)((qrows + kRightBM - 1) / kRightBM) : 0;
         const double dd2 = 2.0 * double(d) * double(d);
         flops_ += dd2 * double(n_ - b) + dd2 * double(a) + (dQ_ ? dd2 * double(n_) : 0.0);
         if (tl > 0) {
@@ -510,6 +532,8 @@ class SchurRunner {
     std::vector<cudaEvent_t> evpool_;
     size_t nev_ = 0;
     std::vector<Span> spans_;
+    FactorSupport qsupp_;
+    std::vector<int64_t> hdesc_rows_;  // factor rows of each window of the round
     double ms_[2] = {0, 0};
     double flops_ = 0;
     bool last_converged_ = true;
