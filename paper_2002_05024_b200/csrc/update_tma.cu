@@ -257,6 +257,7 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
 
     const int gid = lane >> 2, tig = lane & 3;
     double af[2][32];
+    unsigned nz0 = 0, nz1 = 0;  // bit ks: fragment af[mt][ks] is nonzero in some lane (warp-uniform)
     TileWin wd;
     load_win<0>(wd, wins, nwin, wi0);
     int cur = -1, stage = 0, prev = -1;
@@ -275,6 +276,12 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
                     af[mt][ks] = (m < d && k < d) ? __ldg(Qw + k + (long long)m * d) : 0.0;
                 }
             }
+            nz0 = nz1 = 0;
+#pragma unroll
+            for (int ks = 0; ks < 32; ++ks) {
+                nz0 |= (__any_sync(0xffffffffu, af[0][ks] != 0.0) ? 1u : 0u) << ks;
+                nz1 |= (__any_sync(0xffffffffu, af[1][ks] != 0.0) ? 1u : 0u) << ks;
+            }
             cur = wd.wi;
         }
         const int c = wd.r0 + (t - wd.pref) * kLeftBN;
@@ -290,15 +297,22 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
             const int shift = (int)(((long long)wd.a + (long long)(c + kLSub * sub) * lds) & 1);
             const double* sb = ring + stage * (kLeftStage / 8) + gid * kLdB + tig + shift;
             mbar_wait(&full[stage], phase);
+            // Q_w's zero 8x4 fragments (about 45 % of them: a window only mixes
+            // the blocks it moves past each other) are skipped -- their products
+            // are exact zeros and the sums start at +0, so the bits do not change
 #pragma unroll
             for (int ks = 0; ks < 32; ++ks) {
+                const bool u0 = (nz0 >> ks) & 1u, u1 = (nz1 >> ks) & 1u;
+                if (!(u0 | u1)) continue;
                 double bf[kLSub / 8];
 #pragma unroll
                 for (int nt = 0; nt < kLSub / 8; ++nt) bf[nt] = sb[nt * 8 * kLdB + 4 * ks];
+                if (u0)
 #pragma unroll
-                for (int mt = 0; mt < 2; ++mt)
+                    for (int nt = 0; nt < kLSub / 8; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], af[0][ks], bf[nt]);
+                if (u1)
 #pragma unroll
-                    for (int nt = 0; nt < kLSub / 8; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][ks], bf[nt]);
+                    for (int nt = 0; nt < kLSub / 8; ++nt) dmma(acc[1][nt][0], acc[1][nt][1], af[1][ks], bf[nt]);
             }
             // epilogue through the consumed stage: accumulators to smem at the
             // inputs' positions, then one bulk store per column (async: the
@@ -391,6 +405,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
 
     const int gid = lane >> 2, tig = lane & 3;
     double bf[2][32];
+    unsigned nz0 = 0, nz1 = 0;  // bit ks: fragment bf[nt][ks] is nonzero in some lane (warp-uniform)
     TileWin wd;
     load_win<Field>(wd, wins, nwin, wi0);
     int cur = -1, stage = 0;
@@ -409,6 +424,12 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
                     bf[nt][ks] = (nn < d && k < d) ? __ldg(Qw + k + (long long)nn * d) : 0.0;
                 }
             }
+            nz0 = nz1 = 0;
+#pragma unroll
+            for (int ks = 0; ks < 32; ++ks) {
+                nz0 |= (__any_sync(0xffffffffu, bf[0][ks] != 0.0) ? 1u : 0u) << ks;
+                nz1 |= (__any_sync(0xffffffffu, bf[1][ks] != 0.0) ? 1u : 0u) << ks;
+            }
             cur = wd.wi;
         }
         int r0, nrows;
@@ -424,15 +445,20 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
             const int shift = (int)(((long long)r0 + kRSub * sub + (long long)wd.a * ldm) & 1);
             const double* sa = ring + stage * (kRightStage / 8) + tig * kLdA + gid + shift;
             mbar_wait(&full[stage], phase);
+            // zero fragments of Q_w skipped (exact: see the left kernel)
 #pragma unroll
             for (int ks = 0; ks < 32; ++ks) {
+                const bool u0 = (nz0 >> ks) & 1u, u1 = (nz1 >> ks) & 1u;
+                if (!(u0 | u1)) continue;
                 double a[kRSub / 8];
 #pragma unroll
                 for (int mt = 0; mt < kRSub / 8; ++mt) a[mt] = sa[4 * ks * kLdA + 8 * mt];
+                if (u0)
 #pragma unroll
-                for (int mt = 0; mt < kRSub / 8; ++mt)
+                    for (int mt = 0; mt < kRSub / 8; ++mt) dmma(acc[mt][0][0], acc[mt][0][1], a[mt], bf[0][ks]);
+                if (u1)
 #pragma unroll
-                    for (int nt = 0; nt < 2; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt][ks]);
+                    for (int mt = 0; mt < kRSub / 8; ++mt) dmma(acc[mt][1][0], acc[mt][1][1], a[mt], bf[1][ks]);
             }
             // direct stores: with a 3-deep ring of 64-row stages the staged
             // (bulk-store) epilogue of the left kernel delays the refill by one
