@@ -269,18 +269,14 @@ def run_ours(args, rank, world, local):
 
     sampler = ClockSampler(local)
     sampler.start()
-    # the timed steps record per-launch events (profile=True); the last
-    # warm-up does too, so the first timed step does not pay the driver's
-    # first creation of ~4300 events (it ran ~15 % slower)
-    popts = T.ReorderOptions(window_size=args.ws, profile=True)
+    # the timed steps run exactly as a user's call (no per-launch events); the
+    # kernel-level numbers come from one extra serialised, profiled step below
     for k in range(max(args.warmup, 0)):
         reset()
-        res = T.reorder_schur(S, Q, sel, popts if k == args.warmup - 1 else opts)
+        res = T.reorder_schur(S, Q, sel, opts)
     torch.cuda.synchronize()
 
     # ---------------- timed region (device events per step) ----------------
-    prof = {"ms_window": 0.0, "ms_left": 0.0, "ms_right": 0.0, "ms_factor": 0.0, "flops_left": 0.0,
-            "flops_right": 0.0, "flops_factor": 0.0, "flops_factor_exec": 0.0, "n_launches": 0}
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
@@ -291,7 +287,7 @@ def run_ours(args, rank, world, local):
     for k in range(args.steps):
         reset()
         ev[k][0].record(stream)
-        res = T.reorder_schur(S, Q, sel, popts)
+        res = T.reorder_schur(S, Q, sel, opts)
         ev[k][1].record(stream)
         infos.append(res.info)
     torch.cuda.synchronize()
@@ -300,16 +296,12 @@ def run_ours(args, rank, world, local):
         dist.barrier()
     clocks = sampler.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
-    for inf in infos:
-        for key in prof:
-            prof[key] += inf[key]
     ms_step = sum(step_ms) / len(step_ms)
     if world > 1:
         t = torch.tensor([ms_step], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_step = float(t.item())
     info = infos[-1]
-    exec_flops = info["flops_left"] + info["flops_right"] + info["flops_factor_exec"]
 
     # ---------------- parity spot check of the last step (GPU cuBLAS, independent) ----------------
     S0d = S0.to(torch.float64)
@@ -325,20 +317,25 @@ def run_ours(args, rank, world, local):
     reset()
     ser = T.reorder_schur(S, Q, sel, T.ReorderOptions(window_size=args.ws, profile=True, overlap_factor=False)).info
     torch.cuda.synchronize()
+    # executed flops of a step (the plan is deterministic: the serialised step
+    # runs the same windows): DMMA instructions counted on the device
+    exec_flops = ser["flops_dmma"] if ser.get("flops_dmma") else (
+        ser["flops_left"] + ser["flops_right"] + ser["flops_factor_exec"])
 
     # ---------------- roofline of the dominant kernel class ----------------
     # achieved: update flops / summed update-kernel durations of the
     # serialised step (non-overlapped); the timed steps' event sums overlap on
     # two streams and are reported separately (two_stream_event_sum)
-    # executed flops: the factor updates skip rows of Q that are exact zeros
-    # (tracked support, plan.h FactorSupport), so their executed count is
-    # flops_factor_exec, not the reference's 2 d^2 n per window
+    # executed flops: the DMMA instructions the update kernels issued, counted
+    # on the device (512 flops each) -- the factor updates skip Q's exactly-zero
+    # rows (plan.h FactorSupport) and the bulk kernels Q_w's all-zero 8x4
+    # fragments, so neither the reference's count (2 d^2 (2n - d) per window)
+    # nor the row-skipped count is what the tensor pipe executed
     k_ms = ser["ms_left"] + ser["ms_right"] + ser["ms_factor"]
-    k_flops = ser["flops_left"] + ser["flops_right"] + ser["flops_factor_exec"]
+    k_flops = ser["flops_dmma"] if ser.get("flops_dmma") else (
+        ser["flops_left"] + ser["flops_right"] + ser["flops_factor_exec"])
     achieved = k_flops / (k_ms * 1e-3) / 1e12 if k_ms > 0 else 0.0
     steps = args.steps
-    t_ms = prof["ms_left"] + prof["ms_right"] + prof["ms_factor"]
-    t_flops = prof["flops_left"] + prof["flops_right"] + prof["flops_factor_exec"]
     roof = {"bound": "tensor", "kernel": "update_left/right DMMA kernels (all launches of one serialised step)",
             "achieved": round(achieved, 3), "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
             "frac": round(achieved / FP64_DMMA_PEAK_TFLOPS, 4),
@@ -346,9 +343,7 @@ def run_ours(args, rank, world, local):
                            "stream (overlap_factor=0): non-overlapped kernel time",
             "serialised_step_ms": {"window": round(ser["ms_window"], 2), "left": round(ser["ms_left"], 2),
                                    "right": round(ser["ms_right"], 2), "factor": round(ser["ms_factor"], 2)},
-            "two_stream_event_sum": {"achieved": round(t_flops / (t_ms * 1e-3) / 1e12, 3) if t_ms > 0 else None,
-                                     "note": "timed steps: event-bracketed update launches on two concurrent "
-                                             "streams summed -- overlapped time, not a kernel rate"},
+
             "peak_source": "FP64 DMMA.8x8x4 issue peak measured on this pool's B200 "
                            "(tools/microbench/fp64_peak.cu, profiles/r01_fp64_peak.txt); "
                            "MEASURED_PEAKS.json has no FP64 entry",
@@ -356,13 +351,16 @@ def run_ours(args, rank, world, local):
             "aggregate": {"achieved": round(exec_flops / (ms_step * 1e-3) / 1e12, 3),
                           "frac": round(exec_flops / (ms_step * 1e-3) / 1e12 / FP64_DMMA_PEAK_TFLOPS, 4),
                           "note": "executed update flops / step time (both streams, window kernels included)"},
-            "executed_vs_reference_flops": {"executed": exec_flops, "reference_count": info["update_flops"],
-                                            "note": "the reference updates Q over all n rows per window; rows of "
-                                                    "Q[:, a:b] outside the tracked support of its columns are exact "
-                                                    "zeros (Q_in = I) and are skipped, bitwise-identical result"},
+            "executed_vs_reference_flops": {"executed_dmma": exec_flops, "reference_count": info["update_flops"],
+                                            "row_skipped_count": info["flops_left"] + info["flops_right"]
+                                            + info["flops_factor_exec"],
+                                            "note": "executed = DMMA instructions issued x 512 (device counters); "
+                                                    "the reference updates Q over all n rows per window and multiplies "
+                                                    "Q_w's zero blocks too: the kernels skip Q's exactly-zero rows "
+                                                    "and Q_w's all-zero 8x4 fragments, bitwise-identical result"},
             "flops_per_step": k_flops,
             "update_ms_serialised_step": k_ms,
-            "window_ms_per_step": prof["ms_window"] / steps,
+            "window_ms_serialised_step": ser["ms_window"],
             "algorithmic_bytes_per_step": info["update_bytes"]}
 
     out = {
@@ -395,7 +393,7 @@ def run_ours(args, rank, world, local):
                    and eig_pos["pass"]},
         "roofline": roof,
         "e2e": e2e,
-        "gpu_launches": int(prof["n_launches"] / steps),
+        "gpu_launches": int(info["n_launches"]),
         "clocks": clocks,
         "wall_s_timed_region": round(t_wall, 3),
         "step_ms": [round(x, 3) for x in step_ms],

@@ -83,6 +83,9 @@ typedef struct teig_reorder_info {
     double flops_factor_exec;  /* factor-update flops actually executed: rows outside the
                                   tracked support of Q's columns are exact zeros and skipped
                                   (Q_in = I: about half; TEIG_NO_Q_SUPPORT=1 disables) */
+    double flops_dmma;         /* profile only: flops of the DMMA instructions the update
+                                  kernels issued (512 per m8n8k4; Q_w's all-zero fragments are
+                                  skipped by the bulk kernels), from device counters */
 } teig_reorder_info;
 
 void teig_reorder_opts_default(teig_reorder_opts* o);

@@ -43,7 +43,7 @@ class ReorderInfo(C.Structure):
                 ("plan_ms", C.c_double), ("n_launches", C.c_int64), ("ms_window", C.c_double),
                 ("ms_left", C.c_double), ("ms_right", C.c_double), ("ms_factor", C.c_double),
                 ("flops_left", C.c_double), ("flops_right", C.c_double), ("flops_factor", C.c_double),
-                ("flops_factor_exec", C.c_double)]
+                ("flops_factor_exec", C.c_double), ("flops_dmma", C.c_double)]
 
 
 class SchurOpts(C.Structure):

@@ -54,6 +54,12 @@ cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int d
                                 double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream,
                                 long long rows = -1, long long cols = -1, bool short_ctas = false);
 
+// DMMA instructions the update kernels have issued on the current device so
+// far (bulk-copy kernels: zero Q_w fragments skipped; cp.async kernels); x 512
+// = executed flops.  Synchronous reads (profiling only).
+unsigned long long dmma_count_bulk();
+unsigned long long dmma_count_cp();
+
 // update_tma.cu: false = not eligible (caller falls back), *err = launch status
 bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* S,
                             long long lds, long long rows, long long cols, cudaStream_t stream, cudaError_t* err);

@@ -189,6 +189,7 @@ struct PassResult {
     bool deviated = false;
     double ms_window = 0, ms_left = 0, ms_right = 0, ms_factor = 0;
     double flops_factor_exec = 0;
+    double flops_dmma = 0;
 };
 
 }  // namespace
@@ -270,6 +271,13 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     PassResult pr;
     EventLog lg;
     lg.on = profile || g_trace.on;
+    // profiling: the update kernels' DMMA counters around the pass (device
+    // syncs: a measurement mode)
+    unsigned long long dmma0 = 0;
+    if (profile) {
+        TEIG_CUDA(cudaDeviceSynchronize());
+        dmma0 = dmma_count_bulk() + dmma_count_cp();
+    }
     const int64_t nw = (int64_t)plan.windows.size();
     schedule_levels(plan, n);
     const int32_t nl = plan.n_levels;
@@ -474,6 +482,10 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     for (int32_t st : status) pr.windows += (st & kWinSkipped) ? 0 : 1;  // = entries logged in `plan`
     pr.levels = nl;
     pr.launches = launches;
+    if (profile) {
+        TEIG_CUDA(cudaDeviceSynchronize());
+        pr.flops_dmma = 512.0 * double(dmma_count_bulk() + dmma_count_cp() - dmma0);
+    }
     if (g_trace.on) {  // everything above synchronized: the events are complete
         static const char* kCls[4] = {"W", "L", "R", "Q"};
         for (const auto& m : lg.meta) {
@@ -636,6 +648,7 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
                                      sp.short_factor_ctas(o.overlap_factor != 0),
                                      pass == 0 ? drain : nullptr, &qsupp);
             inf.flops_factor_exec += pr.flops_factor_exec;
+            inf.flops_dmma += pr.flops_dmma;
             inf.n_windows += pr.windows;
             inf.n_levels += pr.levels;
             inf.n_launches += pr.launches;

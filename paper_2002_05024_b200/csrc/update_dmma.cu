@@ -27,6 +27,10 @@
 
 namespace teig {
 
+// DMMA instructions issued by the update kernels of this file (every warp adds
+// its count once, at its end): the profiled drivers report executed flops
+__device__ unsigned long long g_dmma_cp = 0;
+
 namespace {
 
 #ifndef TEIG_UPD_KC
@@ -174,6 +178,7 @@ update_left_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __r
         }
     }
     cp_wait<0>();
+    if (warp_active && (threadIdx.x & 31) == 0) atomicAdd(&g_dmma_cp, (unsigned long long)nk * (KC / 4) * MT * NT);
     // all K of this CTA's panel tile has been consumed: write in place
     if (warp_active) {
 #pragma unroll
@@ -279,6 +284,7 @@ update_right_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __
         }
     }
     cp_wait<0>();
+    if (warp_active && (threadIdx.x & 31) == 0) atomicAdd(&g_dmma_cp, (unsigned long long)nk * (KC / 4) * MT * NT);
     if (warp_active) {
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
@@ -351,6 +357,12 @@ cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int d
             update_right_kernel<128, 1><<<ntiles, kUpdThreads, sm, stream>>>(wins, nwin, qw_pool, M, ldm, nrows_total);
     }
     return cudaGetLastError();
+}
+
+unsigned long long dmma_count_cp() {
+    unsigned long long v = 0;
+    if (cudaMemcpyFromSymbol(&v, g_dmma_cp, sizeof v) != cudaSuccess) cudaGetLastError();
+    return v;
 }
 
 }  // namespace teig

@@ -48,6 +48,10 @@
 
 namespace teig {
 
+// DMMA instructions issued by the bulk update kernels (zero fragments skipped
+// are not counted; every warp adds once, at its end)
+__device__ unsigned long long g_dmma_bulk = 0;
+
 namespace {
 
 constexpr int kWarps = 8;
@@ -258,6 +262,7 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
     const int gid = lane >> 2, tig = lane & 3;
     double af[2][32];
     unsigned nz0 = 0, nz1 = 0;  // bit ks: fragment af[mt][ks] is nonzero in some lane (warp-uniform)
+    unsigned long long ndmma = 0;
     TileWin wd;
     load_win<0>(wd, wins, nwin, wi0);
     int cur = -1, stage = 0, prev = -1;
@@ -297,6 +302,7 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
             const int shift = (int)(((long long)wd.a + (long long)(c + kLSub * sub) * lds) & 1);
             const double* sb = ring + stage * (kLeftStage / 8) + gid * kLdB + tig + shift;
             mbar_wait(&full[stage], phase);
+            ndmma += (unsigned long long)(__popc(nz0) + __popc(nz1)) * (kLSub / 8);
             // Q_w's zero 8x4 fragments (about 45 % of them: a window only mixes
             // the blocks it moves past each other) are skipped -- their products
             // are exact zeros and the sums start at +0, so the bits do not change
@@ -346,7 +352,9 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
                 phase ^= 1u;
             }
         }
-    }    bulk_wait_all();  // the last stores land before the CTA retires
+    }
+    if (lane == 0 && ndmma) atomicAdd(&g_dmma_bulk, ndmma);
+    bulk_wait_all();  // the last stores land before the CTA retires
 }
 
 // ---------------------------------------------------------------------------
@@ -406,6 +414,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
     const int gid = lane >> 2, tig = lane & 3;
     double bf[2][32];
     unsigned nz0 = 0, nz1 = 0;  // bit ks: fragment bf[nt][ks] is nonzero in some lane (warp-uniform)
+    unsigned long long ndmma = 0;
     TileWin wd;
     load_win<Field>(wd, wins, nwin, wi0);
     int cur = -1, stage = 0;
@@ -445,6 +454,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
             const int shift = (int)(((long long)r0 + kRSub * sub + (long long)wd.a * ldm) & 1);
             const double* sa = ring + stage * (kRightStage / 8) + tig * kLdA + gid + shift;
             mbar_wait(&full[stage], phase);
+            ndmma += (unsigned long long)(__popc(nz0) + __popc(nz1)) * (kRSub / 8);
             // zero fragments of Q_w skipped (exact: see the left kernel)
 #pragma unroll
             for (int ks = 0; ks < 32; ++ks) {
@@ -482,6 +492,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
             }
         }
     }
+    if (lane == 0 && ndmma) atomicAdd(&g_dmma_bulk, ndmma);
 }
 
 // ---------------------------------------------------------------------------
@@ -546,6 +557,12 @@ bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax
                                                                                  alloc);
     *err = cudaGetLastError();
     return true;
+}
+
+unsigned long long dmma_count_bulk() {
+    unsigned long long v = 0;
+    if (cudaMemcpyFromSymbol(&v, g_dmma_bulk, sizeof v) != cudaSuccess) cudaGetLastError();
+    return v;
 }
 
 }  // namespace teig
