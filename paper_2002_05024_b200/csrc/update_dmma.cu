@@ -154,6 +154,7 @@ update_left_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __r
     const int m_base = wm * (MT * 8);
     const int n_base = wn * (NT * 8);
     const bool warp_active = m_base < d;
+    int nlive = 0;  // executed fragment rows (DMMA count / NT)
     for (int kc = 0; kc < nk; ++kc) {
         cp_wait<STAGES - 2>();
         __syncthreads();
@@ -170,15 +171,22 @@ update_left_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __r
                 for (int i = 0; i < MT; ++i) af[i] = as[(m_base + i * 8 + gid) * LDK + ks + tig];
 #pragma unroll
                 for (int j = 0; j < NT; ++j) bf[j] = bs[(n_base + j * 8 + gid) * LDK + ks + tig];
+                // all-zero 8x4 fragments of Q_w^T contribute exact zeros: skip
+                // them (warp-uniform vote; the sums start at +0, bitwise equal)
+                unsigned live = 0;
+#pragma unroll
+                for (int i = 0; i < MT; ++i) live |= (__any_sync(0xffffffffu, af[i] != 0.0) ? 1u : 0u) << i;
+                nlive += __popc(live);
 #pragma unroll
                 for (int i = 0; i < MT; ++i)
+                    if (live >> i & 1u)
 #pragma unroll
-                    for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                        for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
             }
         }
     }
     cp_wait<0>();
-    if (warp_active && (threadIdx.x & 31) == 0) atomicAdd(&g_dmma_cp, (unsigned long long)nk * (KC / 4) * MT * NT);
+    if (warp_active && (threadIdx.x & 31) == 0) atomicAdd(&g_dmma_cp, (unsigned long long)nlive * NT);
     // all K of this CTA's panel tile has been consumed: write in place
     if (warp_active) {
 #pragma unroll
@@ -260,6 +268,7 @@ update_right_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __
     const int m_base = wm * (MT * 8);
     const int n_base = wn * (NT * 8);
     const bool warp_active = (n_base < d) && (m_base < nrows);
+    int nlive = 0;  // executed fragment columns (DMMA count / MT)
     for (int kc = 0; kc < nk; ++kc) {
         cp_wait<STAGES - 2>();
         __syncthreads();
@@ -276,15 +285,20 @@ update_right_kernel(const WinDesc* __restrict__ wins, int nwin, const double* __
                 for (int i = 0; i < MT; ++i) af[i] = as[(ks + tig) * LDM + m_base + i * 8 + gid];
 #pragma unroll
                 for (int j = 0; j < NT; ++j) bf[j] = bs[(n_base + j * 8 + gid) * LDK + ks + tig];
+                unsigned live = 0;  // zero Q_w fragments skipped, as in the left kernel
 #pragma unroll
-                for (int i = 0; i < MT; ++i)
+                for (int j = 0; j < NT; ++j) live |= (__any_sync(0xffffffffu, bf[j] != 0.0) ? 1u : 0u) << j;
+                nlive += __popc(live);
 #pragma unroll
-                    for (int j = 0; j < NT; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                for (int j = 0; j < NT; ++j)
+                    if (live >> j & 1u)
+#pragma unroll
+                        for (int i = 0; i < MT; ++i) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
             }
         }
     }
     cp_wait<0>();
-    if (warp_active && (threadIdx.x & 31) == 0) atomicAdd(&g_dmma_cp, (unsigned long long)nk * (KC / 4) * MT * NT);
+    if (warp_active && (threadIdx.x & 31) == 0) atomicAdd(&g_dmma_cp, (unsigned long long)nlive * MT);
     if (warp_active) {
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
