@@ -11,10 +11,11 @@
 // transposition: every step swaps ALL adjacent (unselected, selected & not
 // stuck) block pairs at once -- their transformations act on disjoint index
 // sets and commute.  A step is four barrier-separated phases:
-//   1. warp 0 lists the pairs;
-//   2. one thread per pair decides the swap (gswap_math.cuh: generalized
-//      Sylvester + QR of the deflating-subspace bases, DTGEX2 semantics),
-//      pairs grouped by block-size type so each warp runs one code path;
+//   1. warp 0 lists the pairs (ballot ranks, shuffle scan of the row starts);
+//   2. one WARP per pair decides the swap (gswap_warp.cuh: generalized
+//      Sylvester + QR of the deflating-subspace bases, DTGEX2 semantics,
+//      the elimination and products spread over the lanes), pairs
+//      round-robin over the 8 warps;
 //   3. rows of every pair (S and T, columns right of the block) <- Q_m^T;
 //   4. columns of every pair (S and T rows above; all rows of Q_w / Z_w)
 //      <- Q_m / Z_m, and the new diagonal blocks;
@@ -26,7 +27,7 @@
 #include <type_traits>
 
 #include "device_types.h"
-#include "gswap_math.cuh"
+#include "gswap_warp.cuh"
 #include "launch.h"
 
 namespace teig {
@@ -46,38 +47,19 @@ struct GPair {
 struct GShared {
     uint8_t arr[kGMaxBlocks], bsz[kGMaxBlocks], bsel[kGMaxBlocks], bstuck[kGMaxBlocks];
     GPair pairs[kGMaxPairs];
-    int16_t tlist[4][kGMaxPairs];
-    int tcnt[4];
     int npairs;
     int executed;
     int skipped;
     double Qm[kGMaxPairs][16], Zm[kGMaxPairs][16], An[kGMaxPairs][16], Bn[kGMaxPairs][16];
+    GSwapScratch ws[kGThreads / 32];
 };
 
 template <int P, int Q>
-__device__ __forceinline__ void decide(const double* Sw, const double* Tw, int ld, GPair& pr, double* Qo, double* Zo,
-                                       double* Ao, double* Bo) {
-    constexpr int D = P + Q;
-    double A[D][D], B[D][D], Qm[D][D], Zm[D][D], An[D][D], Bn[D][D];
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            A[i][j] = Sw[(pr.pos + i) + (pr.pos + j) * ld];
-            B[i][j] = Tw[(pr.pos + i) + (pr.pos + j) * ld];
-        }
-    const bool ok = gswap<P, Q>(A, B, Qm, Zm, An, Bn);
-    pr.ok = ok ? 1 : 0;
-    if (!ok) return;
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-#pragma unroll
-        for (int j = 0; j < D; ++j) {
-            Qo[i * D + j] = Qm[i][j];
-            Zo[i * D + j] = Zm[i][j];
-            Ao[i * D + j] = An[i][j];
-            Bo[i * D + j] = Bn[i][j];
-        }
+__device__ __forceinline__ void decide(GShared& sh, const double* Sw, const double* Tw, int ld, int pi, int lane,
+                                       GSwapScratch& ws) {
+    GPair& pr = sh.pairs[pi];
+    const bool ok = wgswap<P, Q>(Sw, Tw, ld, pr.pos, ws, lane, sh.Qm[pi], sh.Zm[pi], sh.An[pi], sh.Bn[pi]);
+    if (lane == 0) pr.ok = ok ? 1 : 0;
 }
 
 // rows pos.. of M (ld), columns [pos+D, d) <- U^T rows  (lanes over columns)
@@ -148,6 +130,54 @@ __device__ __forceinline__ void pair_phase_cols(GShared& sh, double* Sw, double*
     }
 }
 
+// warp 0: every adjacent (unselected, selected & not stuck) slot pair of the
+// current arrangement.  Two candidates never overlap (the upper block of one
+// is unselected, the lower of the other selected), so all slots are tested
+// at once: a ballot ranks the pairs, a shuffle scan gives the row starts.
+__device__ __forceinline__ void gfind_pairs(GShared& sh, int nb, int lane) {
+    int loc[2], sum = 0;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const int s = lane * 2 + k;
+        loc[k] = (s < nb) ? sh.bsz[sh.arr[s]] : 0;
+        sum += loc[k];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const int r0 = incl - sum;
+    bool cand[2];
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {  // slot s = 2 lane + k
+        const int s = lane * 2 + k;
+        cand[k] = s + 1 < nb && !sh.bsel[sh.arr[s]] && sh.bsel[sh.arr[s + 1]] && !sh.bstuck[sh.arr[s + 1]];
+    }
+    const unsigned c0 = __ballot_sync(0xffffffffu, cand[0]), c1 = __ballot_sync(0xffffffffu, cand[1]);
+    const int np = __popc(c0) + __popc(c1);
+    const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (!cand[k]) continue;
+        const int s = lane * 2 + k;
+        // rank in slot order: both slots of the lower lanes, and slot 2 lane before 2 lane + 1
+        const int idx = __popc(c0 & below) + __popc(c1 & below) + (k == 1 && cand[0] ? 1 : 0);
+        const int u = sh.arr[s], b = sh.arr[s + 1];
+        GPair pr;
+        pr.pos = (int16_t)(r0 + (k == 1 ? loc[0] : 0));
+        pr.slot = (int16_t)s;
+        pr.p = (int8_t)sh.bsz[u];
+        pr.q = (int8_t)sh.bsz[b];
+        pr.ok = 0;
+        pr.pad = 0;
+        sh.pairs[idx] = pr;
+    }
+    if (lane == 0) sh.npairs = np;
+    __syncwarp();
+}
+
 }  // namespace
 
 __global__ void __launch_bounds__(kGThreads, 1)
@@ -199,45 +229,17 @@ gwindow_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S,
     __syncthreads();
     if (sh.executed) {
         for (;;) {
-            if (warp == 0) {  // list the pairs
-                if (lane == 0) {
-                    int np = 0, row = 0;
-                    for (int t = 0; t < 4; ++t) sh.tcnt[t] = 0;
-                    for (int s = 0; s + 1 < nb; ++s) {
-                        const int u = sh.arr[s], b = sh.arr[s + 1];
-                        if (!sh.bsel[u] && sh.bsel[b] && !sh.bstuck[b] && np < kGMaxPairs) {
-                            GPair pr;
-                            pr.pos = (int16_t)row;
-                            pr.slot = (int16_t)s;
-                            pr.p = (int8_t)sh.bsz[u];
-                            pr.q = (int8_t)sh.bsz[b];
-                            pr.ok = 0;
-                            pr.pad = 0;
-                            sh.pairs[np] = pr;
-                            const int ty = (pr.p - 1) * 2 + (pr.q - 1);
-                            sh.tlist[ty][sh.tcnt[ty]++] = (int16_t)np;
-                            ++np;
-                            row += sh.bsz[u] + sh.bsz[b];
-                            ++s;  // the pair's two slots are taken
-                        } else {
-                            row += sh.bsz[u];
-                        }
-                    }
-                    sh.npairs = np;
-                }
-            }
+            if (warp == 0) gfind_pairs(sh, nb, lane);  // list the pairs
             __syncthreads();
             const int np = sh.npairs;
             if (np == 0) break;
-            if (warp < 4)  // decisions, one code path per warp
-                for (int li = lane; li < sh.tcnt[warp]; li += 32) {
-                    const int pi = sh.tlist[warp][li];
-                    GPair& pr = sh.pairs[pi];
-                    if (warp == 0) decide<1, 1>(Sw, Tw, ld, pr, sh.Qm[pi], sh.Zm[pi], sh.An[pi], sh.Bn[pi]);
-                    else if (warp == 1) decide<1, 2>(Sw, Tw, ld, pr, sh.Qm[pi], sh.Zm[pi], sh.An[pi], sh.Bn[pi]);
-                    else if (warp == 2) decide<2, 1>(Sw, Tw, ld, pr, sh.Qm[pi], sh.Zm[pi], sh.An[pi], sh.Bn[pi]);
-                    else decide<2, 2>(Sw, Tw, ld, pr, sh.Qm[pi], sh.Zm[pi], sh.An[pi], sh.Bn[pi]);
-                }
+            for (int pi = warp; pi < np; pi += NW) {  // decisions, one warp per pair
+                const GPair pr = sh.pairs[pi];
+                if (pr.p == 1 && pr.q == 1) decide<1, 1>(sh, Sw, Tw, ld, pi, lane, sh.ws[warp]);
+                else if (pr.p == 1) decide<1, 2>(sh, Sw, Tw, ld, pi, lane, sh.ws[warp]);
+                else if (pr.q == 1) decide<2, 1>(sh, Sw, Tw, ld, pi, lane, sh.ws[warp]);
+                else decide<2, 2>(sh, Sw, Tw, ld, pi, lane, sh.ws[warp]);
+            }
             __syncthreads();
             for (int pi = warp; pi < np; pi += NW) {
                 const GPair pr = sh.pairs[pi];
@@ -257,17 +259,16 @@ gwindow_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S,
                 else pair_phase_cols<4>(sh, Sw, Tw, Qw, Zw, ld, d, pi, lane);
             }
             __syncthreads();
-            if (tid == 0)
-                for (int pi = 0; pi < np; ++pi) {
-                    const GPair pr = sh.pairs[pi];
-                    const int u = sh.arr[pr.slot], b = sh.arr[pr.slot + 1];
-                    if (pr.ok) {
-                        sh.arr[pr.slot] = (uint8_t)b;
-                        sh.arr[pr.slot + 1] = (uint8_t)u;
-                    } else {
-                        sh.bstuck[b] = 1;
-                    }
+            if (tid < np) {  // commit: the pairs own disjoint slots
+                const GPair pr = sh.pairs[tid];
+                const int u = sh.arr[pr.slot], b = sh.arr[pr.slot + 1];
+                if (pr.ok) {
+                    sh.arr[pr.slot] = (uint8_t)b;
+                    sh.arr[pr.slot + 1] = (uint8_t)u;
+                } else {
+                    sh.bstuck[b] = 1;
                 }
+            }
             __syncthreads();
         }
     }
