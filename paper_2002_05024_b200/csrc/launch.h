@@ -42,9 +42,11 @@ constexpr int kWindowThreads = 256;  // threads of the window kernel (8 warps)
 // rows/cols: the extent of the matrix `S`/`M` points at (absolute indices
 // [0, rows) x [0, cols)); when given, windows of order 65..128 take the TMA
 // kernels of update_tma.cu, otherwise (or for slab bases) the cp.async ones.
+// max_ctas > 0 caps the persistent grid of the bulk kernels (the caller keeps
+// SMs free for window kernels running beside the launch)
 cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
                                double* S, long long lds, int n, cudaStream_t stream, long long rows = -1,
-                               long long cols = -1);
+                               long long cols = -1, int max_ctas = 0);
 
 // short_ctas: launch the bulk factor kernel as short CTAs (8 tiles each)
 // instead of a persistent grid -- for a caller that runs the factor updates on
@@ -52,7 +54,7 @@ cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dm
 // as they free up.
 cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
                                 double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream,
-                                long long rows = -1, long long cols = -1, bool short_ctas = false);
+                                long long rows = -1, long long cols = -1, bool short_ctas = false, int max_ctas = 0);
 
 // DMMA instructions the update kernels have issued on the current device so
 // far (bulk-copy kernels: zero Q_w fragments skipped; cp.async kernels); x 512
@@ -62,10 +64,11 @@ unsigned long long dmma_count_cp();
 
 // update_tma.cu: false = not eligible (caller falls back), *err = launch status
 bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* S,
-                            long long lds, long long rows, long long cols, cudaStream_t stream, cudaError_t* err);
+                            long long lds, long long rows, long long cols, cudaStream_t stream, cudaError_t* err,
+                            int max_ctas = 0);
 bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* M,
                              long long ldm, long long rows, long long cols, bool factor, cudaStream_t stream,
-                             cudaError_t* err, bool short_ctas = false);
+                             cudaError_t* err, bool short_ctas = false, int max_ctas = 0);
 
 
 // synthetic inputs (generate.cu)

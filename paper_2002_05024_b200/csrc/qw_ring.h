@@ -57,6 +57,22 @@ inline QwRing make_qw_ring(std::vector<WinDesc>& descs, const std::vector<int64_
     return r;
 }
 
+// a set of timing-free events (RAII)
+struct StreamEvents {
+    std::vector<cudaEvent_t> ev;
+    explicit StreamEvents(int k) {
+        ev.assign(k, nullptr);
+        for (auto& e : ev) {
+            cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            if (err != cudaSuccess) throw std::runtime_error(std::string("CUDA error ") + cudaGetErrorString(err));
+        }
+    }
+    ~StreamEvents() {
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+    }
+};
+
 // one event per ring region (recorded after the region's last off-stream reader)
 struct RingEvents {
     int n = 0;

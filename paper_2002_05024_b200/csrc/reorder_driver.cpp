@@ -267,7 +267,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                     std::vector<BlockState>& blocks, std::vector<int64_t>& rejected,
                     std::vector<int64_t>& plan_log, bool strict, bool overlap, bool profile,
                     cudaStream_t stream, cudaStream_t stream2, cudaEvent_t ev, bool short_q,
-                    HostDrain* drain = nullptr, FactorSupport* qsupp = nullptr) {
+                    HostDrain* drain = nullptr, FactorSupport* qsupp = nullptr, cudaStream_t stream3 = nullptr) {
     PassResult pr;
     EventLog lg;
     lg.on = profile || g_trace.on;
@@ -327,6 +327,92 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
     // already ordered before it on the critical-path stream)
     const QwRing ring = make_qw_ring(descs, lvl_off, nl, 1);
     qw_total = ring.total;
+    // Look-ahead (overlap mode): the S updates of level L split into the tiles
+    // that touch a level-(L+1) window's diagonal block -- "critical", run on
+    // the window stream right after window L -- and the rest -- "bulk", on a
+    // third stream, concurrently with window L+1 (on SMs the capped bulk grid
+    // leaves free).  A window's right panel meets a next-level window W' only
+    // in rows [a', a) when W' straddles a, its left panel only in columns
+    // [b, b') when W' straddles b, so each window's critical part is one row
+    // range of its right update and one column range of its left update (the
+    // hull over the next-level windows it overlaps).  Every S element still
+    // receives its updates in level order (critical L+1 waits for bulk L) and,
+    // within a level, left before right (below); a row / column of an update
+    // does not depend on how the rows / columns are tiled: the result is bit
+    // for bit the serial order's.
+    // TEIG_NO_LOOKAHEAD=1: the serial order.
+    const bool no_la = getenv("TEIG_NO_LOOKAHEAD") && atoi(getenv("TEIG_NO_LOOKAHEAD"));  // read per pass (tests toggle it)
+    const bool lookahead = overlap && stream3 && !no_la && nl > 1;
+    std::vector<WinDesc> cdesc, bdesc;
+    std::vector<int64_t> ctl(nl, 0), ctr(nl, 0), btl(nl, 0), btr(nl, 0);
+    std::vector<int> bulk_cap(nl, 0);
+    if (lookahead) {
+        cdesc = descs;
+        bdesc = descs;
+        const int sms = device_sm_count();
+        std::vector<std::pair<int32_t, int32_t>> nx;
+        for (int L = 0; L < nl; ++L) {
+            nx.clear();
+            if (L + 1 < nl)
+                for (int64_t k = lvl_off[L + 1]; k < lvl_off[L + 2]; ++k)
+                    nx.push_back({descs[k].a, descs[k].a + descs[k].d});
+            std::sort(nx.begin(), nx.end());  // disjoint: also sorted by end
+            const int64_t k0 = lvl_off[L], k1 = lvl_off[L + 1];
+            std::vector<int32_t> xs(k1 - k0), ys(k1 - k0);
+            for (int64_t k = k0; k < k1; ++k) {
+                const int32_t a = descs[k].a, b = descs[k].a + descs[k].d;
+                int32_t x = a, y = b;
+                auto it = std::partition_point(nx.begin(), nx.end(),
+                                               [&](const std::pair<int32_t, int32_t>& w) { return w.second <= a; });
+                for (; it != nx.end() && it->first < b; ++it) {
+                    x = std::min(x, it->first);
+                    y = std::max(y, it->second);
+                }
+                xs[k - k0] = x;
+                ys[k - k0] = y;
+            }
+            // same-level order: an element where window V's left panel meets
+            // window W's right panel gets V's left update before W's right
+            // one (the serial launch order; the two commute only up to
+            // rounding).  W's critical right rows [x_W, a_W) run before the
+            // bulk left updates, so every V whose rows they reach takes the
+            // columns up to b_W into its critical left range.
+            for (int64_t k = k0; k < k1; ++k) {
+                const int32_t aw = descs[k].a, bw = aw + descs[k].d, xw = xs[k - k0];
+                if (xw >= aw) continue;
+                for (int64_t v = k0; v < k1; ++v) {
+                    const int32_t av = descs[v].a, bv = av + descs[v].d;
+                    if (bv <= aw && bv > xw) ys[v - k0] = std::max(ys[v - k0], bw);
+                }
+            }
+            for (int64_t k = k0; k < k1; ++k) {
+                const int32_t a = descs[k].a, b = descs[k].a + descs[k].d;
+                const int32_t x = xs[k - k0], y = std::min<int32_t>(ys[k - k0], (int32_t)n);
+                WinDesc& c = cdesc[k];
+                WinDesc& u = bdesc[k];
+                c.lc0 = b;
+                c.lc1 = y;
+                c.rr0 = x;
+                c.rr1 = a;
+                u.lc0 = y;
+                u.lc1 = (int32_t)n;
+                u.rr0 = 0;
+                u.rr1 = x;
+                c.tl_pref = (int32_t)ctl[L];
+                c.tr_pref = (int32_t)ctr[L];
+                u.tl_pref = (int32_t)btl[L];
+                u.tr_pref = (int32_t)btr[L];
+                ctl[L] += (y - b + kLeftBN - 1) / kLeftBN;
+                ctr[L] += (a - x + kRightBM - 1) / kRightBM;
+                btl[L] += (n - y + kLeftBN - 1) / kLeftBN;
+                btr[L] += (x + kRightBM - 1) / kRightBM;
+            }
+            if (L + 1 < nl) {  // keep SMs free for the next level's window CTAs
+                const int64_t nwn = lvl_off[L + 2] - lvl_off[L + 1];
+                if (nwn <= sms / 2) bulk_cap[L] = sms - (int)nwn;
+            }
+        }
+    }
     // early host drain: max b / min a over the levels after L
     std::vector<int64_t> after_hi, after_lo;
     if (drain && drain->valid) {
@@ -348,6 +434,14 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         d_status(sizeof(int32_t) * nw, stream), d_devlvl(sizeof(int32_t), stream);
     TEIG_CUDA(cudaMemsetAsync(d_devlvl.p, 0x7f, sizeof(int32_t), stream));
     TEIG_CUDA(cudaMemcpyAsync(d_desc.p, descs.data(), sizeof(WinDesc) * nw, cudaMemcpyHostToDevice, stream));
+    DevBuf d_cdesc(lookahead ? sizeof(WinDesc) * nw : 0, stream), d_bdesc(lookahead ? sizeof(WinDesc) * nw : 0, stream);
+    StreamEvents la_ev(lookahead ? 2 : 0);  // [0] critical(L) done, [1] bulk(L) done
+    if (lookahead) {
+        TEIG_CUDA(cudaMemcpyAsync(d_cdesc.p, cdesc.data(), sizeof(WinDesc) * nw, cudaMemcpyHostToDevice, stream));
+        TEIG_CUDA(cudaMemcpyAsync(d_bdesc.p, bdesc.data(), sizeof(WinDesc) * nw, cudaMemcpyHostToDevice, stream));
+        TEIG_CUDA(cudaEventRecord(la_ev.ev[0], stream));  // the third stream starts after the uploads
+        TEIG_CUDA(cudaStreamWaitEvent(stream3, la_ev.ev[0], 0));
+    }
     TEIG_CUDA(cudaMemcpyAsync(d_sizes.p, plan.sizes.data(), ne, cudaMemcpyHostToDevice, stream));
     TEIG_CUDA(cudaMemcpyAsync(d_sel.p, plan.sel.data(), ne, cudaMemcpyHostToDevice, stream));
 
@@ -398,14 +492,39 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
             });
             if (ring_ev.n) TEIG_CUDA(cudaEventRecord(ring_ev.ev[L % ring.k], stream2));
         }
-        timed(1, stream, tl[L], [&] {
-            return launch_update_left(dd + o, (int)cnt, (int)tl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n, stream,
-                                      n, n);
-        });
-        timed(2, stream, tr[L], [&] {
-            return launch_update_right(dd + o, (int)cnt, (int)tr[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n, false,
-                                       stream, n, n);
-        });
+        if (lookahead) {
+            const WinDesc* cd = d_cdesc.as<WinDesc>() + o;
+            const WinDesc* bd = d_bdesc.as<WinDesc>() + o;
+            if (L > 0) TEIG_CUDA(cudaStreamWaitEvent(stream, la_ev.ev[1], 0));  // bulk(L-1) before critical(L)
+            timed(1, stream, ctl[L], [&] {
+                return launch_update_left(cd, (int)cnt, (int)ctl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
+                                          stream, n, n);
+            });
+            timed(2, stream, ctr[L], [&] {
+                return launch_update_right(cd, (int)cnt, (int)ctr[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
+                                           false, stream, n, n);
+            });
+            TEIG_CUDA(cudaEventRecord(la_ev.ev[0], stream));
+            TEIG_CUDA(cudaStreamWaitEvent(stream3, la_ev.ev[0], 0));
+            timed(1, stream3, btl[L], [&] {
+                return launch_update_left(bd, (int)cnt, (int)btl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
+                                          stream3, n, n, bulk_cap[L]);
+            });
+            timed(2, stream3, btr[L], [&] {
+                return launch_update_right(bd, (int)cnt, (int)btr[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
+                                           false, stream3, n, n, false, bulk_cap[L]);
+            });
+            TEIG_CUDA(cudaEventRecord(la_ev.ev[1], stream3));
+        } else {
+            timed(1, stream, tl[L], [&] {
+                return launch_update_left(dd + o, (int)cnt, (int)tl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
+                                          stream, n, n);
+            });
+            timed(2, stream, tr[L], [&] {
+                return launch_update_right(dd + o, (int)cnt, (int)tr[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
+                                           false, stream, n, n);
+            });
+        }
         if (dQ && !overlap)
             timed(3, stream, tq[L], [&] {
                 return launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
@@ -414,7 +533,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         if (drain && drain->valid && L + 1 < nl) {
             const int64_t hi = after_hi[L + 1], lo = after_lo[L + 1];
             if (drain->s_hi - hi >= drain->min_chunk) {  // S rows [hi, s_hi): final after this level's S work
-                TEIG_CUDA(cudaEventRecord(drain->evS, stream));
+                TEIG_CUDA(cudaEventRecord(drain->evS, lookahead ? stream3 : stream));
                 TEIG_CUDA(cudaStreamWaitEvent(drain->ds, drain->evS, 0));
                 TEIG_CUDA(cudaMemcpy2DAsync(drain->hS + hi, drain->lds * sizeof(double), dS + hi, lds * sizeof(double),
                                             (size_t)(drain->s_hi - hi) * sizeof(double), (size_t)n,
@@ -447,6 +566,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         TEIG_CUDA(cudaEventRecord(ev, stream2));
         TEIG_CUDA(cudaStreamWaitEvent(stream, ev, 0));
     }
+    if (lookahead) TEIG_CUDA(cudaStreamWaitEvent(stream, la_ev.ev[1], 0));  // the last bulk updates
     // one readback of all window outcomes
     std::vector<int32_t> status(nw);
     std::vector<uint8_t> order(ne + 1), stuck(ne + 1);
@@ -521,7 +641,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
 // the destructor joins both internal streams into the caller's stream before
 // releasing them, so no enqueued work outlives the call unordered.
 struct StreamPair {
-    cudaStream_t s1 = nullptr, s2 = nullptr, caller = nullptr;
+    cudaStream_t s1 = nullptr, s2 = nullptr, s3 = nullptr, caller = nullptr;
     cudaEvent_t ev = nullptr, join = nullptr;
     bool prio = true;
     explicit StreamPair(cudaStream_t user) : s1(user), caller(user) {
@@ -530,6 +650,8 @@ struct StreamPair {
             int least = 0, greatest = 0;
             TEIG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
             TEIG_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, prio ? least : 0));
+            // the look-ahead S updates (run_pass): between the two
+            TEIG_CUDA(cudaStreamCreateWithPriority(&s3, cudaStreamNonBlocking, prio ? (least + greatest) / 2 : 0));
             TEIG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             TEIG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
             if (prio) {
@@ -556,14 +678,16 @@ struct StreamPair {
         // join (errors ignored: this also runs on the error path)
         if (join) {
             if (s2 && cudaEventRecord(join, s2) == cudaSuccess) cudaStreamWaitEvent(caller, join, 0);
+            if (s3 && cudaEventRecord(join, s3) == cudaSuccess) cudaStreamWaitEvent(caller, join, 0);
             if (s1 && s1 != caller && cudaEventRecord(join, s1) == cudaSuccess) cudaStreamWaitEvent(caller, join, 0);
         }
         if (ev) cudaEventDestroy(ev);
         if (join) cudaEventDestroy(join);
         if (s2) cudaStreamDestroy(s2);
+        if (s3) cudaStreamDestroy(s3);
         if (s1 && s1 != caller) cudaStreamDestroy(s1);
         ev = join = nullptr;
-        s2 = nullptr;
+        s2 = s3 = nullptr;
         s1 = caller;
         cudaGetLastError();
     }
@@ -646,7 +770,7 @@ int reorder_schur_device(int64_t n, double* dS, int64_t lds, double* dQ, int64_t
             PassResult pr = run_pass(plan, n, dS, lds, dQ, ldq, blocks, rejected, plan_log, o.strict != 0,
                                      o.overlap_factor != 0, o.profile != 0, sp.s1, sp.s2, sp.ev,
                                      sp.short_factor_ctas(o.overlap_factor != 0),
-                                     pass == 0 ? drain : nullptr, &qsupp);
+                                     pass == 0 ? drain : nullptr, &qsupp, sp.s3);
             inf.flops_factor_exec += pr.flops_factor_exec;
             inf.flops_dmma += pr.flops_dmma;
             inf.n_windows += pr.windows;

@@ -323,11 +323,13 @@ constexpr size_t left_smem(int dmax) { return (size_t)STAGES * (dmax * LDK + kLe
 constexpr size_t right_smem(int dmax) { return (size_t)STAGES * (KC * (kRightBM + 4) + dmax * LDK) * sizeof(double); }
 
 cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
-                               double* S, long long lds, int n, cudaStream_t stream, long long rows, long long cols) {
+                               double* S, long long lds, int n, cudaStream_t stream, long long rows, long long cols,
+                               int max_ctas) {
     if (ntiles <= 0) return cudaSuccess;
     if (rows > 0) {
         cudaError_t err;
-        if (launch_update_left_tma(wins, nwin, ntiles, dmax, qw_pool, S, lds, rows, cols, stream, &err)) return err;
+        if (launch_update_left_tma(wins, nwin, ntiles, dmax, qw_pool, S, lds, rows, cols, stream, &err, max_ctas))
+            return err;
     }
     {
         cudaError_t e = set_smem(update_left_kernel<64>, left_smem(64));
@@ -343,12 +345,12 @@ cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dm
 
 cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
                                 double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream,
-                                long long rows, long long cols, bool short_ctas) {
+                                long long rows, long long cols, bool short_ctas, int max_ctas) {
     if (ntiles <= 0) return cudaSuccess;
     if (rows > 0) {
         cudaError_t err;
         if (launch_update_right_tma(wins, nwin, ntiles, dmax, qw_pool, M, ldm, rows, cols, factor, stream, &err,
-                                    short_ctas))
+                                    short_ctas, max_ctas))
             return err;
     }
     {

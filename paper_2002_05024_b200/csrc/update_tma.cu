@@ -522,13 +522,14 @@ bool bulk_eligible(int dmax, const double* base, long long ld, long long rows, l
 }  // namespace
 
 bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* S,
-                            long long lds, long long rows, long long cols, cudaStream_t stream, cudaError_t* err) {
+                            long long lds, long long rows, long long cols, cudaStream_t stream, cudaError_t* err,
+                            int max_ctas) {
     *err = cudaSuccess;
     if (ntiles <= 0) return true;
     if (!bulk_eligible(dmax, S, lds, rows, cols)) return false;
     *err = ensure_dyn_smem((const void*)update_left_bulk_kernel, kLeftSmem);
     if (*err != cudaSuccess) return true;
-    const int grid = grid_for(ntiles);
+    const int grid = max_ctas > 0 ? std::min(grid_for(ntiles), max_ctas) : grid_for(ntiles);
     update_left_bulk_kernel<<<grid, kBulkThreads, kLeftSmem, stream>>>(wins, nwin, ntiles, qw_pool, S, lds,
                                                                         (cols - 1) * lds + rows);
     *err = cudaGetLastError();
@@ -537,7 +538,7 @@ bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax,
 
 bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* M,
                              long long ldm, long long rows, long long cols, bool factor, cudaStream_t stream,
-                             cudaError_t* err, bool short_ctas) {
+                             cudaError_t* err, bool short_ctas, int max_ctas) {
     *err = cudaSuccess;
     if (ntiles <= 0) return true;
     if (!bulk_eligible(dmax, M, ldm, rows, cols)) return false;
@@ -547,7 +548,8 @@ bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax
     // short_ctas: the caller runs these updates on a low-priority stream beside
     // the critical path -- CTAs of 8 tiles, so critical-path CTAs can take SMs
     // as they free up; otherwise a persistent grid
-    const int grid = short_ctas ? (ntiles + 7) / 8 : grid_for(ntiles);
+    int grid = short_ctas ? (ntiles + 7) / 8 : grid_for(ntiles);
+    if (max_ctas > 0 && !short_ctas) grid = std::min(grid, max_ctas);
     const long long alloc = (cols - 1) * ldm + rows;
     if (factor)
         update_right_bulk_kernel<2><<<grid, kBulkThreads, kRightSmem, stream>>>(wins, nwin, ntiles, qw_pool, M, ldm,
