@@ -36,8 +36,13 @@
 // a cuTensorMapEncodeTiled descriptor included -- faults with an illegal
 // instruction while 1-D bulk copies work; tools/microbench/tma_min.cu.)
 //
-// Used for windows of order 65..128 on a matrix whose leading dimension is
-// even and whose base is 16-byte aligned; other calls take update_dmma.cu.
+// Used for windows of order <= 128 on a matrix whose leading dimension is
+// even and whose base is 16-byte aligned (other calls take update_dmma.cu),
+// in two instantiations: order 65..128 (one CTA of 8 warps per SM, 255
+// registers: 64 Q_w fragments per lane) and order <= 64 (the generalized
+// reorder's windows, C5: half the fragments and rows, two CTAs per SM so one
+// CTA's barriers and refills overlap the other's DMMAs; TEIG_NO_BULK64=1
+// sends these windows to the cp.async kernels).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -61,13 +66,35 @@ constexpr int kMinTilesPerCta = 4;  // below this the launch gets more, shorter 
 #define TEIG_LSUB 64
 #endif
 constexpr int kLSub = TEIG_LSUB;                // left: columns per sub-tile
-constexpr int kLStages = kLSub == 64 ? 3 : 4;   // left: ring depth
-constexpr int kLdB = 132;        // left: doubles per panel column in smem (<= 129 rows used, = 4 mod 16)
 constexpr int kRSub = 64;        // right: rows per sub-tile (the whole planner tile)
-constexpr int kRStages = 3;      // right: ring depth
 constexpr int kLdA = 72;         // right: doubles per panel column in smem (<= kRSub+1 rows used, = 8 mod 16)
-constexpr int kLeftStage = kLSub * kLdB * 8;  // kLSub columns x 128(+1) rows
-constexpr int kRightStage = 128 * kLdA * 8;  // 128 columns x kRSub(+1) rows
+
+// Window-order classes: DW = 128 (windows of order 65..128) or 64 (<= 64).
+// Left: warps tile the DW output rows in 16-row slices (DW / 16 of them) and
+// split the sub-tile's columns among the rest; right: DW / 16 slices of 16
+// output columns, the sub-tile's rows split among the rest.  Q_w fragments
+// in registers: 2 x DW / 4 per lane.
+template <int DW>
+struct LeftCfg {
+    static constexpr int kLd = DW == 128 ? 132 : 68;  // doubles per panel column in smem (<= DW+1 used, = 4 mod 16)
+    static constexpr int kStages = kLSub == 64 ? 3 : 4;
+    static constexpr int kStage = kLSub * kLd * 8;    // bytes: kLSub columns x DW(+1) rows
+    static constexpr int kMGroups = DW / 16;          // warps along the rows
+    static constexpr int kNSplit = kWarps / kMGroups; // warps along the sub-tile's columns
+    static constexpr int kNT = kLSub / 8 / kNSplit;   // 8-column tiles per warp
+    static constexpr int kKS = DW / 4;                // k-steps of 4
+    static constexpr size_t kSmem = (size_t)kStages * kStage;
+};
+template <int DW>
+struct RightCfg {
+    static constexpr int kStages = 3;
+    static constexpr int kStage = DW * kLdA * 8;      // bytes: DW columns x kRSub(+1) rows
+    static constexpr int kNGroups = DW / 16;          // warps along the output columns
+    static constexpr int kMSplit = kWarps / kNGroups; // warps along the sub-tile's rows
+    static constexpr int kMT = kRSub / 8 / kMSplit;   // 8-row tiles per warp
+    static constexpr int kKS = DW / 4;
+    static constexpr size_t kSmem = (size_t)kStages * kStage;
+};
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
@@ -214,14 +241,19 @@ __device__ __forceinline__ void init_ring(uint64_t* full, int nstages, double* r
 
 // ---------------------------------------------------------------------------
 // LEFT: S[a:a+d, c:c+64] <- Q_w^T S[a:a+d, c:c+64], in kLSub-column
-// sub-tiles; warp w owns output rows [16w, 16w+16).
-__global__ void __launch_bounds__(kBulkThreads, 1)
+// sub-tiles; warp w owns output rows [16 wm, 16 wm + 16) (wm = w mod DW/16)
+// of the sub-tile's column slice w / (DW/16).
+template <int DW>
+__global__ void __launch_bounds__(kBulkThreads, DW == 64 ? 2 : 1)
 update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, const double* __restrict__ qw_pool,
                         double* __restrict__ S, long long lds, long long alloc) {
+    using C = LeftCfg<DW>;
+    constexpr int kLdB = C::kLd, kLeftStage = C::kStage, kLStages = C::kStages, kNT = C::kNT, kKS = C::kKS;
     extern __shared__ __align__(128) double ring[];
     __shared__ __align__(8) uint64_t full[kLStages];
     init_ring(full, kLStages, ring, kLStages * kLeftStage, kLSub / 32);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp % C::kMGroups, wn = warp / C::kMGroups;
     const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
     const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
 
@@ -260,7 +292,7 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
     for (int sl = 0; sl < kLStages; ++sl) produce(sl);
 
     const int gid = lane >> 2, tig = lane & 3;
-    double af[2][32];
+    double af[2][kKS];
     unsigned nz0 = 0, nz1 = 0;  // bit ks: fragment af[mt][ks] is nonzero in some lane (warp-uniform)
     unsigned long long ndmma = 0;
     TileWin wd;
@@ -270,20 +302,20 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
     for (int t = t0; t < t1; ++t) {
         seek_win<0>(wd, wins, nwin, t);
         const int d = wd.d;
-        if (wd.wi != cur) {  // A = Q_w^T: af[mt][ks] = Q_w(k = 4ks + tig, m = 16 warp + 8 mt + gid)
+        if (wd.wi != cur) {  // A = Q_w^T: af[mt][ks] = Q_w(k = 4ks + tig, m = 16 wm + 8 mt + gid)
             const double* Qw = qw_pool + wd.qw_off;
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
-                const int m = 16 * warp + 8 * mt + gid;
+                const int m = 16 * wm + 8 * mt + gid;
 #pragma unroll
-                for (int ks = 0; ks < 32; ++ks) {
+                for (int ks = 0; ks < kKS; ++ks) {
                     const int k = 4 * ks + tig;
                     af[mt][ks] = (m < d && k < d) ? __ldg(Qw + k + (long long)m * d) : 0.0;
                 }
             }
             nz0 = nz1 = 0;
 #pragma unroll
-            for (int ks = 0; ks < 32; ++ks) {
+            for (int ks = 0; ks < kKS; ++ks) {
                 nz0 |= (__any_sync(0xffffffffu, af[0][ks] != 0.0) ? 1u : 0u) << ks;
                 nz1 |= (__any_sync(0xffffffffu, af[1][ks] != 0.0) ? 1u : 0u) << ks;
             }
@@ -293,32 +325,32 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
         const int ncols = min(kLeftBN, wd.r1 - c);
         double* P = S + (long long)wd.a + (long long)c * lds;
         for (int sub = 0; kLSub * sub < ncols; ++sub) {
-            double acc[2][kLSub / 8][2];
+            double acc[2][kNT][2];
 #pragma unroll
             for (int i = 0; i < 2; ++i)
 #pragma unroll
-                for (int j = 0; j < kLSub / 8; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-            // column 8 nt + gid, row k = 4 ks + tig (+ the sub-tile's shift)
+                for (int j = 0; j < kNT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            // column 8 (wn kNT + nt) + gid, row k = 4 ks + tig (+ the sub-tile's shift)
             const int shift = (int)(((long long)wd.a + (long long)(c + kLSub * sub) * lds) & 1);
-            const double* sb = ring + stage * (kLeftStage / 8) + gid * kLdB + tig + shift;
+            const double* sb = ring + stage * (kLeftStage / 8) + (8 * kNT * wn + gid) * kLdB + tig + shift;
             mbar_wait(&full[stage], phase);
-            ndmma += (unsigned long long)(__popc(nz0) + __popc(nz1)) * (kLSub / 8);
+            ndmma += (unsigned long long)(__popc(nz0) + __popc(nz1)) * kNT;
             // Q_w's zero 8x4 fragments (about 45 % of them: a window only mixes
             // the blocks it moves past each other) are skipped -- their products
             // are exact zeros and the sums start at +0, so the bits do not change
 #pragma unroll
-            for (int ks = 0; ks < 32; ++ks) {
+            for (int ks = 0; ks < kKS; ++ks) {
                 const bool u0 = (nz0 >> ks) & 1u, u1 = (nz1 >> ks) & 1u;
                 if (!(u0 | u1)) continue;
-                double bf[kLSub / 8];
+                double bf[kNT];
 #pragma unroll
-                for (int nt = 0; nt < kLSub / 8; ++nt) bf[nt] = sb[nt * 8 * kLdB + 4 * ks];
+                for (int nt = 0; nt < kNT; ++nt) bf[nt] = sb[nt * 8 * kLdB + 4 * ks];
                 if (u0)
 #pragma unroll
-                    for (int nt = 0; nt < kLSub / 8; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], af[0][ks], bf[nt]);
+                    for (int nt = 0; nt < kNT; ++nt) dmma(acc[0][nt][0], acc[0][nt][1], af[0][ks], bf[nt]);
                 if (u1)
 #pragma unroll
-                    for (int nt = 0; nt < kLSub / 8; ++nt) dmma(acc[1][nt][0], acc[1][nt][1], af[1][ks], bf[nt]);
+                    for (int nt = 0; nt < kNT; ++nt) dmma(acc[1][nt][0], acc[1][nt][1], af[1][ks], bf[nt]);
             }
             // epilogue through the consumed stage: accumulators to smem at the
             // inputs' positions, then one bulk store per column (async: the
@@ -327,10 +359,10 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
             double* so = ring + stage * (kLeftStage / 8) + shift;
 #pragma unroll
             for (int mt = 0; mt < 2; ++mt) {
-                const int r = 16 * warp + 8 * mt + gid;
+                const int r = 16 * wm + 8 * mt + gid;
 #pragma unroll
-                for (int nt = 0; nt < kLSub / 8; ++nt) {
-                    const int cc = 8 * nt + 2 * tig;
+                for (int nt = 0; nt < kNT; ++nt) {
+                    const int cc = 8 * (kNT * wn + nt) + 2 * tig;
                     so[cc * kLdB + r] = acc[mt][nt][0];
                     so[(cc + 1) * kLdB + r] = acc[mt][nt][1];
                 }
@@ -359,17 +391,21 @@ update_left_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, 
 
 // ---------------------------------------------------------------------------
 // RIGHT: M[r0:r0+64, a:a+d] <- M[r0:r0+64, a:a+d] Q_w, in kRSub-row
-// sub-tiles; warp w owns output columns [16w, 16w+16).  (64-row sub-tiles:
+// sub-tiles; warp w owns output columns [16 wn, 16 wn + 16) (wn = w mod DW/16)
+// of the sub-tile's row slice w / (DW/16).  (64-row sub-tiles:
 // the 128 column copies of a stage are 512 bytes each -- 32-row stages of
 // 256-byte copies left the ring starved, the TMA engine's per-copy cost.)
-template <int Field>
-__global__ void __launch_bounds__(kBulkThreads, 1)
+template <int DW, int Field>
+__global__ void __launch_bounds__(kBulkThreads, DW == 64 ? 2 : 1)
 update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, const double* __restrict__ qw_pool,
                          double* __restrict__ M, long long ldm, long long alloc) {
+    using C = RightCfg<DW>;
+    constexpr int kRightStage = C::kStage, kRStages = C::kStages, kMT = C::kMT, kKS = C::kKS;
     extern __shared__ __align__(128) double ring[];
     __shared__ __align__(8) uint64_t full[kRStages];
-    init_ring(full, kRStages, ring, kRStages * kRightStage, 128 / 32);
+    init_ring(full, kRStages, ring, kRStages * kRightStage, DW / 32);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wn = warp % C::kNGroups, wm = warp / C::kNGroups;
     const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
     const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
     auto tile_rows = [&](const TileWin& w, int t, int& r0, int& nrows) {
@@ -378,7 +414,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
     };
 
     // every thread walks the (tile, sub-tile) sequence a ring depth ahead of the
-    // one it computes; thread j < 128 copies panel column j of each refilled
+    // one it computes; thread j < DW copies panel column j of each refilled
     // stage and arrives on its full barrier with its own byte count
     int pt = t0, psub = 0;
     TileWin pw;
@@ -393,7 +429,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
                 psub = 0;
                 continue;
             }
-            if (kk < 128) {
+            if (kk < DW) {
                 const int rs = r0 + kRSub * psub, len = min(kRSub, nrows - kRSub * psub);
                 double* dst = ring + slot * (kRightStage / 8) + kk * kLdA;
                 long long st = 0;
@@ -412,7 +448,7 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
     for (int sl = 0; sl < kRStages; ++sl) produce(sl);
 
     const int gid = lane >> 2, tig = lane & 3;
-    double bf[2][32];
+    double bf[2][kKS];
     unsigned nz0 = 0, nz1 = 0;  // bit ks: fragment bf[nt][ks] is nonzero in some lane (warp-uniform)
     unsigned long long ndmma = 0;
     TileWin wd;
@@ -422,20 +458,20 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
     for (int t = t0; t < t1; ++t) {
         seek_win<Field>(wd, wins, nwin, t);
         const int d = wd.d;
-        if (wd.wi != cur) {  // B = Q_w: bf[nt][ks] = Q_w(k = 4ks + tig, n = 16 warp + 8 nt + gid)
+        if (wd.wi != cur) {  // B = Q_w: bf[nt][ks] = Q_w(k = 4ks + tig, n = 16 wn + 8 nt + gid)
             const double* Qw = qw_pool + wd.qw_off;
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
-                const int nn = 16 * warp + 8 * nt + gid;
+                const int nn = 16 * wn + 8 * nt + gid;
 #pragma unroll
-                for (int ks = 0; ks < 32; ++ks) {
+                for (int ks = 0; ks < kKS; ++ks) {
                     const int k = 4 * ks + tig;
                     bf[nt][ks] = (nn < d && k < d) ? __ldg(Qw + k + (long long)nn * d) : 0.0;
                 }
             }
             nz0 = nz1 = 0;
 #pragma unroll
-            for (int ks = 0; ks < 32; ++ks) {
+            for (int ks = 0; ks < kKS; ++ks) {
                 nz0 |= (__any_sync(0xffffffffu, bf[0][ks] != 0.0) ? 1u : 0u) << ks;
                 nz1 |= (__any_sync(0xffffffffu, bf[1][ks] != 0.0) ? 1u : 0u) << ks;
             }
@@ -445,30 +481,30 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
         tile_rows(wd, t, r0, nrows);
         double* P = M + (long long)r0 + (long long)wd.a * ldm;
         for (int sub = 0; kRSub * sub < nrows; ++sub) {
-            double acc[kRSub / 8][2][2];
+            double acc[kMT][2][2];
 #pragma unroll
-            for (int i = 0; i < kRSub / 8; ++i)
+            for (int i = 0; i < kMT; ++i)
 #pragma unroll
                 for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
             // row 8 mt + gid, column k = 4 ks + tig (+ the sub-tile's shift)
             const int shift = (int)(((long long)r0 + kRSub * sub + (long long)wd.a * ldm) & 1);
-            const double* sa = ring + stage * (kRightStage / 8) + tig * kLdA + gid + shift;
+            const double* sa = ring + stage * (kRightStage / 8) + tig * kLdA + 8 * kMT * wm + gid + shift;
             mbar_wait(&full[stage], phase);
-            ndmma += (unsigned long long)(__popc(nz0) + __popc(nz1)) * (kRSub / 8);
+            ndmma += (unsigned long long)(__popc(nz0) + __popc(nz1)) * kMT;
             // zero fragments of Q_w skipped (exact: see the left kernel)
 #pragma unroll
-            for (int ks = 0; ks < 32; ++ks) {
+            for (int ks = 0; ks < kKS; ++ks) {
                 const bool u0 = (nz0 >> ks) & 1u, u1 = (nz1 >> ks) & 1u;
                 if (!(u0 | u1)) continue;
-                double a[kRSub / 8];
+                double a[kMT];
 #pragma unroll
-                for (int mt = 0; mt < kRSub / 8; ++mt) a[mt] = sa[4 * ks * kLdA + 8 * mt];
+                for (int mt = 0; mt < kMT; ++mt) a[mt] = sa[4 * ks * kLdA + 8 * mt];
                 if (u0)
 #pragma unroll
-                    for (int mt = 0; mt < kRSub / 8; ++mt) dmma(acc[mt][0][0], acc[mt][0][1], a[mt], bf[0][ks]);
+                    for (int mt = 0; mt < kMT; ++mt) dmma(acc[mt][0][0], acc[mt][0][1], a[mt], bf[0][ks]);
                 if (u1)
 #pragma unroll
-                    for (int mt = 0; mt < kRSub / 8; ++mt) dmma(acc[mt][1][0], acc[mt][1][1], a[mt], bf[1][ks]);
+                    for (int mt = 0; mt < kMT; ++mt) dmma(acc[mt][1][0], acc[mt][1][1], a[mt], bf[1][ks]);
             }
             // direct stores: with a 3-deep ring of 64-row stages the staged
             // (bulk-store) epilogue of the left kernel delays the refill by one
@@ -480,12 +516,12 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
                 phase ^= 1u;
             }
 #pragma unroll
-            for (int mt = 0; mt < kRSub / 8; ++mt) {
-                const int r = kRSub * sub + 8 * mt + gid;
+            for (int mt = 0; mt < kMT; ++mt) {
+                const int r = kRSub * sub + 8 * (kMT * wm + mt) + gid;
                 if (r >= nrows) continue;
 #pragma unroll
                 for (int nt = 0; nt < 2; ++nt) {
-                    const int cc = 16 * warp + 8 * nt + 2 * tig;
+                    const int cc = 16 * wn + 8 * nt + 2 * tig;
                     if (cc < d) P[r + (long long)cc * ldm] = acc[mt][nt][0];
                     if (cc + 1 < d) P[r + (long long)(cc + 1) * ldm] = acc[mt][nt][1];
                 }
@@ -505,18 +541,43 @@ bool bulk_disabled() {
     return off;
 }
 
-constexpr size_t kLeftSmem = (size_t)kLStages * kLeftStage;
-constexpr size_t kRightSmem = (size_t)kRStages * kRightStage;
-
-// one CTA per SM while every CTA gets >= kMinTilesPerCta tiles
-int grid_for(int ntiles) {
-    const int sms = device_sm_count();
+// `per_sm` CTAs per SM while every CTA gets >= kMinTilesPerCta tiles
+int grid_for(int ntiles, int per_sm = 1) {
+    const int sms = device_sm_count() * per_sm;
     return std::max(1, std::min(sms, (ntiles + kMinTilesPerCta - 1) / kMinTilesPerCta));
 }
 
+// TEIG_NO_BULK64=1: windows of order <= 64 take the cp.async kernels
+bool bulk64_disabled() {
+    static const bool off = getenv("TEIG_NO_BULK64") && atoi(getenv("TEIG_NO_BULK64"));
+    return off;
+}
+
 bool bulk_eligible(int dmax, const double* base, long long ld, long long rows, long long cols) {
-    return !bulk_disabled() && dmax > 64 && dmax <= 128 && rows > 0 && cols > 0 && (ld % 2) == 0 &&
-           (reinterpret_cast<uintptr_t>(base) % 16) == 0 && kLeftBN == 64 && kRightBM == 64;
+    return !bulk_disabled() && dmax >= 1 && dmax <= 128 && (dmax > 64 || !bulk64_disabled()) && rows > 0 &&
+           cols > 0 && (ld % 2) == 0 && (reinterpret_cast<uintptr_t>(base) % 16) == 0 && kLeftBN == 64 &&
+           kRightBM == 64;
+}
+
+template <int DW>
+cudaError_t left_bulk(const WinDesc* wins, int nwin, int ntiles, const double* qw_pool, double* S, long long lds,
+                      long long alloc, int grid, cudaStream_t stream) {
+    constexpr size_t smem = LeftCfg<DW>::kSmem;
+    cudaError_t e = ensure_dyn_smem((const void*)update_left_bulk_kernel<DW>, smem);
+    if (e != cudaSuccess) return e;
+    update_left_bulk_kernel<DW><<<grid, kBulkThreads, smem, stream>>>(wins, nwin, ntiles, qw_pool, S, lds, alloc);
+    return cudaGetLastError();
+}
+
+template <int DW, int Field>
+cudaError_t right_bulk(const WinDesc* wins, int nwin, int ntiles, const double* qw_pool, double* M, long long ldm,
+                       long long alloc, int grid, cudaStream_t stream) {
+    constexpr size_t smem = RightCfg<DW>::kSmem;
+    cudaError_t e = ensure_dyn_smem((const void*)update_right_bulk_kernel<DW, Field>, smem);
+    if (e != cudaSuccess) return e;
+    update_right_bulk_kernel<DW, Field><<<grid, kBulkThreads, smem, stream>>>(wins, nwin, ntiles, qw_pool, M, ldm,
+                                                                              alloc);
+    return cudaGetLastError();
 }
 
 }  // namespace
@@ -527,12 +588,11 @@ bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax,
     *err = cudaSuccess;
     if (ntiles <= 0) return true;
     if (!bulk_eligible(dmax, S, lds, rows, cols)) return false;
-    *err = ensure_dyn_smem((const void*)update_left_bulk_kernel, kLeftSmem);
-    if (*err != cudaSuccess) return true;
-    const int grid = max_ctas > 0 ? std::min(grid_for(ntiles), max_ctas) : grid_for(ntiles);
-    update_left_bulk_kernel<<<grid, kBulkThreads, kLeftSmem, stream>>>(wins, nwin, ntiles, qw_pool, S, lds,
-                                                                        (cols - 1) * lds + rows);
-    *err = cudaGetLastError();
+    const int per_sm = dmax > 64 ? 1 : 2;  // order <= 64: two CTAs per SM hide each other's barriers
+    const int grid = max_ctas > 0 ? std::min(grid_for(ntiles, per_sm), max_ctas * per_sm) : grid_for(ntiles, per_sm);
+    const long long alloc = (cols - 1) * lds + rows;
+    *err = dmax > 64 ? left_bulk<128>(wins, nwin, ntiles, qw_pool, S, lds, alloc, grid, stream)
+                     : left_bulk<64>(wins, nwin, ntiles, qw_pool, S, lds, alloc, grid, stream);
     return true;
 }
 
@@ -542,22 +602,19 @@ bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax
     *err = cudaSuccess;
     if (ntiles <= 0) return true;
     if (!bulk_eligible(dmax, M, ldm, rows, cols)) return false;
-    *err = ensure_dyn_smem((const void*)update_right_bulk_kernel<1>, kRightSmem);
-    if (*err == cudaSuccess) *err = ensure_dyn_smem((const void*)update_right_bulk_kernel<2>, kRightSmem);
-    if (*err != cudaSuccess) return true;
     // short_ctas: the caller runs these updates on a low-priority stream beside
     // the critical path -- CTAs of 8 tiles, so critical-path CTAs can take SMs
     // as they free up; otherwise a persistent grid
-    int grid = short_ctas ? (ntiles + 7) / 8 : grid_for(ntiles);
-    if (max_ctas > 0 && !short_ctas) grid = std::min(grid, max_ctas);
+    const int per_sm = dmax > 64 ? 1 : 2;
+    int grid = short_ctas ? (ntiles + 7) / 8 : grid_for(ntiles, per_sm);
+    if (max_ctas > 0 && !short_ctas) grid = std::min(grid, max_ctas * per_sm);
     const long long alloc = (cols - 1) * ldm + rows;
-    if (factor)
-        update_right_bulk_kernel<2><<<grid, kBulkThreads, kRightSmem, stream>>>(wins, nwin, ntiles, qw_pool, M, ldm,
-                                                                                 alloc);
+    if (dmax > 64)
+        *err = factor ? right_bulk<128, 2>(wins, nwin, ntiles, qw_pool, M, ldm, alloc, grid, stream)
+                      : right_bulk<128, 1>(wins, nwin, ntiles, qw_pool, M, ldm, alloc, grid, stream);
     else
-        update_right_bulk_kernel<1><<<grid, kBulkThreads, kRightSmem, stream>>>(wins, nwin, ntiles, qw_pool, M, ldm,
-                                                                                 alloc);
-    *err = cudaGetLastError();
+        *err = factor ? right_bulk<64, 2>(wins, nwin, ntiles, qw_pool, M, ldm, alloc, grid, stream)
+                      : right_bulk<64, 1>(wins, nwin, ntiles, qw_pool, M, ldm, alloc, grid, stream);
     return true;
 }
 
