@@ -535,8 +535,11 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
             if (drain->s_hi - hi >= drain->min_chunk) {  // S rows [hi, s_hi): final after this level's S work
                 TEIG_CUDA(cudaEventRecord(drain->evS, lookahead ? stream3 : stream));
                 TEIG_CUDA(cudaStreamWaitEvent(drain->ds, drain->evS, 0));
-                TEIG_CUDA(cudaMemcpy2DAsync(drain->hS + hi, drain->lds * sizeof(double), dS + hi, lds * sizeof(double),
-                                            (size_t)(drain->s_hi - hi) * sizeof(double), (size_t)n,
+                // row r of a Schur form is zero left of column r-1: columns [hi-1, n)
+                const int64_t c0 = std::max<int64_t>(hi - 1, 0);
+                TEIG_CUDA(cudaMemcpy2DAsync(drain->hS + hi + c0 * drain->lds, drain->lds * sizeof(double),
+                                            dS + hi + c0 * lds, lds * sizeof(double),
+                                            (size_t)(drain->s_hi - hi) * sizeof(double), (size_t)(n - c0),
                                             cudaMemcpyDeviceToHost, drain->ds));
                 drain->s_hi = hi;
             }
@@ -908,6 +911,10 @@ void teig_release_memory(void) {
     trim_memory_pools();
 }
 
+// columns per host<->device copy of S's upper Hessenberg part (each copy
+// carries a rectangle: ~kHessCopyCols^2 / 2 extra doubles per block)
+constexpr int64_t kHessCopyCols = 512;
+
 int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_t ldq, int64_t nb,
                             const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
                             int64_t* perm, int64_t* rejected, int64_t* plan, int64_t plan_cap,
@@ -962,13 +969,24 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         if (Q && !no_supp && !(opts && opts->full_factor)) {
             qsupp.lo.resize(n);
             qsupp.hi.resize(n);
-            const int nt = (int)std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+            const int nt = (int)std::max(1u, std::min(64u, std::thread::hardware_concurrency()));
             for (int t = 0; t < nt; ++t)
                 scan.emplace_back([&qsupp, Q, ldq, n, nt, t] {  // nt by value: it leaves scope before the join
                     for (int64_t c = n * t / nt; c < n * (t + 1) / nt; ++c) {
+                        // first / last nonzero bit pattern: 8-word OR blocks (vectorised), then the word
                         const uint64_t* col = reinterpret_cast<const uint64_t*>(Q + c * ldq);
                         int64_t l = 0, h = n - 1;
+                        for (; l + 8 <= n; l += 8) {
+                            uint64_t o = 0;
+                            for (int k = 0; k < 8; ++k) o |= col[l + k];
+                            if (o) break;
+                        }
                         while (l < n && col[l] == 0) ++l;
+                        for (; h - 7 > l; h -= 8) {
+                            uint64_t o = 0;
+                            for (int k = 0; k < 8; ++k) o |= col[h - k];
+                            if (o) break;
+                        }
                         while (h > l && col[h] == 0) --h;
                         qsupp.lo[c] = (int32_t)l;
                         qsupp.hi[c] = l < n ? (int32_t)h : -1;
@@ -982,20 +1000,51 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
                     if (t.joinable()) t.join();
             }
         } join_scan{scan};
-        TEIG_CUDA(cudaMemcpy2DAsync(dS, pitch, S, lds * sizeof(double), pitch, n, cudaMemcpyHostToDevice, stream));
-        if (Q) {  // Q travels on a side stream, after S, while the S-side work starts (measured:
-                  // uploading Q before the work starts costs +0.5 s at n=40000)
-            TEIG_CUDA(cudaStreamCreateWithFlags(&qs, cudaStreamNonBlocking));
-            TEIG_CUDA(cudaEventCreateWithFlags(&q_ready, cudaEventDisableTiming));
-            TEIG_CUDA(cudaEventRecord(q_ready, stream));  // S is on the device
-            TEIG_CUDA(cudaStreamWaitEvent(qs, q_ready, 0));
-            TEIG_CUDA(cudaMemcpy2DAsync(dQ, pitch, Q, ldq * sizeof(double), pitch, n, cudaMemcpyHostToDevice, qs));
-            TEIG_CUDA(cudaEventRecord(q_ready, qs));
+        // S travels as its upper Hessenberg part only (column j: rows 0..j+1,
+        // in blocks of 512 columns): nothing on the path reads or writes below
+        // the first subdiagonal -- neither does the reference (windows and
+        // panels lie on and above it) -- so the strictly lower part keeps its
+        // input values, which is also what comes back (half the bytes each
+        // way).  The device copy's lower part is zeroed first.
+        TEIG_CUDA(cudaMemsetAsync(dS, 0, pitch * n, stream));
+        for (int64_t j0 = 0; j0 < n; j0 += kHessCopyCols) {
+            const int64_t j1 = std::min<int64_t>(n, j0 + kHessCopyCols), rows = std::min<int64_t>(n, j1 + 1);
+            TEIG_CUDA(cudaMemcpy2DAsync(dS + j0 * n, pitch, S + j0 * lds, lds * sizeof(double),
+                                        (size_t)rows * sizeof(double), (size_t)(j1 - j0), cudaMemcpyHostToDevice,
+                                        stream));
         }
         // S on the device before the levels are enqueued: measured, letting the
         // host enqueue thousands of launches while the 12.8 GB upload runs made
         // the device phase 0.3-4.5 s slower and erratic at n=40000
         TEIG_CUDA(cudaStreamSynchronize(stream));
+        for (auto& t : scan) t.join();
+        qsupp.on = !scan.empty();
+        if (Q) {  // Q travels on a side stream while the S-side work starts (measured:
+                  // uploading Q before the work starts costs +0.5 s at n=40000)
+            TEIG_CUDA(cudaStreamCreateWithFlags(&qs, cudaStreamNonBlocking));
+            TEIG_CUDA(cudaEventCreateWithFlags(&q_ready, cudaEventDisableTiming));
+            if (qsupp.on) {
+                // only the row hull of each block of columns (the scan's
+                // support; exact zeros elsewhere, +0.0 bit patterns): Q_in = I
+                // is 0.17 GB instead of 12.8 GB at n=40000
+                TEIG_CUDA(cudaMemsetAsync(dQ, 0, pitch * n, qs));
+                for (int64_t j0 = 0; j0 < n; j0 += kHessCopyCols) {
+                    const int64_t j1 = std::min<int64_t>(n, j0 + kHessCopyCols);
+                    int64_t lo = n, hi = -1;
+                    for (int64_t c = j0; c < j1; ++c) {
+                        lo = std::min<int64_t>(lo, qsupp.lo[c]);
+                        hi = std::max<int64_t>(hi, qsupp.hi[c]);
+                    }
+                    if (hi < lo) continue;
+                    TEIG_CUDA(cudaMemcpy2DAsync(dQ + j0 * n + lo, pitch, Q + j0 * ldq + lo, ldq * sizeof(double),
+                                                (size_t)(hi - lo + 1) * sizeof(double), (size_t)(j1 - j0),
+                                                cudaMemcpyHostToDevice, qs));
+                }
+            } else {
+                TEIG_CUDA(cudaMemcpy2DAsync(dQ, pitch, Q, ldq * sizeof(double), pitch, n, cudaMemcpyHostToDevice, qs));
+            }
+            TEIG_CUDA(cudaEventRecord(q_ready, qs));
+        }
         const auto h2 = now();
         // the final parts of S and Q stream back while the last levels run
         // (TEIG_NO_DRAIN=1: everything after the end)
@@ -1033,8 +1082,6 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         TEIG_CUDA(cudaStreamCreateWithFlags(&dr.ds, cudaStreamNonBlocking));
         TEIG_CUDA(cudaEventCreateWithFlags(&dr.evS, cudaEventDisableTiming));
         TEIG_CUDA(cudaEventCreateWithFlags(&dr.evQ, cudaEventDisableTiming));
-        for (auto& t : scan) t.join();
-        qsupp.on = !scan.empty();
         const int rc = reorder_schur_device(n, dS, n, dQ, n, nb, sizes, flags, opts, perm, rejected, plan, plan_cap,
                                             info, stream, q_ready, drain_on ? &dr : nullptr, &qsupp);
         TEIG_CUDA(cudaStreamSynchronize(stream));
@@ -1053,9 +1100,19 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         }
         TEIG_CUDA(cudaEventRecord(dr.evS, stream));  // all device work (the Q stream joined `stream`)
         TEIG_CUDA(cudaStreamWaitEvent(dr.ds, dr.evS, 0));
-        if (dr.s_hi > 0)
-            TEIG_CUDA(cudaMemcpy2DAsync(S, lds * sizeof(double), dS, pitch, (size_t)dr.s_hi * sizeof(double), n,
-                                        cudaMemcpyDeviceToHost, dr.ds));
+        if (dr.s_hi > 0) {  // rows [0, s_hi): columns < s_hi down to their subdiagonal, the rest whole
+            for (int64_t j0 = 0; j0 < std::min<int64_t>(dr.s_hi, n); j0 += kHessCopyCols) {
+                const int64_t j1 = std::min<int64_t>(dr.s_hi, j0 + kHessCopyCols);
+                const int64_t rows = std::min<int64_t>(dr.s_hi, j1 + 1);
+                TEIG_CUDA(cudaMemcpy2DAsync(S + j0 * lds, lds * sizeof(double), dS + j0 * n, pitch,
+                                            (size_t)rows * sizeof(double), (size_t)(j1 - j0), cudaMemcpyDeviceToHost,
+                                            dr.ds));
+            }
+            if (dr.s_hi < n)
+                TEIG_CUDA(cudaMemcpy2DAsync(S + dr.s_hi * lds, lds * sizeof(double), dS + dr.s_hi * n, pitch,
+                                            (size_t)dr.s_hi * sizeof(double), (size_t)(n - dr.s_hi),
+                                            cudaMemcpyDeviceToHost, dr.ds));
+        }
         if (Q && dr.q_hi > dr.q_lo)
             TEIG_CUDA(cudaMemcpy2DAsync(Q + dr.q_lo * ldq, ldq * sizeof(double), dQ + dr.q_lo * (size_t)n, pitch,
                                         pitch, (size_t)(dr.q_hi - dr.q_lo), cudaMemcpyDeviceToHost, dr.ds));
