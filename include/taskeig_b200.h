@@ -141,6 +141,11 @@ int32_t teig_memory_retention(void);
 void teig_release_memory(void);
 void teig_release_host_staging(void);
 
+/* Bytes the calling thread's last teig_reorder_schur_host call moved host ->
+ * device and device -> host (S's upper Hessenberg part, Q's row hulls, the
+ * drained and final copies).  Both 0 before any such call. */
+void teig_host_transfer_bytes(int64_t* h2d, int64_t* d2h);
+
 /* Diagonal-block scan by exact-zero subdiagonal (reorder.cpp:21-43) on a
  * device matrix.  sizes: host array of capacity n.  Returns nb (>= 0). */
 int64_t teig_scan_blocks_device(int64_t n, const double* dS, int64_t lds, uint8_t* sizes,

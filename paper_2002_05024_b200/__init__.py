@@ -6,7 +6,8 @@ The compute path is the in-tree CUDA library ``_lib/libtaskeig_b200.so``
 (C ABI: ``include/taskeig_b200.h``); this package is the host-side mirror of
 the reference interface.  There is no CPU fallback.
 """
-from ._native import (TaskeigError, build, lib, memory_retention, release_memory, set_memory_retention,  # noqa: F401
+from ._native import (TaskeigError, build, host_transfer_bytes, lib, memory_retention, release_memory,  # noqa: F401
+                      set_memory_retention,
                       trace_enable, trace_json)
 from .reorder import (  # noqa: F401
     Block, GReorderResult, PlanWindow, ReorderOptions, ReorderResult, Selection, WindowReorderOutcome,

@@ -80,6 +80,7 @@ SIGNATURES = {
     "teig_set_memory_retention": (None, [C.c_int32]),
     "teig_memory_retention": (C.c_int32, []),
     "teig_release_memory": (None, []),
+    "teig_host_transfer_bytes": (None, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "teig_trace_enable": (None, [C.c_int32]),
     "teig_trace_json": (C.c_int64, [C.c_char_p, C.c_int64]),
     "teig_trace_task_count": (C.c_int64, []),
@@ -163,6 +164,13 @@ def set_memory_retention(on: bool) -> None:
 
 def memory_retention() -> bool:
     return bool(lib().teig_memory_retention())
+
+
+def host_transfer_bytes():
+    """(h2d, d2h) bytes of this thread's last host-entry-point reorder call."""
+    a, b = C.c_int64(0), C.c_int64(0)
+    lib().teig_host_transfer_bytes(C.byref(a), C.byref(b))
+    return int(a.value), int(b.value)
 
 
 def release_memory() -> None:

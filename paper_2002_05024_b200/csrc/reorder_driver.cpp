@@ -260,6 +260,7 @@ struct HostDrain {
     int64_t s_hi = 0, q_lo = 0, q_hi = 0;
     bool valid = true;
     int64_t min_chunk = 512;
+    int64_t d2h_bytes = 0;  // drained so far
 };
 
 // Executes one planned pass on the device and folds the outcomes into `blocks`.
@@ -541,6 +542,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                                             dS + hi + c0 * lds, lds * sizeof(double),
                                             (size_t)(drain->s_hi - hi) * sizeof(double), (size_t)(n - c0),
                                             cudaMemcpyDeviceToHost, drain->ds));
+                drain->d2h_bytes += (drain->s_hi - hi) * (n - c0) * (int64_t)sizeof(double);
                 drain->s_hi = hi;
             }
             if (dQ && drain->hQ &&
@@ -548,10 +550,12 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                 TEIG_CUDA(cudaEventRecord(drain->evQ, overlap ? stream2 : stream));
                 TEIG_CUDA(cudaStreamWaitEvent(drain->ds, drain->evQ, 0));
                 auto cols = [&](int64_t c0, int64_t c1) {
-                    if (c1 > c0)
+                    if (c1 > c0) {
                         TEIG_CUDA(cudaMemcpy2DAsync(drain->hQ + c0 * drain->ldq, drain->ldq * sizeof(double),
                                                     dQ + c0 * ldq, ldq * sizeof(double), (size_t)n * sizeof(double),
                                                     (size_t)(c1 - c0), cudaMemcpyDeviceToHost, drain->ds));
+                        drain->d2h_bytes += n * (c1 - c0) * (int64_t)sizeof(double);
+                    }
                 };
                 if (drain->q_hi - hi >= drain->min_chunk) {
                     cols(hi, drain->q_hi);
@@ -915,6 +919,13 @@ void teig_release_memory(void) {
 // carries a rectangle: ~kHessCopyCols^2 / 2 extra doubles per block)
 constexpr int64_t kHessCopyCols = 512;
 
+thread_local int64_t g_host_h2d = 0, g_host_d2h = 0;  // teig_host_transfer_bytes
+
+void teig_host_transfer_bytes(int64_t* h2d, int64_t* d2h) {
+    if (h2d) *h2d = g_host_h2d;
+    if (d2h) *d2h = g_host_d2h;
+}
+
 int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_t ldq, int64_t nb,
                             const uint8_t* sizes, const uint8_t* flags, const teig_reorder_opts* opts,
                             int64_t* perm, int64_t* rejected, int64_t* plan, int64_t plan_cap,
@@ -936,6 +947,8 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
     try {
         const size_t pitch = (size_t)n * sizeof(double);
         const size_t need = pitch * n * (Q ? 2 : 1);
+        int64_t h2d = 0;
+        g_host_h2d = g_host_d2h = 0;
         struct Plain {  // per-call staging (cudaFree synchronizes)
             void* p = nullptr;
             ~Plain() {
@@ -1012,6 +1025,7 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
             TEIG_CUDA(cudaMemcpy2DAsync(dS + j0 * n, pitch, S + j0 * lds, lds * sizeof(double),
                                         (size_t)rows * sizeof(double), (size_t)(j1 - j0), cudaMemcpyHostToDevice,
                                         stream));
+            h2d += rows * (j1 - j0) * (int64_t)sizeof(double);
         }
         // S on the device before the levels are enqueued: measured, letting the
         // host enqueue thousands of launches while the 12.8 GB upload runs made
@@ -1039,9 +1053,11 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
                     TEIG_CUDA(cudaMemcpy2DAsync(dQ + j0 * n + lo, pitch, Q + j0 * ldq + lo, ldq * sizeof(double),
                                                 (size_t)(hi - lo + 1) * sizeof(double), (size_t)(j1 - j0),
                                                 cudaMemcpyHostToDevice, qs));
+                    h2d += (hi - lo + 1) * (j1 - j0) * (int64_t)sizeof(double);
                 }
             } else {
                 TEIG_CUDA(cudaMemcpy2DAsync(dQ, pitch, Q, ldq * sizeof(double), pitch, n, cudaMemcpyHostToDevice, qs));
+                h2d += n * n * (int64_t)sizeof(double);
             }
             TEIG_CUDA(cudaEventRecord(q_ready, qs));
         }
@@ -1107,17 +1123,24 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
                 TEIG_CUDA(cudaMemcpy2DAsync(S + j0 * lds, lds * sizeof(double), dS + j0 * n, pitch,
                                             (size_t)rows * sizeof(double), (size_t)(j1 - j0), cudaMemcpyDeviceToHost,
                                             dr.ds));
+                dr.d2h_bytes += rows * (j1 - j0) * (int64_t)sizeof(double);
             }
-            if (dr.s_hi < n)
+            if (dr.s_hi < n) {
                 TEIG_CUDA(cudaMemcpy2DAsync(S + dr.s_hi * lds, lds * sizeof(double), dS + dr.s_hi * n, pitch,
                                             (size_t)dr.s_hi * sizeof(double), (size_t)(n - dr.s_hi),
                                             cudaMemcpyDeviceToHost, dr.ds));
+                dr.d2h_bytes += dr.s_hi * (n - dr.s_hi) * (int64_t)sizeof(double);
+            }
         }
-        if (Q && dr.q_hi > dr.q_lo)
+        if (Q && dr.q_hi > dr.q_lo) {
             TEIG_CUDA(cudaMemcpy2DAsync(Q + dr.q_lo * ldq, ldq * sizeof(double), dQ + dr.q_lo * (size_t)n, pitch,
                                         pitch, (size_t)(dr.q_hi - dr.q_lo), cudaMemcpyDeviceToHost, dr.ds));
+            dr.d2h_bytes += n * (dr.q_hi - dr.q_lo) * (int64_t)sizeof(double);
+        }
         TEIG_CUDA(cudaStreamSynchronize(dr.ds));
         if (qs) TEIG_CUDA(cudaStreamSynchronize(qs));
+        g_host_h2d = h2d;
+        g_host_d2h = dr.d2h_bytes;
         if (hprof)
             fprintf(stderr, "[teig host] alloc %.1f ms  h2d(S) %.1f ms  device %.1f ms  d2h %.1f ms\n", ms(h0, h1),
                     ms(h1, h2), ms(h2, h3), ms(h3, now()));
