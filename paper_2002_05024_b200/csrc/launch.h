@@ -43,7 +43,8 @@ constexpr int kWindowThreads = 256;  // threads of the window kernel (8 warps)
 // [0, rows) x [0, cols)); when given, windows of order 65..128 take the TMA
 // kernels of update_tma.cu, otherwise (or for slab bases) the cp.async ones.
 // max_ctas > 0 caps the persistent grid of the bulk kernels (the caller keeps
-// SMs free for window kernels running beside the launch)
+// SMs free for window kernels running beside the launch); max_ctas < 0: as
+// many CTAs as tiles (up to the SM count) -- latency-critical launches
 cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
                                double* S, long long lds, int n, cudaStream_t stream, long long rows = -1,
                                long long cols = -1, int max_ctas = 0);

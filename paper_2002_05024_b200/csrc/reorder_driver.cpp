@@ -408,7 +408,8 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                 btl[L] += (n - y + kLeftBN - 1) / kLeftBN;
                 btr[L] += (x + kRightBM - 1) / kRightBM;
             }
-            if (L + 1 < nl) {  // keep SMs free for the next level's window CTAs
+            if (L + 1 < nl) {  // keep SMs free for the next level's window CTAs (split only
+                               // when that leaves the bulk updates most of the GPU)
                 const int64_t nwn = lvl_off[L + 2] - lvl_off[L + 1];
                 if (nwn <= sms / 2) bulk_cap[L] = sms - (int)nwn;
             }
@@ -484,7 +485,10 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                                          wprof ? d_prof.as<unsigned long long>() + o * (kWindowThreads / 32) * 4 : nullptr,
                                          d_devlvl.as<int32_t>());
         });
-        if (dQ && overlap) {
+        // the factor updates of level L on the low-priority stream (after the
+        // window; in look-ahead mode after the critical tiles too, so its
+        // short CTAs do not take the SMs those need)
+        auto factor_overlapped = [&] {
             TEIG_CUDA(cudaEventRecord(ev, stream));
             TEIG_CUDA(cudaStreamWaitEvent(stream2, ev, 0));
             timed(3, stream2, tq[L], [&] {
@@ -492,21 +496,28 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                                            true, stream2, n, n, short_q);
             });
             if (ring_ev.n) TEIG_CUDA(cudaEventRecord(ring_ev.ev[L % ring.k], stream2));
-        }
-        if (lookahead) {
+        };
+        // look-ahead split of this level (next level's window kernels find
+        // free SMs beside its bulk updates); otherwise its S updates run
+        // whole on the window stream, as in the serial order
+        const bool split = lookahead && bulk_cap[L] > 0;
+        if (lookahead && L > 0) TEIG_CUDA(cudaStreamWaitEvent(stream, la_ev.ev[1], 0));  // bulk(L-1) first
+        if (dQ && overlap && !split) factor_overlapped();
+        if (split) {
             const WinDesc* cd = d_cdesc.as<WinDesc>() + o;
             const WinDesc* bd = d_bdesc.as<WinDesc>() + o;
-            if (L > 0) TEIG_CUDA(cudaStreamWaitEvent(stream, la_ev.ev[1], 0));  // bulk(L-1) before critical(L)
+            // the critical tiles gate window L+1: one tile per CTA (-1)
             timed(1, stream, ctl[L], [&] {
                 return launch_update_left(cd, (int)cnt, (int)ctl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
-                                          stream, n, n);
+                                          stream, n, n, -1);
             });
             timed(2, stream, ctr[L], [&] {
                 return launch_update_right(cd, (int)cnt, (int)ctr[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
-                                           false, stream, n, n);
+                                           false, stream, n, n, false, -1);
             });
             TEIG_CUDA(cudaEventRecord(la_ev.ev[0], stream));
             TEIG_CUDA(cudaStreamWaitEvent(stream3, la_ev.ev[0], 0));
+            if (dQ) factor_overlapped();
             timed(1, stream3, btl[L], [&] {
                 return launch_update_left(bd, (int)cnt, (int)btl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
                                           stream3, n, n, bulk_cap[L]);
@@ -534,7 +545,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         if (drain && drain->valid && L + 1 < nl) {
             const int64_t hi = after_hi[L + 1], lo = after_lo[L + 1];
             if (drain->s_hi - hi >= drain->min_chunk) {  // S rows [hi, s_hi): final after this level's S work
-                TEIG_CUDA(cudaEventRecord(drain->evS, lookahead ? stream3 : stream));
+                TEIG_CUDA(cudaEventRecord(drain->evS, split ? stream3 : stream));
                 TEIG_CUDA(cudaStreamWaitEvent(drain->ds, drain->evS, 0));
                 // row r of a Schur form is zero left of column r-1: columns [hi-1, n)
                 const int64_t c0 = std::max<int64_t>(hi - 1, 0);

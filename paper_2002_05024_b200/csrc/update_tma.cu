@@ -589,7 +589,9 @@ bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax,
     if (ntiles <= 0) return true;
     if (!bulk_eligible(dmax, S, lds, rows, cols)) return false;
     const int per_sm = dmax > 64 ? 1 : 2;  // order <= 64: two CTAs per SM hide each other's barriers
-    const int grid = max_ctas > 0 ? std::min(grid_for(ntiles, per_sm), max_ctas * per_sm) : grid_for(ntiles, per_sm);
+    const int grid = max_ctas > 0   ? std::min(grid_for(ntiles, per_sm), max_ctas * per_sm)
+                     : max_ctas < 0 ? std::min(ntiles, device_sm_count() * per_sm)
+                                    : grid_for(ntiles, per_sm);
     const long long alloc = (cols - 1) * lds + rows;
     *err = dmax > 64 ? left_bulk<128>(wins, nwin, ntiles, qw_pool, S, lds, alloc, grid, stream)
                      : left_bulk<64>(wins, nwin, ntiles, qw_pool, S, lds, alloc, grid, stream);
@@ -608,6 +610,7 @@ bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax
     const int per_sm = dmax > 64 ? 1 : 2;
     int grid = short_ctas ? (ntiles + 7) / 8 : grid_for(ntiles, per_sm);
     if (max_ctas > 0 && !short_ctas) grid = std::min(grid, max_ctas * per_sm);
+    if (max_ctas < 0 && !short_ctas) grid = std::min(ntiles, device_sm_count() * per_sm);
     const long long alloc = (cols - 1) * ldm + rows;
     if (dmax > 64)
         *err = factor ? right_bulk<128, 2>(wins, nwin, ntiles, qw_pool, M, ldm, alloc, grid, stream)
