@@ -49,13 +49,14 @@ cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dm
                                double* S, long long lds, int n, cudaStream_t stream, long long rows = -1,
                                long long cols = -1, int max_ctas = 0);
 
-// short_ctas: launch the bulk factor kernel as short CTAs (8 tiles each)
+// short_ctas: launch the bulk factor kernel as short CTAs (short_tiles tiles each)
 // instead of a persistent grid -- for a caller that runs the factor updates on
 // a LOW-priority stream beside a critical path, so critical-path CTAs take SMs
 // as they free up.
 cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
                                 double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream,
-                                long long rows = -1, long long cols = -1, bool short_ctas = false, int max_ctas = 0);
+                                long long rows = -1, long long cols = -1, bool short_ctas = false, int max_ctas = 0,
+                                int short_tiles = 8);
 
 // DMMA instructions the update kernels have issued on the current device so
 // far (bulk-copy kernels: zero Q_w fragments skipped; cp.async kernels); x 512
@@ -69,7 +70,7 @@ bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax,
                             int max_ctas = 0);
 bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* M,
                              long long ldm, long long rows, long long cols, bool factor, cudaStream_t stream,
-                             cudaError_t* err, bool short_ctas = false, int max_ctas = 0);
+                             cudaError_t* err, bool short_ctas = false, int max_ctas = 0, int short_tiles = 8);
 
 
 // synthetic inputs (generate.cu)

@@ -408,10 +408,22 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
                 btl[L] += (n - y + kLeftBN - 1) / kLeftBN;
                 btr[L] += (x + kRightBM - 1) / kRightBM;
             }
-            if (L + 1 < nl) {  // keep SMs free for the next level's window CTAs (split only
-                               // when that leaves the bulk updates most of the GPU)
+            if (L + 1 < nl) {
+                // split only where it pays: the bulk and factor updates,
+                // squeezed onto the SMs the next level's window CTAs leave
+                // free, must end before window + bulk would in the serial order
+                // (where the factor updates fill the SMs the window kernel
+                // leaves idle), with a 10 % margin for the extra launches.
+                // Window ~0.65 ms per order-128 step chain on this B200, tiles
+                // ~25 TF/s.  C2's levels split; C4's do not (~92 windows per
+                // level, and 40000-long panels where there are fewer).
                 const int64_t nwn = lvl_off[L + 2] - lvl_off[L + 1];
-                if (nwn <= sms / 2) bulk_cap[L] = sms - (int)nwn;
+                const double tile_ms = 2.0 * 64.0 * double(dmax) * double(dmax) / 25e12 * 1e3;
+                const double bulk_ms = double(btl[L] + btr[L]) * tile_ms;
+                const double side_ms = bulk_ms + (dQ ? double(tq[L]) * tile_ms : 0.0);
+                const double win_ms = 0.65 * double(dmax) / 128.0;
+                if (nwn <= sms / 2 && side_ms * sms / double(sms - nwn) < 0.9 * (win_ms + bulk_ms))
+                    bulk_cap[L] = sms - (int)nwn;
             }
         }
     }
@@ -475,8 +487,9 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         cur_level = L;
         nvtxRangePushA("teig reorder level");
         if (launch_log)
-            fprintf(stderr, "[teig level] %d windows %lld left_tiles %lld right_tiles %lld factor_tiles %lld\n", L,
-                    (long long)cnt, (long long)tl[L], (long long)tr[L], (long long)tq[L]);
+            fprintf(stderr, "[teig level] %d windows %lld left_tiles %lld right_tiles %lld factor_tiles %lld split %d\n",
+                    L, (long long)cnt, (long long)tl[L], (long long)tr[L], (long long)tq[L],
+                    lookahead && bulk_cap[L] > 0 ? 1 : 0);
         if (ring_ev.n && L >= ring.k) TEIG_CUDA(cudaStreamWaitEvent(stream, ring_ev.ev[L % ring.k], 0));
         timed(0, stream, cnt, [&] {
             return launch_window_reorder(dd + o, (int)cnt, dmax_k, dS, lds, d_qw.as<double>(), d_sizes.as<uint8_t>(),
@@ -488,12 +501,12 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         // the factor updates of level L on the low-priority stream (after the
         // window; in look-ahead mode after the critical tiles too, so its
         // short CTAs do not take the SMs those need)
-        auto factor_overlapped = [&] {
+        auto factor_overlapped = [&](int short_tiles) {
             TEIG_CUDA(cudaEventRecord(ev, stream));
             TEIG_CUDA(cudaStreamWaitEvent(stream2, ev, 0));
             timed(3, stream2, tq[L], [&] {
                 return launch_update_right(dd + o, (int)cnt, (int)tq[L], dmax_k, d_qw.as<double>(), dQ, ldq, (int)n,
-                                           true, stream2, n, n, short_q);
+                                           true, stream2, n, n, short_q, 0, short_tiles);
             });
             if (ring_ev.n) TEIG_CUDA(cudaEventRecord(ring_ev.ev[L % ring.k], stream2));
         };
@@ -502,7 +515,7 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
         // whole on the window stream, as in the serial order
         const bool split = lookahead && bulk_cap[L] > 0;
         if (lookahead && L > 0) TEIG_CUDA(cudaStreamWaitEvent(stream, la_ev.ev[1], 0));  // bulk(L-1) first
-        if (dQ && overlap && !split) factor_overlapped();
+        if (dQ && overlap && !split) factor_overlapped(8);
         if (split) {
             const WinDesc* cd = d_cdesc.as<WinDesc>() + o;
             const WinDesc* bd = d_bdesc.as<WinDesc>() + o;
@@ -517,7 +530,9 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
             });
             TEIG_CUDA(cudaEventRecord(la_ev.ev[0], stream));
             TEIG_CUDA(cudaStreamWaitEvent(stream3, la_ev.ev[0], 0));
-            if (dQ) factor_overlapped();
+            // a split level's window chain is the critical path: shorter factor
+            // CTAs (2 tiles) free the SMs the next window kernel needs sooner
+            if (dQ) factor_overlapped(2);
             timed(1, stream3, btl[L], [&] {
                 return launch_update_left(bd, (int)cnt, (int)btl[L], dmax_k, d_qw.as<double>(), dS, lds, (int)n,
                                           stream3, n, n, bulk_cap[L]);

@@ -345,12 +345,12 @@ cudaError_t launch_update_left(const WinDesc* wins, int nwin, int ntiles, int dm
 
 cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool,
                                 double* M, long long ldm, int nrows_total, bool factor, cudaStream_t stream,
-                                long long rows, long long cols, bool short_ctas, int max_ctas) {
+                                long long rows, long long cols, bool short_ctas, int max_ctas, int short_tiles) {
     if (ntiles <= 0) return cudaSuccess;
     if (rows > 0) {
         cudaError_t err;
         if (launch_update_right_tma(wins, nwin, ntiles, dmax, qw_pool, M, ldm, rows, cols, factor, stream, &err,
-                                    short_ctas, max_ctas))
+                                    short_ctas, max_ctas, short_tiles))
             return err;
     }
     {

@@ -600,15 +600,16 @@ bool launch_update_left_tma(const WinDesc* wins, int nwin, int ntiles, int dmax,
 
 bool launch_update_right_tma(const WinDesc* wins, int nwin, int ntiles, int dmax, const double* qw_pool, double* M,
                              long long ldm, long long rows, long long cols, bool factor, cudaStream_t stream,
-                             cudaError_t* err, bool short_ctas, int max_ctas) {
+                             cudaError_t* err, bool short_ctas, int max_ctas, int short_tiles) {
     *err = cudaSuccess;
     if (ntiles <= 0) return true;
     if (!bulk_eligible(dmax, M, ldm, rows, cols)) return false;
     // short_ctas: the caller runs these updates on a low-priority stream beside
-    // the critical path -- CTAs of 8 tiles, so critical-path CTAs can take SMs
-    // as they free up; otherwise a persistent grid
+    // the critical path -- CTAs of short_tiles tiles, so critical-path CTAs can
+    // take SMs as they free up; otherwise a persistent grid
     const int per_sm = dmax > 64 ? 1 : 2;
-    int grid = short_ctas ? (ntiles + 7) / 8 : grid_for(ntiles, per_sm);
+    const int st = std::max(1, short_tiles);
+    int grid = short_ctas ? (ntiles + st - 1) / st : grid_for(ntiles, per_sm);
     if (max_ctas > 0 && !short_ctas) grid = std::min(grid, max_ctas * per_sm);
     if (max_ctas < 0 && !short_ctas) grid = std::min(ntiles, device_sm_count() * per_sm);
     const long long alloc = (cols - 1) * ldm + rows;
