@@ -16,14 +16,14 @@
 // B200 mapping.  The column step is a chain of grid-wide reductions over the
 // m = n-k-1 panel rows -- latency-bound -- plus one GEMV with the trailing
 // block (m x (m-i) doubles read once: the HBM-bound part, ~n^3/3 x 8 bytes
-// over the whole reduction).  Seven stream-ordered kernels per column, every
+// over the whole reduction).  Five stream-ordered kernels per column, every
 // reduction deterministic (per-CTA partials summed in a fixed order, no
 // atomics): col_prep (x update, partial V^T x), col_apply (x -= V T^T V^T x,
 // partial max |x|), col_sumsq (partial sum (x/max)^2: the reference's
 // two-pass scaled nrm2), col_reflect (every CTA forms the same beta / tau,
-// writes v and the finalised panel column, partial V^T v), col_tcol (T
-// column), col_matvec (GEMV over row blocks x column chunks, partials per
-// chunk), col_y (Y column).  The panel's trailing, top-right and Q updates
+// writes v and the finalised panel column, partial V^T v), col_matvec (GEMV
+// over row blocks x column chunks, partials per chunk), col_y (Y column; CTA
+// 0 also the T column; then the next column's col_prep for the same rows).  The panel's trailing, top-right and Q updates
 // are FP64 tensor-core GEMMs (DMMA, dgemm.cuh).
 #include <cuda_runtime.h>
 
@@ -84,7 +84,8 @@ struct Col {
     double* T;        // b x b, ld HB
     long long ldv;
     double* x;        // m
-    double* part;     // NB x HB partials
+    double* part;     // NB x HB partials of V^T v (col_reflect -> col_y)
+    double* pprep;    // NB x HB partials of V^T x (col_prep / col_y_prep -> col_apply)
     double* pscal;    // NB partials: max |x_r|
     double* psum;     // NB partials: sum (x_r / max)^2
     double* scal;     // [0] tau, [1] beta, [2] mx, [3] inv, [4] rescale count
@@ -93,10 +94,8 @@ struct Col {
     int k, m, nb_cta;
 };
 
-// x = A[k+1:, k+i] - Y V(i-1, :)^T ; partial (V^T x)_j
-__global__ void __launch_bounds__(HT) col_prep(Col c, int i) {
-    __shared__ double sh[HT / 32 * HB];
-    const int r = blockIdx.x * HT + threadIdx.x;
+// x = A[k+1:, k+i] - Y V(i-1, :)^T ; partial (V^T x)_j  (row r of the CTA)
+__device__ __forceinline__ void prep_row(const Col& c, int i, int r, double* sh) {
     double x = 0.0;
     if (r < c.m) {
         x = c.A[r + (long long)(c.k + i) * c.lda];
@@ -106,7 +105,12 @@ __global__ void __launch_bounds__(HT) col_prep(Col c, int i) {
         }
         c.x[r] = x;
     }
-    if (i > 0) block_dots(c.V, c.ldv, c.m, i, r, x, c.part + (long long)blockIdx.x * HB, sh);
+    if (i > 0) block_dots(c.V, c.ldv, c.m, i, r, x, c.pprep + (long long)blockIdx.x * HB, sh);
+}
+
+__global__ void __launch_bounds__(HT) col_prep(Col c, int i) {
+    __shared__ double sh[HT / 32 * HB];
+    prep_row(c, i, blockIdx.x * HT + threadIdx.x, sh);
 }
 
 // x -= V (T^T s), s = sum of the partials; partial max |x_r|, r > i
@@ -114,7 +118,7 @@ __global__ void __launch_bounds__(HT) col_apply(Col c, int i) {
     __shared__ double s[HB], tw[HB], red[HT / 32];
     for (int j = threadIdx.x; j < i; j += HT) {
         double a = 0.0;
-        for (int b = 0; b < c.nb_cta; ++b) a += c.part[(long long)b * HB + j];
+        for (int b = 0; b < c.nb_cta; ++b) a += c.pprep[(long long)b * HB + j];
         s[j] = a;
     }
     __syncthreads();
@@ -267,25 +271,6 @@ __global__ void __launch_bounds__(HT) col_reflect(Col c, int i) {
     if (i > 0) block_dots(c.V, c.ldv, c.m, i, r, v, c.part + (long long)blockIdx.x * HB, sh);
 }
 
-// T(:, i) = -tau T(:i, :i) s2, T(i, i) = tau, s2 = V^T v
-__global__ void col_tcol(Col c, int i) {
-    __shared__ double s2[HB];
-    for (int j = threadIdx.x; j < i; j += blockDim.x) {
-        double a = 0.0;
-        for (int b = 0; b < c.nb_cta; ++b) a += c.part[(long long)b * HB + j];
-        s2[j] = a;
-        c.s2[j] = a;
-    }
-    __syncthreads();
-    const double tau = c.scal[0];
-    for (int j = threadIdx.x; j < i; j += blockDim.x) {
-        double a = 0.0;
-        for (int l = j; l < i; ++l) a += c.T[j + l * HB] * s2[l];
-        c.T[j + i * HB] = -tau * a;
-    }
-    if (threadIdx.x == 0) c.T[i + i * HB] = tau;
-}
-
 // ww[chunk][r] = sum over the chunk's columns c >= i of A(k+1+r, k+1+c) v_c
 __global__ void __launch_bounds__(HT) col_matvec(Col c, int i, int chunk) {
     __shared__ double vs[MV_COLS];
@@ -302,17 +287,41 @@ __global__ void __launch_bounds__(HT) col_matvec(Col c, int i, int chunk) {
     c.ww[(long long)blockIdx.y * c.m + r] = acc;
 }
 
-// Y(:, i) = tau (ww - Y s2)
-__global__ void __launch_bounds__(HT) col_y(Col c, int i, int nchunk) {
-    const int r = blockIdx.x * HT + threadIdx.x;
-    if (r >= c.m) return;
-    double w = 0.0;
-    for (int q = 0; q < nchunk; ++q) w += c.ww[(long long)q * c.m + r];
-    for (int j = 0; j < i; ++j) {
-        const double f = c.s2[j];
-        if (f != 0.0) w -= c.Y[r + (long long)j * c.ldv] * f;
+// Y(:, i) = tau (ww - Y s2), s2 = V^T v summed from col_reflect's partials
+// in every CTA (the order of col_tcol's sum); CTA 0 also writes T(:, i) =
+// -tau T(:i, :i) s2, T(i, i) = tau -- col_tcol folded in, one launch less
+// per column
+__global__ void __launch_bounds__(HT) col_y(Col c, int i, int nchunk, int prep_next) {
+    __shared__ double s2[HB];
+    __shared__ double sh[HT / 32 * HB];
+    for (int j = threadIdx.x; j < i; j += HT) {
+        double a = 0.0;
+        for (int b = 0; b < c.nb_cta; ++b) a += c.part[(long long)b * HB + j];
+        s2[j] = a;
     }
-    c.Y[r + (long long)i * c.ldv] = c.scal[0] * w;
+    __syncthreads();
+    const double tau = c.scal[0];
+    if (blockIdx.x == 0) {
+        for (int j = threadIdx.x; j < i; j += HT) {
+            double a = 0.0;
+            for (int l = j; l < i; ++l) a += c.T[j + l * HB] * s2[l];
+            c.T[j + i * HB] = -tau * a;
+        }
+        if (threadIdx.x == 0) c.T[i + i * HB] = tau;
+    }
+    const int r = blockIdx.x * HT + threadIdx.x;
+    if (r < c.m) {
+        double w = 0.0;
+        for (int q = 0; q < nchunk; ++q) w += c.ww[(long long)q * c.m + r];
+        for (int j = 0; j < i; ++j) {
+            const double f = s2[j];
+            if (f != 0.0) w -= c.Y[r + (long long)j * c.ldv] * f;
+        }
+        c.Y[r + (long long)i * c.ldv] = tau * w;
+    }
+    // the next column's col_prep, fused: row r only needs Y(r, 0..i) (this
+    // thread's) and V's row i (earlier kernels); its partials go to pprep
+    if (prep_next) prep_row(c, i + 1, r, sh);
 }
 
 __global__ void zero_kernel(double* p, long long n) {
@@ -360,29 +369,30 @@ int hessenberg_reduce_device(int64_t n, double* dA, int64_t lda, double* dQ, int
             const int nb_cta = (int)((mmax + HT - 1) / HT);
             const int nchunk_max = (int)((mmax + MV_MIN - 1) / MV_MIN);
             Buf V(mmax * HB, s), Y(mmax * HB, s), T(HB * HB, s), X(mmax, s), part((size_t)nb_cta * HB, s),
+                pprep((size_t)nb_cta * HB, s),
                 pscal(nb_cta, s), psum(nb_cta, s), scal(8, s), s2(HB, s), ww((size_t)nchunk_max * mmax, s), W(HB * n, s),
                 W2(HB * n, s), P(n * HB, s), P2(n * HB, s), K(16 * HB * n, s);
             for (int64_t k = 0; k + 2 < n; k += bdef) {
                 const int b = (int)std::min<int64_t>(bdef, n - 2 - k);
                 const int m = (int)(n - k - 1);
-                Col c{dA + (k + 1), lda, V.p, Y.p, T.p, (long long)m, X.p, part.p, pscal.p, psum.p, scal.p, s2.p,
+                Col c{dA + (k + 1), lda, V.p, Y.p, T.p, (long long)m, X.p, part.p, pprep.p, pscal.p, psum.p, scal.p, s2.p,
                       ww.p, (int)k, m, (m + HT - 1) / HT};
                 zero_kernel<<<64, 256, 0, s>>>(V.p, (long long)m * b);
                 zero_kernel<<<1, 256, 0, s>>>(T.p, HB * HB);
                 inf.launches += 2;
+                col_prep<<<c.nb_cta, HT, 0, s>>>(c, 0);  // later columns: fused into col_y
+                inf.launches += 1;
                 for (int i = 0; i < b; ++i) {
-                    col_prep<<<c.nb_cta, HT, 0, s>>>(c, i);
                     col_apply<<<c.nb_cta, HT, 0, s>>>(c, i);
                     col_sumsq<<<c.nb_cta, HT, 0, s>>>(c, i);
                     col_reflect<<<c.nb_cta, HT, 0, s>>>(c, i);
-                    col_tcol<<<1, 64, 0, s>>>(c, i);
                     // column chunks: enough CTAs to fill the GPU at every panel size
                     const int want = std::max(1, MV_CTAS / c.nb_cta);
                     const int chunk = std::min(MV_COLS, std::max(MV_MIN, (m - i + want - 1) / want));
                     const int nchunk = (m - i + chunk - 1) / chunk;
                     col_matvec<<<dim3(c.nb_cta, nchunk), HT, 0, s>>>(c, i, chunk);
-                    col_y<<<c.nb_cta, HT, 0, s>>>(c, i, nchunk);
-                    inf.launches += 7;
+                    col_y<<<c.nb_cta, HT, 0, s>>>(c, i, nchunk, i + 1 < b ? 1 : 0);
+                    inf.launches += 5;
                 }
                 HCUDA(cudaGetLastError());
                 // trailing block (hessenberg.cpp:110-138): G = A[k+1:, k+b:]
