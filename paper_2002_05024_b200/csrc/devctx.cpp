@@ -161,4 +161,31 @@ void trim_memory_pools() {
         if (cudaMemPoolTrimTo(kv.second, 0) != cudaSuccess) cudaGetLastError();
 }
 
+// A non-blocking default-priority stream cached per host thread, device and
+// slot: a stream's hardware work queue is fixed at creation, and fresh
+// streams per call cycle through the device's queues (8 by default), so that
+// every few calls one shares a queue with the caller's stream -- false
+// dependencies and bimodal call times.  Never destroyed before thread exit.
+namespace {
+struct OneStream {
+    cudaStream_t s = nullptr;
+    ~OneStream() {
+        if (s) cudaStreamDestroy(s);
+        cudaGetLastError();
+    }
+};
+}  // namespace
+
+cudaStream_t cached_stream(int slot) {
+    thread_local std::map<std::pair<int, int>, OneStream> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    OneStream& o = cache[{dev, slot}];
+    if (!o.s && cudaStreamCreateWithFlags(&o.s, cudaStreamNonBlocking) != cudaSuccess) {
+        o.s = nullptr;
+        return nullptr;
+    }
+    return o.s;
+}
+
 }  // namespace teig

@@ -209,7 +209,8 @@ int greorder_schur_device(int64_t n, double* dS, int64_t lds, double* dT, int64_
     cudaStream_t s2 = nullptr;
     cudaEvent_t ev = nullptr;
     try {
-        TEIG_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+        s2 = cached_stream(2);  // kept between calls (launch.h)
+        if (!s2) throw std::runtime_error("stream creation failed");
         TEIG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         // row supports of Q's and Z's columns (one device scan each)
         FactorSupport qsupp, zsupp;
@@ -251,16 +252,15 @@ int greorder_schur_device(int64_t n, double* dS, int64_t lds, double* dT, int64_
         }
         inf.flops_factor_exec = exec;
     } catch (const std::domain_error& e) {
+        if (s2) cudaStreamSynchronize(s2);
         if (ev) cudaEventDestroy(ev);
-        if (s2) cudaStreamDestroy(s2);
         return set_error(TEIG_ERR_STRICT, e.what());
     } catch (const std::exception& e) {
+        if (s2) cudaStreamSynchronize(s2);
         if (ev) cudaEventDestroy(ev);
-        if (s2) cudaStreamDestroy(s2);
         return set_error(TEIG_ERR_CUDA, e.what());
     }
     cudaEventDestroy(ev);
-    cudaStreamDestroy(s2);
     bool leading = true, seen = false;
     for (const auto& b : blocks) {
         if (!b.selected) seen = true;

@@ -58,6 +58,11 @@ cudaError_t launch_update_right(const WinDesc* wins, int nwin, int ntiles, int d
                                 long long rows = -1, long long cols = -1, bool short_ctas = false, int max_ctas = 0,
                                 int short_tiles = 8);
 
+// devctx.cpp: a non-blocking stream cached per host thread, device and slot
+// (slots: 0 host-path Q upload, 1 host-path drain, 2 generalized reorder's
+// factor stream, 3 Schur reduction's side stream); nullptr on failure
+cudaStream_t cached_stream(int slot);
+
 // DMMA instructions the update kernels have issued on the current device so
 // far (bulk-copy kernels: zero Q_w fragments skipped; cp.async kernels); x 512
 // = executed flops.  Synchronous reads (profiling only).

@@ -673,6 +673,36 @@ PassResult run_pass(ReorderPlan& plan, int64_t n, double* dS, int64_t lds, doubl
 // Whatever happens inside the call (a CUDA error thrown mid-pass included),
 // the destructor joins both internal streams into the caller's stream before
 // releasing them, so no enqueued work outlives the call unordered.
+// The internal streams are created once per host thread and device and then
+// reused: a stream's hardware work queue is fixed when it is created, and
+// creating three fresh streams per call cycled them through the device's
+// queues (8 by default) so that every few calls one shared a queue with the
+// caller's stream -- false dependencies, C2 calls at 107 instead of 101 ms.
+struct InternalStreams {
+    cudaStream_t hi = nullptr, lo = nullptr, mid = nullptr;
+    ~InternalStreams() {  // thread exit (errors ignored: the context may be gone)
+        if (hi) cudaStreamDestroy(hi);
+        if (lo) cudaStreamDestroy(lo);
+        if (mid) cudaStreamDestroy(mid);
+        cudaGetLastError();
+    }
+};
+InternalStreams& internal_streams(bool prio) {
+    thread_local std::map<std::pair<int, bool>, InternalStreams> cache;
+    int dev = 0;
+    TEIG_CUDA(cudaGetDevice(&dev));
+    InternalStreams& st = cache[{dev, prio}];
+    if (!st.lo) {
+        int least = 0, greatest = 0;
+        TEIG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        TEIG_CUDA(cudaStreamCreateWithPriority(&st.lo, cudaStreamNonBlocking, prio ? least : 0));
+        // the look-ahead S updates (run_pass): between the two
+        TEIG_CUDA(cudaStreamCreateWithPriority(&st.mid, cudaStreamNonBlocking, prio ? (least + greatest) / 2 : 0));
+        if (prio) TEIG_CUDA(cudaStreamCreateWithPriority(&st.hi, cudaStreamNonBlocking, greatest));
+    }
+    return st;
+}
+
 struct StreamPair {
     cudaStream_t s1 = nullptr, s2 = nullptr, s3 = nullptr, caller = nullptr;
     cudaEvent_t ev = nullptr, join = nullptr;
@@ -680,18 +710,17 @@ struct StreamPair {
     explicit StreamPair(cudaStream_t user) : s1(user), caller(user) {
         prio = !(getenv("TEIG_NO_PRIO") && atoi(getenv("TEIG_NO_PRIO")));
         try {
-            int least = 0, greatest = 0;
-            TEIG_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-            TEIG_CUDA(cudaStreamCreateWithPriority(&s2, cudaStreamNonBlocking, prio ? least : 0));
-            // the look-ahead S updates (run_pass): between the two
-            TEIG_CUDA(cudaStreamCreateWithPriority(&s3, cudaStreamNonBlocking, prio ? (least + greatest) / 2 : 0));
             TEIG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             TEIG_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+            InternalStreams& st = internal_streams(prio);
+            s2 = st.lo;
+            s3 = st.mid;
+            // every internal stream starts after the caller's earlier work
+            TEIG_CUDA(cudaEventRecord(join, user));
+            TEIG_CUDA(cudaStreamWaitEvent(s2, join, 0));
+            TEIG_CUDA(cudaStreamWaitEvent(s3, join, 0));
             if (prio) {
-                cudaStream_t hi = nullptr;
-                TEIG_CUDA(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, greatest));
-                s1 = hi;
-                TEIG_CUDA(cudaEventRecord(join, user));
+                s1 = st.hi;
                 TEIG_CUDA(cudaStreamWaitEvent(s1, join, 0));
             }
         } catch (...) {
@@ -715,10 +744,7 @@ struct StreamPair {
             if (s1 && s1 != caller && cudaEventRecord(join, s1) == cudaSuccess) cudaStreamWaitEvent(caller, join, 0);
         }
         if (ev) cudaEventDestroy(ev);
-        if (join) cudaEventDestroy(join);
-        if (s2) cudaStreamDestroy(s2);
-        if (s3) cudaStreamDestroy(s3);
-        if (s1 && s1 != caller) cudaStreamDestroy(s1);
+        if (join) cudaEventDestroy(join);  // (the streams are kept: internal_streams)
         ev = join = nullptr;
         s2 = s3 = nullptr;
         s1 = caller;
@@ -1061,7 +1087,8 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         qsupp.on = !scan.empty();
         if (Q) {  // Q travels on a side stream while the S-side work starts (measured:
                   // uploading Q before the work starts costs +0.5 s at n=40000)
-            TEIG_CUDA(cudaStreamCreateWithFlags(&qs, cudaStreamNonBlocking));
+            qs = cached_stream(0);
+            if (!qs) throw std::runtime_error("stream creation failed");
             TEIG_CUDA(cudaEventCreateWithFlags(&q_ready, cudaEventDisableTiming));
             if (qsupp.on) {
                 // only the row hull of each block of columns (the scan's
@@ -1113,15 +1140,13 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         struct DrainRes {
             HostDrain& d;
             ~DrainRes() {
-                if (d.ds) {
-                    cudaStreamSynchronize(d.ds);
-                    cudaStreamDestroy(d.ds);
-                }
+                if (d.ds) cudaStreamSynchronize(d.ds);  // (cached: not destroyed)
                 if (d.evS) cudaEventDestroy(d.evS);
                 if (d.evQ) cudaEventDestroy(d.evQ);
             }
         } drain_res{dr};
-        TEIG_CUDA(cudaStreamCreateWithFlags(&dr.ds, cudaStreamNonBlocking));
+        dr.ds = cached_stream(1);
+        if (!dr.ds) throw std::runtime_error("stream creation failed");
         TEIG_CUDA(cudaEventCreateWithFlags(&dr.evS, cudaEventDisableTiming));
         TEIG_CUDA(cudaEventCreateWithFlags(&dr.evQ, cudaEventDisableTiming));
         const int rc = reorder_schur_device(n, dS, n, dQ, n, nb, sizes, flags, opts, perm, rejected, plan, plan_cap,
@@ -1132,7 +1157,6 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
         if (rc != 0) {
             if (qs) cudaStreamSynchronize(qs);
             if (q_ready) cudaEventDestroy(q_ready);
-            if (qs) cudaStreamDestroy(qs);
             return rc;
         }
         if (!dr.valid) {  // replanned: move everything
@@ -1171,12 +1195,11 @@ int teig_reorder_schur_host(int64_t n, double* S, int64_t lds, double* Q, int64_
             fprintf(stderr, "[teig host] alloc %.1f ms  h2d(S) %.1f ms  device %.1f ms  d2h %.1f ms\n", ms(h0, h1),
                     ms(h1, h2), ms(h2, h3), ms(h3, now()));
     } catch (const std::exception& e) {
+        if (qs) cudaStreamSynchronize(qs);
         if (q_ready) cudaEventDestroy(q_ready);
-        if (qs) cudaStreamDestroy(qs);
         return set_error(TEIG_ERR_CUDA, e.what());
     }
     if (q_ready) cudaEventDestroy(q_ready);
-    if (qs) cudaStreamDestroy(qs);
     return 0;
 }
 

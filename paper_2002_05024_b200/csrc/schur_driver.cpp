@@ -208,7 +208,8 @@ class SchurRunner {
         if (getenv("TEIG_NO_WAVE") && atoi(getenv("TEIG_NO_WAVE"))) dopts_.flags |= kSchurFlagNoWave;
         if (getenv("TEIG_NO_LOCAL") && atoi(getenv("TEIG_NO_LOCAL"))) dopts_.flags |= kSchurFlagNoLocal;
         tile_ = o.tile_size ? o.tile_size : default_tile_size(n);
-        TEIG_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
+        s2_ = cached_stream(3);  // kept between calls (launch.h)
+        if (!s2_) throw std::runtime_error("stream creation failed");
         TEIG_CUDA(cudaEventCreateWithFlags(&ev_, cudaEventDisableTiming));
         TEIG_CUDA(cudaMallocHost(&h_out_, sizeof(AedDevOut) + sizeof(int) * 4 + sizeof(double) * 2 * kAedMaxWindow + 64));
         h_int_ = reinterpret_cast<int*>(h_out_ + 1);
@@ -263,7 +264,7 @@ class SchurRunner {
         if (h_out_) cudaFreeHost(h_out_);
         for (auto e : evpool_) cudaEventDestroy(e);
         if (ev_) cudaEventDestroy(ev_);
-        if (s2_) cudaStreamDestroy(s2_);
+        if (s2_) cudaStreamSynchronize(s2_);  // (cached: not destroyed)
     }
 
     double hnorm() {

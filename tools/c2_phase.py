@@ -7,7 +7,7 @@ S0 = T.gen_schur_input(n, T.known_spectrum_seed(1), device=dev)
 sel = T.select_fraction(S0, 0.35, 99)
 T.set_memory_retention(True)
 S = T.colmajor_empty(n, dev); Q = T.colmajor_empty(n, dev); Q0 = T.identity(n, dev)
-for it in range(5):
+for it in range(int(sys.argv[1]) if len(sys.argv) > 1 else 5):
     S.copy_(S0); Q.copy_(Q0); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter(); e0.record()
