@@ -841,49 +841,77 @@ struct BRf {
 // first, and bulges 3 rows apart act on disjoint index sets, so this only
 // reorders commuting left/right multiplications; depth 3nb + active instead
 // of ~nb * active.  pairs: (re1, im1, re2, im2) per bulge.
+//
+// A time step is two barrier-separated phases: the left reflections (all
+// warps), then the right ones (warps 0-6) while the last warp builds every
+// bulge's reflector for the NEXT step -- lane j applies bulge j's right
+// reflection to rows g+1..g+3 (the only ones of column g its next reflector
+// reads; no other bulge touches column g) and reads them back, or, for an
+// introduction, the active block's top-left entries (final after this step's
+// left phase).  Same values as a separate reflector phase, one barrier less.
+__device__ __forceinline__ BRf sweep_refl(const Ctx& c, int lo, int l, int ihi, int aw, int j, int t,
+                                          const double* pairs) {
+    const int s = t - 3 * j;
+    BRf b{0.0, 0.0, 0.0, 0.0, 0, 0, 0, 0};
+    if (s == 0) {
+        const double re1 = pairs[4 * j], im1 = pairs[4 * j + 1], re2 = pairs[4 * j + 2], im2 = pairs[4 * j + 3];
+        double sv[3], v[3], tau;
+        shift_vec_dev(c, lo + l, aw, re1 + re2, re1 * re2 - im1 * im2, sv);
+        b.beta = reflector_fast<3>(sv, v, tau);
+        b.v1 = v[1];
+        b.v2 = v[2];
+        b.tau = tau;
+        b.g = lo + l;
+        b.len = 3;
+        b.kind = 2;
+        b.r1 = lo + l + min(4, aw);
+    } else if (s > 0 && l + s < ihi - 1) {
+        const int r = l + s, len = min(3, ihi - r), g = lo + r;
+        if (len == 3) {
+            double x[3] = {c.H(g, g - 1), c.H(g + 1, g - 1), c.H(g + 2, g - 1)}, v[3], tau;
+            b.beta = reflector_fast<3>(x, v, tau);
+            b.v1 = v[1];
+            b.v2 = v[2];
+            b.tau = tau;
+        } else {
+            double x[2] = {c.H(g, g - 1), c.H(g + 1, g - 1)}, v[2], tau;
+            b.beta = reflector_fast<2>(x, v, tau);
+            b.v1 = v[1];
+            b.tau = tau;
+        }
+        b.g = g;
+        b.len = len;
+        b.kind = 1;
+        b.r1 = lo + min(r + len + 1, ihi);
+    }
+    return b;
+}
+
+__device__ __forceinline__ void sweep_right_row(double* p, int cs, const BRf& b) {
+    if (b.len == 3) {
+        const double w = (p[0] + p[cs] * b.v1 + p[2 * cs] * b.v2) * b.tau;
+        p[0] -= w;
+        p[cs] -= w * b.v1;
+        p[2 * cs] -= w * b.v2;
+    } else {
+        const double w = (p[0] + p[cs] * b.v1) * b.tau;
+        p[0] -= w;
+        p[cs] -= w * b.v1;
+    }
+}
+
 __device__ void sweep_pipelined(const Ctx& c, int lo, int l, int ihi, int nb, const double* pairs) {
-    BRf* tb = reinterpret_cast<BRf*>(c.brf);
+    BRf* tbuf = reinterpret_cast<BRf*>(c.brf);  // two tables of 32 (nb <= 31)
     const int aw = ihi - l;
     const int T = 3 * (nb - 1) + (ihi - 1 - l);
     const int M = 2 * c.N + c.nspk;
+    constexpr int NG = NT - 32;      // threads of the general right phase (warps 0-6)
+    const int owner = tid() - NG;    // last warp: lane j owns bulge j
+    if (owner >= 0 && owner < nb) tbuf[owner] = sweep_refl(c, lo, l, ihi, aw, owner, 0, pairs);
+    __syncthreads();
     for (int t = 0; t < T; ++t) {
-        if (tid() < nb) {
-            const int j = tid(), s = t - 3 * j;
-            BRf b{0.0, 0.0, 0.0, 0.0, 0, 0, 0, 0};
-            if (s == 0) {
-                const double re1 = pairs[4 * j], im1 = pairs[4 * j + 1], re2 = pairs[4 * j + 2], im2 = pairs[4 * j + 3];
-                double sv[3], v[3], tau;
-                shift_vec_dev(c, lo + l, aw, re1 + re2, re1 * re2 - im1 * im2, sv);
-                b.beta = reflector_fast<3>(sv, v, tau);
-                b.v1 = v[1];
-                b.v2 = v[2];
-                b.tau = tau;
-                b.g = lo + l;
-                b.len = 3;
-                b.kind = 2;
-                b.r1 = lo + l + min(4, aw);
-            } else if (s > 0 && l + s < ihi - 1) {
-                const int r = l + s, len = min(3, ihi - r), g = lo + r;
-                if (len == 3) {
-                    double x[3] = {c.H(g, g - 1), c.H(g + 1, g - 1), c.H(g + 2, g - 1)}, v[3], tau;
-                    b.beta = reflector_fast<3>(x, v, tau);
-                    b.v1 = v[1];
-                    b.v2 = v[2];
-                    b.tau = tau;
-                } else {
-                    double x[2] = {c.H(g, g - 1), c.H(g + 1, g - 1)}, v[2], tau;
-                    b.beta = reflector_fast<2>(x, v, tau);
-                    b.v1 = v[1];
-                    b.tau = tau;
-                }
-                b.g = g;
-                b.len = len;
-                b.kind = 1;
-                b.r1 = lo + min(r + len + 1, ihi);
-            }
-            tb[j] = b;
-        }
-        __syncthreads();
+        const BRf* tb = tbuf + (t & 1) * 32;
+        BRf* tn = tbuf + ((t + 1) & 1) * 32;
         for (int it = tid(); it < nb * c.N; it += NT) {
             const int j = it / c.N, col = it - j * c.N;
             const BRf b = tb[j];
@@ -903,34 +931,32 @@ __device__ void sweep_pipelined(const Ctx& c, int lo, int l, int ihi, int nb, co
             }
         }
         __syncthreads();
-        for (int it = tid(); it < nb * M; it += NT) {
-            const int j = it / M, k = it - j * M;
-            const BRf b = tb[j];
-            if (!b.kind || b.tau == 0.0) continue;
-            double* p;
-            int cs;
-            if (k < c.N) {
-                if (k >= b.r1) continue;
-                p = &c.H(k, b.g);
-                cs = c.H.ld;
-            } else if (k < 2 * c.N) {
-                p = &c.Q(k - c.N, b.g);
-                cs = c.Q.ld;
-            } else {
-                const Spk& sp = c.spk[k - 2 * c.N];
-                p = sp.p + (b.g - sp.off);
-                cs = 1;
+        if (owner < 0) {
+            for (int it = tid(); it < nb * M; it += NG) {
+                const int j = it / M, k = it - j * M;
+                const BRf b = tb[j];
+                if (!b.kind || b.tau == 0.0) continue;
+                double* p;
+                int cs;
+                if (k < c.N) {
+                    if (k >= b.r1 || (k > b.g && k <= b.g + 3)) continue;  // rows g+1..g+3: the owner
+                    p = &c.H(k, b.g);
+                    cs = c.H.ld;
+                } else if (k < 2 * c.N) {
+                    p = &c.Q(k - c.N, b.g);
+                    cs = c.Q.ld;
+                } else {
+                    const Spk& sp = c.spk[k - 2 * c.N];
+                    p = sp.p + (b.g - sp.off);
+                    cs = 1;
+                }
+                sweep_right_row(p, cs, b);
             }
-            if (b.len == 3) {
-                const double w = (p[0] + p[cs] * b.v1 + p[2 * cs] * b.v2) * b.tau;
-                p[0] -= w;
-                p[cs] -= w * b.v1;
-                p[2 * cs] -= w * b.v2;
-            } else {
-                const double w = (p[0] + p[cs] * b.v1) * b.tau;
-                p[0] -= w;
-                p[cs] -= w * b.v1;
-            }
+        } else if (owner < nb) {
+            const BRf b = tb[owner];
+            if (b.kind && b.tau != 0.0)
+                for (int k = b.g + 1; k <= b.g + 3 && k < b.r1; ++k) sweep_right_row(&c.H(k, b.g), c.H.ld, b);
+            if (t + 1 < T) tn[owner] = sweep_refl(c, lo, l, ihi, aw, owner, t + 1, pairs);
         }
         __syncthreads();
     }
