@@ -32,6 +32,14 @@ import sys
 import threading
 import time
 
+# More hardware work queues than the default 8 (read once, at CUDA
+# initialisation, so before torch touches the device): the library runs a
+# level's window kernels, bulk updates and factor updates on three streams
+# beside the caller's; with 8 queues two of them can share one and pick up
+# false dependencies (C2 calls 100 vs 106 ms depending on stream-creation
+# order).  INTEGRATION.md recommends the same for applications.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
