@@ -69,11 +69,11 @@ constexpr int kLSub = TEIG_LSUB;                // left: columns per sub-tile
 constexpr int kRSub = 64;        // right: rows per sub-tile (the whole planner tile)
 constexpr int kLdA = 72;         // right: doubles per panel column in smem (<= kRSub+1 rows used, = 8 mod 16)
 
-// Window-order classes: DW = 128 (windows of order 65..128) or 64 (<= 64).
-// Left: warps tile the DW output rows in 16-row slices (DW / 16 of them) and
-// split the sub-tile's columns among the rest; right: DW / 16 slices of 16
-// output columns, the sub-tile's rows split among the rest.  Q_w fragments
-// in registers: 2 x DW / 4 per lane.
+// Window-order class DW = 128 (windows of order 65..128; the order <= 64
+// class has its own kernels below).  Left: warps tile the DW output rows in
+// 16-row slices (DW / 16 of them) and split the sub-tile's columns among the
+// rest; right: DW / 16 slices of 16 output columns, the sub-tile's rows split
+// among the rest.  Q_w fragments in registers: 2 x DW / 4 per lane.
 template <int DW>
 struct LeftCfg {
     static constexpr int kLd = DW == 128 ? 132 : 68;  // doubles per panel column in smem (<= DW+1 used, = 4 mod 16)
@@ -93,6 +93,34 @@ struct RightCfg {
     static constexpr int kMSplit = kWarps / kNGroups; // warps along the sub-tile's rows
     static constexpr int kMT = kRSub / 8 / kMSplit;   // 8-row tiles per warp
     static constexpr int kKS = DW / 4;
+    static constexpr size_t kSmem = (size_t)kStages * kStage;
+};
+
+// The order <= 64 kernels (the generalized reorder's windows, C5): each warp
+// owns ONE 8-row (left) / 8-column (right) fragment tile over the whole
+// sub-tile, so the 16 Q_w fragments per lane and the accumulators fit 128
+// registers without spills at two CTAs per SM (the order-128 kernels'
+// 16-row slices on half the warps spilled there: C5 1.47 -> 1.23 s).  Kept
+// apart from the order-128 kernels, whose register allocation is tuned.
+struct Left64Cfg {
+    static constexpr int kLd = 68;                    // doubles per panel column in smem (<= 65 used, = 4 mod 16)
+    static constexpr int kStages = kLSub == 64 ? 3 : 4;
+    static constexpr int kStage = kLSub * kLd * 8;
+    static constexpr int kFT = 1;
+    static constexpr int kMGroups = 8;                // warps along the rows (8 rows each)
+    static constexpr int kNSplit = 1;
+    static constexpr int kNT = kLSub / 8;
+    static constexpr int kKS = 16;
+    static constexpr size_t kSmem = (size_t)kStages * kStage;
+};
+struct Right64Cfg {
+    static constexpr int kStages = 3;
+    static constexpr int kStage = 64 * kLdA * 8;
+    static constexpr int kFT = 1;
+    static constexpr int kNGroups = 8;                // warps along the columns (8 columns each)
+    static constexpr int kMSplit = 1;
+    static constexpr int kMT = kRSub / 8;
+    static constexpr int kKS = 16;
     static constexpr size_t kSmem = (size_t)kStages * kStage;
 };
 
@@ -532,6 +560,315 @@ update_right_bulk_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles,
 }
 
 // ---------------------------------------------------------------------------
+// LEFT, windows of order <= 64: S[a:a+d, c:c+64] <- Q_w^T S[a:a+d, c:c+64], in kLSub-column
+// sub-tiles; warp w owns output rows [16 wm, 16 wm + 16) (wm = w mod DW/16)
+// of the sub-tile's column slice w / (DW/16).
+__global__ void __launch_bounds__(kBulkThreads, 2)
+update_left_bulk64_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, const double* __restrict__ qw_pool,
+                        double* __restrict__ S, long long lds, long long alloc) {
+    constexpr int DW = 64;
+    using C = Left64Cfg;
+    constexpr int kLdB = C::kLd, kLeftStage = C::kStage, kLStages = C::kStages, kNT = C::kNT, kKS = C::kKS;
+    constexpr int FT = C::kFT;
+    extern __shared__ __align__(128) double ring[];
+    __shared__ __align__(8) uint64_t full[kLStages];
+    init_ring(full, kLStages, ring, kLStages * kLeftStage, kLSub / 32);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wm = warp % C::kMGroups, wn = warp / C::kMGroups;
+    const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
+    const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
+
+    // every thread walks the (tile, sub-tile) sequence a ring depth ahead of the
+    // one it computes; thread j < kLSub copies panel column j of each refilled
+    // stage and arrives on its full barrier with its own byte count
+    int pt = t0, psub = 0;
+    TileWin pw;
+    const int jj = threadIdx.x;
+    auto produce = [&](int slot) {  // block-uniform
+        while (pt < t1) {
+            seek_win<0>(pw, wins, nwin, pt);
+            const int c = pw.r0 + (pt - pw.pref) * kLeftBN;
+            const int ncols = min(kLeftBN, pw.r1 - c);
+            if (psub * kLSub >= ncols) {
+                ++pt;
+                psub = 0;
+                continue;
+            }
+            if (jj < kLSub) {
+                double* dst = ring + slot * (kLeftStage / 8) + jj * kLdB;
+                long long start = 0;
+                int n = 0;
+                if (kLSub * psub + jj < ncols)
+                    n = plan_segment(dst, S, (long long)pw.a + (long long)(c + kLSub * psub + jj) * lds, pw.d, alloc,
+                                     start);
+                warp_arrive(&full[slot], (unsigned)n * 8u);
+                if (n > 0) bulk_copy(dst, S + start, (unsigned)n * 8u, &full[slot]);
+            }
+            ++psub;
+            return;
+        }
+    };
+    const int wi0 = window_of<0>(wins, nwin, t0);
+    load_win<0>(pw, wins, nwin, wi0);
+    for (int sl = 0; sl < kLStages; ++sl) produce(sl);
+
+    const int gid = lane >> 2, tig = lane & 3;
+    double af[FT][kKS];
+    unsigned nz[FT];  // bit ks: fragment af[mt][ks] is nonzero in some lane (warp-uniform)
+#pragma unroll
+    for (int f = 0; f < FT; ++f) nz[f] = 0;
+    unsigned long long ndmma = 0;
+    TileWin wd;
+    load_win<0>(wd, wins, nwin, wi0);
+    int cur = -1, stage = 0, prev = -1;
+    unsigned phase = 0;
+    for (int t = t0; t < t1; ++t) {
+        seek_win<0>(wd, wins, nwin, t);
+        const int d = wd.d;
+        if (wd.wi != cur) {  // A = Q_w^T: af[mt][ks] = Q_w(k = 4ks + tig, m = 8 (FT wm + mt) + gid)
+            const double* Qw = qw_pool + wd.qw_off;
+#pragma unroll
+            for (int mt = 0; mt < FT; ++mt) {
+                const int m = 8 * (FT * wm + mt) + gid;
+#pragma unroll
+                for (int ks = 0; ks < kKS; ++ks) {
+                    const int k = 4 * ks + tig;
+                    af[mt][ks] = (m < d && k < d) ? __ldg(Qw + k + (long long)m * d) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int mt = 0; mt < FT; ++mt) nz[mt] = 0;
+#pragma unroll
+            for (int ks = 0; ks < kKS; ++ks)
+#pragma unroll
+                for (int mt = 0; mt < FT; ++mt) nz[mt] |= (__any_sync(0xffffffffu, af[mt][ks] != 0.0) ? 1u : 0u) << ks;
+            cur = wd.wi;
+        }
+        const int c = wd.r0 + (t - wd.pref) * kLeftBN;
+        const int ncols = min(kLeftBN, wd.r1 - c);
+        double* P = S + (long long)wd.a + (long long)c * lds;
+        for (int sub = 0; kLSub * sub < ncols; ++sub) {
+            double acc[FT][kNT][2];
+#pragma unroll
+            for (int i = 0; i < FT; ++i)
+#pragma unroll
+                for (int j = 0; j < kNT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            // column 8 (wn kNT + nt) + gid, row k = 4 ks + tig (+ the sub-tile's shift)
+            const int shift = (int)(((long long)wd.a + (long long)(c + kLSub * sub) * lds) & 1);
+            const double* sb = ring + stage * (kLeftStage / 8) + (8 * kNT * wn + gid) * kLdB + tig + shift;
+            mbar_wait(&full[stage], phase);
+#pragma unroll
+            for (int mt = 0; mt < FT; ++mt) ndmma += (unsigned long long)__popc(nz[mt]) * kNT;
+            // Q_w's zero 8x4 fragments (about 45 % of them: a window only mixes
+            // the blocks it moves past each other) are skipped -- their products
+            // are exact zeros and the sums start at +0, so the bits do not change
+#pragma unroll
+            for (int ks = 0; ks < kKS; ++ks) {
+                bool u[FT], any = false;
+#pragma unroll
+                for (int mt = 0; mt < FT; ++mt) {
+                    u[mt] = (nz[mt] >> ks) & 1u;
+                    any |= u[mt];
+                }
+                if (!any) continue;
+                double bf[kNT];
+#pragma unroll
+                for (int nt = 0; nt < kNT; ++nt) bf[nt] = sb[nt * 8 * kLdB + 4 * ks];
+#pragma unroll
+                for (int mt = 0; mt < FT; ++mt)
+                    if (u[mt])
+#pragma unroll
+                        for (int nt = 0; nt < kNT; ++nt) dmma(acc[mt][nt][0], acc[mt][nt][1], af[mt][ks], bf[nt]);
+            }
+            // epilogue through the consumed stage: accumulators to smem at the
+            // inputs' positions, then one bulk store per column (async: the
+            // warps go on to the next sub-tile while the TMA engine writes)
+            __syncthreads();  // every warp is done reading the stage
+            double* so = ring + stage * (kLeftStage / 8) + shift;
+#pragma unroll
+            for (int mt = 0; mt < FT; ++mt) {
+                const int r = 8 * (FT * wm + mt) + gid;
+#pragma unroll
+                for (int nt = 0; nt < kNT; ++nt) {
+                    const int cc = 8 * (kNT * wn + nt) + 2 * tig;
+                    so[cc * kLdB + r] = acc[mt][nt][0];
+                    so[(cc + 1) * kLdB + r] = acc[mt][nt][1];
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncthreads();
+            if (jj < kLSub && kLSub * sub + jj < ncols)
+                store_column(P + (long long)(kLSub * sub + jj) * lds, so + jj * kLdB, shift, d);
+            bulk_commit();
+            // refill the stage of the previous sub-tile (its stores went out
+            // one sub-tile ago) with the sub-tile a ring depth after it
+            if (prev >= 0) {
+                bulk_wait_read<1>();
+                produce(prev);
+            }
+            prev = stage;
+            if (++stage == kLStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+        }
+    }
+    if (lane == 0 && ndmma) atomicAdd(&g_dmma_bulk, ndmma);
+    bulk_wait_all();  // the last stores land before the CTA retires
+}
+
+// ---------------------------------------------------------------------------
+// RIGHT, windows of order <= 64: M[r0:r0+64, a:a+d] <- M[r0:r0+64, a:a+d] Q_w, in kRSub-row
+// sub-tiles; warp w owns output columns [16 wn, 16 wn + 16) (wn = w mod DW/16)
+// of the sub-tile's row slice w / (DW/16).  (64-row sub-tiles:
+// the 128 column copies of a stage are 512 bytes each -- 32-row stages of
+// 256-byte copies left the ring starved, the TMA engine's per-copy cost.)
+template <int Field>
+__global__ void __launch_bounds__(kBulkThreads, 2)
+update_right_bulk64_kernel(const WinDesc* __restrict__ wins, int nwin, int ntiles, const double* __restrict__ qw_pool,
+                         double* __restrict__ M, long long ldm, long long alloc) {
+    constexpr int DW = 64;
+    using C = Right64Cfg;
+    constexpr int kRightStage = C::kStage, kRStages = C::kStages, kMT = C::kMT, kKS = C::kKS;
+    constexpr int FT = C::kFT;
+    extern __shared__ __align__(128) double ring[];
+    __shared__ __align__(8) uint64_t full[kRStages];
+    init_ring(full, kRStages, ring, kRStages * kRightStage, DW / 32);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int wn = warp % C::kNGroups, wm = warp / C::kNGroups;
+    const int t0 = (int)((long long)ntiles * blockIdx.x / gridDim.x);
+    const int t1 = (int)((long long)ntiles * (blockIdx.x + 1) / gridDim.x);
+    auto tile_rows = [&](const TileWin& w, int t, int& r0, int& nrows) {
+        r0 = w.r0 + (t - w.pref) * kRightBM;
+        nrows = min(kRightBM, w.r1 - r0);
+    };
+
+    // every thread walks the (tile, sub-tile) sequence a ring depth ahead of the
+    // one it computes; thread j < DW copies panel column j of each refilled
+    // stage and arrives on its full barrier with its own byte count
+    int pt = t0, psub = 0;
+    TileWin pw;
+    const int kk = threadIdx.x;
+    auto produce = [&](int slot) {  // block-uniform
+        while (pt < t1) {
+            seek_win<Field>(pw, wins, nwin, pt);
+            int r0, nrows;
+            tile_rows(pw, pt, r0, nrows);
+            if (psub * kRSub >= nrows) {
+                ++pt;
+                psub = 0;
+                continue;
+            }
+            if (kk < DW) {
+                const int rs = r0 + kRSub * psub, len = min(kRSub, nrows - kRSub * psub);
+                double* dst = ring + slot * (kRightStage / 8) + kk * kLdA;
+                long long st = 0;
+                int n = 0;
+                if (kk < pw.d)
+                    n = plan_segment(dst, M, (long long)rs + (long long)(pw.a + kk) * ldm, len, alloc, st);
+                warp_arrive(&full[slot], (unsigned)n * 8u);
+                if (n > 0) bulk_copy(dst, M + st, (unsigned)n * 8u, &full[slot]);
+            }
+            ++psub;
+            return;
+        }
+    };
+    const int wi0 = window_of<Field>(wins, nwin, t0);
+    load_win<Field>(pw, wins, nwin, wi0);
+    for (int sl = 0; sl < kRStages; ++sl) produce(sl);
+
+    const int gid = lane >> 2, tig = lane & 3;
+    double bf[FT][kKS];
+    unsigned nz[FT];  // bit ks: fragment bf[nt][ks] is nonzero in some lane (warp-uniform)
+#pragma unroll
+    for (int f = 0; f < FT; ++f) nz[f] = 0;
+    unsigned long long ndmma = 0;
+    TileWin wd;
+    load_win<Field>(wd, wins, nwin, wi0);
+    int cur = -1, stage = 0;
+    unsigned phase = 0;
+    for (int t = t0; t < t1; ++t) {
+        seek_win<Field>(wd, wins, nwin, t);
+        const int d = wd.d;
+        if (wd.wi != cur) {  // B = Q_w: bf[nt][ks] = Q_w(k = 4ks + tig, n = 8 (FT wn + nt) + gid)
+            const double* Qw = qw_pool + wd.qw_off;
+#pragma unroll
+            for (int nt = 0; nt < FT; ++nt) {
+                const int nn = 8 * (FT * wn + nt) + gid;
+#pragma unroll
+                for (int ks = 0; ks < kKS; ++ks) {
+                    const int k = 4 * ks + tig;
+                    bf[nt][ks] = (nn < d && k < d) ? __ldg(Qw + k + (long long)nn * d) : 0.0;
+                }
+            }
+#pragma unroll
+            for (int nt = 0; nt < FT; ++nt) nz[nt] = 0;
+#pragma unroll
+            for (int ks = 0; ks < kKS; ++ks)
+#pragma unroll
+                for (int nt = 0; nt < FT; ++nt) nz[nt] |= (__any_sync(0xffffffffu, bf[nt][ks] != 0.0) ? 1u : 0u) << ks;
+            cur = wd.wi;
+        }
+        int r0, nrows;
+        tile_rows(wd, t, r0, nrows);
+        double* P = M + (long long)r0 + (long long)wd.a * ldm;
+        for (int sub = 0; kRSub * sub < nrows; ++sub) {
+            double acc[kMT][FT][2];
+#pragma unroll
+            for (int i = 0; i < kMT; ++i)
+#pragma unroll
+                for (int j = 0; j < FT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            // row 8 mt + gid, column k = 4 ks + tig (+ the sub-tile's shift)
+            const int shift = (int)(((long long)r0 + kRSub * sub + (long long)wd.a * ldm) & 1);
+            const double* sa = ring + stage * (kRightStage / 8) + tig * kLdA + 8 * kMT * wm + gid + shift;
+            mbar_wait(&full[stage], phase);
+#pragma unroll
+            for (int nt = 0; nt < FT; ++nt) ndmma += (unsigned long long)__popc(nz[nt]) * kMT;
+            // zero fragments of Q_w skipped (exact: see the left kernel)
+#pragma unroll
+            for (int ks = 0; ks < kKS; ++ks) {
+                bool u[FT], any = false;
+#pragma unroll
+                for (int nt = 0; nt < FT; ++nt) {
+                    u[nt] = (nz[nt] >> ks) & 1u;
+                    any |= u[nt];
+                }
+                if (!any) continue;
+                double a[kMT];
+#pragma unroll
+                for (int mt = 0; mt < kMT; ++mt) a[mt] = sa[4 * ks * kLdA + 8 * mt];
+#pragma unroll
+                for (int nt = 0; nt < FT; ++nt)
+                    if (u[nt])
+#pragma unroll
+                        for (int mt = 0; mt < kMT; ++mt) dmma(acc[mt][nt][0], acc[mt][nt][1], a[mt], bf[nt][ks]);
+            }
+            // direct stores: with a 3-deep ring of 64-row stages the staged
+            // (bulk-store) epilogue of the left kernel delays the refill by one
+            // sub-tile and measured 2-3 % slower here
+            __syncthreads();  // the stage is free
+            produce(stage);
+            if (++stage == kRStages) {
+                stage = 0;
+                phase ^= 1u;
+            }
+#pragma unroll
+            for (int mt = 0; mt < kMT; ++mt) {
+                const int r = kRSub * sub + 8 * (kMT * wm + mt) + gid;
+                if (r >= nrows) continue;
+#pragma unroll
+                for (int nt = 0; nt < FT; ++nt) {
+                    const int cc = 8 * (FT * wn + nt) + 2 * tig;
+                    if (cc < d) P[r + (long long)cc * ldm] = acc[mt][nt][0];
+                    if (cc + 1 < d) P[r + (long long)(cc + 1) * ldm] = acc[mt][nt][1];
+                }
+            }
+        }
+    }
+    if (lane == 0 && ndmma) atomicAdd(&g_dmma_bulk, ndmma);
+}
+
+// ---------------------------------------------------------------------------
 // host side
 
 namespace {
@@ -562,21 +899,36 @@ bool bulk_eligible(int dmax, const double* base, long long ld, long long rows, l
 template <int DW>
 cudaError_t left_bulk(const WinDesc* wins, int nwin, int ntiles, const double* qw_pool, double* S, long long lds,
                       long long alloc, int grid, cudaStream_t stream) {
-    constexpr size_t smem = LeftCfg<DW>::kSmem;
-    cudaError_t e = ensure_dyn_smem((const void*)update_left_bulk_kernel<DW>, smem);
-    if (e != cudaSuccess) return e;
-    update_left_bulk_kernel<DW><<<grid, kBulkThreads, smem, stream>>>(wins, nwin, ntiles, qw_pool, S, lds, alloc);
+    if constexpr (DW == 64) {
+        constexpr size_t smem = Left64Cfg::kSmem;
+        cudaError_t e = ensure_dyn_smem((const void*)update_left_bulk64_kernel, smem);
+        if (e != cudaSuccess) return e;
+        update_left_bulk64_kernel<<<grid, kBulkThreads, smem, stream>>>(wins, nwin, ntiles, qw_pool, S, lds, alloc);
+    } else {
+        constexpr size_t smem = LeftCfg<DW>::kSmem;
+        cudaError_t e = ensure_dyn_smem((const void*)update_left_bulk_kernel<DW>, smem);
+        if (e != cudaSuccess) return e;
+        update_left_bulk_kernel<DW><<<grid, kBulkThreads, smem, stream>>>(wins, nwin, ntiles, qw_pool, S, lds, alloc);
+    }
     return cudaGetLastError();
 }
 
 template <int DW, int Field>
 cudaError_t right_bulk(const WinDesc* wins, int nwin, int ntiles, const double* qw_pool, double* M, long long ldm,
                        long long alloc, int grid, cudaStream_t stream) {
-    constexpr size_t smem = RightCfg<DW>::kSmem;
-    cudaError_t e = ensure_dyn_smem((const void*)update_right_bulk_kernel<DW, Field>, smem);
-    if (e != cudaSuccess) return e;
-    update_right_bulk_kernel<DW, Field><<<grid, kBulkThreads, smem, stream>>>(wins, nwin, ntiles, qw_pool, M, ldm,
-                                                                              alloc);
+    if constexpr (DW == 64) {
+        constexpr size_t smem = Right64Cfg::kSmem;
+        cudaError_t e = ensure_dyn_smem((const void*)update_right_bulk64_kernel<Field>, smem);
+        if (e != cudaSuccess) return e;
+        update_right_bulk64_kernel<Field><<<grid, kBulkThreads, smem, stream>>>(wins, nwin, ntiles, qw_pool, M, ldm,
+                                                                                  alloc);
+    } else {
+        constexpr size_t smem = RightCfg<DW>::kSmem;
+        cudaError_t e = ensure_dyn_smem((const void*)update_right_bulk_kernel<DW, Field>, smem);
+        if (e != cudaSuccess) return e;
+        update_right_bulk_kernel<DW, Field><<<grid, kBulkThreads, smem, stream>>>(wins, nwin, ntiles, qw_pool, M,
+                                                                                  ldm, alloc);
+    }
     return cudaGetLastError();
 }
 
