@@ -19,8 +19,9 @@
 //   3. rows of every pair (S and T, columns right of the block) <- Q_m^T;
 //   4. columns of every pair (S and T rows above; all rows of Q_w / Z_w)
 //      <- Q_m / Z_m, and the new diagonal blocks;
-// then thread 0 commits the arrangement (a rejected swap marks its selected
-// block stuck: it stops, later blocks stack below it).
+// then warp 0 commits the arrangement (a rejected swap marks its selected
+// block stuck: it stops, later blocks stack below it) and lists the next
+// step's pairs behind the same barrier.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -228,9 +229,9 @@ gwindow_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S,
     }
     __syncthreads();
     if (sh.executed) {
+        if (warp == 0) gfind_pairs(sh, nb, lane);  // list the first step's pairs
+        __syncthreads();
         for (;;) {
-            if (warp == 0) gfind_pairs(sh, nb, lane);  // list the pairs
-            __syncthreads();
             const int np = sh.npairs;
             if (np == 0) break;
             for (int pi = warp; pi < np; pi += NW) {  // decisions, one warp per pair
@@ -259,15 +260,19 @@ gwindow_reorder_kernel(const WinDesc* __restrict__ wins, double* __restrict__ S,
                 else pair_phase_cols<4>(sh, Sw, Tw, Qw, Zw, ld, d, pi, lane);
             }
             __syncthreads();
-            if (tid < np) {  // commit: the pairs own disjoint slots
-                const GPair pr = sh.pairs[tid];
-                const int u = sh.arr[pr.slot], b = sh.arr[pr.slot + 1];
-                if (pr.ok) {
-                    sh.arr[pr.slot] = (uint8_t)b;
-                    sh.arr[pr.slot + 1] = (uint8_t)u;
-                } else {
-                    sh.bstuck[b] = 1;
+            if (warp == 0) {  // commit (a lane per pair: disjoint slots), then the next step's pairs
+                if (lane < np) {
+                    const GPair pr = sh.pairs[lane];
+                    const int u = sh.arr[pr.slot], b = sh.arr[pr.slot + 1];
+                    if (pr.ok) {
+                        sh.arr[pr.slot] = (uint8_t)b;
+                        sh.arr[pr.slot + 1] = (uint8_t)u;
+                    } else {
+                        sh.bstuck[b] = 1;
+                    }
                 }
+                __syncwarp();
+                gfind_pairs(sh, nb, lane);
             }
             __syncthreads();
         }
