@@ -162,31 +162,41 @@ __device__ __forceinline__ bool wgswap(const double* Sw, const double* Tw, int l
         int cp[K];
 #pragma unroll
         for (int i = 0; i < K; ++i) cp[i] = i;
+        // (interchanges as select chains: written as conditional swaps the
+        // compiler turned them into dynamically indexed local-memory swaps)
 #pragma unroll
-        for (int s = 0; s < K; ++s)
+        for (int s = 0; s < K; ++s) {
+            const int p = piv_c[s], cs = cp[s];
+            int cq = cs;
 #pragma unroll
-            for (int j = s + 1; j < K; ++j)
-                if (piv_c[s] == j) {
-                    const int t = cp[s];
-                    cp[s] = cp[j];
-                    cp[j] = t;
-                }
+            for (int j = s + 1; j < K; ++j) cq = (p == j) ? cp[j] : cq;
+#pragma unroll
+            for (int j = s + 1; j < K; ++j) cp[j] = (p == j) ? cs : cp[j];
+            cp[s] = cq;
+        }
 #pragma unroll
         for (int i = 0; i < K; ++i)
             if (cp[i] == lane) src = i;
     }
     // GecpLU::solve's operations, every lane on the whole vector (broadcast
     // reads of the factors), each lane keeping its own component
-    auto solve = [&](double (&x)[K]) -> double {
+    // (everything by value -- the pivots and the vector stay in registers;
+    // a by-reference capture put them in local memory)
+    struct Vec {
+        double v[K];
+    };
+    auto solve = [=, &w](Vec xv) -> double {
+        double (&x)[K] = xv.v;
 #pragma unroll
         for (int s = 0; s < K; ++s) {
+            const int p = piv_r[s];
+            const double xs = x[s];
+            double xq = xs;
 #pragma unroll
-            for (int i = s + 1; i < K; ++i)
-                if (piv_r[s] == i) {
-                    const double t = x[s];
-                    x[s] = x[i];
-                    x[i] = t;
-                }
+            for (int i = s + 1; i < K; ++i) xq = (p == i) ? x[i] : xq;
+#pragma unroll
+            for (int i = s + 1; i < K; ++i) x[i] = (p == i) ? xs : x[i];
+            x[s] = xq;
 #pragma unroll
             for (int i = s + 1; i < K; ++i) x[i] -= w.F[i * K + s] * x[s];
         }
@@ -198,11 +208,18 @@ __device__ __forceinline__ bool wgswap(const double* Sw, const double* Tw, int l
             for (int j = kk + 1; j < K; ++j) acc -= w.U[kk * K + j] * y[j];
             y[kk] = acc / w.U[kk * K + kk];
         }
-        double v = 0.0;
+        // y[src] by a tree of selects on src's bits (a linear select chain
+        // was turned back into an indexed local-memory load)
+        double t2[K];
 #pragma unroll
-        for (int i = 0; i < K; ++i)
-            if (i == src) v = y[i];
-        return v;
+        for (int i = 0; i < K; ++i) t2[i] = y[i];
+#pragma unroll
+        for (int w2 = K / 2, bit = 0; w2 >= 1; w2 >>= 1, ++bit) {
+            const bool hi = (src >> bit) & 1;
+#pragma unroll
+            for (int i = 0; i < w2; ++i) t2[i] = hi ? t2[2 * i + 1] : t2[2 * i];
+        }
+        return t2[0];
     };
     double rhs[K];
 #pragma unroll
@@ -214,9 +231,9 @@ __device__ __forceinline__ bool wgswap(const double* Sw, const double* Tw, int l
         }
     double x;
     {
-        double t[K];
+        Vec t;
 #pragma unroll
-        for (int i = 0; i < K; ++i) t[i] = rhs[i];
+        for (int i = 0; i < K; ++i) t.v[i] = rhs[i];
         x = solve(t);  // lane t < K: x_t
     }
     {  // one refinement step: residual row per lane (serial order), gathered
@@ -229,9 +246,9 @@ __device__ __forceinline__ bool wgswap(const double* Sw, const double* Tw, int l
             const double xc = __shfl_sync(kFull, x, c);
             if (lane < K) res -= w.K0[lane * K + c] * xc;
         }
-        double t[K];
+        Vec t;
 #pragma unroll
-        for (int i = 0; i < K; ++i) t[i] = __shfl_sync(kFull, res, i);
+        for (int i = 0; i < K; ++i) t.v[i] = __shfl_sync(kFull, res, i);
         x += solve(t);
     }
     if (lane < K) w.X[lane] = x;
