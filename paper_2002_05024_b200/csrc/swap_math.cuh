@@ -237,17 +237,21 @@ struct GecpLU {
         rcond = ok ? ((amax > 0.0) ? smin / amax : 0.0) : 0.0;
     }
 
-    // rhs <- solution, replaying the interchanges and multipliers
+    // rhs <- solution, replaying the interchanges and multipliers.  The
+    // interchanges are select chains: written as conditional swaps the
+    // compiler turned them into dynamically indexed local-memory swaps on the
+    // window kernels' critical path (same values either way).
     __device__ __forceinline__ void solve(double (&rhs)[K]) const {
 #pragma unroll
         for (int s = 0; s < K; ++s) {
+            const int p = pi[s];
+            const double xs = rhs[s];
+            double xq = xs;
 #pragma unroll
-            for (int i = s + 1; i < K; ++i)
-                if (pi[s] == i) {
-                    const double t = rhs[s];
-                    rhs[s] = rhs[i];
-                    rhs[i] = t;
-                }
+            for (int i = s + 1; i < K; ++i) xq = (p == i) ? rhs[i] : xq;
+#pragma unroll
+            for (int i = s + 1; i < K; ++i) rhs[i] = (p == i) ? xs : rhs[i];
+            rhs[s] = xq;
 #pragma unroll
             for (int i = s + 1; i < K; ++i) rhs[i] -= f[i][s] * rhs[s];
         }
@@ -264,20 +268,20 @@ struct GecpLU {
 #pragma unroll
         for (int i = 0; i < K; ++i) cp[i] = i;
 #pragma unroll
-        for (int s = 0; s < K; ++s)
+        for (int s = 0; s < K; ++s) {
+            const int p = pj[s], cs = cp[s];
+            int cq = cs;
 #pragma unroll
-            for (int j = s + 1; j < K; ++j)
-                if (pj[s] == j) {
-                    const int t = cp[s];
-                    cp[s] = cp[j];
-                    cp[j] = t;
-                }
+            for (int j = s + 1; j < K; ++j) cq = (p == j) ? cp[j] : cq;
+#pragma unroll
+            for (int j = s + 1; j < K; ++j) cp[j] = (p == j) ? cs : cp[j];
+            cp[s] = cq;
+        }
 #pragma unroll
         for (int t = 0; t < K; ++t) {
             double v = 0.0;
 #pragma unroll
-            for (int i = 0; i < K; ++i)
-                if (cp[i] == t) v = x[i];
+            for (int i = 0; i < K; ++i) v = (cp[i] == t) ? x[i] : v;
             rhs[t] = v;
         }
     }
